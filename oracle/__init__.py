@@ -1,0 +1,233 @@
+"""CPU oracle for the LGDM K/R assembly path (arXiv 2301.06503) -- TEST INFRASTRUCTURE.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import this package.  The product
+(``paper_2301_06503_b200``) never imports it; the two share no code.
+
+Thin ctypes wrapper over ``liblgdm_oracle.so`` (plain C++, built from
+``lgdm_oracle.cpp`` with ``-O2 -ffp-contract=off``).  Every function cites the
+PAPER.md passage it implements in the C++ source.  Parity pins live in
+``tests/test_oracle_*.py``.
+
+Parity unpinned: physical fidelity to the paper's load-displacement
+and damage figures (images and parameters missing from PAPER.md).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "lgdm_oracle.cpp")
+_HDR = os.path.join(_HERE, "lgdm_oracle.h")
+_LIB = os.path.join(_HERE, "liblgdm_oracle.so")
+
+BAR2, QUAD4, HEX8 = 1, 2, 3
+# type -> (dim, nen, ndpn, nv, ngp, ndofe)
+FAMILY = {1: (1, 2, 2, 1, 2, 4), 2: (2, 4, 3, 3, 4, 12), 3: (3, 8, 4, 6, 8, 32)}
+
+
+class Material(C.Structure):
+    _fields_ = [("E", C.c_double), ("nu", C.c_double), ("k", C.c_double),
+                ("kappa0", C.c_double), ("alpha", C.c_double), ("beta", C.c_double),
+                ("h", C.c_double), ("h_sigma", C.c_double), ("c", C.c_double),
+                ("R", C.c_double), ("n", C.c_double), ("t", C.c_double),
+                ("eq_variant", C.c_int32), ("pad_", C.c_int32)]
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle (g++, no FMA contraction, no fast-math)."""
+    stale = (not os.path.exists(_LIB) or
+             os.path.getmtime(_LIB) < max(os.path.getmtime(_SRC), os.path.getmtime(_HDR)))
+    if force or stale:
+        cmd = ["g++", "-std=c++17", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
+               "-shared", "-o", _LIB, _SRC]
+        subprocess.check_call(cmd, cwd=_HERE)
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = C.CDLL(_LIB)
+        dp = C.POINTER(C.c_double)
+        i64p = C.POINTER(C.c_int64)
+        i32p = C.POINTER(C.c_int32)
+        mp = C.POINTER(Material)
+        L.oracle_damage.argtypes = [mp, C.c_double, dp, dp]
+        L.oracle_interaction.argtypes = [mp, C.c_double, dp, dp]
+        L.oracle_eqstrain.argtypes = [mp, C.c_int, dp, dp, dp, dp]
+        L.oracle_gauss.argtypes = [C.c_int, dp, dp]
+        L.oracle_shape.argtypes = [C.c_int, dp, dp, dp]
+        L.oracle_element.argtypes = [C.c_int, mp, dp, dp, dp, dp, dp, dp, dp, i32p]
+        L.oracle_pattern_nnz.argtypes = [C.c_int, C.c_int64, C.c_int64, i64p]
+        L.oracle_pattern_nnz.restype = C.c_int64
+        L.oracle_pattern.argtypes = [C.c_int, C.c_int64, C.c_int64, i64p, i64p, i32p]
+        L.oracle_assemble.argtypes = [C.c_int, mp, C.c_int64, dp, C.c_int64, i64p, dp, dp,
+                                      i64p, i32p, dp, dp, dp, i64p]
+        L.oracle_rows_nnz.argtypes = [C.c_int, C.c_int64, C.c_int64, i64p, C.c_int64, i64p]
+        L.oracle_rows_nnz.restype = C.c_int64
+        L.oracle_assemble_rows.argtypes = [C.c_int, mp, C.c_int64, dp, C.c_int64, i64p, dp, dp,
+                                           C.c_int64, i64p, i64p, i32p, dp, dp, dp]
+        L.oracle_update_history.argtypes = [C.c_int, C.c_int64, C.c_int64, i64p, dp, dp]
+        L.oracle_residual_norms.argtypes = [C.c_int, C.c_int64, dp, dp]
+        _lib = L
+    return _lib
+
+
+def _d(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _i64(a):
+    return a.ctypes.data_as(C.POINTER(C.c_int64))
+
+
+def _i32(a):
+    return a.ctypes.data_as(C.POINTER(C.c_int32))
+
+
+def material(**kw) -> Material:
+    m = Material()
+    for k, v in kw.items():
+        setattr(m, k, v)
+    return m
+
+
+def damage(m: Material, kappa: float):
+    D, dD = C.c_double(), C.c_double()
+    lib().oracle_damage(C.byref(m), kappa, C.byref(D), C.byref(dD))
+    return D.value, dD.value
+
+
+def interaction(m: Material, D: float):
+    g, dg = C.c_double(), C.c_double()
+    lib().oracle_interaction(C.byref(m), D, C.byref(g), C.byref(dg))
+    return g.value, dg.value
+
+
+def eqstrain(m: Material, dim: int, eps_v):
+    nv = {1: 1, 2: 3, 3: 6}[dim]
+    ev = np.ascontiguousarray(eps_v, dtype=np.float64)
+    assert ev.shape == (nv,)
+    e = C.c_double()
+    d = np.zeros(nv)
+    H = np.zeros((nv, nv))
+    lib().oracle_eqstrain(C.byref(m), dim, _d(ev), C.byref(e), _d(d), _d(H))
+    return e.value, d, H
+
+
+def gauss(etype: int):
+    dim = FAMILY[etype][0]
+    xi = np.zeros((8, dim))
+    w = np.zeros(8)
+    ng = lib().oracle_gauss(etype, _d(xi), _d(w))
+    return xi[:ng].copy(), w[:ng].copy()
+
+
+def shape(etype: int, xi):
+    dim, nen = FAMILY[etype][0], FAMILY[etype][1]
+    x = np.ascontiguousarray(xi, dtype=np.float64).reshape(dim)
+    N = np.zeros(nen)
+    dN = np.zeros((nen, dim))
+    lib().oracle_shape(etype, _d(x), _d(N), _d(dN))
+    return N, dN
+
+
+def element(etype: int, m: Material, Xe, Ue, kap):
+    """Element blocks: returns (Ke [ndofe,ndofe], Fe, Fabs, sigma [ngp,nv], guard [ngp])."""
+    dim, nen, ndpn, nv, ngp, nd = FAMILY[etype]
+    Xe = np.ascontiguousarray(Xe, dtype=np.float64).reshape(nen, dim)
+    Ue = np.ascontiguousarray(Ue, dtype=np.float64).reshape(nen * ndpn)
+    kap = np.ascontiguousarray(kap, dtype=np.float64).reshape(ngp)
+    Ke = np.zeros((nd, nd))
+    Fe = np.zeros(nd)
+    Fa = np.zeros(nd)
+    sig = np.zeros((ngp, nv))
+    guard = np.zeros(ngp, dtype=np.int32)
+    rc = lib().oracle_element(etype, C.byref(m), _d(Xe), _d(Ue), _d(kap), _d(Ke), _d(Fe),
+                              _d(Fa), _d(sig), _i32(guard))
+    if rc != 0:
+        raise ValueError(f"oracle_element: det J <= 0 at GP {-rc - 1}")
+    return Ke, Fe, Fa, sig, guard
+
+
+def pattern(etype: int, n_nodes: int, conn):
+    ndpn = FAMILY[etype][2]
+    conn = np.ascontiguousarray(conn, dtype=np.int64)
+    ne = conn.shape[0]
+    nnz = lib().oracle_pattern_nnz(etype, n_nodes, ne, _i64(conn))
+    rp = np.zeros(n_nodes * ndpn + 1, dtype=np.int64)
+    ci = np.zeros(nnz, dtype=np.int32)
+    lib().oracle_pattern(etype, n_nodes, ne, _i64(conn), _i64(rp), _i32(ci))
+    return rp, ci
+
+
+def assemble(etype: int, m: Material, coords, conn, dofs, kappa, row_ptr=None, col_idx=None):
+    """Alg. 1 assembly.  Returns dict(row_ptr, col_idx, val, R, S, n_guard)."""
+    dim, nen, ndpn, nv, ngp, nd = FAMILY[etype]
+    coords = np.ascontiguousarray(coords, dtype=np.float64)
+    conn = np.ascontiguousarray(conn, dtype=np.int64)
+    dofs = np.ascontiguousarray(dofs, dtype=np.float64)
+    kappa = np.ascontiguousarray(kappa, dtype=np.float64)
+    nn = coords.shape[0]
+    ne = conn.shape[0]
+    if row_ptr is None:
+        row_ptr, col_idx = pattern(etype, nn, conn)
+    val = np.zeros(int(row_ptr[-1]))
+    R = np.zeros(nn * ndpn)
+    S = np.zeros(nn * ndpn)
+    ng = C.c_int64()
+    rc = lib().oracle_assemble(etype, C.byref(m), nn, _d(coords), ne, _i64(conn), _d(dofs),
+                               _d(kappa), _i64(row_ptr), _i32(col_idx), _d(val), _d(R), _d(S),
+                               C.byref(ng))
+    if rc != 0:
+        raise ValueError(f"oracle_assemble failed rc={rc}")
+    return dict(row_ptr=row_ptr, col_idx=col_idx, val=val, R=R, S=S, n_guard=ng.value)
+
+
+def assemble_rows(etype: int, m: Material, coords, conn, dofs, kappa, sel_nodes):
+    """Block-rows of the selected nodes only (sampled parity at full size)."""
+    dim, nen, ndpn, nv, ngp, nd = FAMILY[etype]
+    coords = np.ascontiguousarray(coords, dtype=np.float64)
+    conn = np.ascontiguousarray(conn, dtype=np.int64)
+    dofs = np.ascontiguousarray(dofs, dtype=np.float64)
+    kappa = np.ascontiguousarray(kappa, dtype=np.float64)
+    sel = np.ascontiguousarray(sel_nodes, dtype=np.int64)
+    nn, ne, ns = coords.shape[0], conn.shape[0], sel.shape[0]
+    nnz = lib().oracle_rows_nnz(etype, nn, ne, _i64(conn), ns, _i64(sel))
+    rp = np.zeros(ns * ndpn + 1, dtype=np.int64)
+    ci = np.zeros(nnz, dtype=np.int32)
+    val = np.zeros(nnz)
+    R = np.zeros(ns * ndpn)
+    S = np.zeros(ns * ndpn)
+    rc = lib().oracle_assemble_rows(etype, C.byref(m), nn, _d(coords), ne, _i64(conn), _d(dofs),
+                                    _d(kappa), ns, _i64(sel), _i64(rp), _i32(ci), _d(val), _d(R),
+                                    _d(S))
+    if rc != 0:
+        raise ValueError(f"oracle_assemble_rows failed rc={rc}")
+    return dict(row_ptr=rp, col_idx=ci, val=val, R=R, S=S)
+
+
+def update_history(etype: int, conn, dofs, kappa):
+    conn = np.ascontiguousarray(conn, dtype=np.int64)
+    dofs = np.ascontiguousarray(dofs, dtype=np.float64)
+    k = np.array(kappa, dtype=np.float64, copy=True)
+    ndpn = FAMILY[etype][2]
+    lib().oracle_update_history(etype, dofs.size // ndpn, conn.shape[0], _i64(conn), _d(dofs),
+                                _d(k))
+    return k
+
+
+def residual_norms(etype: int, R):
+    R = np.ascontiguousarray(R, dtype=np.float64)
+    out = np.zeros(2)
+    lib().oracle_residual_norms(etype, R.size, _d(R), _d(out))
+    return out

@@ -1,0 +1,611 @@
+// lgdm_oracle.cpp -- plain, slow, obviously-correct CPU oracle for the LGDM K/R assembly.
+//
+// TEST INFRASTRUCTURE ONLY (see lgdm_oracle.h).  Nothing under paper_2301_06503_b200/ or
+// include/ uses this file; it shares no code with the CUDA path.
+//
+// Structure follows Algorithm 1 of PAPER.md: loop over elements, loop over Gauss
+// points, form K_local / F_local from Eqs. 11a-f with the constitutive laws of
+// Appendix A, then assemble.  Dense matrices are used throughout (B_u, N, B_e,
+// C, the Voigt tangent X) so that each line can be checked against the printed equations.
+// The readings of garbled / ambiguous passages are the ones listed in DESIGN.md
+// ("Readings of the paper"): R-A3 (de Vree eq. strain), R-PS, R-SH, R-1D, R-11a (h_sigma),
+// R-11f (sign), R-kappa' (L factor in 11b and 11d), R-TH (Fig. 8b thresholds), R-SQ, R-PAT.
+//
+// Compiled with -O2 -ffp-contract=off (no fused multiply-add, no fast-math).
+#include "lgdm_oracle.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <set>
+#include <vector>
+
+namespace {
+
+const double kTolHist = 1e-10;  // Fig. 8b l.22: cond1 = (gp_e_eqv - k0) > 1D-10
+const double kTolDam = 1e-10;   // Fig. 8b l.27: cond2 = (k_gp - ki) < 1D-10
+
+struct Fam {
+  int dim, nen, ndpn, nv, ngp, ndofe;
+};
+
+bool family(int type, Fam* f) {
+  switch (type) {
+    case 1: *f = {1, 2, 2, 1, 2, 4}; return true;     // 2-node bar, (u, ebar) per node
+    case 2: *f = {2, 4, 3, 3, 4, 12}; return true;    // Q4 plane strain, (ux, uy, ebar)
+    case 3: *f = {3, 8, 4, 6, 8, 32}; return true;    // Hex8, (ux, uy, uz, ebar)
+    default: return false;
+  }
+}
+
+// Reference node coordinates: bar -1,+1; Q4 counter-clockwise; Hex8 bottom
+// face counter-clockwise then top face.
+void ref_node(int type, int a, double* xa) {
+  static const double q[4][2] = {{-1, -1}, {1, -1}, {1, 1}, {-1, 1}};
+  if (type == 1) {
+    xa[0] = a == 0 ? -1.0 : 1.0;
+  } else if (type == 2) {
+    xa[0] = q[a][0];
+    xa[1] = q[a][1];
+  } else {
+    xa[0] = q[a % 4][0];
+    xa[1] = q[a % 4][1];
+    xa[2] = a < 4 ? -1.0 : 1.0;
+  }
+}
+
+// Voigt layout of the engineering strain: 1D [e]; 2D [xx, yy, gxy]; 3D [xx, yy, zz, gxy, gyz, gxz].
+// voigt_pair(dim, V) gives the tensor index pair (p, q) of Voigt component V.
+void voigt_pair(int dim, int V, int* p, int* q) {
+  static const int p2[3][2] = {{0, 0}, {1, 1}, {0, 1}};
+  static const int p3[6][2] = {{0, 0}, {1, 1}, {2, 2}, {0, 1}, {1, 2}, {0, 2}};
+  if (dim == 1) { *p = 0; *q = 0; return; }
+  const int(*t)[2] = dim == 2 ? p2 : p3;
+  *p = t[V][0];
+  *q = t[V][1];
+}
+
+// Elasticity matrix C (Voigt, engineering shear).  1D: E.  2D: plane strain.  3D: isotropic.
+void elasticity(const oracle_material* m, int dim, double* C) {
+  if (dim == 1) { C[0] = m->E; return; }
+  const double lam = m->E * m->nu / ((1.0 + m->nu) * (1.0 - 2.0 * m->nu));
+  const double mu = m->E / (2.0 * (1.0 + m->nu));
+  const int nv = dim == 2 ? 3 : 6;
+  for (int V = 0; V < nv * nv; ++V) C[V] = 0.0;
+  for (int V = 0; V < nv; ++V) {
+    int p, q;
+    voigt_pair(dim, V, &p, &q);
+    if (p == q) {
+      for (int W = 0; W < nv; ++W) {
+        int r, s;
+        voigt_pair(dim, W, &r, &s);
+        if (r == s) C[V * nv + W] = lam;
+      }
+      C[V * nv + V] = lam + 2.0 * mu;
+    } else {
+      C[V * nv + V] = mu;
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+// Eq. A.1 with the Fig. 8b threshold: D = 0 when kappa - kappa0 < 1e-10.
+void oracle_damage(const oracle_material* m, double kappa, double* D, double* dD) {
+  if (kappa - m->kappa0 < kTolDam) {
+    *D = 0.0;
+    *dD = 0.0;
+    return;
+  }
+  const double ex = std::exp(-m->beta * (kappa - m->kappa0));
+  const double brace = 1.0 - m->alpha + m->alpha * ex;
+  *D = 1.0 - (m->kappa0 / kappa) * brace;
+  // d/dkappa of 1 - (k0/kappa)*brace  =  (k0/kappa^2)*brace + (k0/kappa)*alpha*beta*ex
+  *dD = (m->kappa0 / (kappa * kappa)) * brace + (m->kappa0 / kappa) * m->alpha * m->beta * ex;
+}
+
+// Eq. A.4: g(D) = ((1-R) e^{-nD} + R - e^{-n}) / (1 - e^{-n}).
+void oracle_interaction(const oracle_material* m, double D, double* g, double* dgdD) {
+  const double en = std::exp(-m->n);
+  const double enD = std::exp(-m->n * D);
+  *g = ((1.0 - m->R) * enD + m->R - en) / (1.0 - en);
+  *dgdD = -m->n * (1.0 - m->R) * enD / (1.0 - en);
+}
+
+// Eq. A.3, de Vree reading R-A3 (eq_variant 0) or the printed constants (1):
+//   eeq = c1 I1 + 1/(2k) sqrt(c2 I1^2 + c3 J2),  I1 = tr eps,  J2 = 1/2 dev(eps):dev(eps)
+//   c1 = (k-1)/(2k(1-2nu)),  c2 = ((k-1)/(1-2nu))^2,  c3 = 12k/(1+nu)^2  [literal: 2k/(1-nu)^2].
+// The strain tensor is rebuilt from Voigt (plane strain: eps33 = 0, reading R-PS; tensor
+// shear = gamma/2, reading R-SH).  d and H are the first and second derivatives with respect
+// to the Voigt vector, by the chain rule through I1 and J2.  1D: eeq = eps (reading R-1D).
+void oracle_eqstrain(const oracle_material* m, int dim, const double* ev, double* eeq, double* d,
+                     double* H) {
+  if (dim == 1) {
+    *eeq = ev[0];
+    d[0] = 1.0;
+    H[0] = 0.0;
+    return;
+  }
+  const int nv = dim == 2 ? 3 : 6;
+  double eps[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+  for (int V = 0; V < nv; ++V) {
+    int p, q;
+    voigt_pair(dim, V, &p, &q);
+    if (p == q) {
+      eps[p][p] = ev[V];
+    } else {
+      eps[p][q] = 0.5 * ev[V];
+      eps[q][p] = 0.5 * ev[V];
+    }
+  }
+  const double I1 = eps[0][0] + eps[1][1] + eps[2][2];
+  double dev[3][3];
+  for (int p = 0; p < 3; ++p)
+    for (int q = 0; q < 3; ++q) dev[p][q] = eps[p][q] - (p == q ? I1 / 3.0 : 0.0);
+  double J2 = 0.0;
+  for (int p = 0; p < 3; ++p)
+    for (int q = 0; q < 3; ++q) J2 += 0.5 * dev[p][q] * dev[p][q];
+
+  const double k = m->k, nu = m->nu;
+  const double c1 = (k - 1.0) / (2.0 * k * (1.0 - 2.0 * nu));
+  const double c2 = ((k - 1.0) / (1.0 - 2.0 * nu)) * ((k - 1.0) / (1.0 - 2.0 * nu));
+  const double c3 = m->eq_variant == 1 ? 2.0 * k / ((1.0 - nu) * (1.0 - nu))
+                                       : 12.0 * k / ((1.0 + nu) * (1.0 + nu));
+  const double Q = c2 * I1 * I1 + c3 * J2;
+  const double sQ = std::sqrt(Q);
+  *eeq = c1 * I1 + sQ / (2.0 * k);
+
+  // dI1/deps_v = mvec; dJ2/deps_v = svec; d2J2/deps_v^2 = P.
+  double mvec[6], svec[6], P[36];
+  for (int V = 0; V < nv; ++V) {
+    int p, q;
+    voigt_pair(dim, V, &p, &q);
+    mvec[V] = p == q ? 1.0 : 0.0;
+    svec[V] = p == q ? dev[p][p] : eps[p][q];  // d(1/2 dev:dev)/d eps_pp = dev_pp; /d gamma = eps_pq
+    for (int W = 0; W < nv; ++W) {
+      int r, s;
+      voigt_pair(dim, W, &r, &s);
+      double v = 0.0;
+      if (p == q && r == s) v = (p == r ? 1.0 : 0.0) - 1.0 / 3.0;
+      if (p != q && V == W) v = 0.5;
+      P[V * nv + W] = v;
+    }
+  }
+  if (Q < 1e-30) {  // reading R-SQ: sqrt term not differentiable at zero strain
+    for (int V = 0; V < nv; ++V) {
+      d[V] = c1 * mvec[V];
+      for (int W = 0; W < nv; ++W) H[V * nv + W] = 0.0;
+    }
+    return;
+  }
+  double qv[6];
+  for (int V = 0; V < nv; ++V) qv[V] = 2.0 * c2 * I1 * mvec[V] + c3 * svec[V];  // dQ/deps_v
+  for (int V = 0; V < nv; ++V) {
+    d[V] = c1 * mvec[V] + qv[V] / (4.0 * k * sQ);
+    for (int W = 0; W < nv; ++W) {
+      const double dq = 2.0 * c2 * mvec[V] * mvec[W] + c3 * P[V * nv + W];
+      H[V * nv + W] = dq / (4.0 * k * sQ) - qv[V] * qv[W] / (8.0 * k * Q * sQ);
+    }
+  }
+}
+
+int oracle_gauss(int type, double* xi, double* w) {
+  Fam f;
+  if (!family(type, &f)) return -1;
+  const double a = 1.0 / std::sqrt(3.0);
+  for (int g = 0; g < f.ngp; ++g) {
+    for (int k = 0; k < f.dim; ++k) xi[g * f.dim + k] = ((g >> k) & 1) ? a : -a;  // xi fastest
+    w[g] = 1.0;
+  }
+  return f.ngp;
+}
+
+void oracle_shape(int type, const double* xi, double* N, double* dNdxi) {
+  Fam f;
+  if (!family(type, &f)) return;
+  const double scale = 1.0 / double(1 << f.dim);
+  for (int a = 0; a < f.nen; ++a) {
+    double xa[3];
+    ref_node(type, a, xa);
+    double prod = scale;
+    for (int k = 0; k < f.dim; ++k) prod *= (1.0 + xa[k] * xi[k]);
+    N[a] = prod;
+    for (int k = 0; k < f.dim; ++k) {
+      double v = scale * xa[k];
+      for (int l = 0; l < f.dim; ++l)
+        if (l != k) v *= (1.0 + xa[l] * xi[l]);
+      dNdxi[a * f.dim + k] = v;
+    }
+  }
+}
+
+int oracle_element(int type, const oracle_material* m, const double* Xe, const double* Ue,
+                   const double* kap, double* Ke, double* Fe, double* Fabs, double* sig,
+                   int32_t* guard) {
+  Fam f;
+  if (!family(type, &f)) return -1000;
+  const int dim = f.dim, nen = f.nen, ndpn = f.ndpn, nv = f.nv, nd = f.ndofe;
+  double xi[24], w[8];
+  oracle_gauss(type, xi, w);
+  double C[36];
+  elasticity(m, dim, C);
+  for (int r = 0; r < nd * nd; ++r) Ke[r] = 0.0;
+  for (int r = 0; r < nd; ++r) Fe[r] = 0.0, Fabs[r] = 0.0;
+
+  for (int g = 0; g < f.ngp; ++g) {  // Alg. 1 line 5: for igp = 1..ngp
+    // ---- geometry (Fig. 3, gp_data): J, det J, grad N ----
+    double N[8], dNdxi[24];
+    oracle_shape(type, xi + g * dim, N, dNdxi);
+    double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+    for (int a = 0; a < nen; ++a)
+      for (int i = 0; i < dim; ++i)
+        for (int j = 0; j < dim; ++j) J[i][j] += Xe[a * dim + i] * dNdxi[a * dim + j];
+    double detJ, Ji[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+    if (dim == 1) {
+      detJ = J[0][0];
+      Ji[0][0] = 1.0 / J[0][0];
+    } else if (dim == 2) {
+      detJ = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+      Ji[0][0] = J[1][1] / detJ;
+      Ji[0][1] = -J[0][1] / detJ;
+      Ji[1][0] = -J[1][0] / detJ;
+      Ji[1][1] = J[0][0] / detJ;
+    } else {
+      detJ = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) -
+             J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+             J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+      Ji[0][0] = (J[1][1] * J[2][2] - J[1][2] * J[2][1]) / detJ;
+      Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) / detJ;
+      Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) / detJ;
+      Ji[1][0] = (J[1][2] * J[2][0] - J[1][0] * J[2][2]) / detJ;
+      Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) / detJ;
+      Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) / detJ;
+      Ji[2][0] = (J[1][0] * J[2][1] - J[1][1] * J[2][0]) / detJ;
+      Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) / detJ;
+      Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) / detJ;
+    }
+    if (!(detJ > 0.0)) return -(g + 1);
+    double gradN[8][3];  // dN_a/dx_i = sum_j Jinv[j][i] dN_a/dxi_j   (grad_x N = J^-T grad_xi N)
+    for (int a = 0; a < nen; ++a)
+      for (int i = 0; i < dim; ++i) {
+        double s = 0.0;
+        for (int j = 0; j < dim; ++j) s += Ji[j][i] * dNdxi[a * dim + j];
+        gradN[a][i] = s;
+      }
+    const double dV = w[g] * detJ * m->t;
+
+    // ---- full-width operators over the element dof vector (node-interleaved) ----
+    // Bu [nv x nd] (strain-displacement, Voigt, engineering shear), Ne [nd], Be [dim x nd].
+    double Bu[6][32], Ne[32], Be[3][32];
+    for (int r = 0; r < nd; ++r) {
+      Ne[r] = 0.0;
+      for (int V = 0; V < 6; ++V) Bu[V][r] = 0.0;
+      for (int i = 0; i < 3; ++i) Be[i][r] = 0.0;
+    }
+    for (int a = 0; a < nen; ++a) {
+      for (int V = 0; V < nv; ++V) {
+        int p, q;
+        voigt_pair(dim, V, &p, &q);
+        if (p == q) {
+          Bu[V][a * ndpn + p] = gradN[a][p];
+        } else {
+          Bu[V][a * ndpn + p] = gradN[a][q];
+          Bu[V][a * ndpn + q] = gradN[a][p];
+        }
+      }
+      Ne[a * ndpn + dim] = N[a];
+      for (int i = 0; i < dim; ++i) Be[i][a * ndpn + dim] = gradN[a][i];
+    }
+
+    // ---- kinematics (Fig. 5b l.12, l.17): eps = B u, ebar = N e, grad ebar = B_e e ----
+    double ev[6] = {0, 0, 0, 0, 0, 0}, ebar = 0.0, gbar[3] = {0, 0, 0};
+    for (int r = 0; r < nd; ++r) {
+      for (int V = 0; V < nv; ++V) ev[V] += Bu[V][r] * Ue[r];
+      ebar += Ne[r] * Ue[r];
+      for (int i = 0; i < dim; ++i) gbar[i] += Be[i][r] * Ue[r];
+    }
+
+    // ---- constitutive (Appendix A; Fig. 8b condition vectors) ----
+    double eeq, dv[6], H[36];
+    oracle_eqstrain(m, dim, ev, &eeq, dv, H);
+    const double kh = kap[g];
+    const bool L = (ebar - kh) > kTolHist;                    // cond1
+    const double kappa = L ? ebar : kh;
+    double D, dD;
+    oracle_damage(m, kappa, &D, &dD);                         // cond2 inside
+    double gI, dgdD;
+    oracle_interaction(m, D, &gI, &dgdD);
+    const double gprime = dgdD * dD;                          // dg/dkappa
+    const double Lf = L ? 1.0 : 0.0;                          // d kappa / d ebar (reading R-kappa')
+    if (guard) {
+      const double sc = 1e-14 * std::max(std::fabs(ebar), m->kappa0);
+      guard[g] = (std::fabs(ebar - kh - kTolHist) < sc ||
+                  std::fabs(kappa - m->kappa0 - kTolDam) < sc) ? 1 : 0;
+    }
+
+    // Eq. 2: sigma = (1-D) C eps + h_sigma (eeq - ebar) d
+    double Ceps[6], sv[6];
+    for (int V = 0; V < nv; ++V) {
+      double s = 0.0;
+      for (int W = 0; W < nv; ++W) s += C[V * nv + W] * ev[W];
+      Ceps[V] = s;
+      sv[V] = (1.0 - D) * Ceps[V] + m->h_sigma * (eeq - ebar) * dv[V];
+    }
+    if (sig)
+      for (int V = 0; V < nv; ++V) sig[g * nv + V] = sv[V];
+
+    // Voigt tangent of Eq. 11a with the term of reading R-11a:
+    //   X = (1-D) C + h_sigma (d d^T + (eeq - ebar) H)
+    double X[36];
+    for (int V = 0; V < nv; ++V)
+      for (int W = 0; W < nv; ++W)
+        X[V * nv + W] = (1.0 - D) * C[V * nv + W] +
+                        m->h_sigma * (dv[V] * dv[W] + (eeq - ebar) * H[V * nv + W]);
+    // Eq. 11b: w = C eps dD/dkappa dkappa/debar + h_sigma d
+    double wv[6];
+    for (int V = 0; V < nv; ++V) wv[V] = Ceps[V] * dD * Lf + m->h_sigma * dv[V];
+
+    // XB = X Bu  [nv x nd]
+    double XB[6][32];
+    for (int V = 0; V < nv; ++V)
+      for (int c = 0; c < nd; ++c) {
+        double s = 0.0;
+        for (int W = 0; W < nv; ++W) s += X[V * nv + W] * Bu[W][c];
+        XB[V][c] = s;
+      }
+
+    for (int r = 0; r < nd; ++r) {
+      double btw = 0.0, btsig = 0.0, btsig_abs = 0.0, bg = 0.0, bg_abs = 0.0;
+      for (int V = 0; V < nv; ++V) {
+        btw += Bu[V][r] * wv[V];
+        btsig += Bu[V][r] * sv[V];
+        btsig_abs += std::fabs(Bu[V][r]) * (std::fabs((1.0 - D) * Ceps[V]) +
+                                            std::fabs(m->h_sigma * (eeq - ebar) * dv[V]));
+      }
+      for (int i = 0; i < dim; ++i) {
+        bg += Be[i][r] * gbar[i];
+        bg_abs += std::fabs(Be[i][r]) * std::fabs(gbar[i]);
+      }
+      for (int c = 0; c < nd; ++c) {
+        double kuu = 0.0, bb = 0.0;
+        for (int V = 0; V < nv; ++V) kuu += Bu[V][r] * XB[V][c];  // 11a: Bu^T X Bu
+        for (int i = 0; i < dim; ++i) bb += Be[i][r] * Be[i][c];
+        double kue = -btw * Ne[c];                                // 11b: -Bu^T w N
+        double keu = 0.0;                                         // 11c: -N^T h d^T Bu
+        for (int V = 0; V < nv; ++V) keu += -Ne[r] * m->h * dv[V] * Bu[V][c];
+        double kee = m->h * Ne[r] * Ne[c]                         // 11d: N^T h N
+                     + m->h * m->c * gprime * Lf * bg * Ne[c]     //      + B^T h c g' grad ebar N
+                     + gI * m->h * m->c * bb;                     //      + B^T g h c B
+        Ke[r * nd + c] += dV * (kuu + kue + keu + kee);
+      }
+      // 11e (t = 0): -Bu^T sigma;  11f (reading R-11f): N h (eeq-ebar) - B^T g h c grad ebar
+      Fe[r] += dV * (-btsig + m->h * Ne[r] * (eeq - ebar) - gI * m->h * m->c * bg);
+      Fabs[r] += dV * (btsig_abs + m->h * std::fabs(Ne[r] * (eeq - ebar)) +
+                       gI * m->h * m->c * bg_abs);
+    }
+  }
+  return 0;
+}
+
+// ---------------- pattern (reading R-PAT) ----------------
+
+static void node_neighbours(int type, int64_t n_nodes, int64_t n_elems, const int64_t* conn,
+                            std::vector<std::set<int64_t>>* nb) {
+  Fam f;
+  family(type, &f);
+  nb->assign(n_nodes, std::set<int64_t>());
+  for (int64_t e = 0; e < n_elems; ++e)
+    for (int a = 0; a < f.nen; ++a)
+      for (int b = 0; b < f.nen; ++b) (*nb)[conn[e * f.nen + a]].insert(conn[e * f.nen + b]);
+}
+
+int64_t oracle_pattern_nnz(int type, int64_t n_nodes, int64_t n_elems, const int64_t* conn) {
+  Fam f;
+  if (!family(type, &f)) return -1;
+  std::vector<std::set<int64_t>> nb;
+  node_neighbours(type, n_nodes, n_elems, conn, &nb);
+  int64_t nnz = 0;
+  for (int64_t a = 0; a < n_nodes; ++a) nnz += int64_t(nb[a].size()) * f.ndpn * f.ndpn;
+  return nnz;
+}
+
+int oracle_pattern(int type, int64_t n_nodes, int64_t n_elems, const int64_t* conn,
+                   int64_t* row_ptr, int32_t* col_idx) {
+  Fam f;
+  if (!family(type, &f)) return -1;
+  std::vector<std::set<int64_t>> nb;
+  node_neighbours(type, n_nodes, n_elems, conn, &nb);
+  int64_t pos = 0;
+  row_ptr[0] = 0;
+  for (int64_t a = 0; a < n_nodes; ++a)
+    for (int i = 0; i < f.ndpn; ++i) {
+      for (int64_t b : nb[a])  // std::set iterates in ascending order
+        for (int j = 0; j < f.ndpn; ++j) col_idx[pos++] = int32_t(f.ndpn * b + j);
+      row_ptr[a * f.ndpn + i + 1] = pos;
+    }
+  return 0;
+}
+
+static int64_t find_col(const int64_t* row_ptr, const int32_t* col_idx, int64_t row, int64_t col) {
+  const int32_t* lo = col_idx + row_ptr[row];
+  const int32_t* hi = col_idx + row_ptr[row + 1];
+  const int32_t* it = std::lower_bound(lo, hi, int32_t(col));
+  if (it == hi || *it != col) return -1;
+  return it - col_idx;
+}
+
+static void gather(const Fam& f, int64_t e, const int64_t* conn, const double* coords,
+                   const double* dofs, double* Xe, double* Ue) {
+  for (int a = 0; a < f.nen; ++a) {
+    const int64_t n = conn[e * f.nen + a];
+    for (int i = 0; i < f.dim; ++i) Xe[a * f.dim + i] = coords[n * f.dim + i];
+    for (int i = 0; i < f.ndpn; ++i) Ue[a * f.ndpn + i] = dofs[n * f.ndpn + i];
+  }
+}
+
+// Alg. 1 lines 4-11; Fig. 2: element loop, K_local, unroll, assemble.
+int oracle_assemble(int type, const oracle_material* m, int64_t n_nodes, const double* coords,
+                    int64_t n_elems, const int64_t* conn, const double* dofs, const double* kappa,
+                    const int64_t* row_ptr, const int32_t* col_idx, double* val, double* R,
+                    double* S, int64_t* n_guard) {
+  Fam f;
+  if (!family(type, &f)) return -1;
+  const int nd = f.ndofe;
+  const int64_t ndof = n_nodes * f.ndpn;
+  std::fill(val, val + row_ptr[ndof], 0.0);
+  std::fill(R, R + ndof, 0.0);
+  std::fill(S, S + ndof, 0.0);
+  std::vector<double> Ke(nd * nd), Fe(nd), Fa(nd);
+  double Xe[24], Ue[32];
+  int32_t guard[8];
+  int64_t ng = 0;
+  for (int64_t e = 0; e < n_elems; ++e) {
+    gather(f, e, conn, coords, dofs, Xe, Ue);
+    const int rc = oracle_element(type, m, Xe, Ue, kappa + e * f.ngp, Ke.data(), Fe.data(),
+                                  Fa.data(), nullptr, guard);
+    if (rc != 0) return -2;  // det J <= 0
+    for (int g = 0; g < f.ngp; ++g) ng += guard[g];
+    for (int a = 0; a < f.nen; ++a)
+      for (int i = 0; i < f.ndpn; ++i) {
+        const int64_t row = f.ndpn * conn[e * f.nen + a] + i;
+        const int r = a * f.ndpn + i;
+        R[row] += Fe[r];
+        S[row] += Fa[r];
+        for (int b = 0; b < f.nen; ++b)
+          for (int j = 0; j < f.ndpn; ++j) {
+            const int64_t col = f.ndpn * conn[e * f.nen + b] + j;
+            const int64_t p = find_col(row_ptr, col_idx, row, col);
+            if (p < 0) return -3;
+            val[p] += Ke[r * nd + b * f.ndpn + j];
+          }
+      }
+  }
+  if (n_guard) *n_guard = ng;
+  return 0;
+}
+
+// Sampled rows: the same sums restricted to the block-rows of selected nodes.
+static void adjacency(const Fam& f, int64_t n_nodes, int64_t n_elems, const int64_t* conn,
+                      std::vector<std::vector<int64_t>>* adj, const std::vector<char>& want) {
+  adj->assign(n_nodes, std::vector<int64_t>());
+  for (int64_t e = 0; e < n_elems; ++e)
+    for (int a = 0; a < f.nen; ++a) {
+      const int64_t n = conn[e * f.nen + a];
+      if (want[n]) (*adj)[n].push_back(e);  // ascending e by construction
+    }
+}
+
+int64_t oracle_rows_nnz(int type, int64_t n_nodes, int64_t n_elems, const int64_t* conn,
+                        int64_t n_sel, const int64_t* sel) {
+  Fam f;
+  if (!family(type, &f)) return -1;
+  std::vector<char> want(n_nodes, 0);
+  for (int64_t s = 0; s < n_sel; ++s) want[sel[s]] = 1;
+  std::vector<std::vector<int64_t>> adj;
+  adjacency(f, n_nodes, n_elems, conn, &adj, want);
+  int64_t nnz = 0;
+  for (int64_t s = 0; s < n_sel; ++s) {
+    std::set<int64_t> nb;
+    for (int64_t e : adj[sel[s]])
+      for (int b = 0; b < f.nen; ++b) nb.insert(conn[e * f.nen + b]);
+    nnz += int64_t(nb.size()) * f.ndpn * f.ndpn;
+  }
+  return nnz;
+}
+
+int oracle_assemble_rows(int type, const oracle_material* m, int64_t n_nodes, const double* coords,
+                         int64_t n_elems, const int64_t* conn, const double* dofs,
+                         const double* kappa, int64_t n_sel, const int64_t* sel,
+                         int64_t* row_ptr_sel, int32_t* col_idx_sel, double* val_sel,
+                         double* R_sel, double* S_sel) {
+  Fam f;
+  if (!family(type, &f)) return -1;
+  const int nd = f.ndofe;
+  std::vector<char> want(n_nodes, 0);
+  for (int64_t s = 0; s < n_sel; ++s) want[sel[s]] = 1;
+  std::vector<std::vector<int64_t>> adj;
+  adjacency(f, n_nodes, n_elems, conn, &adj, want);
+  std::vector<double> Ke(nd * nd), Fe(nd), Fa(nd);
+  double Xe[24], Ue[32];
+  int64_t pos = 0;
+  row_ptr_sel[0] = 0;
+  for (int64_t s = 0; s < n_sel; ++s) {
+    const int64_t a0 = sel[s];
+    std::set<int64_t> nbset;
+    for (int64_t e : adj[a0])
+      for (int b = 0; b < f.nen; ++b) nbset.insert(conn[e * f.nen + b]);
+    std::vector<int64_t> nb(nbset.begin(), nbset.end());
+    const int64_t width = int64_t(nb.size()) * f.ndpn;
+    const int64_t base = pos;
+    for (int i = 0; i < f.ndpn; ++i) {
+      for (int64_t b : nb)
+        for (int j = 0; j < f.ndpn; ++j) {
+          col_idx_sel[pos] = int32_t(f.ndpn * b + j);
+          val_sel[pos] = 0.0;
+          ++pos;
+        }
+      row_ptr_sel[s * f.ndpn + i + 1] = pos;
+      R_sel[s * f.ndpn + i] = 0.0;
+      S_sel[s * f.ndpn + i] = 0.0;
+    }
+    for (int64_t e : adj[a0]) {
+      gather(f, e, conn, coords, dofs, Xe, Ue);
+      if (oracle_element(type, m, Xe, Ue, kappa + e * f.ngp, Ke.data(), Fe.data(), Fa.data(),
+                         nullptr, nullptr) != 0)
+        return -2;
+      for (int a = 0; a < f.nen; ++a) {
+        if (conn[e * f.nen + a] != a0) continue;
+        for (int i = 0; i < f.ndpn; ++i) {
+          const int r = a * f.ndpn + i;
+          R_sel[s * f.ndpn + i] += Fe[r];
+          S_sel[s * f.ndpn + i] += Fa[r];
+          for (int b = 0; b < f.nen; ++b) {
+            const int64_t slot =
+                std::lower_bound(nb.begin(), nb.end(), conn[e * f.nen + b]) - nb.begin();
+            for (int j = 0; j < f.ndpn; ++j)
+              val_sel[base + i * width + slot * f.ndpn + j] += Ke[r * nd + b * f.ndpn + j];
+          }
+        }
+      }
+    }
+  }
+  return 0;
+}
+
+// Eq. A.2 with Fig. 8b l.19-24:
+//   ebar_gp = N(xi_g) e;  cond1 = (ebar_gp - kappa) > 1e-10;  kappa(cond1) = ebar_gp.
+int oracle_update_history(int type, int64_t n_nodes, int64_t n_elems, const int64_t* conn,
+                          const double* dofs, double* kappa) {
+  Fam f;
+  if (!family(type, &f)) return -1;
+  (void)n_nodes;
+  double xi[24], w[8], N[8], dNdxi[24];
+  oracle_gauss(type, xi, w);
+  for (int64_t e = 0; e < n_elems; ++e)
+    for (int g = 0; g < f.ngp; ++g) {
+      oracle_shape(type, xi + g * f.dim, N, dNdxi);
+      double ebar = 0.0;
+      for (int a = 0; a < f.nen; ++a) ebar += N[a] * dofs[conn[e * f.nen + a] * f.ndpn + f.dim];
+      double& k = kappa[e * f.ngp + g];
+      if ((ebar - k) > kTolHist) k = ebar;
+    }
+  return 0;
+}
+
+// ||R restricted to u-rows||_2 and ||R restricted to ebar-rows||_2.
+void oracle_residual_norms(int type, int64_t n_rows, const double* R, double* out2) {
+  Fam f;
+  family(type, &f);
+  double su = 0.0, se = 0.0;
+  for (int64_t r = 0; r < n_rows; ++r) {
+    if (r % f.ndpn == f.dim) se += R[r] * R[r];
+    else su += R[r] * R[r];
+  }
+  out2[0] = std::sqrt(su);
+  out2[1] = std::sqrt(se);
+}
+
+}  // extern "C"
