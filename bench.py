@@ -1,0 +1,345 @@
+#!/usr/bin/env python
+"""Benchmark of the FP64 LGDM K+R assembly path (BASELINE.json metric).
+
+One STEP = one pass of the whole hot path on the current iterate:
+    lgdm_assemble (K and R)  ->  lgdm_residual_norms (NCCL allreduce when N > 1)
+    ->  lgdm_update_history  ->  dofs *= 1.05^(+-1) (next iterate, SURVEY 8d "dofs_t").
+Workload: BASELINE config 4 (Hex8 200^3, 8M elements) as row-owned z-slabs over the N ranks
+(strong scaling; N = 1 holds the whole mesh).  At N = 1 the 1M-element configs 3 (Hex8 100^3)
+and 2 (Q4 1000^2) are also reported under "secondary".  Inputs are far larger than L2
+(126 MB), so no flush is needed between steps.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl lgdm|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "FP64 LGDM K+R assembly: elements/s and % of HBM roofline (Q4, Hex8)"
+UNIT = "elements/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def algorithmic_bytes(ndpn, dim, nen, ngp, nnz, n_rows, n_nodes, n_elems):
+    """8 nnz (K) + 8 ndof (R) + 8 ndof (dofs) + 8 nel ngp (kappa) + 8 d nnodes
+    (coords) + 4 nen nel (conn); rows/dofs/elements are the rank's own."""
+    return (8 * nnz + 8 * n_rows + 8 * n_nodes * ndpn + 8 * n_elems * ngp + 8 * dim * n_nodes +
+            4 * nen * n_elems)
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def build_rank_mesh(cfg, rank, world):
+    from paper_2301_06503_b200 import slabs
+    if world == 1:
+        mesh = synth.structured_mesh(cfg)
+        return mesh, (0, mesh.coords.shape[0])
+    s = slabs.slab(cfg.n, rank, world)
+    mesh = synth.structured_mesh(cfg, elem_layers=s.elem_layers)
+    return mesh, s.owned_local(mesh.node_gid0)
+
+
+def run_lgdm(cfg, steps, warmup, rank, world, local, pg_barrier, allmax, comm_uid=None,
+             e2e=True, kernel=0):
+    import torch
+    from paper_2301_06503_b200 import lgdm
+    torch.cuda.set_device(local)
+    dim, nen, ndpn, ngp = synth.FAM[cfg.etype]
+    t0 = time.time()
+    mesh, owned = build_rank_mesh(cfg, rank, world)
+    dofs, kappa = synth.fields(cfg, mesh)
+    t_gen = time.time() - t0
+    stream = torch.cuda.current_stream()
+    t0 = time.time()
+    m = lgdm.Mesh(cfg.etype, mesh.coords, mesh.conn, lgdm.material(**synth.MATERIAL),
+                  global_node_offset=mesh.node_gid0, n_global_nodes=cfg.n_nodes, owned=owned,
+                  device=local, stream=stream.cuda_stream)
+    if kernel:
+        m.set_kernel(kernel)
+    if comm_uid is not None:
+        m.set_comm(comm_uid, world, rank)
+    t_create = time.time() - t0
+    info = m.info()
+    dofs_h = torch.from_numpy(dofs.reshape(-1)).pin_memory()
+    kappa_d = torch.as_tensor(kappa.reshape(-1), device=f"cuda:{local}")
+    dofs_d = torch.empty_like(dofs_h, device=f"cuda:{local}")
+    dofs_d.copy_(dofs_h)
+    m.set_state(dofs_d, kappa_d)
+
+    def step(t, ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        m.assemble()
+        if ev is not None:
+            ev[1].record(stream)
+        norms = m.residual_norms()       # NCCL allreduce inside when world > 1
+        m.update_history()
+        m.scale_dofs(1.05 if t % 2 == 0 else 1.0 / 1.05)
+        return norms
+
+    for t in range(warmup):
+        step(t)
+    torch.cuda.synchronize()
+    pg_barrier()
+    l0 = m.launches
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        start.record(stream)
+        for t in range(steps):
+            step(t, evs[t])
+        end.record(stream)
+        torch.cuda.synchronize()
+    launches = m.launches - l0
+    pg_barrier()
+    ms_total = allmax(start.elapsed_time(end))
+    asm_ms = allmax(float(np.mean([a.elapsed_time(b) for a, b in evs])))
+    res = dict(ms_per_step=ms_total / steps, assemble_ms=asm_ms, launches=launches,
+               launches_per_step=launches / steps, clocks=clk.summary(), info=info,
+               t_gen=t_gen, t_create=t_create, owned=owned, n_elems_local=mesh.conn.shape[0])
+    res["alg_bytes"] = algorithmic_bytes(ndpn, dim, nen, ngp, info["nnz"], info["n_rows"],
+                                         info["n_nodes"], info["n_elems"])
+    if e2e:
+        # end-to-end through the public API: H2D of this step's dofs from pinned host memory,
+        # the step, D2H of the residual norms (the convergence quantities).
+        m.set_state(dofs_h, None)
+        torch.cuda.synchronize()
+        pg_barrier()
+        s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s2.record(stream)
+        for t in range(steps):
+            m.set_state(dofs_h, None)
+            step(t)
+        e2.record(stream)
+        torch.cuda.synchronize()
+        pg_barrier()
+        res["e2e_ms_per_step"] = allmax(s2.elapsed_time(e2)) / steps
+        res["h2d_bytes"] = int(dofs_h.numel() * 8)
+        res["d2h_bytes"] = 16
+    m.close()
+    return res
+
+
+def cpu_baseline(cfg, target_s=15.0):
+    """The oracle as it stands, single-threaded, on a bounded sample of the workload: the first
+    element layers of the same mesh (all layers are statistically alike)."""
+    import oracle
+    per_layer = int(np.prod(cfg.n[:-1]))
+    rate_guess = 1.0e4 if cfg.etype == 3 else 9.0e4
+    layers = int(max(1, min(cfg.n[-1], round(target_s * rate_guess / per_layer))))
+    mesh = synth.structured_mesh(cfg, elem_layers=(0, layers))
+    dofs, kappa = synth.fields(cfg, mesh)
+    mat = oracle.material(**synth.MATERIAL)
+    rp, ci = oracle.pattern(cfg.etype, mesh.coords.shape[0], mesh.conn)
+    t0 = time.perf_counter()
+    oracle.assemble(cfg.etype, mat, mesh.coords, mesh.conn, dofs, kappa, rp, ci)
+    dt = time.perf_counter() - t0
+    ne = mesh.conn.shape[0]
+    return {"value": ne / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{ne} elements = element layers [0,{layers}) of {cfg.name}, one assemble, "
+                      f"{dt:.2f} s single-threaded (pattern build untimed)"}
+
+
+def secondary(cid, steps, warmup, peak):
+    cfg = synth.CONFIGS[cid]
+    r = run_lgdm(cfg, steps, warmup, 0, 1, int(os.environ.get("LOCAL_RANK", "0")),
+                 lambda: None, lambda x: x, e2e=False)
+    ach = r["alg_bytes"] / (r["assemble_ms"] * 1e-3) / 1e9
+    return {"workload": cfg.name, "config": cid,
+            "value": cfg.n_elems / (r["ms_per_step"] * 1e-3), "unit": UNIT,
+            "ms_per_step": r["ms_per_step"], "assemble_ms": r["assemble_ms"],
+            "assemble_elements_per_s": cfg.n_elems / (r["assemble_ms"] * 1e-3),
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                         "frac": ach / peak, "traffic": None},
+            "clocks": r["clocks"]}
+
+
+def reference_arm(args, cfg):
+    """--impl reference: the CPU oracle (this tier's reference), bounded sample per step."""
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    per_layer = int(np.prod(cfg.n[:-1]))
+    mesh = synth.structured_mesh(cfg, elem_layers=(0, 1))
+    dofs, kappa = synth.fields(cfg, mesh)
+    mat = oracle.material(**synth.MATERIAL)
+    rp, ci = oracle.pattern(cfg.etype, mesh.coords.shape[0], mesh.conn)
+    for _ in range(args.warmup):
+        oracle.assemble(cfg.etype, mat, mesh.coords, mesh.conn, dofs, kappa, rp, ci)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.assemble(cfg.etype, mat, mesh.coords, mesh.conn, dofs, kappa, rp, ci)
+        oracle.update_history(cfg.etype, mesh.conn, dofs, kappa)
+    dt = time.perf_counter() - t0
+    ne = mesh.conn.shape[0]
+    val = ne * args.steps / dt
+    sample = f"{ne} elements (element layer 0 of {cfg.name}) per step, single-threaded"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": cfg.name, "per_layer_elements": per_layer},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--impl", default="lgdm", choices=["lgdm", "reference"])
+    ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 general, 2 sweep")
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = synth.CONFIGS[args.config]
+    if args.impl == "reference":
+        reference_arm(args, cfg)
+        return
+    ws, rank, local = dist_env()
+    import torch
+    torch.cuda.set_device(local)
+    comm_uid = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        from paper_2301_06503_b200 import lgdm
+        obj = [lgdm.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm_uid = obj[0]
+
+        def barrier():
+            dist.barrier()
+
+        def allmax(x):
+            t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t.item())
+    else:
+        def barrier():
+            pass
+
+        def allmax(x):
+            return x
+    peak, peak_src = peaks()
+    r = run_lgdm(cfg, args.steps, args.warmup, rank, ws, local, barrier, allmax, comm_uid,
+                 kernel=args.kernel)
+    n_total = cfg.n_elems
+    value = n_total / (r["ms_per_step"] * 1e-3)
+    achieved = r["alg_bytes"] / (r["assemble_ms"] * 1e-3) / 1e9
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "baseline_config": args.config,
+                   "elements": n_total, "nnz": int(r["info"]["nnz"]) if ws == 1 else None,
+                   "parallelism": f"z-slabs x{ws}, ghost-element recompute",
+                   "step": "assemble + residual_norms(allreduce) + update_history + dofs scale",
+                   "l2": "inputs >> 126 MB L2 (no flush needed)",
+                   "kernel": "sweep" if r["info"]["structured"] and args.kernel != 1 else "general"},
+        "assemble_ms": r["assemble_ms"],
+        "assemble_elements_per_s": n_total / (r["assemble_ms"] * 1e-3) if ws == 1 else None,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                     "kernel": "lgdm_assemble (all launches of one call), rank max"},
+        "gpu_launches": r["launches"],
+        "clocks": r["clocks"],
+        "e2e": {"value": n_total / (r["e2e_ms_per_step"] * 1e-3), "unit": UNIT,
+                "h2d_bytes_per_step": r["h2d_bytes"], "d2h_bytes_per_step": r["d2h_bytes"]},
+        "setup_s": {"generate": r["t_gen"], "create_mesh": r["t_create"]},
+    }
+    if ws == 1 and rank == 0:
+        if not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(cfg)
+        if not args.no_secondary:
+            out["secondary"] = [secondary(c, args.steps, args.warmup, peak) for c in (3, 2)]
+    if rank == 0:
+        print(json.dumps(out))
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,164 @@
+/* lgdm.h -- C ABI of the B200-native LGDM K/R assembly library (liblgdm.so).
+ *
+ * What it computes (PAPER.md = /root/reference/PAPER.md, arXiv 2301.06503):
+ *   For every element and Gauss point (Alg. 1 lines 4-8; Alg. 2 lines 4-5)
+ *   the tangent blocks Kuu, Kue, Keu, Kee (Eqs. 11a-d) and residuals Fu, Fe
+ *   (Eqs. 11e-f) of the localizing gradient damage method, with the damage law
+ *   (Eq. A.1), history (Eq. A.2), modified von Mises equivalent strain
+ *   (Eq. A.3) and interaction function (Eq. A.4), assembled into a
+ *   global CSR matrix K and vector R (Alg. 1 line 11; Fig. 2 lines 28-30).
+ *   Readings of garbled/ambiguous passages: DESIGN.md "Readings of the paper"
+ *   (R-A3, R-PS, R-SH, R-1D, R-11a, R-11f, R-kappa', R-TH, R-HIST, R-SQ, R-PAT, R-ORD).
+ *
+ * Conventions (frozen):
+ *   - FP64 everywhere.  DOFs are node-interleaved: dof = ndpn*global_node + comp,
+ *     comp = (u_x[, u_y[, u_z]], ebar); ndpn = d+1.
+ *   - K = -dR/dx (so K*dx = R is the Newton step of Eq. 11), R = F of Eq. 11 (t = zeta = 0).
+ *   - CSR: row_ptr int64 (config 4 has > 2^31 nonzeros), col_idx int32 holding GLOBAL dof
+ *     ids, columns ascending, structural pattern with explicit zeros (every node pair that
+ *     shares an element, x ndpn^2).  A rank's CSR is the row slice of its owned nodes.
+ *   - Element local node order: bar2 (-1, +1); Q4 counter-clockwise from (-1,-1); Hex8
+ *     bottom face (zeta=-1) counter-clockwise, then top face.  Gauss points 2 / 2x2 / 2x2x2
+ *     at +-1/sqrt(3), xi fastest.  2D is plane strain with unit thickness; 1D uses the area.
+ *
+ * Errors: every call returns lgdm_status; no exception crosses the ABI.  On error outputs
+ * are untouched and lgdm_last_error() (thread-local) describes the failure.
+ * Threading: a mesh is not thread-safe; distinct meshes are independent.
+ * Ownership: host inputs are copied; all device buffers are owned by the mesh and freed by
+ * lgdm_destroy.  Pointers returned by lgdm_assemble stay valid until the next
+ * lgdm_assemble / lgdm_destroy of that mesh.
+ * Asynchrony: create/set_state/assemble/update_history enqueue work on the mesh's CUDA
+ * stream and return without synchronising (create synchronises once for its checks);
+ * lgdm_residual_norms and lgdm_get_kappa synchronise that stream.
+ */
+#ifndef LGDM_H
+#define LGDM_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  LGDM_OK = 0,
+  LGDM_ERR_INVALID_ARGUMENT = 1,  /* bad type, size, material (S:173 invariants), null ptr */
+  LGDM_ERR_INVERTED_ELEMENT = 2,  /* det J <= 0 at a Gauss point; message names it  */
+  LGDM_ERR_INVALID_STATE = 3,     /* assemble before set_state, size mismatch      */
+  LGDM_ERR_OUT_OF_MEMORY = 4,
+  LGDM_ERR_CUDA = 5,
+  LGDM_ERR_NCCL = 6,
+  LGDM_ERR_UNSUPPORTED = 7        /* e.g. NCCL not loadable                                 */
+} lgdm_status;
+
+typedef enum { LGDM_BAR2 = 1, LGDM_QUAD4 = 2, LGDM_HEX8 = 3 } lgdm_elem_type;
+
+/* Material (Eq. 1 4C, Eqs. 2-4, Appendix A).  Validated at create:
+ * E > 0, 0 <= nu < 0.5, k >= 1, kappa0 > 0, 0 < alpha <= 1, beta > 0, h > 0,
+ * h_sigma >= 0, c > 0, 0 < R < 1, n > 0, thickness_or_area > 0. */
+typedef struct {
+  double E, nu;             /* Young's modulus [MPa], Poisson ratio                         */
+  double k;                 /* compressive/tensile strength ratio (Eq. A.3)                 */
+  double kappa0;            /* damage threshold (Eq. A.1; `ki` in Fig. 8b)                  */
+  double alpha, beta;       /* damage law parameters (Eq. A.1)                              */
+  double h;                 /* coupling modulus (Eq. 1)                                     */
+  double h_sigma;           /* coefficient of Eq. 2's h-term (reading R-11a: h = R1, 0 = R2) */
+  double c;                 /* gradient parameter [mm^2] (Eq. 1)                            */
+  double R, n;              /* interaction function parameters (Eq. A.4)                    */
+  double thickness_or_area; /* 1D: bar area [mm^2]; 2D/3D: 1                                */
+  int32_t eq_variant;       /* 0: de Vree constants (reading R-A3); 1: A.3 as printed        */
+  int32_t reserved;         /* must be 0                                                    */
+} lgdm_material;
+
+typedef struct lgdm_mesh_s* lgdm_mesh;
+
+typedef struct {
+  int64_t n_rows;           /* owned rows = ndpn * (owned_node_end - owned_node_begin)      */
+  int64_t n_cols;           /* ndpn * n_global_nodes                                        */
+  int64_t nnz;
+  int64_t first_row;        /* global row id of local row 0 = ndpn*(offset+owned_begin)     */
+  const int64_t* row_ptr;   /* device, [n_rows+1], row_ptr[0] = 0                           */
+  const int32_t* col_idx;   /* device, [nnz], global dof ids, ascending per row             */
+  double* val;              /* device, [nnz]                                                */
+} lgdm_csr;
+
+typedef struct {
+  int32_t elem_type, dim, nen, ndpn, ngp, structured;   /* structured: 1 = sweep kernel path  */
+  int64_t n_nodes, n_elems, n_owned_nodes, n_rows, nnz;
+  int64_t nx, ny, nz;                                    /* element counts if structured      */
+  int64_t device_bytes;                                  /* device memory owned by the mesh  */
+} lgdm_info;
+
+/* Create a mesh (a whole mesh, or one rank's slab).  S:44-70, S:82 (immutable mesh).
+ *   coords  host [n_nodes][d] f64 (copied)           conn host [n_elems][nen] LOCAL node ids
+ *   global_node_offset: global id of local node 0 -- local nodes are the contiguous global
+ *     range [offset, offset+n_nodes) (true for z-slabs of Hex8 / y-slabs of Q4 under x-fastest
+ *     numbering); 0 on one GPU.   n_global_nodes: sets n_cols.
+ *   owned_node_begin/end: local node range whose rows this mesh assembles (the rest are ghost
+ *     nodes of ghost elements, recomputed here so K needs no communication).
+ *   device: CUDA ordinal; cuda_stream: cudaStream_t (NULL = legacy default stream).
+ * Builds the CSR pattern (reading R-PAT) and the element->CSR maps once.  det J <= 0 at any
+ * GP -> LGDM_ERR_INVERTED_ELEMENT.  Connectivity of an x-fastest structured grid (any
+ * coordinates) is detected and enables the fused sweep kernels. */
+lgdm_status lgdm_create_mesh(lgdm_elem_type type, int64_t n_nodes, const double* coords,
+                             int64_t n_elems, const int64_t* conn, const lgdm_material* mat,
+                             int64_t global_node_offset, int64_t n_global_nodes,
+                             int64_t owned_node_begin, int64_t owned_node_end, int device,
+                             void* cuda_stream, lgdm_mesh* out);
+
+/* State of the current Newton iterate (Alg. 2 line 7): dofs [n_nodes][ndpn] node-
+ * interleaved, kappa [n_elems][ngp] = history kappa_hist at the start of the increment.
+ * src_on_device: 1 if both pointers are device pointers (D2D copy), 0 for host (H2D; pinned
+ * host memory makes the copy asynchronous).  Size mismatch -> LGDM_ERR_INVALID_STATE.
+ * kappa may be NULL to keep the mesh's current history (dofs-only update). */
+lgdm_status lgdm_set_state(lgdm_mesh mesh, const double* dofs, int64_t n_dofs,
+                           const double* kappa, int64_t n_kappa, int src_on_device);
+
+/* Assemble K (owned rows) and R = F (owned rows) for the current state (Eqs. 11a-f with the
+ * trial kappa = cond1 ? ebar : kappa_hist, Fig. 8b; history is NOT written, reading R-HIST).
+ * K and *R point to mesh-owned device memory. */
+lgdm_status lgdm_assemble(lgdm_mesh mesh, lgdm_csr* K, double** R);
+
+/* Commit the history: kappa_hist <- (ebar_gp - kappa_hist > 1e-10) ? ebar_gp : kappa_hist for
+ * every local GP (owned and ghost), Eq. A.2 with Fig. 8b lines 22-24. */
+lgdm_status lgdm_update_history(lgdm_mesh mesh);
+
+/* Sums of squares of the last assembled R over owned rows: out2 = {sum Fu^2, sum Fe^2}.
+ * out2 is a device pointer (2 doubles) when on_device = 1 (stream-ordered, no sync; for a
+ * caller-side allreduce), else a host pointer (synchronises). */
+lgdm_status lgdm_residual_sumsq(lgdm_mesh mesh, double* out2, int on_device);
+
+/* Global norms {||Fu||_2, ||Fe||_2}: the convergence quantities of P:297 in residual form.
+ * Local (owned rows) unless lgdm_set_comm was called, then NCCL allreduce(sum) over ranks.
+ * out2 is host memory; synchronises. */
+lgdm_status lgdm_residual_norms(lgdm_mesh mesh, double out2[2]);
+
+/* Attach an NCCL communicator (ncclUniqueId bytes from rank 0, e.g. broadcast through
+ * torch.distributed).  NCCL is loaded at run time (dlopen libnccl.so.2). */
+lgdm_status lgdm_set_comm(lgdm_mesh mesh, const void* nccl_unique_id, int nranks, int rank);
+
+/* Fill out (>= 128 bytes) with a fresh ncclUniqueId (call on rank 0, broadcast to the others
+ * through any channel, e.g. torch.distributed.broadcast_object_list). */
+lgdm_status lgdm_nccl_unique_id(void* out, int64_t out_bytes);
+
+/* Copy the current kappa_hist [n_elems][ngp] to host (tests).  Synchronises. */
+lgdm_status lgdm_get_kappa(lgdm_mesh mesh, double* host_out);
+
+/* dofs *= s on device (benchmark helper: dofs_t = (1 + 0.05 t) dofs_0, SURVEY 8d cfg 2). */
+lgdm_status lgdm_scale_dofs(lgdm_mesh mesh, double s);
+
+/* Select the assembly kernel: 0 = automatic (sweep if structured), 1 = general
+ * (element-batch + node gather, any connectivity), 2 = sweep (structured only). */
+lgdm_status lgdm_set_kernel(lgdm_mesh mesh, int kernel);
+
+lgdm_status lgdm_get_info(lgdm_mesh mesh, lgdm_info* info);
+
+/* Number of kernel launches issued by this mesh since creation (launch accounting). */
+int64_t lgdm_launch_count(lgdm_mesh mesh);
+
+const char* lgdm_last_error(void);
+void lgdm_destroy(lgdm_mesh mesh);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LGDM_H */

@@ -1,0 +1,683 @@
+// lgdm_api.cu -- the C ABI of liblgdm (include/lgdm.h): mesh setup (det J check, CSR
+// pattern, element->CSR maps), state, assembly dispatch, history, residual norms, NCCL.
+//
+// Host-side setup is native C++ (OpenMP over nodes); every per-iteration step runs in the
+// CUDA kernels of lgdm_kernels.cuh / lgdm_sweep.cuh.  There is no CPU fallback: without a
+// usable CUDA device every call fails with LGDM_ERR_CUDA.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+#include <omp.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/lgdm.h"
+#include "lgdm_kernels.cuh"
+
+using namespace lgdm;
+
+namespace {
+
+thread_local std::string g_err;
+
+lgdm_status fail(lgdm_status s, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+#define CU(call)                                                                         \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(e_ == cudaErrorMemoryAllocation ? LGDM_ERR_OUT_OF_MEMORY : LGDM_ERR_CUDA, \
+                  "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__);  \
+  } while (0)
+
+// NCCL entry points, resolved at run time (the library does not link libnccl).
+struct NcclApi {
+  bool loaded = false;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+
+bool load_nccl() {
+  if (g_nccl.loaded) return true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return false;
+  g_nccl.commInitRank = (decltype(g_nccl.commInitRank))dlsym(h, "ncclCommInitRank");
+  g_nccl.allReduce = (decltype(g_nccl.allReduce))dlsym(h, "ncclAllReduce");
+  g_nccl.commDestroy = (decltype(g_nccl.commDestroy))dlsym(h, "ncclCommDestroy");
+  g_nccl.getErrorString = (decltype(g_nccl.getErrorString))dlsym(h, "ncclGetErrorString");
+  g_nccl.getUniqueId = (decltype(g_nccl.getUniqueId))dlsym(h, "ncclGetUniqueId");
+  g_nccl.loaded = g_nccl.commInitRank && g_nccl.allReduce && g_nccl.commDestroy && g_nccl.getUniqueId;
+  return g_nccl.loaded;
+}
+
+struct FamInfo {
+  int dim, nen, ndpn, ngp, ndofe, maxdeg;
+};
+FamInfo fam_info(int type) {
+  switch (type) {
+    case LGDM_BAR2: return {1, 2, 2, 2, 4, 3};
+    case LGDM_QUAD4: return {2, 4, 3, 4, 12, 9};
+    default: return {3, 8, 4, 8, 32, 27};
+  }
+}
+
+template <class T> cudaError_t dalloc(T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) return cudaSuccess;
+  return cudaMalloc((void**)p, count * sizeof(T));
+}
+
+}  // namespace
+
+struct lgdm_mesh_s {
+  int type = 0;
+  FamInfo f{};
+  int64_t n_nodes = 0, n_elems = 0, gid0 = 0, n_global_nodes = 0, own_b = 0, own_e = 0;
+  int64_t n_owned = 0, n_rows = 0, nnz = 0;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  DevMat dm{};
+  // device buffers
+  double* coords = nullptr;
+  int32_t* conn = nullptr;
+  double* dofs = nullptr;
+  double* kappa = nullptr;
+  int64_t* row_ptr = nullptr;
+  int32_t* col_idx = nullptr;
+  double* val = nullptr;
+  double* R = nullptr;
+  int64_t* nbr_ptr = nullptr;   // [n_owned+1]
+  int64_t* base = nullptr;      // [n_owned] val offset of the node's first row
+  int64_t* adj_ptr = nullptr;   // [n_owned+1]
+  AdjEntry* adj = nullptr;      // general-path element->CSR map
+  double* scratchK = nullptr;   // general path element blocks
+  double* scratchF = nullptr;
+  double* sumsq_part = nullptr; // [kSumBlocks*2]
+  double* sumsq_out = nullptr;  // [2]
+  double* host_pinned = nullptr;  // [2]
+  int64_t device_bytes = 0;
+  bool have_state = false, have_kappa = false, assembled = false;
+  int kernel = 0;  // 0 auto, 1 general, 2 sweep
+  // structured topology (x-fastest lexicographic grid) -> sweep kernels
+  bool structured = false;
+  int64_t nx = 0, ny = 0, nz = 0;  // local element counts per axis (nz = layers for 3D, ny for 2D)
+  int64_t launches = 0;
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  void* sweep = nullptr;  // sweep-path state (lgdm_sweep.cuh)
+};
+
+#include "lgdm_sweep.cuh"
+
+namespace {
+
+template <class T> lgdm_status upload(lgdm_mesh m, T** dst, const T* src, size_t count) {
+  CU(dalloc(dst, count));
+  m->device_bytes += int64_t(count * sizeof(T));
+  if (count) CU(cudaMemcpyAsync(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice, m->stream));
+  return LGDM_OK;
+}
+
+lgdm_status check_launch(lgdm_mesh m, const char* what) {
+  ++m->launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(LGDM_ERR_CUDA, "%s launch: %s", what, cudaGetErrorString(e));
+  return LGDM_OK;
+}
+
+bool validate_material(const lgdm_material* p, std::string* why) {
+  const lgdm_material& m = *p;
+  struct {
+    bool ok;
+    const char* msg;
+  } checks[] = {
+      {m.E > 0, "E > 0"},
+      {m.nu >= 0 && m.nu < 0.5, "0 <= nu < 0.5"},
+      {m.k >= 1, "k >= 1"},
+      {m.kappa0 > 0, "kappa0 > 0"},
+      {m.alpha > 0 && m.alpha <= 1, "0 < alpha <= 1"},
+      {m.beta > 0, "beta > 0"},
+      {m.h > 0, "h > 0"},
+      {m.h_sigma >= 0, "h_sigma >= 0"},
+      {m.c > 0, "c > 0"},
+      {m.R > 0 && m.R < 1, "0 < R < 1"},
+      {m.n > 0, "n > 0"},
+      {m.thickness_or_area > 0, "thickness_or_area > 0"},
+      {m.eq_variant == 0 || m.eq_variant == 1, "eq_variant in {0,1}"},
+      {m.reserved == 0, "reserved == 0"},
+  };
+  for (auto& c : checks)
+    if (!c.ok || std::isnan(m.E)) {
+      *why = c.msg;
+      return false;
+    }
+  return true;
+}
+
+DevMat derive(const lgdm_material& m, int dim) {
+  DevMat d{};
+  d.E = m.E;
+  d.lam = m.E * m.nu / ((1.0 + m.nu) * (1.0 - 2.0 * m.nu));
+  d.mu = m.E / (2.0 * (1.0 + m.nu));
+  d.k = m.k;
+  d.kappa0 = m.kappa0;
+  d.alpha = m.alpha;
+  d.beta = m.beta;
+  d.h = m.h;
+  d.hs = m.h_sigma;
+  d.c = m.c;
+  d.n = m.n;
+  const double en = std::exp(-m.n);
+  d.ga = (1.0 - m.R) / (1.0 - en);
+  d.gb = (m.R - en) / (1.0 - en);
+  d.t = m.thickness_or_area;
+  const double k = m.k, nu = m.nu;
+  d.c1 = (k - 1.0) / (2.0 * k * (1.0 - 2.0 * nu));
+  d.c2 = ((k - 1.0) / (1.0 - 2.0 * nu)) * ((k - 1.0) / (1.0 - 2.0 * nu));
+  d.c3 = m.eq_variant == 1 ? 2.0 * k / ((1.0 - nu) * (1.0 - nu)) : 12.0 * k / ((1.0 + nu) * (1.0 + nu));
+  (void)dim;
+  return d;
+}
+
+// Is conn an x-fastest structured grid (any coordinates)?  Fills nx, ny, nz.
+bool detect_structured(int type, int64_t nn, int64_t ne, const int64_t* conn, int64_t* nx,
+                       int64_t* ny, int64_t* nz) {
+  if (ne < 1) return false;
+  if (type == LGDM_BAR2) {
+    for (int64_t e = 0; e < ne; ++e)
+      if (conn[2 * e] != e || conn[2 * e + 1] != e + 1) return false;
+    if (nn != ne + 1) return false;
+    *nx = ne;
+    *ny = *nz = 1;
+    return true;
+  }
+  if (type == LGDM_QUAD4) {
+    const int64_t X = conn[3] - 1;  // conn[0] = {0, 1, X+2, X+1}
+    if (X < 1 || ne % X != 0) return false;
+    const int64_t Y = ne / X;
+    if (nn != (X + 1) * (Y + 1)) return false;
+    bool ok = true;
+#pragma omp parallel for reduction(&& : ok)
+    for (int64_t e = 0; e < ne; ++e) {
+      const int64_t i = e % X, j = e / X, b = i + (X + 1) * j;
+      const int64_t* c = conn + 4 * e;
+      ok = ok && c[0] == b && c[1] == b + 1 && c[2] == b + X + 2 && c[3] == b + X + 1;
+    }
+    if (!ok) return false;
+    *nx = X;
+    *ny = Y;
+    *nz = 1;
+    return true;
+  }
+  const int64_t X = conn[3] - 1;
+  const int64_t SZ = conn[4];
+  if (X < 1 || SZ % (X + 1) != 0) return false;
+  const int64_t Y = SZ / (X + 1) - 1;
+  if (Y < 1 || ne % (X * Y) != 0) return false;
+  const int64_t Z = ne / (X * Y);
+  if (nn != (X + 1) * (Y + 1) * (Z + 1)) return false;
+  bool ok = true;
+#pragma omp parallel for reduction(&& : ok)
+  for (int64_t e = 0; e < ne; ++e) {
+    const int64_t i = e % X, j = (e / X) % Y, k = e / (X * Y);
+    const int64_t b = i + (X + 1) * j + SZ * k;
+    const int64_t* c = conn + 8 * e;
+    const int64_t q[4] = {b, b + 1, b + X + 2, b + X + 1};
+    for (int a = 0; a < 4; ++a) ok = ok && c[a] == q[a] && c[a + 4] == q[a] + SZ;
+  }
+  if (!ok) return false;
+  *nx = X;
+  *ny = Y;
+  *nz = Z;
+  return true;
+}
+
+template <int D> void launch_detj(lgdm_mesh m, unsigned long long* bad) {
+  const int64_t n = m->n_elems * Fam<D>::NGP;
+  k_detj<D><<<unsigned((n + 255) / 256), 256, 0, m->stream>>>(m->n_elems, m->conn, m->coords, bad);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* lgdm_last_error(void) { return g_err.c_str(); }
+
+lgdm_status lgdm_create_mesh(lgdm_elem_type type, int64_t n_nodes, const double* coords,
+                             int64_t n_elems, const int64_t* conn, const lgdm_material* mat,
+                             int64_t global_node_offset, int64_t n_global_nodes,
+                             int64_t owned_node_begin, int64_t owned_node_end, int device,
+                             void* cuda_stream, lgdm_mesh* out) {
+  if (!out) return fail(LGDM_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  if (type != LGDM_BAR2 && type != LGDM_QUAD4 && type != LGDM_HEX8)
+    return fail(LGDM_ERR_INVALID_ARGUMENT, "unknown element type %d", int(type));
+  if (!coords || !conn || !mat) return fail(LGDM_ERR_INVALID_ARGUMENT, "NULL input pointer");
+  if (n_nodes < 2 || n_elems < 1 || n_nodes >= (int64_t(1) << 31))
+    return fail(LGDM_ERR_INVALID_ARGUMENT, "bad sizes n_nodes=%lld n_elems=%lld",
+                (long long)n_nodes, (long long)n_elems);
+  if (global_node_offset < 0 || n_global_nodes < global_node_offset + n_nodes)
+    return fail(LGDM_ERR_INVALID_ARGUMENT, "global node range inconsistent");
+  if (!(0 <= owned_node_begin && owned_node_begin < owned_node_end && owned_node_end <= n_nodes))
+    return fail(LGDM_ERR_INVALID_ARGUMENT, "owned node range [%lld,%lld) invalid",
+                (long long)owned_node_begin, (long long)owned_node_end);
+  const FamInfo f = fam_info(type);
+  if ((n_global_nodes * f.ndpn) >= (int64_t(1) << 31))
+    return fail(LGDM_ERR_INVALID_ARGUMENT, "global dof count exceeds int32 col_idx");
+  std::string why;
+  if (!validate_material(mat, &why)) return fail(LGDM_ERR_INVALID_ARGUMENT, "material: %s", why.c_str());
+  for (int64_t i = 0; i < n_elems * f.nen; ++i)
+    if (conn[i] < 0 || conn[i] >= n_nodes)
+      return fail(LGDM_ERR_INVALID_ARGUMENT, "conn[%lld] = %lld out of range", (long long)i,
+                  (long long)conn[i]);
+
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(LGDM_ERR_CUDA, "no CUDA device available (liblgdm has no CPU path)");
+  if (device < 0 || device >= ndev) return fail(LGDM_ERR_INVALID_ARGUMENT, "bad device %d", device);
+  CU(cudaSetDevice(device));
+
+  lgdm_mesh m = new lgdm_mesh_s();
+  m->type = type;
+  m->f = f;
+  m->n_nodes = n_nodes;
+  m->n_elems = n_elems;
+  m->gid0 = global_node_offset;
+  m->n_global_nodes = n_global_nodes;
+  m->own_b = owned_node_begin;
+  m->own_e = owned_node_end;
+  m->n_owned = owned_node_end - owned_node_begin;
+  m->n_rows = m->n_owned * f.ndpn;
+  m->device = device;
+  m->stream = (cudaStream_t)cuda_stream;
+  m->dm = derive(*mat, f.dim);
+
+  auto bail = [&](lgdm_status s) {
+    std::string keep = g_err;
+    lgdm_destroy(m);
+    g_err = keep;
+    return s;
+  };
+  lgdm_status s;
+
+  // ---- coordinates and connectivity (int32 local ids on device) ----
+  std::vector<int32_t> conn32(size_t(n_elems) * f.nen);
+  for (size_t i = 0; i < conn32.size(); ++i) conn32[i] = int32_t(conn[i]);
+  if ((s = upload(m, &m->coords, coords, size_t(n_nodes) * f.dim)) != LGDM_OK) return bail(s);
+  if ((s = upload(m, &m->conn, conn32.data(), conn32.size())) != LGDM_OK) return bail(s);
+
+  // ---- det J > 0 at every GP ----
+  unsigned long long* bad = nullptr;
+  if (cudaMalloc(&bad, sizeof(unsigned long long)) != cudaSuccess)
+    return bail(fail(LGDM_ERR_OUT_OF_MEMORY, "cudaMalloc"));
+  cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), m->stream);
+  if (f.dim == 1) launch_detj<1>(m, bad);
+  else if (f.dim == 2) launch_detj<2>(m, bad);
+  else launch_detj<3>(m, bad);
+  if ((s = check_launch(m, "k_detj")) != LGDM_OK) { cudaFree(bad); return bail(s); }
+  unsigned long long hbad = 0;
+  cudaMemcpyAsync(&hbad, bad, sizeof(hbad), cudaMemcpyDeviceToHost, m->stream);
+  cudaError_t ce = cudaStreamSynchronize(m->stream);
+  cudaFree(bad);
+  if (ce != cudaSuccess) return bail(fail(LGDM_ERR_CUDA, "det J check: %s", cudaGetErrorString(ce)));
+  if (hbad != ~0ull)
+    return bail(fail(LGDM_ERR_INVERTED_ELEMENT, "det J <= 0 in element %lld at Gauss point %d",
+                     (long long)(hbad / f.ngp), int(hbad % f.ngp)));
+
+  // ---- pattern (reading R-PAT): neighbours of owned nodes, row_ptr, base, element maps ----
+  // node -> adjacent elements (ascending e) by counting sort
+  std::vector<int64_t> nadj(n_nodes + 1, 0);
+  for (int64_t i = 0; i < n_elems * f.nen; ++i) ++nadj[conn[i] + 1];
+  for (int64_t n = 0; n < n_nodes; ++n) nadj[n + 1] += nadj[n];
+  std::vector<int32_t> adj_e(nadj[n_nodes]);
+  std::vector<uint8_t> adj_a(nadj[n_nodes]);
+  {
+    std::vector<int64_t> fillp(nadj.begin(), nadj.end() - 1);
+    for (int64_t e = 0; e < n_elems; ++e)
+      for (int a = 0; a < f.nen; ++a) {
+        const int64_t n = conn[e * f.nen + a];
+        adj_e[fillp[n]] = int32_t(e);
+        adj_a[fillp[n]] = uint8_t(a);
+        ++fillp[n];
+      }
+  }
+  const int64_t no = m->n_owned;
+  std::vector<int64_t> nbr_ptr(no + 1, 0);
+  std::vector<int32_t> nbr(size_t(no) * f.maxdeg);
+  std::vector<int32_t> deg(no);
+#pragma omp parallel for schedule(static)
+  for (int64_t o = 0; o < no; ++o) {
+    const int64_t n = o + owned_node_begin;
+    int32_t tmp[64 * 8];
+    int cnt = 0;
+    for (int64_t k = nadj[n]; k < nadj[n + 1]; ++k)
+      for (int b = 0; b < f.nen; ++b) tmp[cnt++] = int32_t(conn[int64_t(adj_e[k]) * f.nen + b]);
+    std::sort(tmp, tmp + cnt);
+    cnt = int(std::unique(tmp, tmp + cnt) - tmp);
+    deg[o] = cnt;
+    std::copy(tmp, tmp + cnt, nbr.begin() + o * f.maxdeg);
+  }
+  for (int64_t o = 0; o < no; ++o) nbr_ptr[o + 1] = nbr_ptr[o] + deg[o];
+  std::vector<int32_t> nbr_c(nbr_ptr[no]);
+#pragma omp parallel for schedule(static)
+  for (int64_t o = 0; o < no; ++o)
+    std::copy(nbr.begin() + o * f.maxdeg, nbr.begin() + o * f.maxdeg + deg[o], nbr_c.begin() + nbr_ptr[o]);
+  std::vector<int64_t> base(no), row_ptr(m->n_rows + 1);
+  int64_t pos = 0;
+  for (int64_t o = 0; o < no; ++o) {
+    base[o] = pos;
+    for (int i = 0; i < f.ndpn; ++i) {
+      row_ptr[o * f.ndpn + i] = pos;
+      pos += int64_t(deg[o]) * f.ndpn;
+    }
+  }
+  row_ptr[m->n_rows] = pos;
+  m->nnz = pos;
+  // element -> CSR map for owned nodes (general path)
+  std::vector<int64_t> adj_ptr(no + 1, 0);
+  for (int64_t o = 0; o < no; ++o) {
+    const int64_t n = o + owned_node_begin;
+    adj_ptr[o + 1] = adj_ptr[o] + (nadj[n + 1] - nadj[n]);
+  }
+  std::vector<AdjEntry> adj(adj_ptr[no]);
+#pragma omp parallel for schedule(static)
+  for (int64_t o = 0; o < no; ++o) {
+    const int64_t n = o + owned_node_begin;
+    const int32_t* nb = nbr_c.data() + nbr_ptr[o];
+    const int dg = deg[o];
+    for (int64_t k = nadj[n]; k < nadj[n + 1]; ++k) {
+      AdjEntry en{};
+      en.e = adj_e[k];
+      en.aloc = adj_a[k];
+      for (int b = 0; b < f.nen; ++b) {
+        const int32_t nbn = int32_t(conn[int64_t(en.e) * f.nen + b]);
+        en.slot[b] = uint8_t(std::lower_bound(nb, nb + dg, nbn) - nb);
+      }
+      adj[adj_ptr[o] + (k - nadj[n])] = en;
+    }
+  }
+  if ((s = upload(m, &m->row_ptr, row_ptr.data(), row_ptr.size())) != LGDM_OK) return bail(s);
+  if ((s = upload(m, &m->base, base.data(), base.size())) != LGDM_OK) return bail(s);
+  if ((s = upload(m, &m->nbr_ptr, nbr_ptr.data(), nbr_ptr.size())) != LGDM_OK) return bail(s);
+  if ((s = upload(m, &m->adj_ptr, adj_ptr.data(), adj_ptr.size())) != LGDM_OK) return bail(s);
+  if ((s = upload(m, &m->adj, adj.data(), adj.size())) != LGDM_OK) return bail(s);
+  int32_t* nbr_d = nullptr;
+  if (cudaMalloc(&nbr_d, nbr_c.size() * sizeof(int32_t)) != cudaSuccess)
+    return bail(fail(LGDM_ERR_OUT_OF_MEMORY, "cudaMalloc nbr"));
+  cudaMemcpyAsync(nbr_d, nbr_c.data(), nbr_c.size() * sizeof(int32_t), cudaMemcpyHostToDevice, m->stream);
+  if (dalloc(&m->col_idx, size_t(m->nnz)) != cudaSuccess || dalloc(&m->val, size_t(m->nnz)) != cudaSuccess ||
+      dalloc(&m->R, size_t(m->n_rows)) != cudaSuccess) {
+    cudaFree(nbr_d);
+    return bail(fail(LGDM_ERR_OUT_OF_MEMORY, "cudaMalloc CSR (nnz=%lld)", (long long)m->nnz));
+  }
+  m->device_bytes += m->nnz * (4 + 8) + m->n_rows * 8;
+  {
+    const unsigned blocks = unsigned((no * 32 + 255) / 256);
+    if (f.ndpn == 2) k_cols<2><<<blocks, 256, 0, m->stream>>>(no, m->nbr_ptr, nbr_d, m->base, global_node_offset, m->col_idx);
+    else if (f.ndpn == 3) k_cols<3><<<blocks, 256, 0, m->stream>>>(no, m->nbr_ptr, nbr_d, m->base, global_node_offset, m->col_idx);
+    else k_cols<4><<<blocks, 256, 0, m->stream>>>(no, m->nbr_ptr, nbr_d, m->base, global_node_offset, m->col_idx);
+    if ((s = check_launch(m, "k_cols")) != LGDM_OK) { cudaFree(nbr_d); return bail(s); }
+  }
+  // ---- state, reductions ----
+  if (dalloc(&m->dofs, size_t(n_nodes) * f.ndpn) != cudaSuccess ||
+      dalloc(&m->kappa, size_t(n_elems) * f.ngp) != cudaSuccess ||
+      dalloc(&m->sumsq_part, size_t(2 * kSumBlocks)) != cudaSuccess ||
+      dalloc(&m->sumsq_out, 2) != cudaSuccess ||
+      cudaMallocHost(&m->host_pinned, 2 * sizeof(double)) != cudaSuccess) {
+    cudaFree(nbr_d);
+    return bail(fail(LGDM_ERR_OUT_OF_MEMORY, "cudaMalloc state"));
+  }
+  m->device_bytes += (n_nodes * f.ndpn + n_elems * f.ngp) * 8;
+  m->structured = detect_structured(type, n_nodes, n_elems, conn, &m->nx, &m->ny, &m->nz);
+  ce = cudaStreamSynchronize(m->stream);
+  cudaFree(nbr_d);
+  if (ce != cudaSuccess) return bail(fail(LGDM_ERR_CUDA, "create: %s", cudaGetErrorString(ce)));
+  *out = m;
+  return LGDM_OK;
+}
+
+lgdm_status lgdm_set_state(lgdm_mesh m, const double* dofs, int64_t n_dofs, const double* kappa,
+                           int64_t n_kappa, int src_on_device) {
+  if (!m) return fail(LGDM_ERR_INVALID_ARGUMENT, "mesh is NULL");
+  if (!dofs) return fail(LGDM_ERR_INVALID_ARGUMENT, "dofs is NULL");
+  if (n_dofs != m->n_nodes * m->f.ndpn)
+    return fail(LGDM_ERR_INVALID_STATE, "n_dofs = %lld, expected %lld", (long long)n_dofs,
+                (long long)(m->n_nodes * m->f.ndpn));
+  if (kappa && n_kappa != m->n_elems * m->f.ngp)
+    return fail(LGDM_ERR_INVALID_STATE, "n_kappa = %lld, expected %lld", (long long)n_kappa,
+                (long long)(m->n_elems * m->f.ngp));
+  if (!kappa && !m->have_kappa) return fail(LGDM_ERR_INVALID_STATE, "kappa never set");
+  CU(cudaSetDevice(m->device));
+  const cudaMemcpyKind kind = src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  CU(cudaMemcpyAsync(m->dofs, dofs, size_t(n_dofs) * 8, kind, m->stream));
+  if (kappa) CU(cudaMemcpyAsync(m->kappa, kappa, size_t(n_kappa) * 8, kind, m->stream));
+  m->have_state = true;
+  if (kappa) m->have_kappa = true;
+  return LGDM_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+template <int D> lgdm_status assemble_general(lgdm_mesh m) {
+  using F = Fam<D>;
+  using Rc = Rec<D>;
+  constexpr int EPB = D == 3 ? 8 : (D == 2 ? 32 : 64);
+  if (!m->scratchK) {
+    CU(dalloc(&m->scratchK, size_t(m->n_elems) * F::NDOFE * F::NDOFE));
+    CU(dalloc(&m->scratchF, size_t(m->n_elems) * F::NDOFE));
+    m->device_bytes += m->n_elems * (F::NDOFE * F::NDOFE + F::NDOFE) * 8;
+  }
+  const size_t smem = sizeof(double) * (size_t(EPB) * F::NGP * F::NEN * Rc::STRIDE +
+                                        EPB * F::NGP * kScal + EPB * F::NEN * D + EPB * F::NEN * F::NDPN);
+  static bool attr = false;
+  if (!attr) {
+    CU(cudaFuncSetAttribute(k_elem_blocks<D, EPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr = true;
+  }
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_elem_blocks<D, EPB>, EPB * F::NPAIR, smem);
+  const int64_t batches = (m->n_elems + EPB - 1) / EPB;
+  const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(batches, int64_t(nsm) * std::max(per_sm, 1))));
+  k_elem_blocks<D, EPB><<<grid, EPB * F::NPAIR, smem, m->stream>>>(
+      m->dm, m->n_elems, m->conn, m->coords, m->dofs, m->kappa, m->scratchK, m->scratchF);
+  lgdm_status s = check_launch(m, "k_elem_blocks");
+  if (s != LGDM_OK) return s;
+  constexpr int WPB = 8;
+  k_gather<D, WPB><<<unsigned((m->n_owned + WPB - 1) / WPB), WPB * 32, 0, m->stream>>>(
+      m->n_owned, m->adj_ptr, m->adj, m->nbr_ptr, m->base, m->scratchK, m->scratchF, m->val, m->R);
+  return check_launch(m, "k_gather");
+}
+
+}  // namespace
+
+extern "C" {
+
+lgdm_status lgdm_assemble(lgdm_mesh m, lgdm_csr* K, double** R) {
+  if (!m) return fail(LGDM_ERR_INVALID_ARGUMENT, "mesh is NULL");
+  if (!m->have_state || !m->have_kappa) return fail(LGDM_ERR_INVALID_STATE, "assemble before set_state");
+  CU(cudaSetDevice(m->device));
+  lgdm_status s;
+  const bool sweep = m->kernel == 2 || (m->kernel == 0 && m->structured && sweep_supported(m));
+  if (m->kernel == 2 && !(m->structured && sweep_supported(m)))
+    return fail(LGDM_ERR_INVALID_ARGUMENT, "sweep kernel requested but mesh is not structured");
+  if (sweep) s = assemble_sweep(m);
+  else if (m->f.dim == 1) s = assemble_general<1>(m);
+  else if (m->f.dim == 2) s = assemble_general<2>(m);
+  else s = assemble_general<3>(m);
+  if (s != LGDM_OK) return s;
+  m->assembled = true;
+  if (K) {
+    K->n_rows = m->n_rows;
+    K->n_cols = m->n_global_nodes * m->f.ndpn;
+    K->nnz = m->nnz;
+    K->first_row = (m->gid0 + m->own_b) * m->f.ndpn;
+    K->row_ptr = m->row_ptr;
+    K->col_idx = m->col_idx;
+    K->val = m->val;
+  }
+  if (R) *R = m->R;
+  return LGDM_OK;
+}
+
+lgdm_status lgdm_update_history(lgdm_mesh m) {
+  if (!m) return fail(LGDM_ERR_INVALID_ARGUMENT, "mesh is NULL");
+  if (!m->have_state || !m->have_kappa) return fail(LGDM_ERR_INVALID_STATE, "update_history before set_state");
+  CU(cudaSetDevice(m->device));
+  const int64_t n = m->n_elems * m->f.ngp;
+  const unsigned blocks = unsigned((n + 255) / 256);
+  if (m->f.dim == 1) k_update_history<1><<<blocks, 256, 0, m->stream>>>(m->n_elems, m->conn, m->dofs, m->kappa);
+  else if (m->f.dim == 2) k_update_history<2><<<blocks, 256, 0, m->stream>>>(m->n_elems, m->conn, m->dofs, m->kappa);
+  else k_update_history<3><<<blocks, 256, 0, m->stream>>>(m->n_elems, m->conn, m->dofs, m->kappa);
+  return check_launch(m, "k_update_history");
+}
+
+lgdm_status lgdm_residual_sumsq(lgdm_mesh m, double* out2, int on_device) {
+  if (!m || !out2) return fail(LGDM_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (!m->assembled) return fail(LGDM_ERR_INVALID_STATE, "residual before assemble");
+  CU(cudaSetDevice(m->device));
+  k_sumsq_partial<<<kSumBlocks, kSumThreads, 0, m->stream>>>(m->n_rows, m->f.ndpn, m->f.dim, m->R, m->sumsq_part);
+  lgdm_status s = check_launch(m, "k_sumsq_partial");
+  if (s != LGDM_OK) return s;
+  double* dst = on_device ? out2 : m->sumsq_out;
+  k_sumsq_final<<<1, kSumThreads, 0, m->stream>>>(kSumBlocks, m->sumsq_part, dst);
+  if ((s = check_launch(m, "k_sumsq_final")) != LGDM_OK) return s;
+  if (!on_device) {
+    CU(cudaMemcpyAsync(m->host_pinned, m->sumsq_out, 2 * sizeof(double), cudaMemcpyDeviceToHost, m->stream));
+    CU(cudaStreamSynchronize(m->stream));
+    out2[0] = m->host_pinned[0];
+    out2[1] = m->host_pinned[1];
+  }
+  return LGDM_OK;
+}
+
+lgdm_status lgdm_residual_norms(lgdm_mesh m, double out2[2]) {
+  if (!m || !out2) return fail(LGDM_ERR_INVALID_ARGUMENT, "NULL argument");
+  lgdm_status s = lgdm_residual_sumsq(m, m->sumsq_out, 1);
+  if (s != LGDM_OK) return s;
+  if (m->comm) {
+    ncclResult_t r = g_nccl.allReduce(m->sumsq_out, m->sumsq_out, 2, ncclFloat64, ncclSum, m->comm, m->stream);
+    if (r != ncclSuccess)
+      return fail(LGDM_ERR_NCCL, "ncclAllReduce: %s", g_nccl.getErrorString ? g_nccl.getErrorString(r) : "?");
+  }
+  CU(cudaMemcpyAsync(m->host_pinned, m->sumsq_out, 2 * sizeof(double), cudaMemcpyDeviceToHost, m->stream));
+  CU(cudaStreamSynchronize(m->stream));
+  out2[0] = std::sqrt(m->host_pinned[0]);
+  out2[1] = std::sqrt(m->host_pinned[1]);
+  return LGDM_OK;
+}
+
+lgdm_status lgdm_set_comm(lgdm_mesh m, const void* uid, int nranks, int rank) {
+  if (!m || !uid || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(LGDM_ERR_INVALID_ARGUMENT, "bad communicator arguments");
+  if (!load_nccl()) return fail(LGDM_ERR_UNSUPPORTED, "cannot dlopen libnccl.so.2");
+  CU(cudaSetDevice(m->device));
+  ncclUniqueId id;
+  std::memcpy(&id, uid, sizeof(id));
+  if (m->comm) g_nccl.commDestroy(m->comm), m->comm = nullptr;
+  ncclResult_t r = g_nccl.commInitRank(&m->comm, nranks, id, rank);
+  if (r != ncclSuccess)
+    return fail(LGDM_ERR_NCCL, "ncclCommInitRank: %s", g_nccl.getErrorString ? g_nccl.getErrorString(r) : "?");
+  m->nranks = nranks;
+  m->rank = rank;
+  return LGDM_OK;
+}
+
+lgdm_status lgdm_nccl_unique_id(void* out, int64_t out_bytes) {
+  if (!out || out_bytes < int64_t(sizeof(ncclUniqueId)))
+    return fail(LGDM_ERR_INVALID_ARGUMENT, "need %d bytes", int(sizeof(ncclUniqueId)));
+  if (!load_nccl()) return fail(LGDM_ERR_UNSUPPORTED, "cannot dlopen libnccl.so.2");
+  ncclUniqueId id;
+  ncclResult_t r = g_nccl.getUniqueId(&id);
+  if (r != ncclSuccess) return fail(LGDM_ERR_NCCL, "ncclGetUniqueId failed");
+  std::memcpy(out, &id, sizeof(id));
+  return LGDM_OK;
+}
+
+lgdm_status lgdm_get_kappa(lgdm_mesh m, double* host_out) {
+  if (!m || !host_out) return fail(LGDM_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (!m->have_kappa) return fail(LGDM_ERR_INVALID_STATE, "kappa never set");
+  CU(cudaSetDevice(m->device));
+  CU(cudaMemcpyAsync(host_out, m->kappa, size_t(m->n_elems) * m->f.ngp * 8, cudaMemcpyDeviceToHost, m->stream));
+  CU(cudaStreamSynchronize(m->stream));
+  return LGDM_OK;
+}
+
+lgdm_status lgdm_scale_dofs(lgdm_mesh m, double sc) {
+  if (!m) return fail(LGDM_ERR_INVALID_ARGUMENT, "mesh is NULL");
+  if (!m->have_state) return fail(LGDM_ERR_INVALID_STATE, "scale before set_state");
+  CU(cudaSetDevice(m->device));
+  const int64_t n = m->n_nodes * m->f.ndpn;
+  k_scale<<<unsigned((n + 255) / 256), 256, 0, m->stream>>>(n, sc, m->dofs);
+  return check_launch(m, "k_scale");
+}
+
+lgdm_status lgdm_set_kernel(lgdm_mesh m, int kernel) {
+  if (!m || kernel < 0 || kernel > 2) return fail(LGDM_ERR_INVALID_ARGUMENT, "bad kernel selector");
+  if (kernel == 2 && !(m->structured && sweep_supported(m)))
+    return fail(LGDM_ERR_INVALID_ARGUMENT, "sweep kernel needs a structured mesh with whole owned layers");
+  m->kernel = kernel;
+  return LGDM_OK;
+}
+
+lgdm_status lgdm_get_info(lgdm_mesh m, lgdm_info* info) {
+  if (!m || !info) return fail(LGDM_ERR_INVALID_ARGUMENT, "NULL argument");
+  info->elem_type = m->type;
+  info->dim = m->f.dim;
+  info->nen = m->f.nen;
+  info->ndpn = m->f.ndpn;
+  info->ngp = m->f.ngp;
+  info->structured = (m->structured && sweep_supported(m)) ? 1 : 0;
+  info->n_nodes = m->n_nodes;
+  info->n_elems = m->n_elems;
+  info->n_owned_nodes = m->n_owned;
+  info->n_rows = m->n_rows;
+  info->nnz = m->nnz;
+  info->nx = m->nx;
+  info->ny = m->ny;
+  info->nz = m->nz;
+  info->device_bytes = m->device_bytes;
+  return LGDM_OK;
+}
+
+int64_t lgdm_launch_count(lgdm_mesh m) { return m ? m->launches : -1; }
+
+void lgdm_destroy(lgdm_mesh m) {
+  if (!m) return;
+  cudaSetDevice(m->device);
+  if (m->stream) cudaStreamSynchronize(m->stream);
+  if (m->comm && g_nccl.loaded) g_nccl.commDestroy(m->comm);
+  void* ptrs[] = {m->coords, m->conn, m->dofs, m->kappa, m->row_ptr, m->col_idx, m->val, m->R,
+                  m->nbr_ptr, m->base, m->adj_ptr, m->adj, m->scratchK, m->scratchF,
+                  m->sumsq_part, m->sumsq_out};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (m->host_pinned) cudaFreeHost(m->host_pinned);
+  sweep_free(m);
+  delete m;
+}
+
+}  // extern "C"

@@ -1,0 +1,442 @@
+// lgdm_device.cuh -- device-side arithmetic of the LGDM K/R assembly (sm_100a, FP64).
+//
+// The element work is split into three phases so that each FP64 product is formed once:
+//   phase A  (one thread per element x Gauss point): geometry (Fig. 3 / Fig. 6: J, det J,
+//            grad N), kinematics (Fig. 8b l.7, l.19: eps = B u, ebar = N e, grad ebar),
+//            constitutive update (Appendix A; Fig. 8b condition vectors) and the per-node
+//            "expansions" of the Voigt tangent into gradient space (NodeRec below);
+//   phase C  (one thread per element x node pair a<=b): the Gauss sums of Eqs. 11a-f for the
+//            4x4 (Hex8) / 3x3 (Q4) / 2x2 (bar) node-pair blocks (a,b) and (b,a), using the
+//            symmetry of Kuu (every term is B^T X B with X symmetric).
+// The Voigt tangent of Eq. 11a plus the term of reading R-11a,
+//     X = (1-D) C + h_sigma (d d^T + (eeq - ebar) H),
+// is isotropic-plus-rank-2 in the basis {m = dI1/deps, s = dJ2/deps}, so
+//     Kuu_ab[i][j] = lam* dNa_i dNb_j + mu* (dNa_j dNb_i + delta_ij gNa.gNb)
+//                  + Ams (dNa_i (S gNb)_j + (S gNa)_i dNb_j) + Ass (S gNa)_i (S gNb)_j,
+// with S the deviatoric strain tensor.  This is the B200 formulation of the paper's
+// B_mat' * D_mat * B_mat product (Fig. 7): no B matrix is ever materialised.
+#pragma once
+#include <cstdint>
+
+namespace lgdm {
+
+// Material constants derived once on the host (Eq. 1, A.1, A.3, A.4).
+struct DevMat {
+  double E, lam, mu;       // 1D: E; 2D plane strain / 3D: Lame constants
+  double k, kappa0, alpha, beta;
+  double h, hs, c;         // h, h_sigma, c
+  double n, ga, gb;        // g(D) = ga * exp(-n D) + gb   (Eq. A.4 rearranged)
+  double t;                // area (1D) / thickness
+  double c1, c2, c3;       // Eq. A.3 constants (reading R-A3)
+};
+
+template <int D> struct Fam;
+template <> struct Fam<1> {
+  static constexpr int DIM = 1, NEN = 2, NDPN = 2, NGP = 2, NS = 1, NPAIR = 3, NDOFE = 4;
+};
+template <> struct Fam<2> {
+  static constexpr int DIM = 2, NEN = 4, NDPN = 3, NGP = 4, NS = 3, NPAIR = 10, NDOFE = 12;
+};
+template <> struct Fam<3> {
+  static constexpr int DIM = 3, NEN = 8, NDPN = 4, NGP = 8, NS = 6, NPAIR = 36, NDOFE = 32;
+};
+
+// Per (element, GP, node) record produced by phase A.  Field offsets in doubles.
+//   gN[D]   grad N_a                    SgN[D]  S grad N_a
+//   t1[D]   lam* gN + Ams SgN           t2[D]   Ams gN + Ass SgN
+//   WgN[D]  W' grad N_a   (Kue)         DgN[D]  Dt' grad N_a  (Keu)
+//   N       N_a                          e       hN N_a + gvec . gN_a   (Kee)
+//   f[D+1]  (Sigma' gN_a, fe0 N_a + fvec . gN_a)   (Fu, Fe)
+// All coefficients carry dV and the signs of Eq. 11, so phase C only multiplies and adds.
+template <int D> struct Rec {
+  static constexpr int GN = 0, SGN = D, T1 = 2 * D, T2 = 3 * D, WGN = 4 * D, DGN = 5 * D,
+                       N = 6 * D, E = 6 * D + 1, F = 6 * D + 2;
+  static constexpr int USED = 7 * D + 3;
+  // odd stride: conflict-free LDS.64 for up to 16 distinct records per warp access
+  static constexpr int STRIDE = (USED % 2 == 1) ? USED : USED + 1;
+};
+// per (element, GP) scalars used by phase C: mu*, ghc
+constexpr int kScal = 2;
+
+// reference node sign r_ak (SURVEY 8c.1 node order) and Gauss point sign s_gk (xi fastest)
+template <int D> __device__ __forceinline__ int node_sign(int a, int k) {
+  if constexpr (D == 1) return a == 0 ? -1 : 1;
+  if (k == 0) return ((a & 3) == 1 || (a & 3) == 2) ? 1 : -1;
+  if (k == 1) return ((a & 3) >= 2) ? 1 : -1;
+  return a >= 4 ? 1 : -1;
+}
+__device__ __forceinline__ int gp_sign(int g, int k) { return ((g >> k) & 1) ? 1 : -1; }
+
+// 1D Lagrange factors at xi = +-1/sqrt(3): (1 + r s/sqrt3)/2
+#define LGDM_P 0.78867513459481288225   // (1 + 1/sqrt(3)) / 2
+#define LGDM_M 0.21132486540518711775   // (1 - 1/sqrt(3)) / 2
+
+template <int D> __device__ __forceinline__ double shapeN(int a, int g) {
+  double v = 1.0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) v *= (node_sign<D>(a, k) == gp_sign(g, k)) ? LGDM_P : LGDM_M;
+  return v;
+}
+template <int D> __device__ __forceinline__ double shape_dxi(int a, int g, int k) {
+  double v = 0.5 * node_sign<D>(a, k);
+#pragma unroll
+  for (int l = 0; l < D; ++l)
+    if (l != k) v *= (node_sign<D>(a, l) == gp_sign(g, l)) ? LGDM_P : LGDM_M;
+  return v;
+}
+
+// symmetric tensor (sym storage 1D [xx]; 2D [xx,yy,xy]; 3D [xx,yy,zz,xy,yz,xz]) times vector
+template <int D> __device__ __forceinline__ void symv(const double* T, const double* v, double* o) {
+  if constexpr (D == 1) {
+    o[0] = T[0] * v[0];
+  } else if constexpr (D == 2) {
+    o[0] = T[0] * v[0] + T[2] * v[1];
+    o[1] = T[2] * v[0] + T[1] * v[1];
+  } else {
+    o[0] = T[0] * v[0] + T[3] * v[1] + T[5] * v[2];
+    o[1] = T[3] * v[0] + T[1] * v[1] + T[4] * v[2];
+    o[2] = T[5] * v[0] + T[4] * v[1] + T[2] * v[2];
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Phase A: one Gauss point g of one element.  X [NEN][D] coords, U [NEN][NDPN] dofs,
+// kh = kappa_hist.  Writes NEN records at rec + a*STRIDE and 2 scalars at scal.
+// Returns det J (caller treats <= 0 as an inverted element).
+// ---------------------------------------------------------------------------------------
+template <int D>
+__device__ double phaseA(const DevMat& m, const double* __restrict__ X,
+                         const double* __restrict__ U, double kh, int g,
+                         double* __restrict__ rec, double* __restrict__ scal) {
+  using F = Fam<D>;
+  using R = Rec<D>;
+  constexpr int NEN = F::NEN, NDPN = F::NDPN, NS = F::NS;
+
+  // geometry: J_ij = sum_a X_ai dN_a/dxi_j
+  double J[D][D];
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) J[i][j] = 0.0;
+#pragma unroll
+  for (int a = 0; a < NEN; ++a)
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const double dn = shape_dxi<D>(a, g, j);
+#pragma unroll
+      for (int i = 0; i < D; ++i) J[i][j] = fma(X[a * D + i], dn, J[i][j]);
+    }
+  double detJ, Ji[D][D];
+  if constexpr (D == 1) {
+    detJ = J[0][0];
+    Ji[0][0] = 1.0 / detJ;
+  } else if constexpr (D == 2) {
+    detJ = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+    const double r = 1.0 / detJ;
+    Ji[0][0] = J[1][1] * r;
+    Ji[0][1] = -J[0][1] * r;
+    Ji[1][0] = -J[1][0] * r;
+    Ji[1][1] = J[0][0] * r;
+  } else {
+    const double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+    const double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+    const double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+    detJ = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
+    const double r = 1.0 / detJ;
+    Ji[0][0] = c00 * r;
+    Ji[1][0] = c01 * r;
+    Ji[2][0] = c02 * r;
+    Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * r;
+    Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * r;
+    Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * r;
+    Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * r;
+    Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * r;
+    Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * r;
+  }
+  const double dV = detJ * m.t;  // Gauss weights are 1
+
+  // grad N_a = J^-T dN/dxi ; kinematics
+  double gN[NEN][D];
+  double eps[D][D], ebar = 0.0, gb[D];
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    gb[i] = 0.0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) eps[i][j] = 0.0;
+  }
+#pragma unroll
+  for (int a = 0; a < NEN; ++a) {
+    double dxi[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) dxi[j] = shape_dxi<D>(a, g, j);
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) s = fma(Ji[j][i], dxi[j], s);
+      gN[a][i] = s;
+    }
+    const double ea = U[a * NDPN + D];
+    ebar = fma(shapeN<D>(a, g), ea, ebar);
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      gb[i] = fma(gN[a][i], ea, gb[i]);
+#pragma unroll
+      for (int j = 0; j < D; ++j) eps[i][j] = fma(U[a * NDPN + i], gN[a][j], eps[i][j]);
+    }
+  }
+  // symmetrise: eps_ij = (du_i/dx_j + du_j/dx_i)/2
+  double es[NS];
+  if constexpr (D == 1) {
+    es[0] = eps[0][0];
+  } else if constexpr (D == 2) {
+    es[0] = eps[0][0];
+    es[1] = eps[1][1];
+    es[2] = 0.5 * (eps[0][1] + eps[1][0]);
+  } else {
+    es[0] = eps[0][0];
+    es[1] = eps[1][1];
+    es[2] = eps[2][2];
+    es[3] = 0.5 * (eps[0][1] + eps[1][0]);
+    es[4] = 0.5 * (eps[1][2] + eps[2][1]);
+    es[5] = 0.5 * (eps[0][2] + eps[2][0]);
+  }
+
+  // ---- Appendix A: equivalent strain, history, damage, interaction ----
+  double I1, eeq, dm, ds;  // d = dm * m + ds * s
+  double S[NS];            // deviatoric strain tensor (in-plane part in 2D)
+  double A2 = 0.0, Bq = 0.0;  // H = A2 (2 c2 m m^T + c3 P) - Bq q q^T
+  if constexpr (D == 1) {
+    I1 = es[0];
+    eeq = es[0];  // reading R-1D
+    dm = 1.0;
+    ds = 0.0;
+    S[0] = 0.0;
+  } else {
+    I1 = (D == 2) ? es[0] + es[1] : es[0] + es[1] + es[2];
+    const double third = I1 * (1.0 / 3.0);
+    double J2;
+    if constexpr (D == 2) {
+      S[0] = es[0] - third;
+      S[1] = es[1] - third;
+      S[2] = es[2];
+      J2 = 0.5 * (S[0] * S[0] + S[1] * S[1] + third * third) + S[2] * S[2];  // dev_zz = -I1/3
+    } else {
+      S[0] = es[0] - third;
+      S[1] = es[1] - third;
+      S[2] = es[2] - third;
+      S[3] = es[3];
+      S[4] = es[4];
+      S[5] = es[5];
+      J2 = 0.5 * (S[0] * S[0] + S[1] * S[1] + S[2] * S[2]) + S[3] * S[3] + S[4] * S[4] +
+           S[5] * S[5];
+    }
+    const double Q = m.c2 * I1 * I1 + m.c3 * J2;
+    if (Q < 1e-30) {  // reading R-SQ
+      eeq = m.c1 * I1 + sqrt(Q) / (2.0 * m.k);
+      dm = m.c1;
+      ds = 0.0;
+    } else {
+      const double sQ = sqrt(Q);
+      const double r4k = 1.0 / (4.0 * m.k * sQ);
+      eeq = m.c1 * I1 + sQ / (2.0 * m.k);
+      dm = m.c1 + 2.0 * m.c2 * I1 * r4k;
+      ds = m.c3 * r4k;
+      A2 = r4k;                       // 1/(4 k sqrt Q)
+      Bq = r4k / (2.0 * Q);           // 1/(8 k Q sqrt Q)
+    }
+  }
+  const bool L = (ebar - kh) > 1e-10;                  // Fig. 8b l.22 cond1
+  const double kap = L ? ebar : kh;
+  double Dm = 0.0, dD = 0.0;
+  if (!((kap - m.kappa0) < 1e-10)) {                   // Fig. 8b l.27 cond2 (negated)
+    const double ex = exp(-m.beta * (kap - m.kappa0));
+    const double br = 1.0 - m.alpha + m.alpha * ex;
+    const double r = m.kappa0 / kap;
+    Dm = 1.0 - r * br;                                 // Eq. A.1
+    dD = (r / kap) * br + r * m.alpha * m.beta * ex;
+  }
+  const double enD = exp(-m.n * Dm);
+  const double gI = m.ga * enD + m.gb;                 // Eq. A.4
+  const double gp = -m.n * m.ga * enD * dD;            // dg/dkappa
+  const double Lf = L ? 1.0 : 0.0;
+  const double rho = eeq - ebar;
+
+  // ---- coefficients of the gradient-space tangent (all x dV, signs of Eq. 11) ----
+  double lamS, muS, Ams, Ass;
+  double Wt[NS], Dt[NS], Sg[NS];
+  if constexpr (D == 1) {
+    lamS = dV * (m.E * (1.0 - Dm) + m.hs);
+    muS = 0.0;
+    Ams = 0.0;
+    Ass = 0.0;
+    const double Ce = m.E * es[0];
+    Wt[0] = -dV * (Ce * dD * Lf + m.hs);
+    Dt[0] = -m.h * dV;
+    Sg[0] = -dV * ((1.0 - Dm) * Ce + m.hs * rho);
+  } else {
+    const double c2I1 = 2.0 * m.c2 * I1;
+    lamS = dV * (m.lam * (1.0 - Dm) +
+                 m.hs * (dm * dm + rho * (A2 * (2.0 * m.c2 - m.c3 * (1.0 / 3.0)) - Bq * c2I1 * c2I1)));
+    muS = dV * (m.mu * (1.0 - Dm) + m.hs * rho * A2 * m.c3 * 0.5);
+    Ams = dV * m.hs * (dm * ds - rho * Bq * c2I1 * m.c3);
+    Ass = dV * m.hs * (ds * ds - rho * Bq * m.c3 * m.c3);
+    // C eps as a tensor: lam I1 I + 2 mu eps
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+      const bool diag = q < D;
+      const double Ce = (diag ? m.lam * I1 : 0.0) + 2.0 * m.mu * es[q];
+      const double dt = (diag ? dm : 0.0) + ds * S[q];  // tensor form of d
+      Wt[q] = -dV * (Ce * dD * Lf + m.hs * dt);           // Kue (11b)
+      Dt[q] = -m.h * dV * dt;                              // Keu (11c)
+      Sg[q] = -dV * ((1.0 - Dm) * Ce + m.hs * rho * dt);   // Fu  (11e), sigma of Eq. 2
+    }
+  }
+  const double hN = m.h * dV;
+  const double ghc = gI * m.h * m.c * dV;
+  const double fe0 = m.h * dV * rho;
+  double gv[D], fv[D];
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    gv[i] = m.h * m.c * gp * Lf * dV * gb[i];  // Kee gradient term (11d, reading R-kappa')
+    fv[i] = -ghc * gb[i];                      // Fe gradient term (11f, reading R-11f)
+  }
+  scal[0] = muS;
+  scal[1] = ghc;
+
+#pragma unroll
+  for (int a = 0; a < NEN; ++a) {
+    double* r = rec + a * R::STRIDE;
+    double SgN[D], WgN[D], DgN[D], fu[D];
+    symv<D>(S, gN[a], SgN);
+    symv<D>(Wt, gN[a], WgN);
+    symv<D>(Dt, gN[a], DgN);
+    symv<D>(Sg, gN[a], fu);
+    const double Na = shapeN<D>(a, g);
+    double gvd = 0.0, fvd = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      r[R::GN + i] = gN[a][i];
+      r[R::SGN + i] = SgN[i];
+      r[R::T1 + i] = fma(lamS, gN[a][i], Ams * SgN[i]);
+      r[R::T2 + i] = fma(Ams, gN[a][i], Ass * SgN[i]);
+      r[R::WGN + i] = WgN[i];
+      r[R::DGN + i] = DgN[i];
+      r[R::F + i] = fu[i];
+      gvd = fma(gv[i], gN[a][i], gvd);
+      fvd = fma(fv[i], gN[a][i], fvd);
+    }
+    r[R::N] = Na;
+    r[R::E] = fma(hN, Na, gvd);
+    r[R::F + D] = fma(fe0, Na, fvd);
+  }
+  return detJ;
+}
+
+// pair index -> (a, b), a <= b, row-major upper triangle
+template <int NEN> __device__ __forceinline__ void pair_ab(int p, int& a, int& b) {
+  int aa = 0, rem = p;
+  while (rem >= NEN - aa) {
+    rem -= NEN - aa;
+    ++aa;
+  }
+  a = aa;
+  b = aa + rem;
+}
+
+// Phase C accumulators for one node pair (a,b), a <= b.
+template <int D> struct PairAcc {
+  double Kuu[D][D];     // Kuu_ab (Kuu_ba = transpose)
+  double Kue_ab[D], Kue_ba[D], Keu_ab[D], Keu_ba[D];
+  double Kee_ab, Kee_ba;
+  double Fd[D + 1];     // F of node a (diagonal pairs only)
+};
+
+// Gauss sum of one node pair: recs [NGP][NEN][STRIDE], scal [NGP][kScal].
+template <int D>
+__device__ __forceinline__ void phaseC(const double* __restrict__ recs,
+                                       const double* __restrict__ scal, int a, int b,
+                                       PairAcc<D>& acc) {
+  using F = Fam<D>;
+  using R = Rec<D>;
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+#pragma unroll
+    for (int j = 0; j < D; ++j) acc.Kuu[i][j] = 0.0;
+    acc.Kue_ab[i] = acc.Kue_ba[i] = acc.Keu_ab[i] = acc.Keu_ba[i] = 0.0;
+  }
+  acc.Kee_ab = acc.Kee_ba = 0.0;
+#pragma unroll
+  for (int i = 0; i <= D; ++i) acc.Fd[i] = 0.0;
+  const bool diag = a == b;
+#pragma unroll 1
+  for (int g = 0; g < F::NGP; ++g) {
+    const double* A = recs + (g * F::NEN + a) * R::STRIDE;
+    const double* B = recs + (g * F::NEN + b) * R::STRIDE;
+    const double mu = scal[g * kScal + 0];
+    const double ghc = scal[g * kScal + 1];
+    double gA[D], sA[D], gB[D], t1[D], t2[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      gA[i] = A[R::GN + i];
+      sA[i] = A[R::SGN + i];
+      gB[i] = B[R::GN + i];
+      t1[i] = B[R::T1 + i];
+      t2[i] = B[R::T2 + i];
+    }
+    double dot = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) dot = fma(gA[i], gB[i], dot);
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      const double ub = mu * gB[i];
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        double v = acc.Kuu[i][j];
+        v = fma(gA[i], t1[j], v);
+        v = fma(sA[i], t2[j], v);
+        v = fma(gA[j], ub, v);
+        acc.Kuu[i][j] = v;
+      }
+      acc.Kuu[i][i] = fma(mu, dot, acc.Kuu[i][i]);
+    }
+    const double NA = A[R::N], NB = B[R::N];
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      acc.Kue_ab[i] = fma(NB, A[R::WGN + i], acc.Kue_ab[i]);
+      acc.Kue_ba[i] = fma(NA, B[R::WGN + i], acc.Kue_ba[i]);
+      acc.Keu_ab[i] = fma(NA, B[R::DGN + i], acc.Keu_ab[i]);
+      acc.Keu_ba[i] = fma(NB, A[R::DGN + i], acc.Keu_ba[i]);
+    }
+    acc.Kee_ab = fma(NB, A[R::E], fma(ghc, dot, acc.Kee_ab));
+    acc.Kee_ba = fma(NA, B[R::E], fma(ghc, dot, acc.Kee_ba));
+    if (diag) {
+#pragma unroll
+      for (int i = 0; i <= D; ++i) acc.Fd[i] += A[R::F + i];
+    }
+  }
+}
+
+// Element-block entry (row r, col c) setter for an accumulated pair, via callback
+// put(a_local, i, b_local, j, value).
+template <int D, class Put>
+__device__ __forceinline__ void emit_pair(int a, int b, const PairAcc<D>& acc, Put&& put) {
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      put(a, i, b, j, acc.Kuu[i][j]);
+      if (a != b) put(b, j, a, i, acc.Kuu[i][j]);
+    }
+    put(a, i, b, D, acc.Kue_ab[i]);
+    put(a, D, b, i, acc.Keu_ab[i]);
+    if (a != b) {
+      put(b, i, a, D, acc.Kue_ba[i]);
+      put(b, D, a, i, acc.Keu_ba[i]);
+    }
+  }
+  put(a, D, b, D, acc.Kee_ab);
+  if (a != b) put(b, D, a, D, acc.Kee_ba);
+}
+
+}  // namespace lgdm

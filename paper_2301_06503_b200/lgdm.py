@@ -1,0 +1,248 @@
+"""Thin ctypes binding of liblgdm.so (include/lgdm.h) -- argument marshalling only.
+
+Every step of the assembly path runs in the library's CUDA kernels.  There is no CPU
+path: if the compiled library is missing, :func:`load` raises.  PyTorch is used only for
+device memory views (``__cuda_array_interface__``), streams and process groups.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblgdm.so")
+
+BAR2, QUAD4, HEX8 = 1, 2, 3
+# type -> (dim, nen, ndpn, ngp)
+FAMILY = {BAR2: (1, 2, 2, 2), QUAD4: (2, 4, 3, 4), HEX8: (3, 8, 4, 8)}
+KERNEL_AUTO, KERNEL_GENERAL, KERNEL_SWEEP = 0, 1, 2
+
+STATUS = {0: "LGDM_OK", 1: "LGDM_ERR_INVALID_ARGUMENT", 2: "LGDM_ERR_INVERTED_ELEMENT",
+          3: "LGDM_ERR_INVALID_STATE", 4: "LGDM_ERR_OUT_OF_MEMORY", 5: "LGDM_ERR_CUDA",
+          6: "LGDM_ERR_NCCL", 7: "LGDM_ERR_UNSUPPORTED"}
+
+# every symbol include/lgdm.h declares
+EXPORTS = ["lgdm_create_mesh", "lgdm_set_state", "lgdm_assemble", "lgdm_update_history",
+           "lgdm_residual_sumsq", "lgdm_residual_norms", "lgdm_set_comm", "lgdm_nccl_unique_id",
+           "lgdm_get_kappa",
+           "lgdm_scale_dofs", "lgdm_set_kernel", "lgdm_get_info", "lgdm_launch_count",
+           "lgdm_last_error", "lgdm_destroy"]
+
+
+class LGDMError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Material(C.Structure):
+    _fields_ = [("E", C.c_double), ("nu", C.c_double), ("k", C.c_double),
+                ("kappa0", C.c_double), ("alpha", C.c_double), ("beta", C.c_double),
+                ("h", C.c_double), ("h_sigma", C.c_double), ("c", C.c_double),
+                ("R", C.c_double), ("n", C.c_double), ("thickness_or_area", C.c_double),
+                ("eq_variant", C.c_int32), ("reserved", C.c_int32)]
+
+
+class CSR(C.Structure):
+    _fields_ = [("n_rows", C.c_int64), ("n_cols", C.c_int64), ("nnz", C.c_int64),
+                ("first_row", C.c_int64), ("row_ptr", C.c_void_p), ("col_idx", C.c_void_p),
+                ("val", C.c_void_p)]
+
+
+class Info(C.Structure):
+    _fields_ = [("elem_type", C.c_int32), ("dim", C.c_int32), ("nen", C.c_int32),
+                ("ndpn", C.c_int32), ("ngp", C.c_int32), ("structured", C.c_int32),
+                ("n_nodes", C.c_int64), ("n_elems", C.c_int64), ("n_owned_nodes", C.c_int64),
+                ("n_rows", C.c_int64), ("nnz", C.c_int64), ("nx", C.c_int64), ("ny", C.c_int64),
+                ("nz", C.c_int64), ("device_bytes", C.c_int64)]
+
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    """Load liblgdm.so (built by ``__graft_entry__.build()``); raise loudly if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; "
+                          "g.build()'` (there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    vp, dp, i64 = C.c_void_p, C.POINTER(C.c_double), C.c_int64
+    L.lgdm_create_mesh.argtypes = [C.c_int, i64, vp, i64, vp, C.POINTER(Material), i64, i64, i64,
+                                   i64, C.c_int, vp, C.POINTER(vp)]
+    L.lgdm_set_state.argtypes = [vp, vp, i64, vp, i64, C.c_int]
+    L.lgdm_assemble.argtypes = [vp, C.POINTER(CSR), C.POINTER(vp)]
+    L.lgdm_update_history.argtypes = [vp]
+    L.lgdm_residual_sumsq.argtypes = [vp, vp, C.c_int]
+    L.lgdm_residual_norms.argtypes = [vp, dp]
+    L.lgdm_set_comm.argtypes = [vp, C.c_char_p, C.c_int, C.c_int]
+    L.lgdm_nccl_unique_id.argtypes = [vp, i64]
+    L.lgdm_get_kappa.argtypes = [vp, vp]
+    L.lgdm_scale_dofs.argtypes = [vp, C.c_double]
+    L.lgdm_set_kernel.argtypes = [vp, C.c_int]
+    L.lgdm_get_info.argtypes = [vp, C.POINTER(Info)]
+    L.lgdm_launch_count.argtypes = [vp]
+    L.lgdm_launch_count.restype = C.c_int64
+    L.lgdm_last_error.restype = C.c_char_p
+    L.lgdm_destroy.argtypes = [vp]
+    for name in EXPORTS:
+        if name not in ("lgdm_launch_count", "lgdm_last_error", "lgdm_destroy"):
+            getattr(L, name).restype = C.c_int
+    L.lgdm_destroy.restype = None
+    _lib = L
+    return L
+
+
+def _check(status: int):
+    if status != 0:
+        raise LGDMError(status, load().lgdm_last_error().decode())
+
+
+def material(**kw) -> Material:
+    """Material from keyword arguments (``t`` is accepted for ``thickness_or_area``)."""
+    m = Material()
+    for k, v in kw.items():
+        setattr(m, "thickness_or_area" if k == "t" else k, v)
+    return m
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh ncclUniqueId (128 bytes) for lgdm_set_comm; call on rank 0 and broadcast."""
+    buf = C.create_string_buffer(128)
+    _check(load().lgdm_nccl_unique_id(buf, 128))
+    return buf.raw
+
+
+class DeviceArray:
+    """Zero-copy view of mesh-owned device memory (``torch.as_tensor(x, device='cuda')``)."""
+
+    def __init__(self, ptr: int, n: int, typestr: str, owner):
+        self._owner = owner
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": typestr,
+                                         "data": (int(ptr or 0), False), "version": 3,
+                                         "strides": None}
+
+    def torch(self, device=None):
+        import torch
+        return torch.as_tensor(self, device=device or "cuda")
+
+
+def _ptr_and_kind(x):
+    """(pointer, on_device, keepalive) of a float64 contiguous numpy array or torch tensor."""
+    try:
+        import torch
+        if isinstance(x, torch.Tensor):
+            assert x.dtype == torch.float64 and x.is_contiguous(), "need contiguous float64"
+            return x.data_ptr(), 1 if x.is_cuda else 0, x
+    except ImportError:
+        pass
+    a = np.ascontiguousarray(x, dtype=np.float64)
+    return a.ctypes.data, 0, a
+
+
+class Mesh:
+    """One mesh (whole or one rank's slab) on one GPU.  See include/lgdm.h."""
+
+    def __init__(self, etype: int, coords, conn, mat: Material, global_node_offset: int = 0,
+                 n_global_nodes: int | None = None, owned=None, device: int = 0, stream=None):
+        L = load()
+        self.etype = etype
+        self.dim, self.nen, self.ndpn, self.ngp = FAMILY[etype]
+        coords = np.ascontiguousarray(coords, dtype=np.float64)
+        conn = np.ascontiguousarray(conn, dtype=np.int64)
+        self.n_nodes, self.n_elems = coords.shape[0], conn.shape[0]
+        if n_global_nodes is None:
+            n_global_nodes = global_node_offset + self.n_nodes
+        owned = (0, self.n_nodes) if owned is None else owned
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream(device).cuda_stream
+        self.device = device
+        self._h = C.c_void_p()
+        _check(L.lgdm_create_mesh(etype, self.n_nodes, coords.ctypes.data, self.n_elems,
+                                  conn.ctypes.data, C.byref(mat), global_node_offset,
+                                  n_global_nodes, owned[0], owned[1], device, stream,
+                                  C.byref(self._h)))
+        self._keep = []
+
+    # -- state / assembly -------------------------------------------------------------
+    def set_state(self, dofs, kappa=None):
+        pd, on_dev, kd = _ptr_and_kind(dofs)
+        n_d = self.n_nodes * self.ndpn
+        if kappa is None:
+            _check(load().lgdm_set_state(self._h, pd, n_d, None, 0, on_dev))
+            self._keep = [kd]
+            return
+        pk, on_dev_k, kk = _ptr_and_kind(kappa)
+        if on_dev_k != on_dev:
+            raise ValueError("dofs and kappa must both be host or both be device")
+        _check(load().lgdm_set_state(self._h, pd, int(np.prod(getattr(dofs, "shape", (n_d,)))),
+                                     pk, int(np.prod(getattr(kappa, "shape", (0,)))), on_dev))
+        self._keep = [kd, kk]   # host copies are async only for pinned memory; keep alive
+
+    def assemble(self):
+        """Returns (row_ptr, col_idx, val, R, first_row, n_cols) as zero-copy device views."""
+        csr = CSR()
+        r = C.c_void_p()
+        _check(load().lgdm_assemble(self._h, C.byref(csr), C.byref(r)))
+        self.csr = csr
+        return dict(row_ptr=DeviceArray(csr.row_ptr, csr.n_rows + 1, "<i8", self),
+                    col_idx=DeviceArray(csr.col_idx, csr.nnz, "<i4", self),
+                    val=DeviceArray(csr.val, csr.nnz, "<f8", self),
+                    R=DeviceArray(r.value, csr.n_rows, "<f8", self),
+                    first_row=csr.first_row, n_cols=csr.n_cols, n_rows=csr.n_rows, nnz=csr.nnz)
+
+    def update_history(self):
+        _check(load().lgdm_update_history(self._h))
+
+    def residual_sumsq(self, out_device_ptr: int | None = None):
+        """Device-side (stream-ordered) if a device pointer is given, else returns host [2]."""
+        if out_device_ptr is not None:
+            _check(load().lgdm_residual_sumsq(self._h, out_device_ptr, 1))
+            return None
+        out = np.zeros(2)
+        _check(load().lgdm_residual_sumsq(self._h, out.ctypes.data, 0))
+        return out
+
+    def residual_norms(self):
+        out = np.zeros(2)
+        _check(load().lgdm_residual_norms(self._h, out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+    def set_comm(self, unique_id: bytes, nranks: int, rank: int):
+        _check(load().lgdm_set_comm(self._h, unique_id, nranks, rank))
+
+    def get_kappa(self):
+        out = np.zeros((self.n_elems, self.ngp))
+        _check(load().lgdm_get_kappa(self._h, out.ctypes.data))
+        return out
+
+    def scale_dofs(self, s: float):
+        _check(load().lgdm_scale_dofs(self._h, s))
+
+    def set_kernel(self, kernel: int):
+        _check(load().lgdm_set_kernel(self._h, kernel))
+
+    def info(self) -> dict:
+        inf = Info()
+        _check(load().lgdm_get_info(self._h, C.byref(inf)))
+        return {k: getattr(inf, k) for k, _ in Info._fields_}
+
+    @property
+    def launches(self) -> int:
+        return int(load().lgdm_launch_count(self._h))
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            load().lgdm_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

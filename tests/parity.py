@@ -1,0 +1,86 @@
+"""Helpers shared by the GPU parity tests: run the CUDA path through the C ABI, slice the
+oracle's CSR, and compare with the tolerances of north_star / DESIGN.md:
+  * row_ptr, col_idx bit-exact;
+  * K: |dK_ij| <= 1e-12 * max_j |K_ij| (row max of the oracle row);
+  * R: |dR_i| <= 1e-12 * S_i, S_i = sum over elements and GPs of |contribution| (reading R-TOL).
+"""
+import numpy as np
+
+import oracle
+import synth
+from paper_2301_06503_b200 import lgdm
+
+KTOL = 1e-12
+RTOL = 1e-12
+
+
+def gpu_assemble(etype, coords, conn, dofs, kappa, mat_kw=None, kernel=lgdm.KERNEL_AUTO,
+                 offset=0, n_global=None, owned=None):
+    import torch
+    mat = lgdm.material(**(mat_kw or synth.MATERIAL))
+    m = lgdm.Mesh(etype, coords, conn, mat, global_node_offset=offset, n_global_nodes=n_global,
+                  owned=owned)
+    m.set_kernel(kernel)
+    m.set_state(dofs, kappa)
+    out = m.assemble()
+    torch.cuda.synchronize()
+    res = dict(row_ptr=out["row_ptr"].torch().cpu().numpy(),
+               col_idx=out["col_idx"].torch().cpu().numpy(),
+               val=out["val"].torch().cpu().numpy(), R=out["R"].torch().cpu().numpy(),
+               first_row=out["first_row"], info=m.info(), mesh=m)
+    return res
+
+
+def oracle_assemble(etype, coords, conn, dofs, kappa, mat_kw=None):
+    return oracle.assemble(etype, oracle.material(**(mat_kw or synth.MATERIAL)), coords, conn,
+                           dofs, kappa)
+
+
+def slice_rows(ref, r0, r1):
+    rp = ref["row_ptr"]
+    lo, hi = rp[r0], rp[r1]
+    return dict(row_ptr=rp[r0:r1 + 1] - lo, col_idx=ref["col_idx"][lo:hi], val=ref["val"][lo:hi],
+                R=ref["R"][r0:r1], S=ref["S"][r0:r1])
+
+
+def compare(ref, got, what=""):
+    """Assert parity; returns (max K error / rowmax, max R error / S)."""
+    assert np.array_equal(got["row_ptr"], ref["row_ptr"]), f"{what}: row_ptr differs"
+    assert np.array_equal(got["col_idx"], ref["col_idx"]), f"{what}: col_idx differs"
+    rp = ref["row_ptr"]
+    nrows = rp.size - 1
+    rows = np.repeat(np.arange(nrows), np.diff(rp))
+    absv = np.abs(ref["val"])
+    rowmax = np.zeros(nrows)
+    np.maximum.at(rowmax, rows, absv)
+    dk = np.abs(got["val"] - ref["val"])
+    kerr = dk / np.maximum(rowmax[rows], 1e-300)
+    assert np.all(dk <= KTOL * rowmax[rows]), (
+        f"{what}: K mismatch, worst {kerr.max():.3e} at entry {kerr.argmax()}")
+    dr = np.abs(got["R"] - ref["R"])
+    rerr = dr / np.maximum(ref["S"], 1e-300)
+    assert np.all(dr <= RTOL * ref["S"] + 1e-300), (
+        f"{what}: R mismatch, worst {rerr.max():.3e} at row {rerr.argmax()}")
+    return float(kerr.max(initial=0.0)), float(rerr.max(initial=0.0))
+
+
+def compare_sampled(ref_rows, got, sel_nodes, ndpn, owned_begin=0):
+    """Parity on sampled node block-rows: ref_rows from oracle.assemble_rows."""
+    rp = got["row_ptr"]
+    worst_k = worst_r = 0.0
+    for s, a in enumerate(sel_nodes):
+        for i in range(ndpn):
+            r = ndpn * (a - owned_begin) + i
+            lo, hi = rp[r], rp[r + 1]
+            plo, phi = ref_rows["row_ptr"][s * ndpn + i], ref_rows["row_ptr"][s * ndpn + i + 1]
+            assert np.array_equal(got["col_idx"][lo:hi], ref_rows["col_idx"][plo:phi]), (a, i)
+            rv = ref_rows["val"][plo:phi]
+            rmax = np.abs(rv).max()
+            dk = np.abs(got["val"][lo:hi] - rv)
+            assert np.all(dk <= KTOL * rmax), (a, i, (dk / rmax).max())
+            worst_k = max(worst_k, float((dk / rmax).max()))
+            dr = abs(got["R"][r] - ref_rows["R"][s * ndpn + i])
+            S = ref_rows["S"][s * ndpn + i]
+            assert dr <= RTOL * S + 1e-300, (a, i, dr / S)
+            worst_r = max(worst_r, dr / S)
+    return worst_k, worst_r

@@ -1,0 +1,179 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded
+inputs.  Pattern bit-exact; K within 1e-12 of the row max; R within 1e-12 of S (R-TOL)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from paper_2301_06503_b200 import lgdm
+
+from parity import compare, compare_sampled, gpu_assemble, oracle_assemble, slice_rows
+
+pytestmark = pytest.mark.gpu
+
+KERNELS = [lgdm.KERNEL_GENERAL, lgdm.KERNEL_AUTO]
+
+CASES = [
+    (lgdm.BAR2, (1,)), (lgdm.BAR2, (7,)), (lgdm.BAR2, (100,)),
+    (lgdm.QUAD4, (1, 1)), (lgdm.QUAD4, (3, 5)), (lgdm.QUAD4, (37, 29)), (lgdm.QUAD4, (1, 40)),
+    (lgdm.QUAD4, (65, 3)),
+    (lgdm.HEX8, (1, 1, 1)), (lgdm.HEX8, (3, 4, 5)), (lgdm.HEX8, (17, 9, 11)), (lgdm.HEX8, (1, 1, 9)),
+    (lgdm.HEX8, (9, 6, 2)),
+]
+
+
+def _case(etype, n, distort=0.0):
+    cfg = synth.small_config(etype, n)
+    mesh = synth.structured_mesh(cfg)
+    coords = synth.distort(mesh, distort) if (distort and etype != lgdm.BAR2) else mesh.coords
+    dofs, kappa = synth.fields(cfg, mesh)
+    return cfg, mesh, coords, dofs, kappa
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("etype,n", CASES)
+def test_parity_small(etype, n, kernel):
+    cfg, mesh, coords, dofs, kappa = _case(etype, n, distort=0.2)
+    ref = oracle_assemble(etype, coords, mesh.conn, dofs, kappa)
+    assert ref["n_guard"] == 0
+    got = gpu_assemble(etype, coords, mesh.conn, dofs, kappa, kernel=kernel)
+    compare(ref, got, f"{etype}{n} kernel={kernel}")
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("variant", [dict(h_sigma=0.0), dict(eq_variant=1), dict(h_sigma=7e3, c=0.5, k=3.0, nu=0.3)])
+@pytest.mark.parametrize("etype,n", [(lgdm.QUAD4, (11, 8)), (lgdm.HEX8, (5, 4, 3)), (lgdm.BAR2, (9,))])
+def test_parity_readings(etype, n, variant, kernel):
+    cfg, mesh, coords, dofs, kappa = _case(etype, n, distort=0.15)
+    kw = dict(synth.MATERIAL)
+    kw.update(variant)
+    ref = oracle_assemble(etype, coords, mesh.conn, dofs, kappa, kw)
+    got = gpu_assemble(etype, coords, mesh.conn, dofs, kappa, kw, kernel=kernel)
+    compare(ref, got, f"{etype}{n} {variant}")
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_parity_config0_and_1(kernel):
+    for cid in (0, 1):
+        cfg = synth.CONFIGS[cid]
+        mesh = synth.structured_mesh(cfg)
+        dofs, kappa = synth.fields(cfg, mesh)
+        ref = oracle_assemble(cfg.etype, mesh.coords, mesh.conn, dofs, kappa)
+        got = gpu_assemble(cfg.etype, mesh.coords, mesh.conn, dofs, kappa, kernel=kernel)
+        kerr, rerr = compare(ref, got, f"config {cid}")
+        print(f"config {cid} kernel {kernel}: max K err/rowmax {kerr:.2e}, max R err/S {rerr:.2e}")
+
+
+def test_parity_damage_edge_states():
+    """All-unloading (kappa_hist = big), all at kappa0 (D = 0), zero field (sqrt guard)."""
+    for etype, n in ((lgdm.QUAD4, (6, 5)), (lgdm.HEX8, (3, 3, 2))):
+        cfg, mesh, coords, dofs, kappa = _case(etype, n, distort=0.1)
+        for dd, kk in ((dofs, np.full_like(kappa, 5e-3)),
+                       (dofs * 0.0, np.full_like(kappa, 1e-4)),
+                       (dofs * 1e-3, np.full_like(kappa, 1e-4))):
+            ref = oracle_assemble(etype, coords, mesh.conn, dd, kk)
+            for kernel in KERNELS:
+                got = gpu_assemble(etype, coords, mesh.conn, dd, kk, kernel=kernel)
+                compare(ref, got, "edge state")
+
+
+@pytest.mark.parametrize("cid", [2, 3])
+def test_parity_full_size_sampled(cid):
+    """BASELINE configs 2 and 3 at full size, in the bench's launch configuration; sampled
+    node block-rows against the oracle, pattern checked by the closed-form nnz."""
+    cfg = synth.CONFIGS[cid]
+    mesh = synth.structured_mesh(cfg)
+    dofs, kappa = synth.fields(cfg, mesh)
+    got = gpu_assemble(cfg.etype, mesh.coords, mesh.conn, dofs, kappa)
+    ndpn = lgdm.FAMILY[cfg.etype][2]
+    assert got["row_ptr"][-1] == ndpn * ndpn * int(np.prod([3 * k + 1 for k in cfg.n]))
+    sel = synth.sample_nodes(mesh.coords.shape[0], 1500, seed=cid)
+    sel = np.unique(np.concatenate([sel, [0, mesh.coords.shape[0] - 1]]))
+    ref = oracle.assemble_rows(cfg.etype, oracle.material(**synth.MATERIAL), mesh.coords,
+                               mesh.conn, dofs, kappa, sel)
+    wk, wr = compare_sampled(ref, got, sel, ndpn)
+    print(f"config {cid}: sampled {sel.size} nodes, max K err {wk:.2e}, R err {wr:.2e}")
+
+
+@pytest.mark.parametrize("etype,n,P", [(lgdm.QUAD4, (23, 31), 3), (lgdm.HEX8, (7, 5, 13), 4),
+                                       (lgdm.BAR2, (50,), 2)])
+def test_slabs_stitch_bitwise(etype, n, P):
+    """Row-owned slabs with ghost-element recompute: stitched CSR == one-mesh CSR, bitwise."""
+    from paper_2301_06503_b200 import slabs
+    cfg, mesh, coords, dofs, kappa = _case(etype, n)
+    whole = gpu_assemble(etype, mesh.coords, mesh.conn, dofs, kappa)
+    rows_rp = whole["row_ptr"]
+    ndpn = lgdm.FAMILY[etype][2]
+    for p in range(P):
+        part = slabs.slab(cfg.n, p, P)
+        sm = synth.structured_mesh(cfg, elem_layers=part.elem_layers)
+        sd, sk = synth.fields(cfg, sm)
+        got = gpu_assemble(etype, sm.coords, sm.conn, sd, sk, offset=sm.node_gid0,
+                           n_global=cfg.n_nodes, owned=part.owned_local(sm.node_gid0))
+        r0 = ndpn * part.owned_nodes[0]
+        r1 = ndpn * part.owned_nodes[1]
+        assert got["first_row"] == r0
+        lo, hi = rows_rp[r0], rows_rp[r1]
+        np.testing.assert_array_equal(got["row_ptr"], rows_rp[r0:r1 + 1] - lo)
+        np.testing.assert_array_equal(got["col_idx"], whole["col_idx"][lo:hi])
+        np.testing.assert_array_equal(got["val"], whole["val"][lo:hi])
+        np.testing.assert_array_equal(got["R"], whole["R"][r0:r1])
+
+
+def test_update_history_parity():
+    for etype, n in ((lgdm.QUAD4, (30, 20)), (lgdm.HEX8, (6, 5, 4)), (lgdm.BAR2, (40,))):
+        cfg, mesh, coords, dofs, kappa = _case(etype, n)
+        m = lgdm.Mesh(etype, mesh.coords, mesh.conn, lgdm.material(**synth.MATERIAL))
+        m.set_state(dofs, kappa)
+        m.update_history()
+        got = m.get_kappa()
+        ref = oracle.update_history(etype, mesh.conn, dofs, kappa)
+        unloading = ref == kappa
+        np.testing.assert_array_equal(got[unloading], kappa[unloading])
+        np.testing.assert_allclose(got[~unloading], ref[~unloading], rtol=1e-14, atol=0)
+        assert 0 < (~unloading).sum() < kappa.size
+        m.update_history()          # idempotent
+        np.testing.assert_array_equal(m.get_kappa(), got)
+
+
+def test_residual_norms():
+    cfg, mesh, coords, dofs, kappa = _case(lgdm.QUAD4, (25, 19))
+    ref = oracle_assemble(lgdm.QUAD4, coords, mesh.conn, dofs, kappa)
+    expect = oracle.residual_norms(lgdm.QUAD4, ref["R"])
+    m = lgdm.Mesh(lgdm.QUAD4, coords, mesh.conn, lgdm.material(**synth.MATERIAL))
+    m.set_state(dofs, kappa)
+    m.assemble()
+    np.testing.assert_allclose(m.residual_norms(), expect, rtol=1e-10)
+    ss = m.residual_sumsq()
+    np.testing.assert_allclose(np.sqrt(ss), expect, rtol=1e-10)
+
+
+def test_determinism_and_device_state():
+    import torch
+    cfg, mesh, coords, dofs, kappa = _case(lgdm.HEX8, (6, 7, 5))
+    m = lgdm.Mesh(lgdm.HEX8, coords, mesh.conn, lgdm.material(**synth.MATERIAL))
+    m.set_state(dofs, kappa)
+    a = m.assemble()
+    v1 = a["val"].torch().clone()
+    r1 = a["R"].torch().clone()
+    m.set_state(torch.as_tensor(dofs, device="cuda"), torch.as_tensor(kappa, device="cuda"))
+    a = m.assemble()
+    assert torch.equal(a["val"].torch(), v1) and torch.equal(a["R"].torch(), r1)
+
+
+def test_errors():
+    cfg, mesh, coords, dofs, kappa = _case(lgdm.QUAD4, (4, 4))
+    mat = lgdm.material(**synth.MATERIAL)
+    m = lgdm.Mesh(lgdm.QUAD4, coords, mesh.conn, mat)
+    with pytest.raises(lgdm.LGDMError) as ei:
+        m.assemble()
+    assert ei.value.status == 3
+    with pytest.raises(lgdm.LGDMError) as ei:
+        m.set_state(dofs[:-1], kappa)
+    assert ei.value.status == 3
+    bad = coords.copy()
+    c = mesh.conn[5]
+    bad[c[0]], bad[c[2]] = coords[c[2]].copy(), coords[c[0]].copy()   # fold element 5
+    with pytest.raises(lgdm.LGDMError) as ei:
+        lgdm.Mesh(lgdm.QUAD4, bad, mesh.conn, mat)
+    assert ei.value.status == 2 and "element" in str(ei.value)
