@@ -49,34 +49,47 @@ def algorithmic_bytes(ndpn, dim, nen, ngp, nnz, n_rows, n_nodes, n_elems):
 
 
 class Clocks:
-    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+    """nvidia-smi sampler (B200_PROFILING.md clocks line).  Started before the warm-up so that
+    it is sampling when the timed region begins; summary() keeps the samples taken inside
+    [mark_start, mark_end]."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, device: int):
         self.device = device
         self.rows = []
         self.proc = None
+        self.t0 = self.t1 = None
 
-    def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
+    def start(self):
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.th = threading.Thread(target=self._read, daemon=True)
             self.th.start()
+            time.sleep(0.3)
         except Exception:
             self.proc = None
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append((time.time(), [x.strip() for x in line.split(",")]))
 
-    def __exit__(self, *a):
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+
+    def stop(self):
         if self.proc:
+            time.sleep(0.05)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -84,16 +97,25 @@ class Clocks:
                 self.proc.kill()
 
     def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        inside = [r for t, r in self.rows if self.t0 and self.t1 and self.t0 <= t <= self.t1 + 0.05]
+        where = "timed region"
+        if not inside:   # region shorter than the sampling period: nearest samples after warm-up
+            inside = [r for t, r in self.rows if self.t0 and t >= self.t0 - 0.5][:3]
+            where = "nearest to timed region"
+        if not inside:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [v for v in (num(r[0]) for r in inside) if v is not None]
+        mx = [v for v in (num(r[1]) for r in inside) if v is not None]
+        reasons = sorted({self.NAMES[i] for r in inside for i in range(4)
                           if len(r) > 3 + i and r[3 + i].lower() == "active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+                "samples": len(inside), "window": where}
 
 
 def dist_env():
@@ -151,6 +173,7 @@ def run_lgdm(cfg, steps, warmup, rank, world, local, pg_barrier, allmax, comm_ui
         m.scale_dofs(1.05 if t % 2 == 0 else 1.0 / 1.05)
         return norms
 
+    clk = Clocks(local).start()
     for t in range(warmup):
         step(t)
     torch.cuda.synchronize()
@@ -159,13 +182,15 @@ def run_lgdm(cfg, steps, warmup, rank, world, local, pg_barrier, allmax, comm_ui
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(local) as clk:
-        torch.cuda.synchronize()
-        start.record(stream)
-        for t in range(steps):
-            step(t, evs[t])
-        end.record(stream)
-        torch.cuda.synchronize()
+    torch.cuda.synchronize()
+    clk.mark_start()
+    start.record(stream)
+    for t in range(steps):
+        step(t, evs[t])
+    end.record(stream)
+    torch.cuda.synchronize()
+    clk.mark_end()
+    clk.stop()
     launches = m.launches - l0
     pg_barrier()
     ms_total = allmax(start.elapsed_time(end))
@@ -316,7 +341,8 @@ def main():
                    "parallelism": f"z-slabs x{ws}, ghost-element recompute",
                    "step": "assemble + residual_norms(allreduce) + update_history + dofs scale",
                    "l2": "inputs >> 126 MB L2 (no flush needed)",
-                   "kernel": "sweep" if r["info"]["structured"] and args.kernel != 1 else "general"},
+                   "kernel": ("k_sweep (fused structured sweep)" if r["info"]["structured"] and
+                              args.kernel != 1 else "k_elem_blocks + k_gather (general)")},
         "assemble_ms": r["assemble_ms"],
         "assemble_elements_per_s": n_total / (r["assemble_ms"] * 1e-3) if ws == 1 else None,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

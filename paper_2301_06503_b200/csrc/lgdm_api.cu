@@ -127,8 +127,6 @@ struct lgdm_mesh_s {
   void* sweep = nullptr;  // sweep-path state (lgdm_sweep.cuh)
 };
 
-#include "lgdm_sweep.cuh"
-
 namespace {
 
 template <class T> lgdm_status upload(lgdm_mesh m, T** dst, const T* src, size_t count) {
@@ -258,6 +256,8 @@ template <int D> void launch_detj(lgdm_mesh m, unsigned long long* bad) {
 }
 
 }  // namespace
+
+#include "lgdm_sweep.cuh"
 
 extern "C" {
 
@@ -482,14 +482,13 @@ namespace {
 
 template <int D> lgdm_status assemble_general(lgdm_mesh m) {
   using F = Fam<D>;
-  using Rc = Rec<D>;
   constexpr int EPB = D == 3 ? 8 : (D == 2 ? 32 : 64);
   if (!m->scratchK) {
     CU(dalloc(&m->scratchK, size_t(m->n_elems) * F::NDOFE * F::NDOFE));
     CU(dalloc(&m->scratchF, size_t(m->n_elems) * F::NDOFE));
     m->device_bytes += m->n_elems * (F::NDOFE * F::NDOFE + F::NDOFE) * 8;
   }
-  const size_t smem = sizeof(double) * (size_t(EPB) * F::NGP * F::NEN * Rc::STRIDE +
+  const size_t smem = sizeof(double) * (size_t(EPB) * F::NGP * GpBlock<D>::STRIDE +
                                         EPB * F::NGP * kScal + EPB * F::NEN * D + EPB * F::NEN * F::NDPN);
   static bool attr = false;
   if (!attr) {

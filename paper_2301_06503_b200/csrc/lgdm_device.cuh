@@ -57,6 +57,12 @@ template <int D> struct Rec {
 };
 // per (element, GP) scalars used by phase C: mu*, ghc
 constexpr int kScal = 2;
+// doubles per (element, GP) record block: NEN records + 1 pad so that consecutive (e,g)
+// blocks start in different bank pairs (odd stride in doubles)
+template <int D> struct GpBlock {
+  static constexpr int N = Fam<D>::NEN * Rec<D>::STRIDE;
+  static constexpr int STRIDE = (N % 2 == 1) ? N : N + 1;
+};
 
 // reference node sign r_ak (SURVEY 8c.1 node order) and Gauss point sign s_gk (xi fastest)
 template <int D> __device__ __forceinline__ int node_sign(int a, int k) {
@@ -155,8 +161,16 @@ __device__ double phaseA(const DevMat& m, const double* __restrict__ X,
   }
   const double dV = detJ * m.t;  // Gauss weights are 1
 
-  // grad N_a = J^-T dN/dxi ; kinematics
-  double gN[NEN][D];
+  // grad N_a = J^-T dN/dxi (recomputed where needed instead of kept live); kinematics
+  auto gradN = [&](int a, double* gn) {
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) s = fma(Ji[j][i], shape_dxi<D>(a, g, j), s);
+      gn[i] = s;
+    }
+  };
   double eps[D][D], ebar = 0.0, gb[D];
 #pragma unroll
   for (int i = 0; i < D; ++i) {
@@ -166,23 +180,15 @@ __device__ double phaseA(const DevMat& m, const double* __restrict__ X,
   }
 #pragma unroll
   for (int a = 0; a < NEN; ++a) {
-    double dxi[D];
-#pragma unroll
-    for (int j = 0; j < D; ++j) dxi[j] = shape_dxi<D>(a, g, j);
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-      double s = 0.0;
-#pragma unroll
-      for (int j = 0; j < D; ++j) s = fma(Ji[j][i], dxi[j], s);
-      gN[a][i] = s;
-    }
+    double gn[D];
+    gradN(a, gn);
     const double ea = U[a * NDPN + D];
     ebar = fma(shapeN<D>(a, g), ea, ebar);
 #pragma unroll
     for (int i = 0; i < D; ++i) {
-      gb[i] = fma(gN[a][i], ea, gb[i]);
+      gb[i] = fma(gn[i], ea, gb[i]);
 #pragma unroll
-      for (int j = 0; j < D; ++j) eps[i][j] = fma(U[a * NDPN + i], gN[a][j], eps[i][j]);
+      for (int j = 0; j < D; ++j) eps[i][j] = fma(U[a * NDPN + i], gn[j], eps[i][j]);
     }
   }
   // symmetrise: eps_ij = (du_i/dx_j + du_j/dx_i)/2
@@ -307,24 +313,25 @@ __device__ double phaseA(const DevMat& m, const double* __restrict__ X,
 #pragma unroll
   for (int a = 0; a < NEN; ++a) {
     double* r = rec + a * R::STRIDE;
-    double SgN[D], WgN[D], DgN[D], fu[D];
-    symv<D>(S, gN[a], SgN);
-    symv<D>(Wt, gN[a], WgN);
-    symv<D>(Dt, gN[a], DgN);
-    symv<D>(Sg, gN[a], fu);
+    double gn[D], SgN[D], WgN[D], DgN[D], fu[D];
+    gradN(a, gn);
+    symv<D>(S, gn, SgN);
+    symv<D>(Wt, gn, WgN);
+    symv<D>(Dt, gn, DgN);
+    symv<D>(Sg, gn, fu);
     const double Na = shapeN<D>(a, g);
     double gvd = 0.0, fvd = 0.0;
 #pragma unroll
     for (int i = 0; i < D; ++i) {
-      r[R::GN + i] = gN[a][i];
+      r[R::GN + i] = gn[i];
       r[R::SGN + i] = SgN[i];
-      r[R::T1 + i] = fma(lamS, gN[a][i], Ams * SgN[i]);
-      r[R::T2 + i] = fma(Ams, gN[a][i], Ass * SgN[i]);
+      r[R::T1 + i] = fma(lamS, gn[i], Ams * SgN[i]);
+      r[R::T2 + i] = fma(Ams, gn[i], Ass * SgN[i]);
       r[R::WGN + i] = WgN[i];
       r[R::DGN + i] = DgN[i];
       r[R::F + i] = fu[i];
-      gvd = fma(gv[i], gN[a][i], gvd);
-      fvd = fma(fv[i], gN[a][i], fvd);
+      gvd = fma(gv[i], gn[i], gvd);
+      fvd = fma(fv[i], gn[i], fvd);
     }
     r[R::N] = Na;
     r[R::E] = fma(hN, Na, gvd);
@@ -352,7 +359,7 @@ template <int D> struct PairAcc {
   double Fd[D + 1];     // F of node a (diagonal pairs only)
 };
 
-// Gauss sum of one node pair: recs [NGP][NEN][STRIDE], scal [NGP][kScal].
+// Gauss sum of one node pair: recs [NGP][GpBlock::STRIDE], scal [NGP][kScal].
 template <int D>
 __device__ __forceinline__ void phaseC(const double* __restrict__ recs,
                                        const double* __restrict__ scal, int a, int b,
@@ -371,8 +378,8 @@ __device__ __forceinline__ void phaseC(const double* __restrict__ recs,
   const bool diag = a == b;
 #pragma unroll 1
   for (int g = 0; g < F::NGP; ++g) {
-    const double* A = recs + (g * F::NEN + a) * R::STRIDE;
-    const double* B = recs + (g * F::NEN + b) * R::STRIDE;
+    const double* A = recs + g * GpBlock<D>::STRIDE + a * R::STRIDE;
+    const double* B = recs + g * GpBlock<D>::STRIDE + b * R::STRIDE;
     const double mu = scal[g * kScal + 0];
     const double ghc = scal[g * kScal + 1];
     double gA[D], sA[D], gB[D], t1[D], t2[D];

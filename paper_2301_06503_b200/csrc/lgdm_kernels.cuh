@@ -67,7 +67,7 @@ __global__ void k_cols(int64_t n_owned, const int64_t* __restrict__ nbr_ptr,
 
 // ----------------------------------------------------------------------------------------
 // GENERAL path step 1.  One CTA = batches of EPB elements (grid-stride).
-// Shared memory: recs [EPB][NGP][NEN][STRIDE] | scal [EPB][NGP][kScal] | X [EPB][NEN][D] |
+// Shared memory: recs [EPB][NGP][GpBlock::STRIDE] | scal [EPB][NGP][kScal] | X [EPB][NEN][D] |
 // U [EPB][NEN][NDPN].  Threads: EPB * NPAIR.
 template <int D, int EPB>
 __global__ void __launch_bounds__(EPB * Fam<D>::NPAIR)
@@ -80,7 +80,7 @@ k_elem_blocks(DevMat m, int64_t ne, const int32_t* __restrict__ conn,
   constexpr int NT = EPB * F::NPAIR;
   extern __shared__ double sm[];
   double* recs = sm;
-  double* scal = recs + EPB * F::NGP * F::NEN * R::STRIDE;
+  double* scal = recs + EPB * F::NGP * GpBlock<D>::STRIDE;
   double* Xs = scal + EPB * F::NGP * kScal;
   double* Us = Xs + EPB * F::NEN * D;
   const int tid = threadIdx.x;
@@ -102,7 +102,7 @@ k_elem_blocks(DevMat m, int64_t ne, const int32_t* __restrict__ conn,
       const int64_t e = e0 + el;
       if (e < ne)
         phaseA<D>(m, Xs + el * F::NEN * D, Us + el * F::NEN * F::NDPN, kappa[e * F::NGP + g], g,
-                  recs + size_t(t) * F::NEN * R::STRIDE, scal + t * kScal);
+                  recs + size_t(t) * GpBlock<D>::STRIDE, scal + t * kScal);
     }
     __syncthreads();
     {
@@ -112,7 +112,7 @@ k_elem_blocks(DevMat m, int64_t ne, const int32_t* __restrict__ conn,
         int a, b;
         pair_ab<F::NEN>(p, a, b);
         PairAcc<D> acc;
-        phaseC<D>(recs + size_t(el) * F::NGP * F::NEN * R::STRIDE, scal + el * F::NGP * kScal, a,
+        phaseC<D>(recs + size_t(el) * F::NGP * GpBlock<D>::STRIDE, scal + el * F::NGP * kScal, a,
                   b, acc);
         double* Ke = Ke_out + e * (F::NDOFE * F::NDOFE);
         emit_pair<D>(a, b, acc, [&](int ra, int ri, int cb, int cj, double v) {
