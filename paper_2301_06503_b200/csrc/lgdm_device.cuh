@@ -105,15 +105,28 @@ template <int D> __device__ __forceinline__ void symv(const double* T, const dou
   }
 }
 
+// Compact per-(element, GP) state produced by the core of phase A (offsets in doubles):
+//   JI[D*D]  J^-1 (row j, col i = Ji[j][i])     S, WT, DT, SG [NS]  S, W', Dt', Sigma'
+//   LAM, AMS, ASS, HN, FE0, MU, GHC               GV[D], FV[D]
+template <int D> struct Core {
+  static constexpr int NS = Fam<D>::NS;
+  static constexpr int JI = 0, S = D * D, WT = S + NS, DT = WT + NS, SG = DT + NS,
+                       LAM = SG + NS, AMS = LAM + 1, ASS = AMS + 1, HN = ASS + 1, FE0 = HN + 1,
+                       MU = FE0 + 1, GHC = MU + 1, GV = GHC + 1, FV = GV + D;
+  static constexpr int USED = FV + D;
+  static constexpr int STRIDE = (USED % 2 == 1) ? USED : USED + 1;
+};
+
 // ---------------------------------------------------------------------------------------
-// Phase A: one Gauss point g of one element.  X [NEN][D] coords, U [NEN][NDPN] dofs,
-// kh = kappa_hist.  Writes NEN records at rec + a*STRIDE and 2 scalars at scal.
+// Phase A, part 1 ("core"): one Gauss point g of one element.  X [NEN][D] coords,
+// U [NEN][NDPN] dofs, kh = kappa_hist.  Writes the compact GP state (Core<D> layout) to core.
 // Returns det J (caller treats <= 0 as an inverted element).
 // ---------------------------------------------------------------------------------------
 template <int D>
-__device__ double phaseA(const DevMat& m, const double* __restrict__ X,
-                         const double* __restrict__ U, double kh, int g,
-                         double* __restrict__ rec, double* __restrict__ scal) {
+__device__ __forceinline__ double gpCore(const DevMat& m, const double* __restrict__ X,
+                                         const double* __restrict__ U, double kh, int g,
+                                         double* __restrict__ core) {
+  using Co = Core<D>;
   using F = Fam<D>;
   using R = Rec<D>;
   constexpr int NEN = F::NEN, NDPN = F::NDPN, NS = F::NS;
@@ -307,36 +320,82 @@ __device__ double phaseA(const DevMat& m, const double* __restrict__ X,
     gv[i] = m.h * m.c * gp * Lf * dV * gb[i];  // Kee gradient term (11d, reading R-kappa')
     fv[i] = -ghc * gb[i];                      // Fe gradient term (11f, reading R-11f)
   }
-  scal[0] = muS;
-  scal[1] = ghc;
-
 #pragma unroll
-  for (int a = 0; a < NEN; ++a) {
-    double* r = rec + a * R::STRIDE;
-    double gn[D], SgN[D], WgN[D], DgN[D], fu[D];
-    gradN(a, gn);
-    symv<D>(S, gn, SgN);
-    symv<D>(Wt, gn, WgN);
-    symv<D>(Dt, gn, DgN);
-    symv<D>(Sg, gn, fu);
-    const double Na = shapeN<D>(a, g);
-    double gvd = 0.0, fvd = 0.0;
+  for (int j = 0; j < D; ++j)
 #pragma unroll
-    for (int i = 0; i < D; ++i) {
-      r[R::GN + i] = gn[i];
-      r[R::SGN + i] = SgN[i];
-      r[R::T1 + i] = fma(lamS, gn[i], Ams * SgN[i]);
-      r[R::T2 + i] = fma(Ams, gn[i], Ass * SgN[i]);
-      r[R::WGN + i] = WgN[i];
-      r[R::DGN + i] = DgN[i];
-      r[R::F + i] = fu[i];
-      gvd = fma(gv[i], gn[i], gvd);
-      fvd = fma(fv[i], gn[i], fvd);
-    }
-    r[R::N] = Na;
-    r[R::E] = fma(hN, Na, gvd);
-    r[R::F + D] = fma(fe0, Na, fvd);
+    for (int i = 0; i < D; ++i) core[Co::JI + j * D + i] = Ji[j][i];
+#pragma unroll
+  for (int q = 0; q < NS; ++q) {
+    core[Co::S + q] = S[q];
+    core[Co::WT + q] = Wt[q];
+    core[Co::DT + q] = Dt[q];
+    core[Co::SG + q] = Sg[q];
   }
+  core[Co::LAM] = lamS;
+  core[Co::AMS] = Ams;
+  core[Co::ASS] = Ass;
+  core[Co::HN] = hN;
+  core[Co::FE0] = fe0;
+  core[Co::MU] = muS;
+  core[Co::GHC] = ghc;
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    core[Co::GV + i] = gv[i];
+    core[Co::FV + i] = fv[i];
+  }
+  return detJ;
+}
+
+
+// Phase A, part 2 ("expansion"): the record of node a at GP g from the compact state.
+template <int D>
+__device__ __forceinline__ void gpExpand(const double* __restrict__ core, int a, int g,
+                                         double* __restrict__ r) {
+  using Co = Core<D>;
+  using R = Rec<D>;
+  double gn[D], SgN[D], WgN[D], DgN[D], fu[D];
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) s = fma(core[Co::JI + j * D + i], shape_dxi<D>(a, g, j), s);
+    gn[i] = s;
+  }
+  symv<D>(core + Co::S, gn, SgN);
+  symv<D>(core + Co::WT, gn, WgN);
+  symv<D>(core + Co::DT, gn, DgN);
+  symv<D>(core + Co::SG, gn, fu);
+  const double Na = shapeN<D>(a, g);
+  const double lamS = core[Co::LAM], Ams = core[Co::AMS], Ass = core[Co::ASS];
+  double gvd = 0.0, fvd = 0.0;
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    r[R::GN + i] = gn[i];
+    r[R::SGN + i] = SgN[i];
+    r[R::T1 + i] = fma(lamS, gn[i], Ams * SgN[i]);
+    r[R::T2 + i] = fma(Ams, gn[i], Ass * SgN[i]);
+    r[R::WGN + i] = WgN[i];
+    r[R::DGN + i] = DgN[i];
+    r[R::F + i] = fu[i];
+    gvd = fma(core[Co::GV + i], gn[i], gvd);
+    fvd = fma(core[Co::FV + i], gn[i], fvd);
+  }
+  r[R::N] = Na;
+  r[R::E] = fma(core[Co::HN], Na, gvd);
+  r[R::F + D] = fma(core[Co::FE0], Na, fvd);
+}
+
+// Phase A for one GP, all nodes (general path): core into registers, then expansions.
+template <int D>
+__device__ __forceinline__ double phaseA(const DevMat& m, const double* __restrict__ X,
+                                         const double* __restrict__ U, double kh, int g,
+                                         double* __restrict__ rec, double* __restrict__ scal) {
+  double core[Core<D>::STRIDE];
+  const double detJ = gpCore<D>(m, X, U, kh, g, core);
+#pragma unroll
+  for (int a = 0; a < Fam<D>::NEN; ++a) gpExpand<D>(core, a, g, rec + a * Rec<D>::STRIDE);
+  scal[0] = core[Core<D>::MU];
+  scal[1] = core[Core<D>::GHC];
   return detJ;
 }
 
@@ -360,7 +419,7 @@ template <int D> struct PairAcc {
 };
 
 // Gauss sum of one node pair: recs [NGP][GpBlock::STRIDE], scal [NGP][kScal].
-template <int D>
+template <int D, int SCAL_STRIDE = kScal, int MU_OFF = 0, int GHC_OFF = 1>
 __device__ __forceinline__ void phaseC(const double* __restrict__ recs,
                                        const double* __restrict__ scal, int a, int b,
                                        PairAcc<D>& acc) {
@@ -380,8 +439,8 @@ __device__ __forceinline__ void phaseC(const double* __restrict__ recs,
   for (int g = 0; g < F::NGP; ++g) {
     const double* A = recs + g * GpBlock<D>::STRIDE + a * R::STRIDE;
     const double* B = recs + g * GpBlock<D>::STRIDE + b * R::STRIDE;
-    const double mu = scal[g * kScal + 0];
-    const double ghc = scal[g * kScal + 1];
+    const double mu = scal[g * SCAL_STRIDE + MU_OFF];
+    const double ghc = scal[g * SCAL_STRIDE + GHC_OFF];
     double gA[D], sA[D], gB[D], t1[D], t2[D];
 #pragma unroll
     for (int i = 0; i < D; ++i) {

@@ -22,8 +22,17 @@
 namespace lgdm {
 
 template <int D> struct SweepCfg;
-template <> struct SweepCfg<2> { static constexpr int TX = 32, TY = 1, E = 16, NCOL = 2, MINB = 3; };
-template <> struct SweepCfg<3> { static constexpr int TX = 4, TY = 4, E = 4, NCOL = 4, MINB = 3; };
+// TX x TY node columns per CTA, E elements per batch, NCOL colours per layer.
+template <> struct SweepCfg<2> { static constexpr int TX = 64, TY = 1, E = 16, NCOL = 2, MINB = 2; };
+template <> struct SweepCfg<3> { static constexpr int TX = 6, TY = 6, E = 4, NCOL = 4, MINB = 2; };
+
+template <int D> struct SweepThreads {
+  // named-barrier thread counts must be whole warps
+  static constexpr int P = (SweepCfg<D>::E * Fam<D>::NGP + 31) / 32 * 32;    // producers: (element, GP)
+  static constexpr int C = (SweepCfg<D>::E * Fam<D>::NPAIR + 31) / 32 * 32;  // consumers: (element, pair)
+  static constexpr int T = P + C;
+  static_assert(P % 32 == 0 && C % 32 == 0, "whole warps");
+};
 
 struct SweepGeom {
   int64_t nx, nyE, nyN, nl;        // elements in x; elements / nodes in y (D=2: 1 / 1); layers
@@ -57,20 +66,120 @@ __device__ __forceinline__ void slot_of(const SweepGeom& G, int64_t x, int64_t y
   W = wx * wy * wz * ndpn;
 }
 
+// named barriers with immediate ids (so ptxas reserves only ids 0..5)
+template <int ID> __device__ __forceinline__ void bar_sync(int n) {
+  asm volatile("bar.sync %0, %1;" ::"n"(ID), "r"(n) : "memory");
+}
+template <int ID> __device__ __forceinline__ void bar_arrive(int n) {
+  asm volatile("bar.arrive %0, %1;" ::"n"(ID), "r"(n) : "memory");
+}
+enum { BAR_FULL0 = 1, BAR_EMPTY0 = 3, BAR_CONS = 5 };
+__device__ __forceinline__ void bar_sync_full(int buf, int n) {
+  if (buf) bar_sync<BAR_FULL0 + 1>(n); else bar_sync<BAR_FULL0>(n);
+}
+__device__ __forceinline__ void bar_arrive_full(int buf, int n) {
+  if (buf) bar_arrive<BAR_FULL0 + 1>(n); else bar_arrive<BAR_FULL0>(n);
+}
+__device__ __forceinline__ void bar_sync_empty(int buf, int n) {
+  if (buf) bar_sync<BAR_EMPTY0 + 1>(n); else bar_sync<BAR_EMPTY0>(n);
+}
+__device__ __forceinline__ void bar_arrive_empty(int buf, int n) {
+  if (buf) bar_arrive<BAR_EMPTY0 + 1>(n); else bar_arrive<BAR_EMPTY0>(n);
+}
+
+// Add the node-pair blocks of one pair thread into the owned block-rows: rows of node A
+// (rowA, may be null), rows of node B (rowB, may be null) and R of A (rA, may be null).  All
+// loads are issued before any store so the L2 round trip is paid once (.cg: L2, not L1).
 template <int D>
-__global__ void __launch_bounds__(SweepCfg<D>::E * Fam<D>::NPAIR, SweepCfg<D>::MINB)
+__device__ __forceinline__ void rmw_pair(double* __restrict__ rowA, int WA,
+                                         double* __restrict__ rowB, int WB,
+                                         double* __restrict__ rA,
+                                         const double (&vA)[Fam<D>::NDPN][Fam<D>::NDPN],
+                                         const double (&vB)[Fam<D>::NDPN][Fam<D>::NDPN],
+                                         const double (&fA)[Fam<D>::NDPN]) {
+  constexpr int NDPN = Fam<D>::NDPN;
+  double uA[NDPN][NDPN], uB[NDPN][NDPN], uR[NDPN];
+#pragma unroll
+  for (int i = 0; i < NDPN; ++i)
+#pragma unroll
+    for (int j = 0; j < NDPN; ++j) uA[i][j] = uB[i][j] = 0.0;
+#pragma unroll
+  for (int i = 0; i < NDPN; ++i) uR[i] = 0.0;
+  if constexpr (NDPN == 4) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (rowA) {
+        const double2* q = reinterpret_cast<const double2*>(rowA + int64_t(i) * WA);
+        const double2 a0 = __ldcg(q), a1 = __ldcg(q + 1);
+        uA[i][0] = a0.x; uA[i][1] = a0.y; uA[i][2] = a1.x; uA[i][3] = a1.y;
+      }
+      if (rowB) {
+        const double2* q = reinterpret_cast<const double2*>(rowB + int64_t(i) * WB);
+        const double2 b0 = __ldcg(q), b1 = __ldcg(q + 1);
+        uB[i][0] = b0.x; uB[i][1] = b0.y; uB[i][2] = b1.x; uB[i][3] = b1.y;
+      }
+    }
+    if (rA) {
+      const double2* q = reinterpret_cast<const double2*>(rA);
+      const double2 r0 = __ldcg(q), r1 = __ldcg(q + 1);
+      uR[0] = r0.x; uR[1] = r0.y; uR[2] = r1.x; uR[3] = r1.y;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (rowA) {
+        double2* q = reinterpret_cast<double2*>(rowA + int64_t(i) * WA);
+        __stcg(q, make_double2(uA[i][0] + vA[i][0], uA[i][1] + vA[i][1]));
+        __stcg(q + 1, make_double2(uA[i][2] + vA[i][2], uA[i][3] + vA[i][3]));
+      }
+      if (rowB) {
+        double2* q = reinterpret_cast<double2*>(rowB + int64_t(i) * WB);
+        __stcg(q, make_double2(uB[i][0] + vB[i][0], uB[i][1] + vB[i][1]));
+        __stcg(q + 1, make_double2(uB[i][2] + vB[i][2], uB[i][3] + vB[i][3]));
+      }
+    }
+    if (rA) {
+      double2* q = reinterpret_cast<double2*>(rA);
+      __stcg(q, make_double2(uR[0] + fA[0], uR[1] + fA[1]));
+      __stcg(q + 1, make_double2(uR[2] + fA[2], uR[3] + fA[3]));
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < NDPN; ++i)
+#pragma unroll
+      for (int j = 0; j < NDPN; ++j) {
+        if (rowA) uA[i][j] = __ldcg(rowA + int64_t(i) * WA + j);
+        if (rowB) uB[i][j] = __ldcg(rowB + int64_t(i) * WB + j);
+      }
+    if (rA)
+#pragma unroll
+      for (int i = 0; i < NDPN; ++i) uR[i] = __ldcg(rA + i);
+#pragma unroll
+    for (int i = 0; i < NDPN; ++i)
+#pragma unroll
+      for (int j = 0; j < NDPN; ++j) {
+        if (rowA) __stcg(rowA + int64_t(i) * WA + j, uA[i][j] + vA[i][j]);
+        if (rowB) __stcg(rowB + int64_t(i) * WB + j, uB[i][j] + vB[i][j]);
+      }
+    if (rA)
+#pragma unroll
+      for (int i = 0; i < NDPN; ++i) __stcg(rA + i, uR[i] + fA[i]);
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(SweepThreads<D>::T, SweepCfg<D>::MINB)
 k_sweep(DevMat m, SweepGeom G, const double* __restrict__ coords, const double* __restrict__ dofs,
         const double* __restrict__ kappa, const int64_t* __restrict__ base,
         double* __restrict__ val, double* __restrict__ Rv) {
   using F = Fam<D>;
-  using C = SweepCfg<D>;
-  constexpr int E = C::E, NT = E * F::NPAIR, NDPN = F::NDPN, NEN = F::NEN, NGP = F::NGP;
+  using Cf = SweepCfg<D>;
+  using Th = SweepThreads<D>;
+  constexpr int E = Cf::E, NDPN = F::NDPN, NEN = F::NEN, NGP = F::NGP;
+  constexpr int CS = Core<D>::STRIDE, GB = GpBlock<D>::STRIDE;
   extern __shared__ double sm[];
-  double* recs = sm;                                   // [E][NGP][GpBlock]
-  double* scal = recs + E * NGP * GpBlock<D>::STRIDE;  // [E][NGP][kScal]
-  double* Xs = scal + E * NGP * kScal;                 // [E][NEN][D]
-  double* Us = Xs + E * NEN * D;                       // [E][NEN][NDPN]
-  __shared__ int64_t s_i[E], s_j[E];
+  double* cores = sm;                            // [2][E][NGP][CS]
+  double* recs = cores + 2 * E * NGP * CS;       // [E][NGP][GB]
+  __shared__ int64_t s_base_all[2][Cf::TX * Cf::TY];   // val offsets of the tile's block-rows, by layer parity
   const int tid = threadIdx.x;
 
   int bid = blockIdx.x;
@@ -78,167 +187,172 @@ k_sweep(DevMat m, SweepGeom G, const double* __restrict__ coords, const double* 
   bid /= G.tiles_x;
   const int ty = bid % G.tiles_y;
   const int ch = bid / G.tiles_y;
-  const int64_t x0 = int64_t(tx) * C::TX, x1 = min(x0 + C::TX, G.nx + 1);
-  const int64_t y0 = int64_t(ty) * C::TY, y1 = min(y0 + C::TY, G.nyN);
+  const int64_t x0 = int64_t(tx) * Cf::TX, x1 = min(x0 + Cf::TX, G.nx + 1);
+  const int64_t y0 = int64_t(ty) * Cf::TY, y1 = min(y0 + Cf::TY, G.nyN);
   const int64_t z0 = G.lay_own_b + int64_t(ch) * G.chunk_len;
   const int64_t z1 = min(z0 + G.chunk_len, G.lay_own_e);
   if (z0 >= z1) return;
   const int64_t nxN = G.nx + 1;
-  const int64_t cols_x = x1 - x0, cols = cols_x * (y1 - y0);
-
   auto node_id = [&](int64_t x, int64_t y, int64_t z) { return x + nxN * (y + G.nyN * z); };
-
-  // zero the block-rows and R entries of the tile's nodes in layer z (first touch)
-  auto zero_layer = [&](int64_t z) {
-    for (int64_t c = 0; c < cols; ++c) {
-      const int64_t x = x0 + c % cols_x, y = y0 + c / cols_x;
-      int sl, W;
-      slot_of(G, x, y, z, 0, 0, 0, NDPN, sl, W);
-      const int64_t o = node_id(x, y, z) - G.own_node_b;
-      double* row = val + base[o];
-      const int n = NDPN * W;
-      if constexpr (NDPN == 4) {
-        for (int k = tid; k < n / 2; k += NT) __stcg(reinterpret_cast<double2*>(row) + k, make_double2(0.0, 0.0));
-      } else {
-        for (int k = tid; k < n; k += NT) __stcg(row + k, 0.0);
-      }
-      if (tid < NDPN) __stcg(Rv + o * NDPN + tid, 0.0);
-    }
-  };
 
   const int64_t s_first = max(z0 - 1, int64_t(0));
   const int64_t s_last = min(z1, G.nl) - 1;
-  if (s_first == z0) zero_layer(z0);
-
   const int64_t ilo = max(x0 - 1, int64_t(0)), ihi = min(x1, G.nx);
   const int64_t jlo = (D == 3) ? max(y0 - 1, int64_t(0)) : 0;
   const int64_t jhi = (D == 3) ? min(y1, G.nyE) : 1;
 
-  for (int64_t s = s_first; s <= s_last; ++s) {
-    if (s + 1 >= z0 && s + 1 < z1) zero_layer(s + 1);
-    __syncthreads();
-    for (int c = 0; c < C::NCOL; ++c) {
-      const int ci = c & 1, cj = c >> 1;
-      const int64_t ifst = ilo + ((ilo & 1) != ci ? 1 : 0);
-      const int64_t ni = ifst < ihi ? (ihi - ifst + 1) / 2 : 0;
-      int64_t jfst = 0, nj = 1;
-      if constexpr (D == 3) {
-        jfst = jlo + ((jlo & 1) != cj ? 1 : 0);
-        nj = jfst < jhi ? (jhi - jfst + 1) / 2 : 0;
+  // the batch schedule, identical for producers and consumers:
+  // for each element layer s, each colour c, batches of E elements of that colour
+  auto for_each_batch = [&](auto&& body) {
+    for (int64_t s = s_first; s <= s_last; ++s)
+      for (int c = 0; c < Cf::NCOL; ++c) {
+        const int ci = c & 1;
+        const int64_t ifst = ilo + ((ilo & 1) != ci ? 1 : 0);
+        const int64_t ni = ifst < ihi ? (ihi - ifst + 1) / 2 : 0;
+        int64_t jfst = 0, nj = 1;
+        if constexpr (D == 3) {
+          const int cj = c >> 1;
+          jfst = jlo + ((jlo & 1) != cj ? 1 : 0);
+          nj = jfst < jhi ? (jhi - jfst + 1) / 2 : 0;
+        }
+        const int64_t nc = ni * nj;
+        for (int64_t b0 = 0; b0 < nc; b0 += E) body(s, b0, ifst, ni, jfst, nc);
       }
-      const int64_t nc = ni * nj;
-      for (int64_t b0 = 0; b0 < nc; b0 += E) {
-        if (tid < E) {
-          const int64_t k = b0 + tid;
-          s_i[tid] = k < nc ? ifst + 2 * (k % ni) : -1;
-          s_j[tid] = k < nc ? jfst + 2 * (k / ni) : -1;
+  };
+
+  if (tid < Th::P) {
+    // ------------------------------ producer warps ------------------------------
+    const int el = tid / NGP, g = tid % NGP;   // el may be >= E in padding threads
+    int t = 0;
+    for_each_batch([&](int64_t s, int64_t b0, int64_t ifst, int64_t ni, int64_t jfst, int64_t nc) {
+      const int buf = t & 1;
+      if (t >= 2) bar_sync_empty(buf, Th::T);
+      const int64_t k = b0 + el;
+      if (el < E && k < nc) {
+        const int64_t i = ifst + 2 * (k % ni), j = jfst + 2 * (k / ni);
+        double X[NEN * D], U[NEN * NDPN];
+#pragma unroll
+        for (int a = 0; a < NEN; ++a) {
+          int ox, oy, oz;
+          node_off<D>(a, ox, oy, oz);
+          const int64_t n = node_id(i + ox, j + oy, s + oz);
+#pragma unroll
+          for (int q = 0; q < D; ++q) X[a * D + q] = __ldg(coords + n * D + q);
+#pragma unroll
+          for (int q = 0; q < NDPN; ++q) U[a * NDPN + q] = __ldg(dofs + n * NDPN + q);
         }
-        __syncthreads();
-        // gather node data of the batch elements
-        for (int t = tid; t < E * NEN; t += NT) {
-          const int el = t / NEN, a = t % NEN;
-          if (s_i[el] >= 0) {
-            int ox, oy, oz;
-            node_off<D>(a, ox, oy, oz);
-            const int64_t n = node_id(s_i[el] + ox, s_j[el] + oy, s + oz);
+        const int64_t e = i + G.nx * (j + G.nyE * s);
+        gpCore<D>(m, X, U, __ldg(kappa + e * NGP + g), g, cores + (size_t(buf) * E * NGP + tid) * CS);
+      }
+      bar_arrive_full(buf, Th::T);
+      ++t;
+    });
+    for (int k = max(t - 2, 0); k < t; ++k) bar_sync_empty(k & 1, Th::T);
+    return;
+  }
+
+  // -------------------------------- consumer warps --------------------------------
+  const int ct = tid - Th::P;
+  const int cel = ct / F::NPAIR, cp = ct % F::NPAIR;
+  int pa, pb;
+  pair_ab<NEN>(cp, pa, pb);
+  int oax, oay, oaz, obx, oby, obz;
+  node_off<D>(pa, oax, oay, oaz);
+  node_off<D>(pb, obx, oby, obz);
+  const int64_t cols_x = x1 - x0, cols = cols_x * (y1 - y0);
+
+  // first touch of the tile's block-rows in layer z: stage their val offsets in shared
+  // memory (one parallel load), then zero them (one warp per node, coalesced)
+  auto zero_layer = [&](int64_t z) {
+    int64_t* sb = s_base_all[z & 1];
+    for (int c = ct; c < cols; c += Th::C) {
+      const int64_t x = x0 + c % cols_x, y = y0 + c / cols_x;
+      sb[c] = base[node_id(x, y, z) - G.own_node_b];
+    }
+    bar_sync<BAR_CONS>(Th::C);
+    const int warp = ct >> 5, lane = ct & 31;
+    for (int64_t c = warp; c < cols; c += Th::C / 32) {
+      const int64_t x = x0 + c % cols_x, y = y0 + c / cols_x;
+      int sl, W;
+      slot_of(G, x, y, z, 0, 0, 0, NDPN, sl, W);
+      double* row = val + sb[c];
+      const int n = NDPN * W;
+      if constexpr (NDPN == 4) {
+        for (int k = lane; k < n / 2; k += 32)
+          __stcg(reinterpret_cast<double2*>(row) + k, make_double2(0.0, 0.0));
+      } else {
+        for (int k = lane; k < n; k += 32) __stcg(row + k, 0.0);
+      }
+      if (lane < NDPN) __stcg(Rv + (node_id(x, y, z) - G.own_node_b) * NDPN + lane, 0.0);
+    }
+  };
+
+  int t = 0;
+  int64_t cur_s = -1;
+  for_each_batch([&](int64_t s, int64_t b0, int64_t ifst, int64_t ni, int64_t jfst, int64_t nc) {
+    const int buf = t & 1;
+    if (s != cur_s) {
+      if (cur_s < 0 && s == z0) zero_layer(z0);
+      if (s + 1 >= z0 && s + 1 < z1) zero_layer(s + 1);
+      cur_s = s;
+    }
+    bar_sync_full(buf, Th::T);
+    // expansion: (element, GP, node) records from the compact GP states
+    const double* cb = cores + size_t(buf) * E * NGP * CS;
+    for (int it = ct; it < E * NGP * NEN; it += Th::C) {
+      const int eg = it / NEN, a = it % NEN;
+      if (b0 + eg / NGP < nc) gpExpand<D>(cb + eg * CS, a, eg % NGP, recs + size_t(eg) * GB + a * Rec<D>::STRIDE);
+    }
+    bar_sync<BAR_CONS>(Th::C);
+    // pair Gauss sums and accumulation into the owned block-rows
+    const int64_t k = b0 + cel;
+    if (cel < E && k < nc) {
+      const int64_t i = ifst + 2 * (k % ni), j = jfst + 2 * (k / ni);
+      const int64_t ax = i + oax, ay = j + oay, az = s + oaz;
+      const int64_t bx = i + obx, by = j + oby, bz = s + obz;
+      const bool own_a = ax >= x0 && ax < x1 && ay >= y0 && ay < y1 && az >= z0 && az < z1;
+      const bool own_b = bx >= x0 && bx < x1 && by >= y0 && by < y1 && bz >= z0 && bz < z1;
+      if (own_a || own_b) {
+        PairAcc<D> acc;
+        phaseC<D, CS, Core<D>::MU, Core<D>::GHC>(recs + size_t(cel) * NGP * GB, cb + cel * NGP * CS,
+                                                  pa, pb, acc);
+        double vA[NDPN][NDPN], vB[NDPN][NDPN], fA[NDPN];
 #pragma unroll
-            for (int i = 0; i < D; ++i) Xs[t * D + i] = coords[n * D + i];
+        for (int r = 0; r < D; ++r) {
 #pragma unroll
-            for (int i = 0; i < NDPN; ++i) Us[t * NDPN + i] = dofs[n * NDPN + i];
+          for (int q = 0; q < D; ++q) {
+            vA[r][q] = acc.Kuu[r][q];
+            vB[r][q] = acc.Kuu[q][r];
           }
+          vA[r][D] = acc.Kue_ab[r];
+          vA[D][r] = acc.Keu_ab[r];
+          vB[r][D] = acc.Kue_ba[r];
+          vB[D][r] = acc.Keu_ba[r];
         }
-        __syncthreads();
-        // phase A
-        for (int t = tid; t < E * NGP; t += NT) {
-          const int el = t / NGP, g = t % NGP;
-          if (s_i[el] >= 0) {
-            const int64_t e = s_i[el] + G.nx * (s_j[el] + G.nyE * s);
-            phaseA<D>(m, Xs + el * NEN * D, Us + el * NEN * NDPN, kappa[e * NGP + g], g,
-                      recs + size_t(t) * GpBlock<D>::STRIDE, scal + t * kScal);
-          }
+        vA[D][D] = acc.Kee_ab;
+        vB[D][D] = acc.Kee_ba;
+#pragma unroll
+        for (int r = 0; r < NDPN; ++r) fA[r] = acc.Fd[r];
+        double *rowA = nullptr, *rowB = nullptr, *rA = nullptr;
+        int WA = 0, WB = 0;
+        if (own_a) {
+          int sl;
+          slot_of(G, ax, ay, az, obx - oax, oby - oay, obz - oaz, NDPN, sl, WA);
+          rowA = val + s_base_all[az & 1][(ax - x0) + cols_x * (ay - y0)] + NDPN * sl;
+          if (pa == pb) rA = Rv + (node_id(ax, ay, az) - G.own_node_b) * NDPN;
         }
-        __syncthreads();
-        // phase C + accumulation into owned block-rows
-        {
-          const int el = tid / F::NPAIR, p = tid % F::NPAIR;
-          if (el < E && s_i[el] >= 0) {
-            int a, b;
-            pair_ab<NEN>(p, a, b);
-            int oax, oay, oaz, obx, oby, obz;
-            node_off<D>(a, oax, oay, oaz);
-            node_off<D>(b, obx, oby, obz);
-            const int64_t ax = s_i[el] + oax, ay = s_j[el] + oay, az = s + oaz;
-            const int64_t bx = s_i[el] + obx, by = s_j[el] + oby, bz = s + obz;
-            const bool own_a = ax >= x0 && ax < x1 && ay >= y0 && ay < y1 && az >= z0 && az < z1;
-            const bool own_b = bx >= x0 && bx < x1 && by >= y0 && by < y1 && bz >= z0 && bz < z1;
-            if (own_a || own_b) {
-              PairAcc<D> acc;
-              phaseC<D>(recs + size_t(el) * NGP * GpBlock<D>::STRIDE, scal + el * NGP * kScal, a,
-                        b, acc);
-              // rows of node A: K(A,i; B,j)
-              if (own_a) {
-                int sl, W;
-                slot_of(G, ax, ay, az, obx - oax, oby - oay, obz - oaz, NDPN, sl, W);
-                const int64_t o = node_id(ax, ay, az) - G.own_node_b;
-                double* row0 = val + base[o] + NDPN * sl;
-#pragma unroll
-                for (int i = 0; i < NDPN; ++i) {
-                  double v[NDPN];
-#pragma unroll
-                  for (int j = 0; j < D; ++j) v[j] = (i < D) ? acc.Kuu[i < D ? i : 0][j] : acc.Keu_ab[j];
-                  v[D] = (i < D) ? acc.Kue_ab[i < D ? i : 0] : acc.Kee_ab;
-                  double* q = row0 + int64_t(i) * W;
-                  if constexpr (NDPN == 4) {
-                    double2* q2 = reinterpret_cast<double2*>(q);
-                    double2 u0 = __ldcg(q2), u1 = __ldcg(q2 + 1);
-                    u0.x += v[0]; u0.y += v[1]; u1.x += v[2]; u1.y += v[3];
-                    __stcg(q2, u0);
-                    __stcg(q2 + 1, u1);
-                  } else {
-#pragma unroll
-                    for (int j = 0; j < NDPN; ++j) __stcg(q + j, __ldcg(q + j) + v[j]);
-                  }
-                }
-                if (a == b) {
-#pragma unroll
-                  for (int i = 0; i < NDPN; ++i) {
-                    double* r = Rv + o * NDPN + i;
-                    __stcg(r, __ldcg(r) + acc.Fd[i]);
-                  }
-                }
-              }
-              // rows of node B (a != b): K(B,i; A,j) = transpose of Kuu_ab, *_ba blocks
-              if (own_b && a != b) {
-                int sl, W;
-                slot_of(G, bx, by, bz, oax - obx, oay - oby, oaz - obz, NDPN, sl, W);
-                const int64_t o = node_id(bx, by, bz) - G.own_node_b;
-                double* row0 = val + base[o] + NDPN * sl;
-#pragma unroll
-                for (int i = 0; i < NDPN; ++i) {
-                  double v[NDPN];
-#pragma unroll
-                  for (int j = 0; j < D; ++j) v[j] = (i < D) ? acc.Kuu[j][i < D ? i : 0] : acc.Keu_ba[j];
-                  v[D] = (i < D) ? acc.Kue_ba[i < D ? i : 0] : acc.Kee_ba;
-                  double* q = row0 + int64_t(i) * W;
-                  if constexpr (NDPN == 4) {
-                    double2* q2 = reinterpret_cast<double2*>(q);
-                    double2 u0 = __ldcg(q2), u1 = __ldcg(q2 + 1);
-                    u0.x += v[0]; u0.y += v[1]; u1.x += v[2]; u1.y += v[3];
-                    __stcg(q2, u0);
-                    __stcg(q2 + 1, u1);
-                  } else {
-#pragma unroll
-                    for (int j = 0; j < NDPN; ++j) __stcg(q + j, __ldcg(q + j) + v[j]);
-                  }
-                }
-              }
-            }
-          }
+        if (own_b && pa != pb) {
+          int sl;
+          slot_of(G, bx, by, bz, oax - obx, oay - oby, oaz - obz, NDPN, sl, WB);
+          rowB = val + s_base_all[bz & 1][(bx - x0) + cols_x * (by - y0)] + NDPN * sl;
         }
-        __syncthreads();
+        rmw_pair<D>(rowA, WA, rowB, WB, rA, vA, vB, fA);
       }
     }
-  }
+    bar_arrive_empty(buf, Th::T);   // cores[buf] (incl. mu*, ghc read by phase C) is free
+    bar_sync<BAR_CONS>(Th::C);
+    ++t;
+  });
 }
 
 }  // namespace lgdm
@@ -254,6 +368,7 @@ bool sweep_supported(lgdm_mesh m) {
 template <int D> lgdm_status launch_sweep(lgdm_mesh m) {
   using F = Fam<D>;
   using Cf = SweepCfg<D>;
+  using Th = SweepThreads<D>;
   SweepGeom G{};
   G.nx = m->nx;
   if (D == 3) {
@@ -271,9 +386,8 @@ template <int D> lgdm_status launch_sweep(lgdm_mesh m) {
   G.own_node_b = m->own_b;
   G.tiles_x = int((G.nx + 1 + Cf::TX - 1) / Cf::TX);
   G.tiles_y = int((G.nyN + Cf::TY - 1) / Cf::TY);
-  const size_t smem = sizeof(double) * (size_t(Cf::E) * F::NGP * GpBlock<D>::STRIDE +
-                                        Cf::E * F::NGP * kScal + Cf::E * F::NEN * D +
-                                        Cf::E * F::NEN * F::NDPN);
+  const size_t smem = sizeof(double) * (size_t(2) * Cf::E * F::NGP * Core<D>::STRIDE +
+                                        size_t(Cf::E) * F::NGP * GpBlock<D>::STRIDE);
   static bool attr = false;
   if (!attr) {
     CU(cudaFuncSetAttribute(k_sweep<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -281,7 +395,7 @@ template <int D> lgdm_status launch_sweep(lgdm_mesh m) {
   }
   int nsm = 148, per_sm = 1;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep<D>, Cf::E * F::NPAIR, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep<D>, Th::T, smem);
   per_sm = std::max(per_sm, 1);
   const int64_t layers = G.lay_own_e - G.lay_own_b;
   const int64_t tiles = int64_t(G.tiles_x) * G.tiles_y;
@@ -291,7 +405,7 @@ template <int D> lgdm_status launch_sweep(lgdm_mesh m) {
   G.chunk_len = (layers + chunks - 1) / chunks;
   G.chunks = int((layers + G.chunk_len - 1) / G.chunk_len);
   const int64_t grid = tiles * G.chunks;
-  k_sweep<D><<<unsigned(grid), Cf::E * F::NPAIR, smem, m->stream>>>(
+  k_sweep<D><<<unsigned(grid), Th::T, smem, m->stream>>>(
       m->dm, G, m->coords, m->dofs, m->kappa, m->base, m->val, m->R);
   return check_launch(m, "k_sweep");
 }

@@ -1,0 +1,90 @@
+"""Multi-process host logic of the N > 1 path on CPU (gloo, world_size 2).
+
+Each rank builds its row-owned slab (owned node layers + one ghost element layer, global
+ids), assembles it with the CPU oracle, keeps its owned rows, and the ranks reduce the sums
+of squares of R exactly as lgdm_residual_norms does with NCCL.  Checks: the slabs' owned rows
+equal the whole-mesh rows bitwise (ghost recompute is sufficient, global column ids), and the
+reduced norms equal the whole-mesh norms.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import synth
+from paper_2301_06503_b200 import slabs
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, etype, n, q):
+    import torch
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = synth.small_config(etype, n)
+        ndpn = synth.FAM[etype][2]
+        sl = slabs.slab(cfg.n, rank, world)
+        mesh = synth.structured_mesh(cfg, elem_layers=sl.elem_layers)
+        dofs, kappa = synth.fields(cfg, mesh)
+        res = oracle.assemble(etype, oracle.material(**synth.MATERIAL), mesh.coords, mesh.conn,
+                              dofs, kappa)
+        ob, oe = sl.owned_local(mesh.node_gid0)
+        r0, r1 = ndpn * ob, ndpn * oe
+        R = res["R"][r0:r1]
+        lo, hi = res["row_ptr"][r0], res["row_ptr"][r1]
+        cols_global = res["col_idx"][lo:hi].astype(np.int64) + ndpn * mesh.node_gid0
+        # partial sums of squares (u rows, ebar rows) -> allreduce(sum), as lgdm_residual_norms
+        dim = synth.FAM[etype][0]
+        comp = np.arange(r0, r1) % ndpn
+        part = torch.tensor([np.sum(R[comp != dim] ** 2), np.sum(R[comp == dim] ** 2)],
+                            dtype=torch.float64)
+        dist.all_reduce(part, op=dist.ReduceOp.SUM)
+        q.put((rank, sl.owned_nodes, res["row_ptr"][r0:r1 + 1] - lo, cols_global,
+               res["val"][lo:hi], R, np.sqrt(part.numpy())))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("etype,n", [(synth.QUAD4, (9, 11)), (synth.HEX8, (3, 4, 7))])
+def test_two_rank_slabs_gloo(etype, n):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, etype, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted([q.get(timeout=120) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    cfg = synth.small_config(etype, n)
+    ndpn = synth.FAM[etype][2]
+    mesh = synth.structured_mesh(cfg)
+    dofs, kappa = synth.fields(cfg, mesh)
+    full = oracle.assemble(etype, oracle.material(**synth.MATERIAL), mesh.coords, mesh.conn,
+                           dofs, kappa)
+    norms = oracle.residual_norms(etype, full["R"])
+    covered = 0
+    for rank, (b, e), rp, cols, val, R, rnorm in out:
+        r0, r1 = ndpn * b, ndpn * e
+        lo, hi = full["row_ptr"][r0], full["row_ptr"][r1]
+        np.testing.assert_array_equal(rp, full["row_ptr"][r0:r1 + 1] - lo)
+        np.testing.assert_array_equal(cols, full["col_idx"][lo:hi])
+        np.testing.assert_array_equal(val, full["val"][lo:hi])
+        np.testing.assert_array_equal(R, full["R"][r0:r1])
+        np.testing.assert_allclose(rnorm, norms, rtol=1e-13)
+        covered += e - b
+    assert covered == mesh.coords.shape[0]
