@@ -41,27 +41,55 @@ template <> struct Fam<3> {
   static constexpr int DIM = 3, NEN = 8, NDPN = 4, NGP = 8, NS = 6, NPAIR = 36, NDOFE = 32;
 };
 
-// Per (element, GP, node) record produced by phase A.  Field offsets in doubles.
-//   gN[D]   grad N_a                    SgN[D]  S grad N_a
-//   t1[D]   lam* gN + Ams SgN           t2[D]   Ams gN + Ass SgN
-//   WgN[D]  W' grad N_a   (Kue)         DgN[D]  Dt' grad N_a  (Keu)
-//   N       N_a                          e       hN N_a + gvec . gN_a   (Kee)
-//   f[D+1]  (Sigma' gN_a, fe0 N_a + fvec . gN_a)   (Fu, Fe)
+// Per (element, GP, node) record produced by phase A (offsets in doubles, by accessor):
+//   gN   grad N_a                    SgN  S grad N_a
+//   t1   lam* gN + Ams SgN           t2   Ams gN + Ass SgN
+//   WgN  W' grad N_a   (Kue)         DgN  Dt' grad N_a  (Keu)
+//   N    N_a                          E    hN N_a + gvec . gN_a   (Kee)
+//   F    (Sigma' gN_a, fe0 N_a + fvec . gN_a)   (Fu, Fe)
 // All coefficients carry dV and the signs of Eq. 11, so phase C only multiplies and adds.
-template <int D> struct Rec {
-  static constexpr int GN = 0, SGN = D, T1 = 2 * D, T2 = 3 * D, WGN = 4 * D, DGN = 5 * D,
-                       N = 6 * D, E = 6 * D + 1, F = 6 * D + 2;
-  static constexpr int USED = 7 * D + 3;
-  // odd stride: conflict-free LDS.64 for up to 16 distinct records per warp access
-  static constexpr int STRIDE = (USED % 2 == 1) ? USED : USED + 1;
+// Hex8 layout pairs the fields read together so phase C uses 16-byte shared loads:
+//   [gN0 gN1][gN2 N][SgN0 SgN1][SgN2 E][t1_0 t1_1][t2_0 t2_1][t1_2 t2_2][WgN0 WgN1]
+//   [WgN2 DgN2][DgN0 DgN1][F0 F1][F2 F3][pad pad]     (26 doubles = 13 x 16 B: odd, so
+//   8 distinct records of a quarter-warp hit distinct 16-byte bank groups)
+template <int D> struct Rec;
+template <> struct Rec<3> {
+  static constexpr int N = 3, E = 7, STRIDE = 26;
+  __host__ __device__ static constexpr int gn(int i) { return i; }
+  __host__ __device__ static constexpr int sgn(int i) { return 4 + i; }
+  __host__ __device__ static constexpr int t1(int i) { return i < 2 ? 8 + i : 12; }
+  __host__ __device__ static constexpr int t2(int i) { return i < 2 ? 10 + i : 13; }
+  __host__ __device__ static constexpr int wgn(int i) { return 14 + i; }
+  __host__ __device__ static constexpr int dgn(int i) { return i < 2 ? 18 + i : 17; }
+  __host__ __device__ static constexpr int f(int i) { return 20 + i; }
+};
+template <> struct Rec<2> {  // 18 doubles = 9 x 16 B
+  static constexpr int N = 12, E = 13, STRIDE = 18;
+  __host__ __device__ static constexpr int gn(int i) { return i; }
+  __host__ __device__ static constexpr int sgn(int i) { return 2 + i; }
+  __host__ __device__ static constexpr int t1(int i) { return 4 + i; }
+  __host__ __device__ static constexpr int t2(int i) { return 6 + i; }
+  __host__ __device__ static constexpr int wgn(int i) { return 8 + i; }
+  __host__ __device__ static constexpr int dgn(int i) { return 10 + i; }
+  __host__ __device__ static constexpr int f(int i) { return 14 + i; }
+};
+template <> struct Rec<1> {  // 10 doubles = 5 x 16 B
+  static constexpr int N = 6, E = 7, STRIDE = 10;
+  __host__ __device__ static constexpr int gn(int i) { return i; }
+  __host__ __device__ static constexpr int sgn(int i) { return 1 + i; }
+  __host__ __device__ static constexpr int t1(int i) { return 2 + i; }
+  __host__ __device__ static constexpr int t2(int i) { return 3 + i; }
+  __host__ __device__ static constexpr int wgn(int i) { return 4 + i; }
+  __host__ __device__ static constexpr int dgn(int i) { return 5 + i; }
+  __host__ __device__ static constexpr int f(int i) { return 8 + i; }
 };
 // per (element, GP) scalars used by phase C: mu*, ghc
 constexpr int kScal = 2;
-// doubles per (element, GP) record block: NEN records + 1 pad so that consecutive (e,g)
-// blocks start in different bank pairs (odd stride in doubles)
+// doubles per (element, GP) record block: NEN records, padded to an odd number of 16-byte
+// units so consecutive (e,g) blocks start in different bank groups
 template <int D> struct GpBlock {
   static constexpr int N = Fam<D>::NEN * Rec<D>::STRIDE;
-  static constexpr int STRIDE = (N % 2 == 1) ? N : N + 1;
+  static constexpr int STRIDE = ((N / 2) % 2 == 1) ? N : N + 2;
 };
 
 // reference node sign r_ak (SURVEY 8c.1 node order) and Gauss point sign s_gk (xi fastest)
@@ -122,9 +150,8 @@ template <int D> struct Core {
 // U [NEN][NDPN] dofs, kh = kappa_hist.  Writes the compact GP state (Core<D> layout) to core.
 // Returns det J (caller treats <= 0 as an inverted element).
 // ---------------------------------------------------------------------------------------
-template <int D>
-__device__ __forceinline__ double gpCore(const DevMat& m, const double* __restrict__ X,
-                                         const double* __restrict__ U, double kh, int g,
+template <int D, class XF, class UF>
+__device__ __forceinline__ double gpCore(const DevMat& m, XF&& X, UF&& U, double kh, int g,
                                          double* __restrict__ core) {
   using Co = Core<D>;
   using F = Fam<D>;
@@ -143,7 +170,7 @@ __device__ __forceinline__ double gpCore(const DevMat& m, const double* __restri
     for (int j = 0; j < D; ++j) {
       const double dn = shape_dxi<D>(a, g, j);
 #pragma unroll
-      for (int i = 0; i < D; ++i) J[i][j] = fma(X[a * D + i], dn, J[i][j]);
+      for (int i = 0; i < D; ++i) J[i][j] = fma(X(a, i), dn, J[i][j]);
     }
   double detJ, Ji[D][D];
   if constexpr (D == 1) {
@@ -195,13 +222,17 @@ __device__ __forceinline__ double gpCore(const DevMat& m, const double* __restri
   for (int a = 0; a < NEN; ++a) {
     double gn[D];
     gradN(a, gn);
-    const double ea = U[a * NDPN + D];
+    const double ea = U(a, D);
     ebar = fma(shapeN<D>(a, g), ea, ebar);
 #pragma unroll
     for (int i = 0; i < D; ++i) {
       gb[i] = fma(gn[i], ea, gb[i]);
 #pragma unroll
-      for (int j = 0; j < D; ++j) eps[i][j] = fma(U[a * NDPN + i], gn[j], eps[i][j]);
+      {
+        const double ua = U(a, i);
+#pragma unroll
+        for (int j = 0; j < D; ++j) eps[i][j] = fma(ua, gn[j], eps[i][j]);
+      }
     }
   }
   // symmetrise: eps_ij = (du_i/dx_j + du_j/dx_i)/2
@@ -370,19 +401,19 @@ __device__ __forceinline__ void gpExpand(const double* __restrict__ core, int a,
   double gvd = 0.0, fvd = 0.0;
 #pragma unroll
   for (int i = 0; i < D; ++i) {
-    r[R::GN + i] = gn[i];
-    r[R::SGN + i] = SgN[i];
-    r[R::T1 + i] = fma(lamS, gn[i], Ams * SgN[i]);
-    r[R::T2 + i] = fma(Ams, gn[i], Ass * SgN[i]);
-    r[R::WGN + i] = WgN[i];
-    r[R::DGN + i] = DgN[i];
-    r[R::F + i] = fu[i];
+    r[R::gn(i)] = gn[i];
+    r[R::sgn(i)] = SgN[i];
+    r[R::t1(i)] = fma(lamS, gn[i], Ams * SgN[i]);
+    r[R::t2(i)] = fma(Ams, gn[i], Ass * SgN[i]);
+    r[R::wgn(i)] = WgN[i];
+    r[R::dgn(i)] = DgN[i];
+    r[R::f(i)] = fu[i];
     gvd = fma(core[Co::GV + i], gn[i], gvd);
     fvd = fma(core[Co::FV + i], gn[i], fvd);
   }
   r[R::N] = Na;
   r[R::E] = fma(core[Co::HN], Na, gvd);
-  r[R::F + D] = fma(core[Co::FE0], Na, fvd);
+  r[R::f(D)] = fma(core[Co::FE0], Na, fvd);
 }
 
 // Phase A for one GP, all nodes (general path): core into registers, then expansions.
@@ -391,7 +422,9 @@ __device__ __forceinline__ double phaseA(const DevMat& m, const double* __restri
                                          const double* __restrict__ U, double kh, int g,
                                          double* __restrict__ rec, double* __restrict__ scal) {
   double core[Core<D>::STRIDE];
-  const double detJ = gpCore<D>(m, X, U, kh, g, core);
+  const double detJ = gpCore<D>(
+      m, [&](int a, int i) { return X[a * D + i]; },
+      [&](int a, int i) { return U[a * Fam<D>::NDPN + i]; }, kh, g, core);
 #pragma unroll
   for (int a = 0; a < Fam<D>::NEN; ++a) gpExpand<D>(core, a, g, rec + a * Rec<D>::STRIDE);
   scal[0] = core[Core<D>::MU];
@@ -418,13 +451,84 @@ template <int D> struct PairAcc {
   double Fd[D + 1];     // F of node a (diagonal pairs only)
 };
 
-// Gauss sum of one node pair: recs [NGP][GpBlock::STRIDE], scal [NGP][kScal].
+// Gauss sum of one node pair: recs [NGP][GpBlock::STRIDE], per-GP scalars (mu*, ghc) at
+// scal[g * SCAL_STRIDE + MU_OFF / GHC_OFF].
+template <int D> struct PairIn {
+  double gA[D], sA[D], wA[D], dA[D], NA, EA;   // row node a
+  double gB[D], t1[D], t2[D], wB[D], dB[D], NB, EB;   // column node b
+};
+template <int D>
+__device__ __forceinline__ void load_pair(const double* __restrict__ A, const double* __restrict__ B,
+                                          PairIn<D>& in) {
+  using R = Rec<D>;
+  if constexpr (D == 3) {
+    const double2* A2 = reinterpret_cast<const double2*>(A);
+    const double2* B2 = reinterpret_cast<const double2*>(B);
+    double2 v;
+    v = A2[0]; in.gA[0] = v.x; in.gA[1] = v.y;
+    v = A2[1]; in.gA[2] = v.x; in.NA = v.y;
+    v = A2[2]; in.sA[0] = v.x; in.sA[1] = v.y;
+    v = A2[3]; in.sA[2] = v.x; in.EA = v.y;
+    v = A2[7]; in.wA[0] = v.x; in.wA[1] = v.y;
+    v = A2[8]; in.wA[2] = v.x; in.dA[2] = v.y;
+    v = A2[9]; in.dA[0] = v.x; in.dA[1] = v.y;
+    v = B2[0]; in.gB[0] = v.x; in.gB[1] = v.y;
+    v = B2[1]; in.gB[2] = v.x; in.NB = v.y;
+    v = B2[4]; in.t1[0] = v.x; in.t1[1] = v.y;
+    v = B2[5]; in.t2[0] = v.x; in.t2[1] = v.y;
+    v = B2[6]; in.t1[2] = v.x; in.t2[2] = v.y;
+    v = B2[7]; in.wB[0] = v.x; in.wB[1] = v.y;
+    v = B2[8]; in.wB[2] = v.x; in.dB[2] = v.y;
+    v = B2[9]; in.dB[0] = v.x; in.dB[1] = v.y;
+    in.EB = B[R::E];
+  } else {
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      in.gA[i] = A[R::gn(i)]; in.sA[i] = A[R::sgn(i)]; in.wA[i] = A[R::wgn(i)]; in.dA[i] = A[R::dgn(i)];
+      in.gB[i] = B[R::gn(i)]; in.t1[i] = B[R::t1(i)]; in.t2[i] = B[R::t2(i)];
+      in.wB[i] = B[R::wgn(i)]; in.dB[i] = B[R::dgn(i)];
+    }
+    in.NA = A[R::N]; in.EA = A[R::E]; in.NB = B[R::N]; in.EB = B[R::E];
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void accumulate_pair(const PairIn<D>& in, double mu, double ghc,
+                                                PairAcc<D>& acc) {
+  double dot = 0.0;
+#pragma unroll
+  for (int i = 0; i < D; ++i) dot = fma(in.gA[i], in.gB[i], dot);
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    const double ub = mu * in.gB[i];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      double v = acc.Kuu[i][j];
+      v = fma(in.gA[i], in.t1[j], v);
+      v = fma(in.sA[i], in.t2[j], v);
+      v = fma(in.gA[j], ub, v);
+      acc.Kuu[i][j] = v;
+    }
+    acc.Kuu[i][i] = fma(mu, dot, acc.Kuu[i][i]);
+  }
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    acc.Kue_ab[i] = fma(in.NB, in.wA[i], acc.Kue_ab[i]);
+    acc.Kue_ba[i] = fma(in.NA, in.wB[i], acc.Kue_ba[i]);
+    acc.Keu_ab[i] = fma(in.NA, in.dB[i], acc.Keu_ab[i]);
+    acc.Keu_ba[i] = fma(in.NB, in.dA[i], acc.Keu_ba[i]);
+  }
+  acc.Kee_ab = fma(in.NB, in.EA, fma(ghc, dot, acc.Kee_ab));
+  acc.Kee_ba = fma(in.NA, in.EB, fma(ghc, dot, acc.Kee_ba));
+}
+
 template <int D, int SCAL_STRIDE = kScal, int MU_OFF = 0, int GHC_OFF = 1>
 __device__ __forceinline__ void phaseC(const double* __restrict__ recs,
                                        const double* __restrict__ scal, int a, int b,
                                        PairAcc<D>& acc) {
   using F = Fam<D>;
   using R = Rec<D>;
+  constexpr int GB = GpBlock<D>::STRIDE;
 #pragma unroll
   for (int i = 0; i < D; ++i) {
 #pragma unroll
@@ -434,52 +538,19 @@ __device__ __forceinline__ void phaseC(const double* __restrict__ recs,
   acc.Kee_ab = acc.Kee_ba = 0.0;
 #pragma unroll
   for (int i = 0; i <= D; ++i) acc.Fd[i] = 0.0;
-  const bool diag = a == b;
-#pragma unroll 1
+  const double* Ab = recs + a * R::STRIDE;
+  const double* Bb = recs + b * R::STRIDE;
+#pragma unroll 2
   for (int g = 0; g < F::NGP; ++g) {
-    const double* A = recs + g * GpBlock<D>::STRIDE + a * R::STRIDE;
-    const double* B = recs + g * GpBlock<D>::STRIDE + b * R::STRIDE;
-    const double mu = scal[g * SCAL_STRIDE + MU_OFF];
-    const double ghc = scal[g * SCAL_STRIDE + GHC_OFF];
-    double gA[D], sA[D], gB[D], t1[D], t2[D];
+    PairIn<D> in;
+    load_pair<D>(Ab + g * GB, Bb + g * GB, in);
+    accumulate_pair<D>(in, scal[g * SCAL_STRIDE + MU_OFF], scal[g * SCAL_STRIDE + GHC_OFF], acc);
+  }
+  if (a == b) {
+#pragma unroll 1
+    for (int g = 0; g < F::NGP; ++g)
 #pragma unroll
-    for (int i = 0; i < D; ++i) {
-      gA[i] = A[R::GN + i];
-      sA[i] = A[R::SGN + i];
-      gB[i] = B[R::GN + i];
-      t1[i] = B[R::T1 + i];
-      t2[i] = B[R::T2 + i];
-    }
-    double dot = 0.0;
-#pragma unroll
-    for (int i = 0; i < D; ++i) dot = fma(gA[i], gB[i], dot);
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-      const double ub = mu * gB[i];
-#pragma unroll
-      for (int j = 0; j < D; ++j) {
-        double v = acc.Kuu[i][j];
-        v = fma(gA[i], t1[j], v);
-        v = fma(sA[i], t2[j], v);
-        v = fma(gA[j], ub, v);
-        acc.Kuu[i][j] = v;
-      }
-      acc.Kuu[i][i] = fma(mu, dot, acc.Kuu[i][i]);
-    }
-    const double NA = A[R::N], NB = B[R::N];
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-      acc.Kue_ab[i] = fma(NB, A[R::WGN + i], acc.Kue_ab[i]);
-      acc.Kue_ba[i] = fma(NA, B[R::WGN + i], acc.Kue_ba[i]);
-      acc.Keu_ab[i] = fma(NA, B[R::DGN + i], acc.Keu_ab[i]);
-      acc.Keu_ba[i] = fma(NB, A[R::DGN + i], acc.Keu_ba[i]);
-    }
-    acc.Kee_ab = fma(NB, A[R::E], fma(ghc, dot, acc.Kee_ab));
-    acc.Kee_ba = fma(NA, B[R::E], fma(ghc, dot, acc.Kee_ba));
-    if (diag) {
-#pragma unroll
-      for (int i = 0; i <= D; ++i) acc.Fd[i] += A[R::F + i];
-    }
+      for (int i = 0; i <= D; ++i) acc.Fd[i] += Ab[g * GB + R::f(i)];
   }
 }
 

@@ -21,6 +21,23 @@
 
 namespace lgdm {
 
+#ifdef LGDM_PHASE_TIMING
+// debug build only: cycles spent per phase by thread 0 of each role, summed over CTAs
+__device__ unsigned long long g_phase[16];
+#define PT_DECL unsigned long long pt_t0 = clock64();
+#define PT_MARK(slot, cond)                                          \
+  do {                                                               \
+    if (cond) {                                                      \
+      const unsigned long long pt_t1 = clock64();                    \
+      atomicAdd(&g_phase[slot], pt_t1 - pt_t0);                      \
+      pt_t0 = pt_t1;                                                 \
+    }                                                                \
+  } while (0)
+#else
+#define PT_DECL
+#define PT_MARK(slot, cond) do {} while (0)
+#endif
+
 template <int D> struct SweepCfg;
 // TX x TY node columns per CTA, E elements per batch, NCOL colours per layer.
 template <> struct SweepCfg<2> { static constexpr int TX = 64, TY = 1, E = 16, NCOL = 2, MINB = 2; };
@@ -66,6 +83,35 @@ __device__ __forceinline__ void slot_of(const SweepGeom& G, int64_t x, int64_t y
   W = wx * wy * wz * ndpn;
 }
 
+// Is element (i, j, k) the FIRST contributor, in sweep order (element layer, then colour), to
+// the entries coupling nodes A and B?  The elements containing both are those with
+// i' in [max(ax,bx)-1, min(ax,bx)] (likewise j', k'), clipped to the mesh.  The first stores,
+// the others read-modify-write, so no zero fill of K is needed.
+template <int D>
+__device__ __forceinline__ bool first_contrib(const SweepGeom& G, int i, int j, int k, int ax,
+                                              int ay, int az, int bx, int by, int bz) {
+  const int kmin = max(max(az, bz) - 1, 0);
+  if (k != kmin) return false;
+  const int i0 = max(max(ax, bx) - 1, 0), i1 = min(min(ax, bx), int(G.nx) - 1);
+  int best = 4;
+  for (int ii = i0; ii <= i1; ++ii) {
+    if constexpr (D == 3) {
+      const int j0 = max(max(ay, by) - 1, 0), j1 = min(min(ay, by), int(G.nyE) - 1);
+      for (int jj = j0; jj <= j1; ++jj) best = min(best, (ii & 1) + 2 * (jj & 1));
+    } else {
+      best = min(best, ii & 1);
+    }
+  }
+  const int mine = (D == 3) ? (i & 1) + 2 * (j & 1) : (i & 1);
+  return mine == best;
+}
+
+// local node -> position of its column block in a CSR row (nodes sorted by (z, y, x)):
+// Q4 0,1,3,2; Hex8 0,1,3,2,4,5,7,6 (an involution)
+template <int D> __device__ __forceinline__ int slot_perm(int b) {
+  return (D == 1) ? b : ((b & 2) ? (b ^ 1) : b);
+}
+
 // named barriers with immediate ids (so ptxas reserves only ids 0..5)
 template <int ID> __device__ __forceinline__ void bar_sync(int n) {
   asm volatile("bar.sync %0, %1;" ::"n"(ID), "r"(n) : "memory");
@@ -91,9 +137,9 @@ __device__ __forceinline__ void bar_arrive_empty(int buf, int n) {
 // (rowA, may be null), rows of node B (rowB, may be null) and R of A (rA, may be null).  All
 // loads are issued before any store so the L2 round trip is paid once (.cg: L2, not L1).
 template <int D>
-__device__ __forceinline__ void rmw_pair(double* __restrict__ rowA, int WA,
-                                         double* __restrict__ rowB, int WB,
-                                         double* __restrict__ rA,
+__device__ __forceinline__ void rmw_pair(double* __restrict__ rowA, int WA, bool ldA,
+                                         double* __restrict__ rowB, int WB, bool ldB,
+                                         double* __restrict__ rA, bool ldR,
                                          const double (&vA)[Fam<D>::NDPN][Fam<D>::NDPN],
                                          const double (&vB)[Fam<D>::NDPN][Fam<D>::NDPN],
                                          const double (&fA)[Fam<D>::NDPN]) {
@@ -108,18 +154,18 @@ __device__ __forceinline__ void rmw_pair(double* __restrict__ rowA, int WA,
   if constexpr (NDPN == 4) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      if (rowA) {
+      if (rowA && ldA) {
         const double2* q = reinterpret_cast<const double2*>(rowA + int64_t(i) * WA);
         const double2 a0 = __ldcg(q), a1 = __ldcg(q + 1);
         uA[i][0] = a0.x; uA[i][1] = a0.y; uA[i][2] = a1.x; uA[i][3] = a1.y;
       }
-      if (rowB) {
+      if (rowB && ldB) {
         const double2* q = reinterpret_cast<const double2*>(rowB + int64_t(i) * WB);
         const double2 b0 = __ldcg(q), b1 = __ldcg(q + 1);
         uB[i][0] = b0.x; uB[i][1] = b0.y; uB[i][2] = b1.x; uB[i][3] = b1.y;
       }
     }
-    if (rA) {
+    if (rA && ldR) {
       const double2* q = reinterpret_cast<const double2*>(rA);
       const double2 r0 = __ldcg(q), r1 = __ldcg(q + 1);
       uR[0] = r0.x; uR[1] = r0.y; uR[2] = r1.x; uR[3] = r1.y;
@@ -147,10 +193,10 @@ __device__ __forceinline__ void rmw_pair(double* __restrict__ rowA, int WA,
     for (int i = 0; i < NDPN; ++i)
 #pragma unroll
       for (int j = 0; j < NDPN; ++j) {
-        if (rowA) uA[i][j] = __ldcg(rowA + int64_t(i) * WA + j);
-        if (rowB) uB[i][j] = __ldcg(rowB + int64_t(i) * WB + j);
+        if (rowA && ldA) uA[i][j] = __ldcg(rowA + int64_t(i) * WA + j);
+        if (rowB && ldB) uB[i][j] = __ldcg(rowB + int64_t(i) * WB + j);
       }
-    if (rA)
+    if (rA && ldR)
 #pragma unroll
       for (int i = 0; i < NDPN; ++i) uR[i] = __ldcg(rA + i);
 #pragma unroll
@@ -207,16 +253,16 @@ k_sweep(DevMat m, SweepGeom G, const double* __restrict__ coords, const double* 
     for (int64_t s = s_first; s <= s_last; ++s)
       for (int c = 0; c < Cf::NCOL; ++c) {
         const int ci = c & 1;
-        const int64_t ifst = ilo + ((ilo & 1) != ci ? 1 : 0);
-        const int64_t ni = ifst < ihi ? (ihi - ifst + 1) / 2 : 0;
-        int64_t jfst = 0, nj = 1;
+        const int ifst = int(ilo) + ((ilo & 1) != ci ? 1 : 0);
+        const int ni = ifst < ihi ? (int(ihi) - ifst + 1) / 2 : 0;
+        int jfst = 0, nj = 1;
         if constexpr (D == 3) {
           const int cj = c >> 1;
-          jfst = jlo + ((jlo & 1) != cj ? 1 : 0);
-          nj = jfst < jhi ? (jhi - jfst + 1) / 2 : 0;
+          jfst = int(jlo) + ((jlo & 1) != cj ? 1 : 0);
+          nj = jfst < jhi ? (int(jhi) - jfst + 1) / 2 : 0;
         }
-        const int64_t nc = ni * nj;
-        for (int64_t b0 = 0; b0 < nc; b0 += E) body(s, b0, ifst, ni, jfst, nc);
+        const int nc = ni * nj;
+        for (int b0 = 0; b0 < nc; b0 += E) body(s, b0, ifst, ni, jfst, nc);
       }
   };
 
@@ -224,26 +270,25 @@ k_sweep(DevMat m, SweepGeom G, const double* __restrict__ coords, const double* 
     // ------------------------------ producer warps ------------------------------
     const int el = tid / NGP, g = tid % NGP;   // el may be >= E in padding threads
     int t = 0;
-    for_each_batch([&](int64_t s, int64_t b0, int64_t ifst, int64_t ni, int64_t jfst, int64_t nc) {
+    PT_DECL
+    for_each_batch([&](int64_t s, int b0, int ifst, int ni, int jfst, int nc) {
       const int buf = t & 1;
       if (t >= 2) bar_sync_empty(buf, Th::T);
-      const int64_t k = b0 + el;
+      PT_MARK(0, tid == 0);
+      const int k = b0 + el;
       if (el < E && k < nc) {
-        const int64_t i = ifst + 2 * (k % ni), j = jfst + 2 * (k / ni);
-        double X[NEN * D], U[NEN * NDPN];
-#pragma unroll
-        for (int a = 0; a < NEN; ++a) {
+        const int i = ifst + 2 * (k % ni), j = jfst + 2 * (k / ni);
+        auto nid = [&](int a) {
           int ox, oy, oz;
           node_off<D>(a, ox, oy, oz);
-          const int64_t n = node_id(i + ox, j + oy, s + oz);
-#pragma unroll
-          for (int q = 0; q < D; ++q) X[a * D + q] = __ldg(coords + n * D + q);
-#pragma unroll
-          for (int q = 0; q < NDPN; ++q) U[a * NDPN + q] = __ldg(dofs + n * NDPN + q);
-        }
-        const int64_t e = i + G.nx * (j + G.nyE * s);
+          return node_id(i + ox, j + oy, s + oz);
+        };
+        auto X = [&](int a, int q) { return __ldg(coords + nid(a) * D + q); };
+        auto U = [&](int a, int q) { return __ldg(dofs + nid(a) * NDPN + q); };
+        const int64_t e = i + G.nx * (j + G.nyE * s);  // int64: config 4 has 8M elements x 8 GPs
         gpCore<D>(m, X, U, __ldg(kappa + e * NGP + g), g, cores + (size_t(buf) * E * NGP + tid) * CS);
       }
+      PT_MARK(1, tid == 0);
       bar_arrive_full(buf, Th::T);
       ++t;
     });
@@ -261,53 +306,43 @@ k_sweep(DevMat m, SweepGeom G, const double* __restrict__ coords, const double* 
   node_off<D>(pb, obx, oby, obz);
   const int64_t cols_x = x1 - x0, cols = cols_x * (y1 - y0);
 
-  // first touch of the tile's block-rows in layer z: stage their val offsets in shared
-  // memory (one parallel load), then zero them (one warp per node, coalesced)
-  auto zero_layer = [&](int64_t z) {
+  // stage the val offsets of the tile's block-rows in layer z in shared memory
+  // (made visible by the consumer barrier that follows the expansion)
+  auto stage_layer = [&](int64_t z) {
     int64_t* sb = s_base_all[z & 1];
     for (int c = ct; c < cols; c += Th::C) {
       const int64_t x = x0 + c % cols_x, y = y0 + c / cols_x;
       sb[c] = base[node_id(x, y, z) - G.own_node_b];
     }
-    bar_sync<BAR_CONS>(Th::C);
-    const int warp = ct >> 5, lane = ct & 31;
-    for (int64_t c = warp; c < cols; c += Th::C / 32) {
-      const int64_t x = x0 + c % cols_x, y = y0 + c / cols_x;
-      int sl, W;
-      slot_of(G, x, y, z, 0, 0, 0, NDPN, sl, W);
-      double* row = val + sb[c];
-      const int n = NDPN * W;
-      if constexpr (NDPN == 4) {
-        for (int k = lane; k < n / 2; k += 32)
-          __stcg(reinterpret_cast<double2*>(row) + k, make_double2(0.0, 0.0));
-      } else {
-        for (int k = lane; k < n; k += 32) __stcg(row + k, 0.0);
-      }
-      if (lane < NDPN) __stcg(Rv + (node_id(x, y, z) - G.own_node_b) * NDPN + lane, 0.0);
-    }
   };
 
   int t = 0;
   int64_t cur_s = -1;
-  for_each_batch([&](int64_t s, int64_t b0, int64_t ifst, int64_t ni, int64_t jfst, int64_t nc) {
+  PT_DECL
+  for_each_batch([&](int64_t s, int b0, int ifst, int ni, int jfst, int nc) {
     const int buf = t & 1;
+    PT_MARK(7, ct == 0);
     if (s != cur_s) {
-      if (cur_s < 0 && s == z0) zero_layer(z0);
-      if (s + 1 >= z0 && s + 1 < z1) zero_layer(s + 1);
+      if (cur_s < 0 && s == z0) stage_layer(z0);
+      if (s + 1 >= z0 && s + 1 < z1) stage_layer(s + 1);
       cur_s = s;
     }
+    PT_MARK(2, ct == 0);
     bar_sync_full(buf, Th::T);
+    PT_MARK(3, ct == 0);
     // expansion: (element, GP, node) records from the compact GP states
     const double* cb = cores + size_t(buf) * E * NGP * CS;
     for (int it = ct; it < E * NGP * NEN; it += Th::C) {
       const int eg = it / NEN, a = it % NEN;
       if (b0 + eg / NGP < nc) gpExpand<D>(cb + eg * CS, a, eg % NGP, recs + size_t(eg) * GB + a * Rec<D>::STRIDE);
     }
+    PT_MARK(4, ct == 0);
     bar_sync<BAR_CONS>(Th::C);
+    PT_MARK(5, ct == 0);
     // pair Gauss sums and accumulation into the owned block-rows
-    const int64_t k = b0 + cel;
+    const int k = b0 + cel;
     if (cel < E && k < nc) {
-      const int64_t i = ifst + 2 * (k % ni), j = jfst + 2 * (k / ni);
+      const int i = ifst + 2 * (k % ni), j = jfst + 2 * (k / ni);
       const int64_t ax = i + oax, ay = j + oay, az = s + oaz;
       const int64_t bx = i + obx, by = j + oby, bz = s + obz;
       const bool own_a = ax >= x0 && ax < x1 && ay >= y0 && ay < y1 && az >= z0 && az < z1;
@@ -316,6 +351,7 @@ k_sweep(DevMat m, SweepGeom G, const double* __restrict__ coords, const double* 
         PairAcc<D> acc;
         phaseC<D, CS, Core<D>::MU, Core<D>::GHC>(recs + size_t(cel) * NGP * GB, cb + cel * NGP * CS,
                                                   pa, pb, acc);
+        PT_MARK(6, ct == 0);
         double vA[NDPN][NDPN], vB[NDPN][NDPN], fA[NDPN];
 #pragma unroll
         for (int r = 0; r < D; ++r) {
@@ -346,16 +382,24 @@ k_sweep(DevMat m, SweepGeom G, const double* __restrict__ coords, const double* 
           slot_of(G, bx, by, bz, oax - obx, oay - oby, oaz - obz, NDPN, sl, WB);
           rowB = val + s_base_all[bz & 1][(bx - x0) + cols_x * (by - y0)] + NDPN * sl;
         }
-        rmw_pair<D>(rowA, WA, rowB, WB, rA, vA, vB, fA);
+        const bool first = first_contrib<D>(G, i, j, int(s), int(ax), int(ay), int(az), int(bx),
+                                            int(by), int(bz));
+        const bool firstR = first_contrib<D>(G, i, j, int(s), int(ax), int(ay), int(az), int(ax),
+                                             int(ay), int(az));
+        rmw_pair<D>(rowA, WA, !first, rowB, WB, !first, rA, !firstR, vA, vB, fA);
       }
     }
+    PT_MARK(8, ct == 0);
     bar_arrive_empty(buf, Th::T);   // cores[buf] (incl. mu*, ghc read by phase C) is free
     bar_sync<BAR_CONS>(Th::C);
+    PT_MARK(9, ct == 0);
     ++t;
   });
 }
 
 }  // namespace lgdm
+
+#include "lgdm_sweep_acc.cuh"
 
 namespace {
 
@@ -410,11 +454,76 @@ template <int D> lgdm_status launch_sweep(lgdm_mesh m) {
   return check_launch(m, "k_sweep");
 }
 
+template <int D> lgdm_status launch_sweep_acc(lgdm_mesh m) {
+  using F = Fam<D>;
+  using Cf = AccCfg<D>;
+  using Th = AccThreads<D>;
+  SweepGeom G{};
+  G.nx = m->nx;
+  if (D == 3) {
+    G.nyE = m->ny;
+    G.nyN = m->ny + 1;
+    G.nl = m->nz;
+  } else {
+    G.nyE = 1;
+    G.nyN = 1;
+    G.nl = m->ny;
+  }
+  const int64_t per_layer = (G.nx + 1) * G.nyN;
+  G.lay_own_b = m->own_b / per_layer;
+  G.lay_own_e = m->own_e / per_layer;
+  G.own_node_b = m->own_b;
+  G.tiles_x = int((G.nx + 1 + Cf::TX - 1) / Cf::TX);
+  G.tiles_y = int((G.nyN + Cf::TY - 1) / Cf::TY);
+  const size_t smem = sizeof(double) * (size_t(2) * Cf::E * F::NGP * Core<D>::STRIDE +
+                                        size_t(Cf::E) * F::NGP * GpBlock<D>::STRIDE +
+                                        size_t(2) * Cf::TX * Cf::TY * AccLayout<D>::NODE_PAD);
+  static bool attr = false;
+  if (!attr) {
+    CU(cudaFuncSetAttribute(k_sweep_acc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr = true;
+  }
+  int nsm = 148, per_sm = 1;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_acc<D>, Th::T, smem);
+  per_sm = std::max(per_sm, 1);
+  const int64_t layers = G.lay_own_e - G.lay_own_b;
+  const int64_t tiles = int64_t(G.tiles_x) * G.tiles_y;
+  int64_t chunks = (4 * int64_t(nsm) * per_sm + tiles - 1) / tiles;
+  chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, (layers + 7) / 8));
+  G.chunk_len = (layers + chunks - 1) / chunks;
+  G.chunks = int((layers + G.chunk_len - 1) / G.chunk_len);
+  const int64_t grid = tiles * G.chunks;
+  k_sweep_acc<D><<<unsigned(grid), Th::T, smem, m->stream>>>(m->dm, G, m->coords, m->dofs,
+                                                              m->kappa, m->base, m->val, m->R);
+  return check_launch(m, "k_sweep_acc");
+}
+
 lgdm_status assemble_sweep(lgdm_mesh m) {
-  if (m->f.dim == 2) return launch_sweep<2>(m);
+  if (m->f.dim == 2) return launch_sweep_acc<2>(m);
   return launch_sweep<3>(m);
 }
 
 void sweep_free(lgdm_mesh) {}
+
+}  // namespace
+
+extern "C" int lgdm_debug_phase_cycles(unsigned long long* out16, int reset) {
+#ifdef LGDM_PHASE_TIMING
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out16, lgdm::g_phase, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(lgdm::g_phase, z, sizeof(z));
+  }
+  return 0;
+#else
+  (void)out16;
+  (void)reset;
+  return -1;
+#endif
+}
+
+namespace {
 
 }  // namespace

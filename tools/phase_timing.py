@@ -1,0 +1,31 @@
+"""Per-phase cycle breakdown of k_sweep (debug build tools/liblgdm_timing.so)."""
+import ctypes as C
+import sys
+import os
+import numpy as np
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import synth
+from paper_2301_06503_b200 import lgdm
+lgdm.LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "liblgdm_timing.so")
+L = lgdm.load()
+L.lgdm_debug_phase_cycles.argtypes = [C.c_void_p, C.c_int]
+names = ["prod: wait EMPTY", "prod: core", "cons: loop top", "cons: wait FULL", "cons: expansion",
+         "cons: barrier after expansion", "cons: pair sums(+acc)", "cons: other", "cons: RMW / flush+zero", "cons: end barrier"]
+for cid in [int(c) for c in sys.argv[1:]] or [3, 2]:
+    cfg = synth.CONFIGS[cid]
+    mesh = synth.structured_mesh(cfg)
+    d, k = synth.fields(cfg, mesh)
+    m = lgdm.Mesh(cfg.etype, mesh.coords, mesh.conn, lgdm.material(**synth.MATERIAL))
+    m.set_state(d, k)
+    m.assemble()
+    torch.cuda.synchronize()
+    buf = np.zeros(16, dtype=np.uint64)
+    L.lgdm_debug_phase_cycles(buf.ctypes.data, 1)
+    m.assemble()
+    torch.cuda.synchronize()
+    L.lgdm_debug_phase_cycles(buf.ctypes.data, 1)
+    tot = float(buf[2:10].sum())
+    print(cfg.name, "consumer total (per CTA-thread0, summed) %.3e cycles" % tot)
+    for i, n in enumerate(names):
+        print(f"  {n:32s} {float(buf[i]):.3e}  {100*float(buf[i])/tot:5.1f}%" if i >= 2 else f"  {n:32s} {float(buf[i]):.3e}")
