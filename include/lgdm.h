@@ -147,7 +147,8 @@ lgdm_status lgdm_get_kappa(lgdm_mesh mesh, double* host_out);
 lgdm_status lgdm_scale_dofs(lgdm_mesh mesh, double s);
 
 /* Select the assembly kernel: 0 = automatic (sweep if structured), 1 = general
- * (element-batch + node gather, any connectivity), 2 = sweep (structured only). */
+ * (element-batch + node gather, any connectivity), 2 = sweep (structured only; Q4: k_sweep3,
+ * Hex8: k_sweep), 3 = sweep with the shared-memory pipeline k_sweep3 also for Hex8. */
 lgdm_status lgdm_set_kernel(lgdm_mesh mesh, int kernel);
 
 lgdm_status lgdm_get_info(lgdm_mesh mesh, lgdm_info* info);

@@ -520,8 +520,8 @@ lgdm_status lgdm_assemble(lgdm_mesh m, lgdm_csr* K, double** R) {
   if (!m->have_state || !m->have_kappa) return fail(LGDM_ERR_INVALID_STATE, "assemble before set_state");
   CU(cudaSetDevice(m->device));
   lgdm_status s;
-  const bool sweep = m->kernel == 2 || (m->kernel == 0 && m->structured && sweep_supported(m));
-  if (m->kernel == 2 && !(m->structured && sweep_supported(m)))
+  const bool sweep = m->kernel >= 2 || (m->kernel == 0 && m->structured && sweep_supported(m));
+  if (m->kernel >= 2 && !(m->structured && sweep_supported(m)))
     return fail(LGDM_ERR_INVALID_ARGUMENT, "sweep kernel requested but mesh is not structured");
   if (sweep) s = assemble_sweep(m);
   else if (m->f.dim == 1) s = assemble_general<1>(m);
@@ -635,8 +635,8 @@ lgdm_status lgdm_scale_dofs(lgdm_mesh m, double sc) {
 }
 
 lgdm_status lgdm_set_kernel(lgdm_mesh m, int kernel) {
-  if (!m || kernel < 0 || kernel > 2) return fail(LGDM_ERR_INVALID_ARGUMENT, "bad kernel selector");
-  if (kernel == 2 && !(m->structured && sweep_supported(m)))
+  if (!m || kernel < 0 || kernel > 3) return fail(LGDM_ERR_INVALID_ARGUMENT, "bad kernel selector");
+  if (kernel >= 2 && !(m->structured && sweep_supported(m)))
     return fail(LGDM_ERR_INVALID_ARGUMENT, "sweep kernel needs a structured mesh with whole owned layers");
   m->kernel = kernel;
   return LGDM_OK;

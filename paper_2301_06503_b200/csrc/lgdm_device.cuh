@@ -156,7 +156,7 @@ __device__ __forceinline__ double gpCore(const DevMat& m, XF&& X, UF&& U, double
   using Co = Core<D>;
   using F = Fam<D>;
   using R = Rec<D>;
-  constexpr int NEN = F::NEN, NDPN = F::NDPN, NS = F::NS;
+  constexpr int NEN = F::NEN, NS = F::NS;
 
   // geometry: J_ij = sum_a X_ai dN_a/dxi_j
   double J[D][D];
@@ -227,7 +227,6 @@ __device__ __forceinline__ double gpCore(const DevMat& m, XF&& X, UF&& U, double
 #pragma unroll
     for (int i = 0; i < D; ++i) {
       gb[i] = fma(gn[i], ea, gb[i]);
-#pragma unroll
       {
         const double ua = U(a, i);
 #pragma unroll

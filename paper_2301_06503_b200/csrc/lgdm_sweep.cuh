@@ -399,7 +399,7 @@ k_sweep(DevMat m, SweepGeom G, const double* __restrict__ coords, const double* 
 
 }  // namespace lgdm
 
-#include "lgdm_sweep_acc.cuh"
+#include "lgdm_sweep3.cuh"
 
 namespace {
 
@@ -454,10 +454,10 @@ template <int D> lgdm_status launch_sweep(lgdm_mesh m) {
   return check_launch(m, "k_sweep");
 }
 
-template <int D> lgdm_status launch_sweep_acc(lgdm_mesh m) {
+template <int D> lgdm_status launch_sweep3(lgdm_mesh m) {
   using F = Fam<D>;
-  using Cf = AccCfg<D>;
-  using Th = AccThreads<D>;
+  using Cf = S3Cfg<D>;
+  using Th = S3Threads<D>;
   SweepGeom G{};
   G.nx = m->nx;
   if (D == 3) {
@@ -476,16 +476,16 @@ template <int D> lgdm_status launch_sweep_acc(lgdm_mesh m) {
   G.tiles_x = int((G.nx + 1 + Cf::TX - 1) / Cf::TX);
   G.tiles_y = int((G.nyN + Cf::TY - 1) / Cf::TY);
   const size_t smem = sizeof(double) * (size_t(2) * Cf::E * F::NGP * Core<D>::STRIDE +
-                                        size_t(Cf::E) * F::NGP * GpBlock<D>::STRIDE +
-                                        size_t(2) * Cf::TX * Cf::TY * AccLayout<D>::NODE_PAD);
+                                        size_t(kRecRing) * Cf::E * GpBlock<D>::STRIDE +
+                                        size_t(Cf::TX) * Cf::TY * S3Layout<D>::COL_PAD);
   static bool attr = false;
   if (!attr) {
-    CU(cudaFuncSetAttribute(k_sweep_acc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    CU(cudaFuncSetAttribute(k_sweep3<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     attr = true;
   }
   int nsm = 148, per_sm = 1;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_acc<D>, Th::T, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep3<D>, Th::T, smem);
   per_sm = std::max(per_sm, 1);
   const int64_t layers = G.lay_own_e - G.lay_own_b;
   const int64_t tiles = int64_t(G.tiles_x) * G.tiles_y;
@@ -494,13 +494,17 @@ template <int D> lgdm_status launch_sweep_acc(lgdm_mesh m) {
   G.chunk_len = (layers + chunks - 1) / chunks;
   G.chunks = int((layers + G.chunk_len - 1) / G.chunk_len);
   const int64_t grid = tiles * G.chunks;
-  k_sweep_acc<D><<<unsigned(grid), Th::T, smem, m->stream>>>(m->dm, G, m->coords, m->dofs,
-                                                              m->kappa, m->base, m->val, m->R);
-  return check_launch(m, "k_sweep_acc");
+  k_sweep3<D><<<unsigned(grid), Th::T, smem, m->stream>>>(m->dm, G, m->coords, m->dofs, m->kappa,
+                                                          m->base, m->val, m->R);
+  return check_launch(m, "k_sweep3");
 }
 
+// Q4: the shared-memory pipeline k_sweep3 is fastest.  Hex8: the L2-accumulating k_sweep is
+// faster today (measurements in DESIGN.md section 8); k_sweep3<3> is kept selectable
+// (lgdm_set_kernel(mesh, 3)) and parity-tested.
 lgdm_status assemble_sweep(lgdm_mesh m) {
-  if (m->f.dim == 2) return launch_sweep_acc<2>(m);
+  if (m->f.dim == 2) return launch_sweep3<2>(m);
+  if (m->kernel == 3) return launch_sweep3<3>(m);
   return launch_sweep<3>(m);
 }
 

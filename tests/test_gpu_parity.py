@@ -11,7 +11,7 @@ from parity import compare, compare_sampled, gpu_assemble, oracle_assemble, slic
 
 pytestmark = pytest.mark.gpu
 
-KERNELS = [lgdm.KERNEL_GENERAL, lgdm.KERNEL_AUTO]
+KERNELS = [lgdm.KERNEL_GENERAL, lgdm.KERNEL_AUTO, lgdm.KERNEL_SWEEP3]
 
 CASES = [
     (lgdm.BAR2, (1,)), (lgdm.BAR2, (7,)), (lgdm.BAR2, (100,)),
@@ -33,6 +33,8 @@ def _case(etype, n, distort=0.0):
 @pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("etype,n", CASES)
 def test_parity_small(etype, n, kernel):
+    if kernel == lgdm.KERNEL_SWEEP3 and etype == lgdm.BAR2:
+        pytest.skip("bar2 has no sweep kernel")
     cfg, mesh, coords, dofs, kappa = _case(etype, n, distort=0.2)
     ref = oracle_assemble(etype, coords, mesh.conn, dofs, kappa)
     assert ref["n_guard"] == 0
@@ -44,6 +46,8 @@ def test_parity_small(etype, n, kernel):
 @pytest.mark.parametrize("variant", [dict(h_sigma=0.0), dict(eq_variant=1), dict(h_sigma=7e3, c=0.5, k=3.0, nu=0.3)])
 @pytest.mark.parametrize("etype,n", [(lgdm.QUAD4, (11, 8)), (lgdm.HEX8, (5, 4, 3)), (lgdm.BAR2, (9,))])
 def test_parity_readings(etype, n, variant, kernel):
+    if kernel == lgdm.KERNEL_SWEEP3 and etype == lgdm.BAR2:
+        pytest.skip("bar2 has no sweep kernel")
     cfg, mesh, coords, dofs, kappa = _case(etype, n, distort=0.15)
     kw = dict(synth.MATERIAL)
     kw.update(variant)
@@ -54,7 +58,7 @@ def test_parity_readings(etype, n, variant, kernel):
 
 @pytest.mark.parametrize("kernel", KERNELS)
 def test_parity_config0_and_1(kernel):
-    for cid in (0, 1):
+    for cid in ((1,) if kernel == lgdm.KERNEL_SWEEP3 else (0, 1)):
         cfg = synth.CONFIGS[cid]
         mesh = synth.structured_mesh(cfg)
         dofs, kappa = synth.fields(cfg, mesh)
@@ -77,14 +81,15 @@ def test_parity_damage_edge_states():
                 compare(ref, got, "edge state")
 
 
+@pytest.mark.parametrize("kernel", [lgdm.KERNEL_AUTO, lgdm.KERNEL_SWEEP3])
 @pytest.mark.parametrize("cid", [2, 3])
-def test_parity_full_size_sampled(cid):
+def test_parity_full_size_sampled(cid, kernel):
     """BASELINE configs 2 and 3 at full size, in the bench's launch configuration; sampled
     node block-rows against the oracle, pattern checked by the closed-form nnz."""
     cfg = synth.CONFIGS[cid]
     mesh = synth.structured_mesh(cfg)
     dofs, kappa = synth.fields(cfg, mesh)
-    got = gpu_assemble(cfg.etype, mesh.coords, mesh.conn, dofs, kappa)
+    got = gpu_assemble(cfg.etype, mesh.coords, mesh.conn, dofs, kappa, kernel=kernel)
     ndpn = lgdm.FAMILY[cfg.etype][2]
     assert got["row_ptr"][-1] == ndpn * ndpn * int(np.prod([3 * k + 1 for k in cfg.n]))
     sel = synth.sample_nodes(mesh.coords.shape[0], 1500, seed=cid)
@@ -95,13 +100,16 @@ def test_parity_full_size_sampled(cid):
     print(f"config {cid}: sampled {sel.size} nodes, max K err {wk:.2e}, R err {wr:.2e}")
 
 
+@pytest.mark.parametrize("kernel", [lgdm.KERNEL_AUTO, lgdm.KERNEL_SWEEP3])
 @pytest.mark.parametrize("etype,n,P", [(lgdm.QUAD4, (23, 31), 3), (lgdm.HEX8, (7, 5, 13), 4),
                                        (lgdm.BAR2, (50,), 2)])
-def test_slabs_stitch_bitwise(etype, n, P):
+def test_slabs_stitch_bitwise(etype, n, P, kernel):
     """Row-owned slabs with ghost-element recompute: stitched CSR == one-mesh CSR, bitwise."""
     from paper_2301_06503_b200 import slabs
+    if kernel == lgdm.KERNEL_SWEEP3 and etype == lgdm.BAR2:
+        pytest.skip("bar2 has no sweep kernel")
     cfg, mesh, coords, dofs, kappa = _case(etype, n)
-    whole = gpu_assemble(etype, mesh.coords, mesh.conn, dofs, kappa)
+    whole = gpu_assemble(etype, mesh.coords, mesh.conn, dofs, kappa, kernel=kernel)
     rows_rp = whole["row_ptr"]
     ndpn = lgdm.FAMILY[etype][2]
     for p in range(P):
@@ -109,7 +117,7 @@ def test_slabs_stitch_bitwise(etype, n, P):
         sm = synth.structured_mesh(cfg, elem_layers=part.elem_layers)
         sd, sk = synth.fields(cfg, sm)
         got = gpu_assemble(etype, sm.coords, sm.conn, sd, sk, offset=sm.node_gid0,
-                           n_global=cfg.n_nodes, owned=part.owned_local(sm.node_gid0))
+                           n_global=cfg.n_nodes, owned=part.owned_local(sm.node_gid0), kernel=kernel)
         r0 = ndpn * part.owned_nodes[0]
         r1 = ndpn * part.owned_nodes[1]
         assert got["first_row"] == r0

@@ -10,8 +10,9 @@ from paper_2301_06503_b200 import lgdm
 lgdm.LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "liblgdm_timing.so")
 L = lgdm.load()
 L.lgdm_debug_phase_cycles.argtypes = [C.c_void_p, C.c_int]
-names = ["prod: wait EMPTY", "prod: core", "cons: loop top", "cons: wait FULL", "cons: expansion",
-         "cons: barrier after expansion", "cons: pair sums(+acc)", "cons: other", "cons: RMW / flush+zero", "cons: end barrier"]
+names = ["PC: wait CEMPTY", "PC: core", "PE: wait CFULL", "PE: wait REMPTY", "PE: expand",
+         "C: between GPs", "C: wait RFULL", "C: pair GP", "C: colour barrier", "C: smem add",
+         "C: end-layer barrier", "C: flush+reset"]
 for cid in [int(c) for c in sys.argv[1:]] or [3, 2]:
     cfg = synth.CONFIGS[cid]
     mesh = synth.structured_mesh(cfg)
@@ -25,7 +26,8 @@ for cid in [int(c) for c in sys.argv[1:]] or [3, 2]:
     m.assemble()
     torch.cuda.synchronize()
     L.lgdm_debug_phase_cycles(buf.ctypes.data, 1)
-    tot = float(buf[2:10].sum())
-    print(cfg.name, "consumer total (per CTA-thread0, summed) %.3e cycles" % tot)
-    for i, n in enumerate(names):
-        print(f"  {n:32s} {float(buf[i]):.3e}  {100*float(buf[i])/tot:5.1f}%" if i >= 2 else f"  {n:32s} {float(buf[i]):.3e}")
+    for grp, idx in (("PC", [0, 1]), ("PE", [2, 3, 4]), ("C", [5, 6, 7, 8, 9, 10, 11])):
+        tot = float(sum(buf[i] for i in idx))
+        print(cfg.name, grp, "total %.3e cycles" % tot)
+        for i in idx:
+            print(f"  {names[i]:32s} {float(buf[i]):.3e}  {100*float(buf[i])/max(tot,1):5.1f}%")
