@@ -41,6 +41,21 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def measured_traffic(workload: str):
+    """DRAM bytes per launch of the assembly kernel from the latest committed ncu capture
+    (profiles/rNN/traffic.json), or None."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "traffic.json")), reverse=True):
+        try:
+            with open(path) as f:
+                t = json.load(f)
+            if workload in t:
+                return float(t[workload])
+        except Exception:
+            pass
+    return None
+
+
 def algorithmic_bytes(ndpn, dim, nen, ngp, nnz, n_rows, n_nodes, n_elems):
     """8 nnz (K) + 8 ndof (R) + 8 ndof (dofs) + 8 nel ngp (kappa) + 8 d nnodes
     (coords) + 4 nen nel (conn); rows/dofs/elements are the rank's own."""
@@ -251,7 +266,8 @@ def secondary(cid, steps, warmup, peak):
             "ms_per_step": r["ms_per_step"], "assemble_ms": r["assemble_ms"],
             "assemble_elements_per_s": cfg.n_elems / (r["assemble_ms"] * 1e-3),
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                         "frac": ach / peak, "traffic": None},
+                         "frac": ach / peak, "traffic": measured_traffic(cfg.name),
+                         "algorithmic_bytes": r["alg_bytes"]},
             "clocks": r["clocks"]}
 
 
@@ -346,7 +362,8 @@ def main():
         "assemble_ms": r["assemble_ms"],
         "assemble_elements_per_s": n_total / (r["assemble_ms"] * 1e-3) if ws == 1 else None,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                     "frac": achieved / peak, "traffic": measured_traffic(cfg.name) if ws == 1 else None,
+                     "algorithmic_bytes": r["alg_bytes"], "peak_source": peak_src,
                      "kernel": "lgdm_assemble (all launches of one call), rank max"},
         "gpu_launches": r["launches"],
         "clocks": r["clocks"],
