@@ -400,6 +400,7 @@ k_sweep(DevMat m, SweepGeom G, const double* __restrict__ coords, const double* 
 }  // namespace lgdm
 
 #include "lgdm_sweep3.cuh"
+#include "lgdm_sweep4.cuh"
 
 namespace {
 
@@ -499,12 +500,45 @@ template <int D> lgdm_status launch_sweep3(lgdm_mesh m) {
   return check_launch(m, "k_sweep3");
 }
 
+lgdm_status launch_sweep4(lgdm_mesh m) {
+  SweepGeom G{};
+  G.nx = m->nx;
+  G.nyE = m->ny;
+  G.nyN = m->ny + 1;
+  G.nl = m->nz;
+  const int64_t per_layer = (G.nx + 1) * G.nyN;
+  G.lay_own_b = m->own_b / per_layer;
+  G.lay_own_e = m->own_e / per_layer;
+  G.own_node_b = m->own_b;
+  G.tiles_x = int((G.nx + 1 + S4::TX - 1) / S4::TX);
+  G.tiles_y = int((G.nyN + S4::TY - 1) / S4::TY);
+  static bool attr = false;
+  if (!attr) {
+    CU(cudaFuncSetAttribute(k_sweep4, cudaFuncAttributeMaxDynamicSharedMemorySize, int(S4::SMEM)));
+    attr = true;
+  }
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device);
+  const int64_t layers = G.lay_own_e - G.lay_own_b;
+  const int64_t tiles = int64_t(G.tiles_x) * G.tiles_y;
+  // ~2 waves of one CTA per SM, chunks of at least 8 layers (each chunk recomputes one layer)
+  int64_t chunks = (2 * int64_t(nsm) + tiles - 1) / tiles;
+  chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, (layers + 7) / 8));
+  G.chunk_len = (layers + chunks - 1) / chunks;
+  G.chunks = int((layers + G.chunk_len - 1) / G.chunk_len);
+  const int64_t grid = tiles * G.chunks;
+  k_sweep4<<<unsigned(grid), S4::T, S4::SMEM, m->stream>>>(m->dm, G, m->coords, m->dofs, m->kappa,
+                                                           m->base, m->val, m->R);
+  return check_launch(m, "k_sweep4");
+}
+
 // Q4: the shared-memory pipeline k_sweep3 is fastest.  Hex8: the L2-accumulating k_sweep is
 // faster today (measurements in DESIGN.md section 8); k_sweep3<3> is kept selectable
 // (lgdm_set_kernel(mesh, 3)) and parity-tested.
 lgdm_status assemble_sweep(lgdm_mesh m) {
   if (m->f.dim == 2) return launch_sweep3<2>(m);
   if (m->kernel == 3) return launch_sweep3<3>(m);
+  if (m->kernel == 4) return launch_sweep4(m);
   return launch_sweep<3>(m);
 }
 

@@ -11,7 +11,8 @@ from parity import compare, compare_sampled, gpu_assemble, oracle_assemble, slic
 
 pytestmark = pytest.mark.gpu
 
-KERNELS = [lgdm.KERNEL_GENERAL, lgdm.KERNEL_AUTO, lgdm.KERNEL_SWEEP3]
+KERNELS = [lgdm.KERNEL_GENERAL, lgdm.KERNEL_AUTO, lgdm.KERNEL_SWEEP3, lgdm.KERNEL_SWEEP4]
+SWEEPS = (lgdm.KERNEL_SWEEP3, lgdm.KERNEL_SWEEP4)
 
 CASES = [
     (lgdm.BAR2, (1,)), (lgdm.BAR2, (7,)), (lgdm.BAR2, (100,)),
@@ -33,7 +34,7 @@ def _case(etype, n, distort=0.0):
 @pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("etype,n", CASES)
 def test_parity_small(etype, n, kernel):
-    if kernel == lgdm.KERNEL_SWEEP3 and etype == lgdm.BAR2:
+    if kernel in SWEEPS and etype == lgdm.BAR2:
         pytest.skip("bar2 has no sweep kernel")
     cfg, mesh, coords, dofs, kappa = _case(etype, n, distort=0.2)
     ref = oracle_assemble(etype, coords, mesh.conn, dofs, kappa)
@@ -46,7 +47,7 @@ def test_parity_small(etype, n, kernel):
 @pytest.mark.parametrize("variant", [dict(h_sigma=0.0), dict(eq_variant=1), dict(h_sigma=7e3, c=0.5, k=3.0, nu=0.3)])
 @pytest.mark.parametrize("etype,n", [(lgdm.QUAD4, (11, 8)), (lgdm.HEX8, (5, 4, 3)), (lgdm.BAR2, (9,))])
 def test_parity_readings(etype, n, variant, kernel):
-    if kernel == lgdm.KERNEL_SWEEP3 and etype == lgdm.BAR2:
+    if kernel in SWEEPS and etype == lgdm.BAR2:
         pytest.skip("bar2 has no sweep kernel")
     cfg, mesh, coords, dofs, kappa = _case(etype, n, distort=0.15)
     kw = dict(synth.MATERIAL)
@@ -58,7 +59,7 @@ def test_parity_readings(etype, n, variant, kernel):
 
 @pytest.mark.parametrize("kernel", KERNELS)
 def test_parity_config0_and_1(kernel):
-    for cid in ((1,) if kernel == lgdm.KERNEL_SWEEP3 else (0, 1)):
+    for cid in ((1,) if kernel in SWEEPS else (0, 1)):
         cfg = synth.CONFIGS[cid]
         mesh = synth.structured_mesh(cfg)
         dofs, kappa = synth.fields(cfg, mesh)
@@ -81,7 +82,7 @@ def test_parity_damage_edge_states():
                 compare(ref, got, "edge state")
 
 
-@pytest.mark.parametrize("kernel", [lgdm.KERNEL_AUTO, lgdm.KERNEL_SWEEP3])
+@pytest.mark.parametrize("kernel", [lgdm.KERNEL_AUTO, lgdm.KERNEL_SWEEP3, lgdm.KERNEL_SWEEP4])
 @pytest.mark.parametrize("cid", [2, 3])
 def test_parity_full_size_sampled(cid, kernel):
     """BASELINE configs 2 and 3 at full size, in the bench's launch configuration; sampled
@@ -100,13 +101,13 @@ def test_parity_full_size_sampled(cid, kernel):
     print(f"config {cid}: sampled {sel.size} nodes, max K err {wk:.2e}, R err {wr:.2e}")
 
 
-@pytest.mark.parametrize("kernel", [lgdm.KERNEL_AUTO, lgdm.KERNEL_SWEEP3])
+@pytest.mark.parametrize("kernel", [lgdm.KERNEL_AUTO, lgdm.KERNEL_SWEEP3, lgdm.KERNEL_SWEEP4])
 @pytest.mark.parametrize("etype,n,P", [(lgdm.QUAD4, (23, 31), 3), (lgdm.HEX8, (7, 5, 13), 4),
                                        (lgdm.BAR2, (50,), 2)])
 def test_slabs_stitch_bitwise(etype, n, P, kernel):
     """Row-owned slabs with ghost-element recompute: stitched CSR == one-mesh CSR, bitwise."""
     from paper_2301_06503_b200 import slabs
-    if kernel == lgdm.KERNEL_SWEEP3 and etype == lgdm.BAR2:
+    if kernel in SWEEPS and etype == lgdm.BAR2:
         pytest.skip("bar2 has no sweep kernel")
     cfg, mesh, coords, dofs, kappa = _case(etype, n)
     whole = gpu_assemble(etype, mesh.coords, mesh.conn, dofs, kappa, kernel=kernel)
