@@ -146,9 +146,13 @@ lgdm_status lgdm_get_kappa(lgdm_mesh mesh, double* host_out);
 /* dofs *= s on device (benchmark helper: dofs_t = (1 + 0.05 t) dofs_0, SURVEY 8d cfg 2). */
 lgdm_status lgdm_scale_dofs(lgdm_mesh mesh, double s);
 
-/* Select the assembly kernel: 0 = automatic (sweep if structured), 1 = general
- * (element-batch + node gather, any connectivity), 2 = sweep (structured only; Q4: k_sweep3,
- * Hex8: k_sweep), 3 = sweep with the shared-memory pipeline k_sweep3 also for Hex8. */
+/* Select the assembly kernel (all produce the same K and R up to rounding, parity-tested):
+ *   0 = automatic: structured meshes (x-fastest grids, whole owned layers) -> 4, else 1
+ *   1 = general (element-batch + node gather, any connectivity)
+ *   2 = first structured sweep (Q4: k_sweep3, Hex8: k_sweep, L2-accumulating)
+ *   3 = shared-memory pipeline k_sweep3 (Q4 and Hex8)
+ *   4 = round-1 redesign: Q4 k_sweepq, Hex8 k_sweep4 (row-sum diagonals)
+ * Kernels 2-4 need a structured mesh: LGDM_ERR_INVALID_ARGUMENT otherwise. */
 lgdm_status lgdm_set_kernel(lgdm_mesh mesh, int kernel);
 
 lgdm_status lgdm_get_info(lgdm_mesh mesh, lgdm_info* info);

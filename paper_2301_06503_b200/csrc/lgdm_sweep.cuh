@@ -401,6 +401,7 @@ k_sweep(DevMat m, SweepGeom G, const double* __restrict__ coords, const double* 
 
 #include "lgdm_sweep3.cuh"
 #include "lgdm_sweep4.cuh"
+#include "lgdm_sweepq.cuh"
 
 namespace {
 
@@ -500,6 +501,26 @@ template <int D> lgdm_status launch_sweep3(lgdm_mesh m) {
   return check_launch(m, "k_sweep3");
 }
 
+// Chunking of the sweep axis: each chunk of len node layers processes len + 1 element layers
+// (one recomputed).  Pick the chunk count that minimises waves x (len + 1), i.e. the
+// makespan of tiles x chunks equal CTAs on per_wave resident slots.
+inline int64_t pick_chunks(int64_t tiles, int64_t layers, int64_t per_wave, int64_t min_len) {
+  int64_t best = 1;
+  double best_t = 1e300;
+  for (int64_t c = 1; c <= std::max<int64_t>(1, layers); ++c) {
+    const int64_t len = (layers + c - 1) / c;
+    if (c > 1 && len < min_len) break;
+    const int64_t n = (layers + len - 1) / len;
+    const int64_t waves = (tiles * n + per_wave - 1) / per_wave;
+    const double t = double(waves) * double(len + 1);
+    if (t < best_t * 0.999) {
+      best_t = t;
+      best = n;
+    }
+  }
+  return best;
+}
+
 lgdm_status launch_sweep4(lgdm_mesh m) {
   SweepGeom G{};
   G.nx = m->nx;
@@ -521,9 +542,7 @@ lgdm_status launch_sweep4(lgdm_mesh m) {
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device);
   const int64_t layers = G.lay_own_e - G.lay_own_b;
   const int64_t tiles = int64_t(G.tiles_x) * G.tiles_y;
-  // ~2 waves of one CTA per SM, chunks of at least 8 layers (each chunk recomputes one layer)
-  int64_t chunks = (2 * int64_t(nsm) + tiles - 1) / tiles;
-  chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, (layers + 7) / 8));
+  const int64_t chunks = pick_chunks(tiles, layers, nsm, 8);
   G.chunk_len = (layers + chunks - 1) / chunks;
   G.chunks = int((layers + G.chunk_len - 1) / G.chunk_len);
   const int64_t grid = tiles * G.chunks;
@@ -532,14 +551,44 @@ lgdm_status launch_sweep4(lgdm_mesh m) {
   return check_launch(m, "k_sweep4");
 }
 
-// Q4: the shared-memory pipeline k_sweep3 is fastest.  Hex8: the L2-accumulating k_sweep is
-// faster today (measurements in DESIGN.md section 8); k_sweep3<3> is kept selectable
-// (lgdm_set_kernel(mesh, 3)) and parity-tested.
+lgdm_status launch_sweepq(lgdm_mesh m) {
+  SweepGeom G{};
+  G.nx = m->nx;
+  G.nyE = 1;
+  G.nyN = 1;
+  G.nl = m->ny;
+  const int64_t per_layer = G.nx + 1;
+  G.lay_own_b = m->own_b / per_layer;
+  G.lay_own_e = m->own_e / per_layer;
+  G.own_node_b = m->own_b;
+  G.tiles_x = int((G.nx + 1 + SQ::TX - 1) / SQ::TX);
+  G.tiles_y = 1;
+  static bool attr = false;
+  if (!attr) {
+    CU(cudaFuncSetAttribute(k_sweepq, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SQ::SMEM)));
+    attr = true;
+  }
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device);
+  const int64_t layers = G.lay_own_e - G.lay_own_b;
+  const int64_t tiles = G.tiles_x;
+  const int64_t chunks = pick_chunks(tiles, layers, nsm, 8);
+  G.chunk_len = (layers + chunks - 1) / chunks;
+  G.chunks = int((layers + G.chunk_len - 1) / G.chunk_len);
+  const int64_t grid = tiles * G.chunks;
+  k_sweepq<<<unsigned(grid), SQ::T, SQ::SMEM, m->stream>>>(m->dm, G, m->coords, m->dofs, m->kappa,
+                                                           m->base, m->val, m->R);
+  return check_launch(m, "k_sweepq");
+}
+
+// Automatic choice (kernel 0 or 2): the round-1 redesigns k_sweepq (Q4) and k_sweep4 (Hex8)
+// are the fastest measured; k_sweep / k_sweep3 stay selectable (2 / 3)
+// and parity-tested.
 lgdm_status assemble_sweep(lgdm_mesh m) {
-  if (m->f.dim == 2) return launch_sweep3<2>(m);
+  if (m->f.dim == 2) return m->kernel == 3 ? launch_sweep3<2>(m) : m->kernel == 2 ? launch_sweep3<2>(m) : launch_sweepq(m);
   if (m->kernel == 3) return launch_sweep3<3>(m);
-  if (m->kernel == 4) return launch_sweep4(m);
-  return launch_sweep<3>(m);
+  if (m->kernel == 2) return launch_sweep<3>(m);
+  return launch_sweep4(m);
 }
 
 void sweep_free(lgdm_mesh) {}

@@ -21,11 +21,11 @@
 //     Gauss point, only one per batch (the core ring).
 //  3. Node sums (R = F, U, V) accumulate in registers and are reduced with shuffles.
 //  4. The Appendix A core (exp, sqrt, divide: a long FP64 dependency chain) runs in two PC
-//     warp pairs on alternate batches, 3-slot core ring, 16-byte core stores/loads.
+//     warp pairs on alternate batches, one core slot each, 16-byte core stores/loads.
 //  5. Flush: vectorised row copies, the -sum of plane -1 kept in the (never accumulated)
 //     self slot of plane 0.
 //
-//   PC warps (element x GP)   gpCore -> core ring [3][E][NGP][CSP]
+//   PC warps (element x GP)   gpCore -> core slots [2][E][NGP][CSP] (one per PC pair)
 //   C  warps (one per element) expansions -> records [4 GP][8 node]; Gauss sums of the 28
 //                              off-diagonal pairs; adds into the block-row planes; flush
 #pragma once
@@ -42,7 +42,7 @@ struct S4 {
   // core ring [3][E][NGP][CSP]: core = Core<3> values with a pad after J^-1 so every field
   // group is 16-byte aligned (48 doubles); CSP = 50 (25 x 16 B) puts the 4 cores a C warp
   // reads at once into distinct bank groups
-  static constexpr int CSP = 50, CEL = NGP * CSP + 2, CSLOT = E * CEL;
+  static constexpr int CSP = 50, CEL = NGP * CSP + 2, CSLOT = E * CEL, NCSLOT = 2;
   // warp-private records [4 GP][8 node][RS] + (mu*, ghc) per GP
   static constexpr int RS = 22, RGP = NEN * RS + 2, RWARP = 4 * RGP;
   // accumulator column: planes Z0, Z1 (in-plane, by node-layer parity), UP, DN; each plane
@@ -50,10 +50,10 @@ struct S4 {
   static constexpr int PL = 146, Z0 = 0, Z1 = PL, UP = 2 * PL, DN = 3 * PL, NS = 4 * PL,
                        COL = NS + 16 + 2;                 // 602 doubles = 301 x 16 B (odd)
   static constexpr int NCOLS = TX * TY;
-  static constexpr size_t SMEM = sizeof(double) * (size_t(SHT) + size_t(3) * CSLOT +
+  static constexpr size_t SMEM = sizeof(double) * (size_t(SHT) + size_t(NCSLOT) * CSLOT +
                                                    size_t(NC) * RWARP + size_t(NCOLS) * COL);
-  // named barriers: core full 1-3, core empty 4-6, C warps 7
-  static constexpr int B_CF = 1, B_CE = 4, B_C = 7;
+  // named barriers: core full 1-2, core empty 3-4 (slot = PC pair), C warps 5
+  static constexpr int B_CF = 1, B_CE = 3, B_C = 5;
 };
 
 // shifted Core<3> offsets in the ring (J^-1 at 0..8, pad, then the rest +1)
@@ -161,7 +161,7 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
   extern __shared__ double sm[];
   double* shtab = sm;                              // [NGP][NEN][4]
   double* cores = shtab + S4::SHT;                 // [3][E][CEL]
-  double* recs = cores + 3 * S4::CSLOT;            // [NC][RWARP]
+  double* recs = cores + S4::NCSLOT * S4::CSLOT;   // [NC][RWARP]
   double* acc = recs + S4::NC * S4::RWARP;         // [NCOLS][COL]
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -222,8 +222,8 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
     schedule(
         [&](int64_t s, int, int b0, int ifst, int ni, int jfst, int nc) {
           if ((t & 1) == pair) {
-            const int slot = t % 3;
-            if (t >= 3) bsync(S4::B_CE + slot, NPC_T + NC_T);
+            const int slot = pair;   // each PC pair owns one core slot (fixed producer)
+            if (t >= 2) bsync(S4::B_CE + slot, NPC_T + NC_T);
             const int k = b0 + el;
             if (k < nc) {
               const int i = ifst + 2 * (k % ni), j = jfst + 2 * (k / ni);
@@ -251,9 +251,9 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
           ++t;
         },
         [](int64_t) {});
-    // drain: the core-empty arrivals of the last three batches (the syncs batch t+3 would do)
-    for (int tt = max(t - 3, 0); tt < t; ++tt)
-      if (((tt + 3) & 1) == pair) bsync(S4::B_CE + tt % 3, NPC_T + NC_T);
+    // drain: the core-empty arrival of this pair's last batch
+    for (int tt = max(t - 2, 0); tt < t; ++tt)
+      if ((tt & 1) == pair) bsync(S4::B_CE + pair, NPC_T + NC_T);
     return;
   }
 
@@ -341,7 +341,7 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
       [&](int64_t s, int c, int b0, int ifst, int ni, int jfst, int nc) {
         const int k = b0 + cw;
         const bool live = k < nc;   // warp-uniform
-        const int cslot = t % 3;
+        const int cslot = t & 1;
         ++t;
         bsync(S4::B_CF + cslot, NPC_T + NC_T);
         if (!live) {
