@@ -236,6 +236,17 @@ def run_lgdm(cfg, steps, warmup, rank, world, local, pg_barrier, allmax, comm_ui
     return res
 
 
+def kernel_name(etype, structured, kernel):
+    """Assembly kernel that lgdm_assemble runs (lgdm_set_kernel, include/lgdm.h)."""
+    if not structured or kernel == 1 or etype == 1:
+        return "k_elem_blocks + k_gather (general path)"
+    if kernel in (0, 4):
+        return "k_sweep4 (Hex8 structured sweep)" if etype == 3 else "k_sweepq (Q4 structured sweep)"
+    if kernel == 3:
+        return "k_sweep3 (shared-memory pipeline sweep)"
+    return "k_sweep (L2 sweep)" if etype == 3 else "k_sweep3 (shared-memory pipeline sweep)"
+
+
 def cpu_baseline(cfg, target_s=15.0):
     """The oracle as it stands, single-threaded, on a bounded sample of the workload: the first
     element layers of the same mesh (all layers are statistically alike)."""
@@ -261,7 +272,7 @@ def secondary(cid, steps, warmup, peak):
     r = run_lgdm(cfg, steps, warmup, 0, 1, int(os.environ.get("LOCAL_RANK", "0")),
                  lambda: None, lambda x: x, e2e=False)
     ach = r["alg_bytes"] / (r["assemble_ms"] * 1e-3) / 1e9
-    return {"workload": cfg.name, "config": cid,
+    return {"workload": cfg.name, "config": cid, "kernel": kernel_name(cfg.etype, True, 0),
             "value": cfg.n_elems / (r["ms_per_step"] * 1e-3), "unit": UNIT,
             "ms_per_step": r["ms_per_step"], "assemble_ms": r["assemble_ms"],
             "assemble_elements_per_s": cfg.n_elems / (r["assemble_ms"] * 1e-3),
@@ -308,7 +319,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", default="lgdm", choices=["lgdm", "reference"])
-    ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 general, 2 sweep")
+    ap.add_argument("--kernel", type=int, default=0, help="lgdm_set_kernel: 0 auto, 1 general, 2-4 sweeps")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -357,8 +368,7 @@ def main():
                    "parallelism": f"z-slabs x{ws}, ghost-element recompute",
                    "step": "assemble + residual_norms(allreduce) + update_history + dofs scale",
                    "l2": "inputs >> 126 MB L2 (no flush needed)",
-                   "kernel": ("k_sweep (fused structured sweep)" if r["info"]["structured"] and
-                              args.kernel != 1 else "k_elem_blocks + k_gather (general)")},
+                   "kernel": kernel_name(cfg.etype, r["info"]["structured"], args.kernel)},
         "assemble_ms": r["assemble_ms"],
         "assemble_elements_per_s": n_total / (r["assemble_ms"] * 1e-3) if ws == 1 else None,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
