@@ -78,6 +78,12 @@ __device__ __forceinline__ void barrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+// Row layout inside a plane: 9 slots x 4 doubles = 18 double2 chunks per row.  The two chunks
+// of slot sl are swizzled, chunk (sl, h) -> 2 sl + (h ^ bit2(sl)), so that the 16-byte adds of
+// lanes targeting slots sl and sl+4 (same bank group otherwise) land in different bank groups.
+__host__ __device__ constexpr int swz(int sl, int h) { return 2 * sl + (h ^ ((sl >> 2) & 1)); }
+__host__ __device__ constexpr int soff(int sl, int j) { return 2 * swz(sl, j >> 1) + (j & 1); }
+
 // off-diagonal pair p (0..27) -> (a, b), a < b
 __device__ __forceinline__ void offdiag_ab(int p, int& a, int& b) {
   int aa = 0, rem = p;
@@ -219,11 +225,14 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
     const int lid = (warp & 1) * 32 + lane;
     const int el = lid >> 3, g = lid & 7;
     int t = 0;
+    PT_DECL
     schedule(
         [&](int64_t s, int, int b0, int ifst, int ni, int jfst, int nc) {
           if ((t & 1) == pair) {
             const int slot = pair;   // each PC pair owns one core slot (fixed producer)
+            PT_MARK(12, tid == 0);
             if (t >= 2) bsync(S4::B_CE + slot, NPC_T + NC_T);
+            PT_MARK(10, tid == 0);
             const int k = b0 + el;
             if (k < nc) {
               const int i = ifst + 2 * (k % ni), j = jfst + 2 * (k / ni);
@@ -246,6 +255,7 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
               for (int k2 = 5; k2 < 23; ++k2) dst[k2] = make_double2(core[2 * k2 - 1], core[2 * k2]);
               dst[23] = make_double2(core[45], 0.0);
             }
+            PT_MARK(11, tid == 0);
             barrive(S4::B_CF + slot, NPC_T + NC_T);
           }
           ++t;
@@ -280,41 +290,43 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
     return colp + (zs ? S4::UP : S4::DN);
   };
 
+  __shared__ int64_t sbase[2][S4::NCOLS];   // CSR offsets of node layers (by parity)
   // ---- flush helpers (one warp per column) ----
   // copy plane P ([row 4][9 slots][4]) of node (x, y, z) to its compacted CSR position
   auto write_plane = [&](int x, int y, int64_t z, int dz, const double* P, bool inner) {
     const int zlo = z > 0 ? -1 : 0, zhi = z < G.nl ? 1 : 0;
     if (inner) {
       const int W2 = 18 * (zhi - zlo + 1);   // row width in double2
-      double2* out = reinterpret_cast<double2*>(val + base[node_id(x, y, z) - G.own_node_b]) + (dz - zlo) * 18;
+      double2* out = reinterpret_cast<double2*>(val + sbase[z & 1][(x - ix0) + cols_x * (y - iy0)]) + (dz - zlo) * 18;
       const double2* src = reinterpret_cast<const double2*>(P);
 #pragma unroll
       for (int r = 0; r < 4; ++r)
-        if (lane < 18) __stcs(out + r * W2 + lane, src[r * 18 + lane]);
+        if (lane < 18) __stcs(out + r * W2 + lane, src[r * 18 + (lane ^ ((lane >> 3) & 1))]);
       return;
     }
     const int xlo = x > 0 ? -1 : 0, xhi = x < G.nx ? 1 : 0;
     const int ylo = y > 0 ? -1 : 0, yhi = y < G.nyN - 1 ? 1 : 0;
     const int wx = xhi - xlo + 1, wy = yhi - ylo + 1, wz = zhi - zlo + 1;
     const int W = 4 * wx * wy * wz;
-    double* out = val + base[node_id(x, y, z) - G.own_node_b] + (dz - zlo) * (4 * wx * wy);
+    double* out = val + sbase[z & 1][(x - ix0) + cols_x * (y - iy0)] + (dz - zlo) * (4 * wx * wy);
     for (int it = lane; it < 36; it += 32) {
       const int i = it / 9, sl = it - 9 * i;
       const int dy = sl / 3 - 1, dx = sl - 3 * (dy + 1) - 1;
       if (dx < xlo || dx > xhi || dy < ylo || dy > yhi) continue;
-      const double2* src = reinterpret_cast<const double2*>(P + i * 36 + sl * 4);
+      const double2* src = reinterpret_cast<const double2*>(P + i * 36);
       double2* dst = reinterpret_cast<double2*>(out + i * W + 4 * ((dy - ylo) * wx + (dx - xlo)));
-      __stcs(dst, src[0]);
-      __stcs(dst + 1, src[1]);
+      __stcs(dst, src[swz(sl, 0)]);
+      __stcs(dst + 1, src[swz(sl, 1)]);
     }
   };
   // lanes 0..15: entry (i, j) = (lane / 4, lane % 4) of the 4x4 blocks, summed over slots
   auto plane_sum = [&](const double* P, bool skip_self) {
     double s = 0.0;
-    const double* p = P + (lane >> 2) * 36 + (lane & 3);
+    const double* p = P + (lane >> 2) * 36;
+    const int j = lane & 3;
 #pragma unroll
     for (int sl = 0; sl < 9; ++sl)
-      if (!(skip_self && sl == 4)) s += p[sl * 4];
+      if (!(skip_self && sl == 4)) s += p[soff(sl, j)];
     return s;
   };
   // finish node (x, y, z): diagonal block = -sum(plane -1) [kept in the self slot]
@@ -324,7 +336,7 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
     const double* ns = colp + S4::NS + (z & 1) * 8;
     if (lane < 16) {
       const int i = lane >> 2, j = lane & 3;
-      double* self = Zp + i * 36 + 4 * 4 + j;
+      double* self = Zp + i * 36 + soff(4, j);
       double d = *self - plane_sum(Zp, true);
       if (has_up) d -= plane_sum(colp + S4::UP, false);
       if (j == 3) d += (i < 3) ? ns[4 + i] : ns[7];
@@ -337,13 +349,28 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
   };
 
   int prev_c = -1, t = 0;
+  const bool ptc = ct == 0;
+  PT_DECL
   schedule(
       [&](int64_t s, int c, int b0, int ifst, int ni, int jfst, int nc) {
         const int k = b0 + cw;
         const bool live = k < nc;   // warp-uniform
         const int cslot = t & 1;
         ++t;
+        if (prev_c < 0) {
+          // first batch of element layer s: fetch the CSR offsets of the block-rows of node
+          // layers s and s+1 for this layer's flush (the loads overlap the batch)
+          for (int q = ct; q < 2 * cols; q += NC_T) {
+            const int cc = q % cols;
+            const int64_t zq = s + q / cols;
+            const int cy = cc / cols_x;
+            if (zq >= z0 && zq < z1)
+              sbase[zq & 1][cc] = base[node_id(ix0 + (cc - cy * cols_x), iy0 + cy, zq) - G.own_node_b];
+          }
+        }
+        PT_MARK(9, ptc);
         bsync(S4::B_CF + cslot, NPC_T + NC_T);
+        PT_MARK(0, ptc);
         if (!live) {
           barrive(S4::B_CE + cslot, NPC_T + NC_T);
           if (c != prev_c) bsync(S4::B_C, NC_T);
@@ -377,6 +404,7 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
           }
           if (rnd == 1) barrive(S4::B_CE + cslot, NPC_T + NC_T);   // core slot no longer read
           __syncwarp();
+          PT_MARK(1, ptc);
 #pragma unroll 1
           for (int gg = 0; gg < 4; ++gg) {
             const double* blk = myrec + gg * S4::RGP;
@@ -426,6 +454,7 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
             P.Kee_ba = fma(NA, EB, fma(ghc, dot, P.Kee_ba));
           }
           __syncwarp();
+          PT_MARK(2, ptc);
         }
         // node sums: reduce the four Gauss-point lanes of each node (lanes xa + 8 xg)
 #pragma unroll
@@ -433,9 +462,11 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
           ns[k2] += __shfl_xor_sync(0xffffffffu, ns[k2], 8);
           ns[k2] += __shfl_xor_sync(0xffffffffu, ns[k2], 16);
         }
+        PT_MARK(3, ptc);
         // batches of one colour share no node; a new colour waits for the previous adds
         if (c != prev_c) bsync(S4::B_C, NC_T);
         prev_c = c;
+        PT_MARK(4, ptc);
         const int zpar_s = int(s & 1);
         if (xg == 0) {
           const int nx_ = i + xox, ny_ = j + xoy;
@@ -457,39 +488,41 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
           const bool own_a = ax >= ix0 && ax < ix1 && ay >= iy0 && ay < iy1 && azr >= 0 && s + oaz < z1;
           const bool own_b = bx >= ix0 && bx < ix1 && by >= iy0 && by < iy1 && bzr >= 0 && s + obz < z1;
           if (own_a) {
-            double* Pp = plane_of(col_of(ax, ay), (zpar_s ^ oaz) & 1, oaz == 0, dzAB) + psAB * 4;
+            double* Pp = plane_of(col_of(ax, ay), (zpar_s ^ oaz) & 1, oaz == 0, dzAB);
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
               double2* q = reinterpret_cast<double2*>(Pp + r * 36);
-              double2 lo = q[0], hi = q[1];
+              double2 lo = q[swz(psAB, 0)], hi = q[swz(psAB, 1)];
               if (r < 3) {
                 lo.x += P.Kuu[r][0]; lo.y += P.Kuu[r][1]; hi.x += P.Kuu[r][2]; hi.y += P.Kue_ab[r];
               } else {
                 lo.x += P.Keu_ab[0]; lo.y += P.Keu_ab[1]; hi.x += P.Keu_ab[2]; hi.y += P.Kee_ab;
               }
-              q[0] = lo;
-              q[1] = hi;
+              q[swz(psAB, 0)] = lo;
+              q[swz(psAB, 1)] = hi;
             }
           }
           if (own_b) {
-            double* Pp = plane_of(col_of(bx, by), (zpar_s ^ obz) & 1, obz == 0, -dzAB) + psBA * 4;
+            double* Pp = plane_of(col_of(bx, by), (zpar_s ^ obz) & 1, obz == 0, -dzAB);
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
               double2* q = reinterpret_cast<double2*>(Pp + r * 36);
-              double2 lo = q[0], hi = q[1];
+              double2 lo = q[swz(psBA, 0)], hi = q[swz(psBA, 1)];
               if (r < 3) {
                 lo.x += P.Kuu[0][r]; lo.y += P.Kuu[1][r]; hi.x += P.Kuu[2][r]; hi.y += P.Kue_ba[r];
               } else {
                 lo.x += P.Keu_ba[0]; lo.y += P.Keu_ba[1]; hi.x += P.Keu_ba[2]; hi.y += P.Kee_ba;
               }
-              q[0] = lo;
-              q[1] = hi;
+              q[swz(psBA, 0)] = lo;
+              q[swz(psBA, 1)] = hi;
             }
           }
         }
       },
       [&](int64_t s) {
+        PT_MARK(5, ptc);
         bsync(S4::B_C, NC_T);   // all adds of layer s are in
+        PT_MARK(6, ptc);
         prev_c = -1;
         const bool own_s = s >= z0 && s < z1, own_s1 = s + 1 >= z0 && s + 1 < z1;
         const bool top = s == s_last && own_s1;   // node layer s+1 has no element layer above
@@ -502,7 +535,7 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
             // plane -1 of node layer s+1 is complete: out, and minus its row sums go to the
             // self slot of that node's plane 0 (never accumulated by pair adds)
             if (lane < 16)
-              colp[(((s + 1) & 1) ? S4::Z1 : S4::Z0) + (lane >> 2) * 36 + 16 + (lane & 3)] =
+              colp[(((s + 1) & 1) ? S4::Z1 : S4::Z0) + (lane >> 2) * 36 + soff(4, lane & 3)] =
                   -plane_sum(colp + S4::DN, false);
             write_plane(x, y, s + 1, -1, colp + S4::DN, inner);
           }
@@ -518,7 +551,9 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
           for (int k2 = lane; k2 < S4::PL; k2 += 32) ud[k2] = zero;
           if (lane < 4) reinterpret_cast<double2*>(colp + S4::NS + (s & 1) * 8)[lane] = zero;
         }
+        PT_MARK(7, ptc);
         bsync(S4::B_C, NC_T);
+        PT_MARK(8, ptc);
       });
 }
 

@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblgdm.so")
+LIB_PATH = os.environ.get("LGDM_LIB") or os.path.join(_HERE, "liblgdm.so")   # override: experiments
 
 BAR2, QUAD4, HEX8 = 1, 2, 3
 # type -> (dim, nen, ndpn, ngp)

@@ -1,0 +1,34 @@
+"""Per-phase cycle breakdown of k_sweep4 (debug build exp/lib_timing.so, -DLGDM_PHASE_TIMING):
+thread 0 of the PC role and of the C role accumulate clock64 deltas per phase."""
+import ctypes as C
+import os
+import sys
+import numpy as np
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+os.environ["LGDM_LIB"] = os.path.join(ROOT, "exp", "lib_timing.so")
+import torch
+import synth
+from paper_2301_06503_b200 import lgdm
+L = lgdm.load()
+L.lgdm_debug_phase_cycles.argtypes = [C.c_void_p, C.c_int]
+names = {0: "C wait core-full", 1: "C expansion round", 2: "C pair GPs (4)", 3: "C ns shuffle",
+         4: "C colour barrier", 5: "C adds", 6: "C end-layer barrier", 7: "C flush", 8: "C reset barrier",
+         9: "C batch prologue", 10: "PC wait core-empty", 11: "PC core", 12: "PC other"}
+cid = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+cfg = synth.CONFIGS[cid]
+mesh = synth.structured_mesh(cfg)
+d, k = synth.fields(cfg, mesh)
+m = lgdm.Mesh(cfg.etype, mesh.coords, mesh.conn, lgdm.material(**synth.MATERIAL))
+m.set_state(d, k)
+m.assemble(); torch.cuda.synchronize()
+buf = np.zeros(16, dtype=np.uint64)
+L.lgdm_debug_phase_cycles(buf.ctypes.data, 1)
+m.assemble(); torch.cuda.synchronize()
+L.lgdm_debug_phase_cycles(buf.ctypes.data, 1)
+for grp in ("C", "PC"):
+    idx = [i for i, n in names.items() if n.startswith(grp + " ")]
+    tot = float(sum(buf[i] for i in idx))
+    print(cfg.name, grp, "total %.4e cycles (sum over CTAs of thread 0)" % tot)
+    for i in idx:
+        print(f"  {names[i]:24s} {float(buf[i]):.3e}  {100 * float(buf[i]) / max(tot, 1):5.1f}%")
