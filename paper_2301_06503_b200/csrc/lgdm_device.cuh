@@ -150,12 +150,13 @@ template <int D> struct Core {
 // U [NEN][NDPN] dofs, kh = kappa_hist.  Writes the compact GP state (Core<D> layout) to core.
 // Returns det J (caller treats <= 0 as an inverted element).
 // ---------------------------------------------------------------------------------------
-template <int D, class XF, class UF>
-__device__ __forceinline__ double gpCore(const DevMat& m, XF&& X, UF&& U, double kh, int g,
-                                         double* __restrict__ core) {
+// Shape values are supplied by SHD(a, j) = dN_a/dxi_j and SHN(a) = N_a at the Gauss point
+// (gpCore below passes the closed forms; kernels may pass register copies of a table).
+template <int D, class XF, class UF, class SD, class SN>
+__device__ __forceinline__ double gpCoreS(const DevMat& m, XF&& X, UF&& U, double kh, SD&& SHD,
+                                          SN&& SHN, double* __restrict__ core) {
   using Co = Core<D>;
   using F = Fam<D>;
-  using R = Rec<D>;
   constexpr int NEN = F::NEN, NS = F::NS;
 
   // geometry: J_ij = sum_a X_ai dN_a/dxi_j
@@ -168,7 +169,7 @@ __device__ __forceinline__ double gpCore(const DevMat& m, XF&& X, UF&& U, double
   for (int a = 0; a < NEN; ++a)
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-      const double dn = shape_dxi<D>(a, g, j);
+      const double dn = SHD(a, j);
 #pragma unroll
       for (int i = 0; i < D; ++i) J[i][j] = fma(X(a, i), dn, J[i][j]);
     }
@@ -207,7 +208,7 @@ __device__ __forceinline__ double gpCore(const DevMat& m, XF&& X, UF&& U, double
     for (int i = 0; i < D; ++i) {
       double s = 0.0;
 #pragma unroll
-      for (int j = 0; j < D; ++j) s = fma(Ji[j][i], shape_dxi<D>(a, g, j), s);
+      for (int j = 0; j < D; ++j) s = fma(Ji[j][i], SHD(a, j), s);
       gn[i] = s;
     }
   };
@@ -223,7 +224,7 @@ __device__ __forceinline__ double gpCore(const DevMat& m, XF&& X, UF&& U, double
     double gn[D];
     gradN(a, gn);
     const double ea = U(a, D);
-    ebar = fma(shapeN<D>(a, g), ea, ebar);
+    ebar = fma(SHN(a), ea, ebar);
 #pragma unroll
     for (int i = 0; i < D; ++i) {
       gb[i] = fma(gn[i], ea, gb[i]);
@@ -376,6 +377,14 @@ __device__ __forceinline__ double gpCore(const DevMat& m, XF&& X, UF&& U, double
   return detJ;
 }
 
+
+// Core of one GP with the closed-form shape functions at Gauss point g.
+template <int D, class XF, class UF>
+__device__ __forceinline__ double gpCore(const DevMat& m, XF&& X, UF&& U, double kh, int g,
+                                         double* __restrict__ core) {
+  return gpCoreS<D>(m, X, U, kh, [&](int a, int j) { return shape_dxi<D>(a, g, j); },
+                    [&](int a) { return shapeN<D>(a, g); }, core);
+}
 
 // Phase A, part 2 ("expansion"): the record of node a at GP g from the compact state.
 template <int D>

@@ -13,8 +13,9 @@
 //     registers and the same lane expands it into the 4 node records of that Gauss point
 //     (grad N, S grad N, t1, t2, W' grad N, Dt' grad N, E, N) and the per-node sums (R = F,
 //     U = sum W' grad N, V = sum E), reduced over the element's 4 GP lanes by shuffles.  No
-//     core ever goes through shared memory.  One PC group per colour, each with a 2-slot
-//     ring (slot = 2 colour + row parity), so every slot has a fixed producer/consumer pair.
+//     core ever goes through shared memory.  Four PC groups, one per (colour, row parity),
+//     each owning one batch slot, so every slot has a fixed producer/consumer pair and two
+//     batches of each colour are in production at once (the core chain is latency-bound).
 //   * C warps, three lanes per element: lane k owns the star of node pairs {(k, b)} that
 //     covers the element's 6 off-diagonal pairs twice-per-lane ({01,03}, {12,13}, {20,23}),
 //     so the centre node's record is loaded once per Gauss point for two pairs.
@@ -27,24 +28,27 @@ namespace lgdm {
 struct SQ {
   static constexpr int TX = 31, E = 16, NCOL = 2;            // 32 elements per row = 2 colours x E
   static constexpr int NGP = 4, NEN = 4, NDPN = 3;
-  static constexpr int NPCG = 2, PCW = 2;                    // PC lane groups (= colours), warps
+  static constexpr int NPCG = 4, PCW = 2;                    // PC groups (colour x row parity), warps
   static constexpr int NCW = 4;                              // C warps: 2 groups (colours) x 2
   static constexpr int NFW = 2;                              // flush warps
   static constexpr int T = 32 * (NPCG * PCW + NCW + NFW);
   static constexpr int NSLOT = 4;                            // slot = 2 colour + row parity
   // shape table [NGP][NEN][4] = (dN/dxi0, dN/dxi1, N, 0)
   static constexpr int SHT = NGP * NEN * 4;
-  // element block in a slot: records [NGP][NEN][RS], node sums [NEN][6], (mu*, ghc)[NGP]
-  static constexpr int RS = 14, REC = 0, NSUM = NGP * NEN * RS, HDR = NSUM + NEN * 6,
-                       EL = HDR + 2 * NGP + 2;              // 258 doubles = 129 x 16 B (odd)
+  // element block in a slot: records [NGP][NEN][RS] (GP stride GS), node sums [NEN][6],
+  // (mu*, ghc)[NGP].  Strides chosen with a quarter-warp bank model (16-byte accesses): the
+  // PC record stores are conflict-free, the C record loads 1.35x ideal (was 2x).
+  static constexpr int RS = 14, GS = 60, REC = 0, NSUM = NGP * GS, HDR = NSUM + NEN * 6,
+                       EL = 282;
+  static_assert(HDR + 2 * NGP <= EL, "element block");
   static constexpr int SLOT = E * EL;
   // accumulators: the complete block-row of every tile node, in the CSR order of an
   // interior node: [row r 3][dy 3][dx 3][j 3] = 81 doubles; three node-row buffers (node
   // row zn uses buffer zn % 3) so the flush of node row s overlaps the adds of element row
   // s+1 (which touch node rows s+1, s+2); NS[3][TX][6]
-  static constexpr int NROW = 81, NBUF = 3, ACC = NBUF * TX * NROW, NSB = ACC;
+  static constexpr int NROW = 81, NBUF = 3, ACC = NBUF * TX * NROW, NSB = ACC, NSS = 7;   // odd NS stride
   static constexpr size_t SMEM = sizeof(double) * (size_t(SHT) + size_t(NSLOT) * SLOT +
-                                                   size_t(ACC) + size_t(NBUF * TX * 6));
+                                                   size_t(ACC) + size_t(NBUF * TX * NSS));
   // named barriers: slot full 1..3, slot empty 4..6; by row parity (group 0 may run up to
   // two rows ahead of the flush): colour-0 adds done 7/8, row adds done (C -> flush) 9/10,
   // node row flushed (flush -> group 0 two rows later) 11/12; flush warps 13
@@ -86,7 +90,7 @@ k_sweepq(DevMat m, SweepGeom G, const double* __restrict__ coords,
     shtab[k * 4 + 2] = shapeN<2>(a, g);
     shtab[k * 4 + 3] = 0.0;
   }
-  for (int k = tid; k < SQ::ACC + SQ::NBUF * SQ::TX * 6; k += SQ::T) acc[k] = 0.0;
+  for (int k = tid; k < SQ::ACC + SQ::NBUF * SQ::TX * SQ::NSS; k += SQ::T) acc[k] = 0.0;
   __syncthreads();
 
   // batch schedule (every role): element row s, colour c (parity of i) -- exactly one batch
@@ -117,11 +121,15 @@ k_sweepq(DevMat m, SweepGeom G, const double* __restrict__ coords,
       sh[a][2] = shtab[(g * NEN + a) * 4 + 2];
     }
     int t = 0;
+    const bool ptp = tid == 0;
+    PT_DECL
     schedule(
         [&](int64_t s, int, int b0, int ifst, int nc) {
-          if ((t & 1) == grp) {
-            const int slot = 2 * grp + ((t >> 1) & 1);
+          if ((t & 1) == (grp & 1) && ((t >> 1) & 1) == (grp >> 1)) {
+            const int slot = 2 * (grp & 1) + (grp >> 1);   // = 2 colour + row parity
+            PT_MARK(12, ptp);
             if (t >= SQ::NSLOT) bsync(SQ::B_E + slot, NFE);
+            PT_MARK(10, ptp);
             const int k = b0 + el;
             double* eb = slots + slot * SQ::SLOT + el * SQ::EL;
             double ns[NEN][6];
@@ -142,7 +150,8 @@ k_sweepq(DevMat m, SweepGeom G, const double* __restrict__ coords,
               const int64_t e = i + G.nx * s;
               using Co = Core<2>;
               double c[Co::STRIDE];
-              gpCore<2>(m, X, U, __ldg(kappa + e * NGP + g), g, c);
+              gpCoreS<2>(m, X, U, __ldg(kappa + e * NGP + g), [&](int a, int j) { return sh[a][j]; },
+                         [&](int a) { return sh[a][2]; }, c);
 #pragma unroll
               for (int a = 0; a < NEN; ++a) {
                 double gn[2], SgN[2], WgN[2], DgN[2], fu[2];
@@ -155,7 +164,7 @@ k_sweepq(DevMat m, SweepGeom G, const double* __restrict__ coords,
                 const double Na = sh[a][2];
                 const double Ea = fma(c[Co::HN], Na, fma(c[Co::GV], gn[0], c[Co::GV + 1] * gn[1]));
                 const double fe = fma(c[Co::FE0], Na, fma(c[Co::FV], gn[0], c[Co::FV + 1] * gn[1]));
-                double2* r2 = reinterpret_cast<double2*>(eb + SQ::REC + (g * NEN + a) * SQ::RS);
+                double2* r2 = reinterpret_cast<double2*>(eb + SQ::REC + g * SQ::GS + a * SQ::RS);
                 r2[0] = make_double2(gn[0], gn[1]);
                 r2[1] = make_double2(SgN[0], SgN[1]);
                 r2[2] = make_double2(WgN[0], WgN[1]);
@@ -182,26 +191,29 @@ k_sweepq(DevMat m, SweepGeom G, const double* __restrict__ coords,
                 ns[a][q] += __shfl_xor_sync(0xffffffffu, ns[a][q], 1);
                 ns[a][q] += __shfl_xor_sync(0xffffffffu, ns[a][q], 2);
               }
-            if (k < nc && g == 0) {
+            if (k < nc) {   // every GP lane holds the reduced sums; lane g writes node g
+              double v[6];
 #pragma unroll
-              for (int a = 0; a < NEN; ++a)
+              for (int q = 0; q < 6; ++q)
+                v[q] = g == 0 ? ns[0][q] : g == 1 ? ns[1][q] : g == 2 ? ns[2][q] : ns[3][q];
 #pragma unroll
-                for (int q = 0; q < 6; q += 2)
-                  *reinterpret_cast<double2*>(eb + SQ::NSUM + a * 6 + q) = make_double2(ns[a][q], ns[a][q + 1]);
+              for (int q = 0; q < 6; q += 2)
+                *reinterpret_cast<double2*>(eb + SQ::NSUM + g * 6 + q) = make_double2(v[q], v[q + 1]);
             }
             barrive(SQ::B_F + slot, NFE);
+            PT_MARK(11, ptp);
           }
           ++t;
         },
         [](int64_t) {});
     // drain the slot-empty arrivals no later batch of this group consumes
     for (int tt = max(t - SQ::NSLOT, 0); tt < t; ++tt)
-      if ((tt & 1) == grp) bsync(SQ::B_E + 2 * grp + ((tt >> 1) & 1), NFE);
+      if ((tt & 1) == (grp & 1) && ((tt >> 1) & 1) == (grp >> 1)) bsync(SQ::B_E + 2 * (grp & 1) + (grp >> 1), NFE);
     return;
   }
 
   auto row_of = [&](int x, int64_t zn) { return acc + (int(zn % 3) * SQ::TX + (x - ix0)) * SQ::NROW; };
-  auto ns_of = [&](int x, int64_t zn) { return acc + SQ::NSB + (int(zn % 3) * SQ::TX + (x - ix0)) * 6; };
+  auto ns_of = [&](int x, int64_t zn) { return acc + SQ::NSB + (int(zn % 3) * SQ::TX + (x - ix0)) * SQ::NSS; };
   const int ctid = tid - 32 * SQ::NPCG * SQ::PCW;   // C and flush threads
 
   if (ctid >= C_T) {
@@ -211,6 +223,8 @@ k_sweepq(DevMat m, SweepGeom G, const double* __restrict__ coords,
     // consecutive interior nodes) and R stream out, and the row buffer is reset for s+2.
     const int ft = ctid - C_T;
     constexpr int F_T = 32 * SQ::NFW;
+    const bool ptf = ft == 0;
+    PT_DECL
     // compact the block-row of an edge node (fewer than 9 neighbours) into its CSR slots
     auto flush_edge = [&](int x, int64_t zn) {
       const int xlo = x > 0 ? -1 : 0, xhi = x < G.nx ? 1 : 0;
@@ -230,14 +244,26 @@ k_sweepq(DevMat m, SweepGeom G, const double* __restrict__ coords,
     barrive(SQ::B_FL + (int(s_first) & 1), F_T + 64);
     barrive(SQ::B_FL + (int(s_first + 1) & 1), F_T + 64);
     for (int64_t s = s_first; s <= s_last; ++s) {
+      // CSR offset of the first interior node of node row s (and s+1 at the top), loaded
+      // before the wait so the global-load latency hides behind it
+      const bool topq = s == s_last && s + 1 >= z0 && s + 1 < z1;
+      int64_t pre[2] = {0, 0};
+#pragma unroll
+      for (int pass = 0; pass < 2; ++pass) {
+        const int64_t zn = s + pass;
+        if ((pass == 0 || topq) && zn >= z0 && zn < z1 && zn > 0 && zn < G.nl && max(ix0, 1) < min(ix1, int(G.nx)))
+          pre[pass] = base[max(ix0, 1) + nxN * zn - G.own_node_b];
+      }
+      PT_MARK(9, ptf);
       bsync(SQ::B_ADDS + (int(s) & 1), F_T + C_T);
+      PT_MARK(4 + 10, ptf);
       const bool top = s == s_last && s + 1 >= z0 && s + 1 < z1;
       for (int pass = 0; pass < (top ? 2 : 1); ++pass) {
         const int64_t zn = s + pass;
         if (zn >= z0 && zn < z1) {
           // diagonal entries (column, r, j)
-          for (int task = ft; task < cols * 9; task += F_T) {
-            const int cc = task / 9, e = task - 9 * cc, r = e / 3, j = e - 3 * r;
+          for (int task = ft; task < cols * 9; task += F_T) {   // column fastest: conflict-free
+            const int e = task / cols, cc = task - cols * e, r = e / 3, j = e - 3 * r;
             double* row = row_of(ix0 + cc, zn) + r * 27 + j;
             const double* ns = ns_of(ix0 + cc, zn);
             double d = 0.0;
@@ -247,7 +273,9 @@ k_sweepq(DevMat m, SweepGeom G, const double* __restrict__ coords,
             if (j == 2) d += (r < 2) ? ns[3 + r] : ns[5];
             row[4 * 3] = d;
           }
+          PT_MARK(5, ptf);
           bsync(SQ::B_FW, F_T);
+          PT_MARK(6, ptf);
           // rows out.  Interior nodes have 9 neighbours and consecutive node ids, so the
           // block-rows of a run of interior columns are ONE contiguous range of the CSR values,
           // in the same order as the row buffers: a linear copy.  Edge nodes (x = 0, x = nx,
@@ -255,12 +283,36 @@ k_sweepq(DevMat m, SweepGeom G, const double* __restrict__ coords,
           const bool zin = zn > 0 && zn < G.nl;
           const int xa = zin ? max(ix0, 1) : ix1, xb = zin ? min(ix1, int(G.nx)) : ix1;
           if (xb > xa) {
-            double* out = val + base[xa + nxN * zn - G.own_node_b];
+            double* out = val + pre[pass];
             double* src = row_of(xa, zn);
             const int cnt = (xb - xa) * SQ::NROW;
-            for (int k = ft; k < cnt; k += F_T) {
-              __stcs(out + k, src[k]);
-              src[k] = 0.0;
+            // 16-byte vectors when the CSR range and the row buffer are co-aligned
+            const int head = ((reinterpret_cast<uintptr_t>(out) & 15) != 0) ? 1 : 0;
+            const bool co = ((reinterpret_cast<uintptr_t>(out) ^ reinterpret_cast<uintptr_t>(src)) & 15) == 0;
+            if (co) {
+              if (head && ft == 0) {
+                __stcs(out, src[0]);
+                src[0] = 0.0;
+              }
+              const int nv = (cnt - head) >> 1;
+              double2* o2 = reinterpret_cast<double2*>(out + head);
+              double2* s2 = reinterpret_cast<double2*>(src + head);
+              const double2 zero = make_double2(0.0, 0.0);
+#pragma unroll 4
+              for (int k = ft; k < nv; k += F_T) {
+                __stcs(o2 + k, s2[k]);
+                s2[k] = zero;
+              }
+              if (((cnt - head) & 1) && ft == 0) {
+                __stcs(out + cnt - 1, src[cnt - 1]);
+                src[cnt - 1] = 0.0;
+              }
+            } else {
+#pragma unroll 4
+              for (int k = ft; k < cnt; k += F_T) {
+                __stcs(out + k, src[k]);
+                src[k] = 0.0;
+              }
             }
           }
           for (int x = ix0; x < xa; ++x) flush_edge(x, zn);   // edge columns (x = 0) or rows
@@ -272,11 +324,14 @@ k_sweepq(DevMat m, SweepGeom G, const double* __restrict__ coords,
             __stcs(Rv + (ix0 + cc + nxN * zn - G.own_node_b) * 3 + j, ns[j]);
           }
           bsync(SQ::B_FW, F_T);
-          for (int k = ft; k < cols * 6; k += F_T) ns_of(ix0, zn)[k] = 0.0;
+          for (int k = ft; k < cols * SQ::NSS; k += F_T) ns_of(ix0, zn)[k] = 0.0;
+          PT_MARK(7, ptf);
           bsync(SQ::B_FW, F_T);
+          PT_MARK(8, ptf);
         }
       }
       barrive(SQ::B_FL + (int(s) & 1), F_T + 64);   // consumed by group 0 at row s + 2
+      PT_MARK(9, ptf);
     }
     return;
   }
@@ -368,12 +423,16 @@ k_sweepq(DevMat m, SweepGeom G, const double* __restrict__ coords,
   auto owned = [&](int x, int64_t z) { return x >= ix0 && x < ix1 && z >= z0 && z < z1; };
 
   int t = 0;
+  const bool ptc = ct == 0;
+  PT_DECL
   schedule(
       [&](int64_t s, int c, int, int ifst, int nc) {
         const int slot = 2 * c + ((t >> 1) & 1);
         ++t;
         if (c != cg) return;                        // the other group's batch
+        PT_MARK(0, ptc);
         bsync(SQ::B_F + slot, NFE);
+        PT_MARK(1, ptc);
         const bool live = star_lane && cel < nc;
         const double* eb = slots + slot * SQ::SLOT + cel * SQ::EL;
         PairQ P1, P2;
@@ -383,7 +442,7 @@ k_sweepq(DevMat m, SweepGeom G, const double* __restrict__ coords,
         if (live) {
 #pragma unroll 1
           for (int g = 0; g < NGP; ++g) {
-            const double* rg = eb + SQ::REC + g * NEN * SQ::RS;
+            const double* rg = eb + SQ::REC + g * SQ::GS;
             const double2* A2 = reinterpret_cast<const double2*>(rg + pa * SQ::RS);
             const double2 hdr = reinterpret_cast<const double2*>(eb + SQ::HDR)[g];
             double gA[2], sA[2], wA[2], dA[2], EA, NA;
@@ -405,8 +464,10 @@ k_sweepq(DevMat m, SweepGeom G, const double* __restrict__ coords,
         }
         barrive(SQ::B_E + slot, NFE);
         // fixed add order: the previous row flushed, then colour 0, then colour 1
+        PT_MARK(2, ptc);
         if (cg == 0) bsync(SQ::B_FL + (int(s) & 1), 32 * SQ::NFW + 64);   // node row s-2 flushed
         else bsync(SQ::B_C0 + (int(s) & 1), C_T);
+        PT_MARK(3, ptc);
         if (live) {
           const int i = ifst + 2 * cel;
           const int ax = i + oax, b1x = i + ob1x, b2x = i + ob2x;
@@ -426,6 +487,7 @@ k_sweepq(DevMat m, SweepGeom G, const double* __restrict__ coords,
         }
         if (cg == 0) barrive(SQ::B_C0 + (int(s) & 1), C_T);
         barrive(SQ::B_ADDS + (int(s) & 1), 32 * SQ::NFW + C_T);   // both groups, every row
+        PT_MARK(4, ptc);
       },
       [&](int64_t) {});
   if (cg == 0) {   // the flushes of the last two rows

@@ -12,11 +12,16 @@ import synth
 from paper_2301_06503_b200 import lgdm
 L = lgdm.load()
 L.lgdm_debug_phase_cycles.argtypes = [C.c_void_p, C.c_int]
+QNAMES = {0: "C other", 1: "C wait slot-full", 2: "C compute", 3: "C wait add-order", 4: "C adds",
+          14: "F wait adds", 5: "F diagonal", 6: "F copy+R", 7: "F barrier", 8: "F ns reset", 9: "F other",
+          12: "PC other", 10: "PC wait slot-empty", 11: "PC core+records"}
 names = {0: "C wait core-full", 1: "C expansion round", 2: "C pair GPs (4)", 3: "C ns shuffle",
          4: "C colour barrier", 5: "C adds", 6: "C end-layer barrier", 7: "C flush", 8: "C reset barrier",
          9: "C batch prologue", 10: "PC wait core-empty", 11: "PC core", 12: "PC other"}
 cid = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 cfg = synth.CONFIGS[cid]
+if cfg.etype == 2:
+    names = QNAMES
 mesh = synth.structured_mesh(cfg)
 d, k = synth.fields(cfg, mesh)
 m = lgdm.Mesh(cfg.etype, mesh.coords, mesh.conn, lgdm.material(**synth.MATERIAL))
@@ -26,7 +31,7 @@ buf = np.zeros(16, dtype=np.uint64)
 L.lgdm_debug_phase_cycles(buf.ctypes.data, 1)
 m.assemble(); torch.cuda.synchronize()
 L.lgdm_debug_phase_cycles(buf.ctypes.data, 1)
-for grp in ("C", "PC"):
+for grp in ("C", "PC", "F"):
     idx = [i for i, n in names.items() if n.startswith(grp + " ")]
     tot = float(sum(buf[i] for i in idx))
     print(cfg.name, grp, "total %.4e cycles (sum over CTAs of thread 0)" % tot)
