@@ -152,7 +152,8 @@ lgdm_status lgdm_scale_dofs(lgdm_mesh mesh, double s);
  *   2 = first structured sweep (Q4: k_sweep3, Hex8: k_sweep, L2-accumulating)
  *   3 = shared-memory pipeline k_sweep3 (Q4 and Hex8)
  *   4 = round-1 redesign: Q4 k_sweepq, Hex8 k_sweep4 (row-sum diagonals)
- * Kernels 2-4 need a structured mesh: LGDM_ERR_INVALID_ARGUMENT otherwise. */
+ *   5 = Hex8 k_sweep5 (node expansions in the core lanes; experimental, slower today), Q4 as 4
+ * Kernels 2-5 need a structured mesh: LGDM_ERR_INVALID_ARGUMENT otherwise. */
 lgdm_status lgdm_set_kernel(lgdm_mesh mesh, int kernel);
 
 lgdm_status lgdm_get_info(lgdm_mesh mesh, lgdm_info* info);

@@ -635,7 +635,7 @@ lgdm_status lgdm_scale_dofs(lgdm_mesh m, double sc) {
 }
 
 lgdm_status lgdm_set_kernel(lgdm_mesh m, int kernel) {
-  if (!m || kernel < 0 || kernel > 4) return fail(LGDM_ERR_INVALID_ARGUMENT, "bad kernel selector");
+  if (!m || kernel < 0 || kernel > 5) return fail(LGDM_ERR_INVALID_ARGUMENT, "bad kernel selector");
   if (kernel >= 2 && !(m->structured && sweep_supported(m)))
     return fail(LGDM_ERR_INVALID_ARGUMENT, "sweep kernel needs a structured mesh with whole owned layers");
   m->kernel = kernel;

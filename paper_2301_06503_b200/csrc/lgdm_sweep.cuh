@@ -401,6 +401,7 @@ k_sweep(DevMat m, SweepGeom G, const double* __restrict__ coords, const double* 
 
 #include "lgdm_sweep3.cuh"
 #include "lgdm_sweep4.cuh"
+#include "lgdm_sweep5.cuh"
 #include "lgdm_sweepq.cuh"
 
 namespace {
@@ -551,6 +552,36 @@ lgdm_status launch_sweep4(lgdm_mesh m) {
   return check_launch(m, "k_sweep4");
 }
 
+lgdm_status launch_sweep5(lgdm_mesh m) {
+  SweepGeom G{};
+  G.nx = m->nx;
+  G.nyE = m->ny;
+  G.nyN = m->ny + 1;
+  G.nl = m->nz;
+  const int64_t per_layer = (G.nx + 1) * G.nyN;
+  G.lay_own_b = m->own_b / per_layer;
+  G.lay_own_e = m->own_e / per_layer;
+  G.own_node_b = m->own_b;
+  G.tiles_x = int((G.nx + 1 + S5::TX - 1) / S5::TX);
+  G.tiles_y = int((G.nyN + S5::TY - 1) / S5::TY);
+  static bool attr = false;
+  if (!attr) {
+    CU(cudaFuncSetAttribute(k_sweep5, cudaFuncAttributeMaxDynamicSharedMemorySize, int(S5::SMEM)));
+    attr = true;
+  }
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device);
+  const int64_t layers = G.lay_own_e - G.lay_own_b;
+  const int64_t tiles = int64_t(G.tiles_x) * G.tiles_y;
+  const int64_t chunks = pick_chunks(tiles, layers, nsm, 8);
+  G.chunk_len = (layers + chunks - 1) / chunks;
+  G.chunks = int((layers + G.chunk_len - 1) / G.chunk_len);
+  const int64_t grid = tiles * G.chunks;
+  k_sweep5<<<unsigned(grid), S5::T, S5::SMEM, m->stream>>>(m->dm, G, m->coords, m->dofs, m->kappa,
+                                                           m->base, m->val, m->R);
+  return check_launch(m, "k_sweep5");
+}
+
 lgdm_status launch_sweepq(lgdm_mesh m) {
   SweepGeom G{};
   G.nx = m->nx;
@@ -585,9 +616,10 @@ lgdm_status launch_sweepq(lgdm_mesh m) {
 // are the fastest measured; k_sweep / k_sweep3 stay selectable (2 / 3)
 // and parity-tested.
 lgdm_status assemble_sweep(lgdm_mesh m) {
-  if (m->f.dim == 2) return m->kernel == 3 ? launch_sweep3<2>(m) : m->kernel == 2 ? launch_sweep3<2>(m) : launch_sweepq(m);
+  if (m->f.dim == 2) return (m->kernel == 2 || m->kernel == 3) ? launch_sweep3<2>(m) : launch_sweepq(m);
   if (m->kernel == 3) return launch_sweep3<3>(m);
   if (m->kernel == 2) return launch_sweep<3>(m);
+  if (m->kernel == 5) return launch_sweep5(m);
   return launch_sweep4(m);
 }
 

@@ -17,7 +17,7 @@ LIB_PATH = os.environ.get("LGDM_LIB") or os.path.join(_HERE, "liblgdm.so")   # o
 BAR2, QUAD4, HEX8 = 1, 2, 3
 # type -> (dim, nen, ndpn, ngp)
 FAMILY = {BAR2: (1, 2, 2, 2), QUAD4: (2, 4, 3, 4), HEX8: (3, 8, 4, 8)}
-KERNEL_AUTO, KERNEL_GENERAL, KERNEL_SWEEP, KERNEL_SWEEP3, KERNEL_SWEEP4 = 0, 1, 2, 3, 4
+KERNEL_AUTO, KERNEL_GENERAL, KERNEL_SWEEP, KERNEL_SWEEP3, KERNEL_SWEEP4, KERNEL_SWEEP5 = 0, 1, 2, 3, 4, 5
 
 STATUS = {0: "LGDM_OK", 1: "LGDM_ERR_INVALID_ARGUMENT", 2: "LGDM_ERR_INVERTED_ELEMENT",
           3: "LGDM_ERR_INVALID_STATE", 4: "LGDM_ERR_OUT_OF_MEMORY", 5: "LGDM_ERR_CUDA",

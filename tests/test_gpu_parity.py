@@ -11,8 +11,9 @@ from parity import compare, compare_sampled, gpu_assemble, oracle_assemble, slic
 
 pytestmark = pytest.mark.gpu
 
-KERNELS = [lgdm.KERNEL_GENERAL, lgdm.KERNEL_AUTO, lgdm.KERNEL_SWEEP3, lgdm.KERNEL_SWEEP4]
-SWEEPS = (lgdm.KERNEL_SWEEP3, lgdm.KERNEL_SWEEP4)
+KERNELS = [lgdm.KERNEL_GENERAL, lgdm.KERNEL_AUTO, lgdm.KERNEL_SWEEP3, lgdm.KERNEL_SWEEP4,
+           lgdm.KERNEL_SWEEP5]
+SWEEPS = (lgdm.KERNEL_SWEEP3, lgdm.KERNEL_SWEEP4, lgdm.KERNEL_SWEEP5)
 
 CASES = [
     (lgdm.BAR2, (1,)), (lgdm.BAR2, (7,)), (lgdm.BAR2, (100,)),
@@ -82,7 +83,8 @@ def test_parity_damage_edge_states():
                 compare(ref, got, "edge state")
 
 
-@pytest.mark.parametrize("kernel", [lgdm.KERNEL_AUTO, lgdm.KERNEL_SWEEP3, lgdm.KERNEL_SWEEP4])
+@pytest.mark.parametrize("kernel", [lgdm.KERNEL_AUTO, lgdm.KERNEL_SWEEP3, lgdm.KERNEL_SWEEP4,
+                                    lgdm.KERNEL_SWEEP5])
 @pytest.mark.parametrize("cid", [2, 3])
 def test_parity_full_size_sampled(cid, kernel):
     """BASELINE configs 2 and 3 at full size, in the bench's launch configuration; sampled
@@ -101,7 +103,8 @@ def test_parity_full_size_sampled(cid, kernel):
     print(f"config {cid}: sampled {sel.size} nodes, max K err {wk:.2e}, R err {wr:.2e}")
 
 
-@pytest.mark.parametrize("kernel", [lgdm.KERNEL_AUTO, lgdm.KERNEL_SWEEP3, lgdm.KERNEL_SWEEP4])
+@pytest.mark.parametrize("kernel", [lgdm.KERNEL_AUTO, lgdm.KERNEL_SWEEP3, lgdm.KERNEL_SWEEP4,
+                                    lgdm.KERNEL_SWEEP5])
 @pytest.mark.parametrize("etype,n,P", [(lgdm.QUAD4, (23, 31), 3), (lgdm.HEX8, (7, 5, 13), 4),
                                        (lgdm.BAR2, (50,), 2)])
 def test_slabs_stitch_bitwise(etype, n, P, kernel):

@@ -25,6 +25,8 @@ if cfg.etype == 2:
 mesh = synth.structured_mesh(cfg)
 d, k = synth.fields(cfg, mesh)
 m = lgdm.Mesh(cfg.etype, mesh.coords, mesh.conn, lgdm.material(**synth.MATERIAL))
+if len(sys.argv) > 2:
+    m.set_kernel(int(sys.argv[2]))
 m.set_state(d, k)
 m.assemble(); torch.cuda.synchronize()
 buf = np.zeros(16, dtype=np.uint64)
