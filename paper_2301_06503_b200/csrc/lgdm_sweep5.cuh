@@ -27,8 +27,10 @@ struct S5 {
   static constexpr int PL = S4::PL, Z0 = S4::Z0, Z1 = S4::Z1, UP = S4::UP, DN = S4::DN,
                        NS = S4::NS, COL = S4::COL, NCOLS = S4::NCOLS;
   static constexpr size_t SMEM = sizeof(double) * (size_t(SHT) + size_t(SLOT) + size_t(NCOLS) * COL);
-  // named barriers: slot full by producer pair 1-2, slot empty by producer pair 3-4, C 5
-  static constexpr int B_FULL = 1, B_EMPTY = 3, B_C = 5;
+  // The slot is split by Gauss point into halves h (GPs 4h .. 4h+3) written by PC warp (pair
+  // p, half h) and released by C half by half, so the next batch's first half is written
+  // while C still reads the second.  Named barriers: full [pair][half] 1-4, empty 5-8, C 9.
+  static constexpr int B_FULL = 1, B_EMPTY = 5, B_C = 9;
 };
 
 __global__ void __launch_bounds__(S5::T, 1)
@@ -91,8 +93,9 @@ k_sweep5(DevMat m, SweepGeom G, const double* __restrict__ coords,
   if (warp < S5::NPC) {
     // ---------- PC: core + 8 node expansions per lane (element, GP), straight to the slot ----------
     const int pair = warp >> 1;                       // batches t with t % 2 == pair
-    const int lid = (warp & 1) * 32 + lane;
-    const int el = lid >> 3, g = lid & 7;
+    const int half = warp & 1;                        // this warp writes GPs 4 half .. +3
+    const int el = lane >> 2, g = 4 * half + (lane & 3);
+    const int bsel = pair * 2 + half;
     const double* shg = shtab + g * NEN * 4;   // (dN/dxi, N) of the 8 nodes at this lane's GP
     auto sh = [&](int a, int j) { return shg[a * 4 + j]; };
     int t = 0;
@@ -116,7 +119,7 @@ k_sweep5(DevMat m, SweepGeom G, const double* __restrict__ coords,
               gpCoreS<3>(m, X, U, __ldg(kappa + e * NGP + g), [&](int a, int jj) { return sh(a, jj); },
                          [&](int a) { return sh(a, 3); }, c);
             }
-            if (t >= 1) bsync(S5::B_EMPTY + pair, NPC_T + NC_T);   // slot released by C
+            if (t >= 1) bsync(S5::B_EMPTY + bsel, 32 + NC_T);   // half released by C
             if (live) {
               using Co = Core<3>;
               double* rg = recs + el * S5::REL + g * S5::RGP;
@@ -161,13 +164,13 @@ k_sweep5(DevMat m, SweepGeom G, const double* __restrict__ coords,
               }
               *reinterpret_cast<double2*>(rg + NEN * S5::RS) = make_double2(c[Co::MU], c[Co::GHC]);
             }
-            barrive(S5::B_FULL + pair, NPC_T + NC_T);
+            barrive(S5::B_FULL + bsel, 32 + NC_T);
           }
           ++t;
         },
         [](int64_t) {});
     // drain: C's slot release after the last batch is meant for the other pair's next batch
-    if (t >= 1 && (t & 1) == pair) bsync(S5::B_EMPTY + pair, NPC_T + NC_T);
+    if (t >= 1 && (t & 1) == pair) bsync(S5::B_EMPTY + bsel, 32 + NC_T);
     return;
   }
 
@@ -265,8 +268,6 @@ k_sweep5(DevMat m, SweepGeom G, const double* __restrict__ coords,
           }
         }
         PT_MARK(9, ptc);
-        bsync(S5::B_FULL + prod, NPC_T + NC_T);
-        PT_MARK(0, ptc);
         Pair4 P;
 #pragma unroll
         for (int r = 0; r < 3; ++r) {
@@ -276,10 +277,13 @@ k_sweep5(DevMat m, SweepGeom G, const double* __restrict__ coords,
         }
         P.Kee_ab = P.Kee_ba = 0.0;
         double nsa[2] = {0.0, 0.0};
-        if (live) {
-          const double* re = recs + cw * S5::REL;
+        const double* re = recs + cw * S5::REL;
 #pragma unroll 1
-          for (int g = 0; g < NGP; ++g) {
+        for (int h = 0; h < 2; ++h) {
+          bsync(S5::B_FULL + prod * 2 + h, 32 + NC_T);
+          if (live) {
+#pragma unroll 1
+          for (int g = 4 * h; g < 4 * h + 4; ++g) {
             const double* blk = re + g * S5::RGP;
             const double2* A2 = reinterpret_cast<const double2*>(blk + pa * S5::RS);
             const double2* B2 = reinterpret_cast<const double2*>(blk + pb * S5::RS);
@@ -326,28 +330,26 @@ k_sweep5(DevMat m, SweepGeom G, const double* __restrict__ coords,
             P.Kee_ab = fma(NB, EA, fma(ghc, dot, P.Kee_ab));
             P.Kee_ba = fma(NA, EB, fma(ghc, dot, P.Kee_ba));
           }
-          // node sums {Fu[3], Fe, U = sum W' grad N [3], V = sum E} over the 8 GPs: lane =
-          // (node a = lane / 4, quarter q) owns two of the eight values (branch-free loop)
+          // node sums {Fu[3], Fe, U = sum W' grad N [3], V = sum E} over this half's GPs:
+          // lane = (node a = lane / 4, quarter q) owns two of the eight values
           {
             const int a = lane >> 2, q = lane & 3;
             // record chunks: q0 (fu0, fu1) = 10, q1 (fu2, fe) = 11, q2 (w1, w2) = 4,
             // q3 (w0 = chunk 3 .y, E = chunk 1 .y)
             const int c0 = q == 0 ? 10 : q == 1 ? 11 : q == 2 ? 4 : 3;
-            double v0 = 0.0, v1 = 0.0;
 #pragma unroll
-            for (int g = 0; g < NGP; ++g) {
+            for (int g = 4 * h; g < 4 * h + 4; ++g) {
               const double2* r2 = reinterpret_cast<const double2*>(re + g * S5::RGP + a * S5::RS);
               const double2 x = r2[c0];
               const double2 y = r2[1];
-              v0 += q == 3 ? x.y : x.x;
-              v1 += q == 3 ? y.y : x.y;
+              nsa[0] += q == 3 ? x.y : x.x;
+              nsa[1] += q == 3 ? y.y : x.y;
             }
-            nsa[0] = v0;
-            nsa[1] = v1;
           }
+          }
+          // this half is free for the other PC pair's next batch
+          barrive(S5::B_EMPTY + (prod ^ 1) * 2 + h, 32 + NC_T);
         }
-        // the slot is free for the other PC pair's next batch
-        barrive(S5::B_EMPTY + (prod ^ 1), NPC_T + NC_T);
         PT_MARK(2, ptc);
         if (c != prev_c) bsync(S5::B_C, NC_T);
         prev_c = c;

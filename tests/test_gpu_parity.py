@@ -190,3 +190,16 @@ def test_errors():
     with pytest.raises(lgdm.LGDMError) as ei:
         lgdm.Mesh(lgdm.QUAD4, bad, mesh.conn, mat)
     assert ei.value.status == 2 and "element" in str(ei.value)
+
+
+@pytest.mark.parametrize("kernel", [lgdm.KERNEL_SWEEP3, lgdm.KERNEL_SWEEP4, lgdm.KERNEL_SWEEP5])
+@pytest.mark.parametrize("etype,n", [(lgdm.QUAD4, (61, 40)), (lgdm.HEX8, (17, 9, 11))])
+def test_sweep_bitwise_reproducible(etype, n, kernel):
+    """The warp-specialised sweeps hand data between roles through named barriers only and
+    sum every entry in a fixed (element layer, colour) order: repeated assemblies -- several
+    hundred CTAs in flight -- must agree bitwise (a missing barrier shows up as a difference)."""
+    cfg, mesh, coords, dofs, kappa = _case(etype, n)
+    runs = [gpu_assemble(etype, coords, mesh.conn, dofs, kappa, kernel=kernel) for _ in range(3)]
+    for r in runs[1:]:
+        np.testing.assert_array_equal(r["val"], runs[0]["val"])
+        np.testing.assert_array_equal(r["R"], runs[0]["R"])
