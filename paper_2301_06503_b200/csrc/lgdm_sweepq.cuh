@@ -30,7 +30,7 @@ struct SQ {
   static constexpr int NGP = 4, NEN = 4, NDPN = 3;
   static constexpr int NPCG = 4, PCW = 2;                    // PC groups (colour x row parity), warps
   static constexpr int NCW = 4;                              // C warps: 2 groups (colours) x 2
-  static constexpr int NFW = 2;                              // flush warps
+  static constexpr int NFW = 4;                              // flush warps
   static constexpr int T = 32 * (NPCG * PCW + NCW + NFW);
   static constexpr int NSLOT = 4;                            // slot = 2 colour + row parity
   // shape table [NGP][NEN][4] = (dN/dxi0, dN/dxi1, N, 0)
@@ -46,9 +46,14 @@ struct SQ {
   // interior node: [row r 3][dy 3][dx 3][j 3] = 81 doubles; three node-row buffers (node
   // row zn uses buffer zn % 3) so the flush of node row s overlaps the adds of element row
   // s+1 (which touch node rows s+1, s+2); NS[3][TX][6]
-  static constexpr int NROW = 81, NBUF = 3, ACC = NBUF * TX * NROW, NSB = ACC, NSS = 7;   // odd NS stride
+  // Node sums are kept per colour (NSC apart) and added at flush: the colour-0 adds of
+  // element row s+1 may run while the colour-1 adds of row s are still in flight, and both
+  // touch the node sums of node row s+1 (never the same K entry: elements of different
+  // colours in adjacent rows share no node pair).
+  static constexpr int NROW = 81, NBUF = 3, ACC = NBUF * TX * NROW, NSB = ACC, NSS = 7,   // odd NS stride
+                       NSC = NBUF * TX * NSS;
   static constexpr size_t SMEM = sizeof(double) * (size_t(SHT) + size_t(NSLOT) * SLOT +
-                                                   size_t(ACC) + size_t(NBUF * TX * NSS));
+                                                   size_t(ACC) + size_t(NCOL * NSC));
   // named barriers: slot full 1..3, slot empty 4..6; by row parity (group 0 may run up to
   // two rows ahead of the flush): colour-0 adds done 7/8, row adds done (C -> flush) 9/10,
   // node row flushed (flush -> group 0 two rows later) 11/12; flush warps 13
@@ -90,7 +95,7 @@ k_sweepq(DevMat m, SweepGeom G, const double* __restrict__ coords,
     shtab[k * 4 + 2] = shapeN<2>(a, g);
     shtab[k * 4 + 3] = 0.0;
   }
-  for (int k = tid; k < SQ::ACC + SQ::NBUF * SQ::TX * SQ::NSS; k += SQ::T) acc[k] = 0.0;
+  for (int k = tid; k < SQ::ACC + SQ::NCOL * SQ::NSC; k += SQ::T) acc[k] = 0.0;
   __syncthreads();
 
   // batch schedule (every role): element row s, colour c (parity of i) -- exactly one batch
@@ -265,12 +270,14 @@ k_sweepq(DevMat m, SweepGeom G, const double* __restrict__ coords,
           for (int task = ft; task < cols * 9; task += F_T) {   // column fastest: conflict-free
             const int e = task / cols, cc = task - cols * e, r = e / 3, j = e - 3 * r;
             double* row = row_of(ix0 + cc, zn) + r * 27 + j;
-            const double* ns = ns_of(ix0 + cc, zn);
-            double d = 0.0;
-#pragma unroll
-            for (int sl = 0; sl < 9; ++sl)
-              if (sl != 4) d -= row[sl * 3];
-            if (j == 2) d += (r < 2) ? ns[3 + r] : ns[5];
+            const double* ns0 = ns_of(ix0 + cc, zn);
+            const double d0 = (row[0] + row[3]) + (row[6] + row[9]);
+            const double d1 = (row[15] + row[18]) + (row[21] + row[24]);
+            double d = -(d0 + d1);
+            if (j == 2) {
+              const int q = (r < 2) ? 3 + r : 5;
+              d += ns0[q] + ns0[q + SQ::NSC];
+            }
             row[4 * 3] = d;
           }
           PT_MARK(5, ptf);
@@ -320,11 +327,14 @@ k_sweepq(DevMat m, SweepGeom G, const double* __restrict__ coords,
           // R: consecutive nodes, 3 values each
           for (int k = ft; k < cols * 3; k += F_T) {
             const int cc = k / 3, j = k - 3 * cc;
-            double* ns = ns_of(ix0 + cc, zn);
-            __stcs(Rv + (ix0 + cc + nxN * zn - G.own_node_b) * 3 + j, ns[j]);
+            const double* ns0 = ns_of(ix0 + cc, zn);
+            __stcs(Rv + (ix0 + cc + nxN * zn - G.own_node_b) * 3 + j, ns0[j] + ns0[j + SQ::NSC]);
           }
           bsync(SQ::B_FW, F_T);
-          for (int k = ft; k < cols * SQ::NSS; k += F_T) ns_of(ix0, zn)[k] = 0.0;
+          for (int k = ft; k < cols * SQ::NSS; k += F_T) {
+            ns_of(ix0, zn)[k] = 0.0;
+            ns_of(ix0, zn)[k + SQ::NSC] = 0.0;
+          }
           PT_MARK(7, ptf);
           bsync(SQ::B_FW, F_T);
           PT_MARK(8, ptf);
@@ -478,9 +488,12 @@ k_sweepq(DevMat m, SweepGeom G, const double* __restrict__ coords,
           add_blocks(oa ? blk_of(ax, az, b2x - ax, int(b2z - az)) : nullptr,
                      ob2 ? blk_of(b2x, b2z, ax - b2x, int(az - b2z)) : nullptr, P2);
           auto add_ns = [&](int x, int64_t z, const double (&v)[6]) {
-            double* np = ns_of(x, z);
+            double* np = ns_of(x, z) + cg * SQ::NSC;   // this colour's node sums
+            double w[6];
 #pragma unroll
-            for (int q = 0; q < 6; ++q) np[q] += v[q];
+            for (int q = 0; q < 6; ++q) w[q] = np[q];
+#pragma unroll
+            for (int q = 0; q < 6; ++q) np[q] = w[q] + v[q];
           };
           if (oa) add_ns(ax, az, nsum);
           if (ck == 0 && ob2) add_ns(b2x, b2z, nsum3);

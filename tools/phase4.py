@@ -17,7 +17,8 @@ QNAMES = {0: "C other", 1: "C wait slot-full", 2: "C compute", 3: "C wait add-or
           12: "PC other", 10: "PC wait slot-empty", 11: "PC core+records"}
 names = {0: "C wait core-full", 1: "C expansion round", 2: "C pair GPs (4)", 3: "C ns shuffle",
          4: "C colour barrier", 5: "C adds", 6: "C end-layer barrier", 7: "C flush", 8: "C reset barrier",
-         9: "C batch prologue", 10: "PC wait core-empty", 11: "PC core", 12: "PC other"}
+         9: "C batch prologue", 10: "PC wait core-empty", 11: "PC core", 12: "PC other",
+         15: "PC wait adds-done", 14: "PC flush"}
 cid = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 cfg = synth.CONFIGS[cid]
 if cfg.etype == 2:
