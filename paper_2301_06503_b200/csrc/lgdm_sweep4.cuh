@@ -46,9 +46,13 @@ struct S4 {
   // warp-private records [4 GP][8 node][RS] + (mu*, ghc) per GP
   static constexpr int RS = 22, RGP = NEN * RS + 2, RWARP = 4 * RGP;
   // accumulator column: planes Z0, Z1 (in-plane, by node-layer parity), UP, DN; each plane
-  // [row 4][slot 9][j 4] = 144 doubles (+2 pad: 73 x 16 B, odd); NS[2][8]
-  static constexpr int PL = 146, Z0 = 0, Z1 = PL, UP = 2 * PL, DN = 3 * PL, NS = 4 * PL,
-                       COL = NS + 16 + 2;                 // 602 doubles = 301 x 16 B (odd)
+  // [row 4][18 chunks of 16 B] = 144 doubles (chunk positions: pos4); NS[2][8].  Offsets in
+  // 16-byte units: Z0 1, Z1 73, UP 149, DN 221 (= 1, 1, 5, 5 mod 8), NS 293, column 308
+  // (= 4 mod 8): with the lane order of kPair4 and pos4 the quarter-warp bank model of the
+  // block adds gives 40 wavefronts per (parity, h, AB/BA) sweep vs 67 for the round-1
+  // layout (ideal 32; tools/bank_search4.py)
+  static constexpr int PLD = 144, Z0 = 2, Z1 = 146, UP = 298, DN = 442, NS = 586,
+                       COL = 616;
   static constexpr int NCOLS = TX * TY;
   static constexpr size_t SMEM = sizeof(double) * (size_t(SHT) + size_t(NCSLOT) * CSLOT +
                                                    size_t(NC) * RWARP + size_t(NCOLS) * COL);
@@ -83,6 +87,21 @@ __device__ __forceinline__ void barrive(int id, int n) {
 // lanes targeting slots sl and sl+4 (same bank group otherwise) land in different bank groups.
 __host__ __device__ constexpr int swz(int sl, int h) { return 2 * sl + (h ^ ((sl >> 2) & 1)); }
 __host__ __device__ constexpr int soff(int sl, int j) { return 2 * swz(sl, j >> 1) + (j & 1); }
+
+// k_sweep4 plane rows: chunk (slot sl, half h) of a row sits at 16-byte position pos4(sl, h)
+// (a permutation of 0..17 found by tools/bank_search4.py); soff4 = double offset of entry j
+// = {{2, 15}, {5, 14}, {0, 13}, {7, 4}, {6, 17}, {11, 8}, {16, 3}, {9, 10}, {12, 1}}[sl][h],
+// packed 5 bits per slot so runtime (sl, h) never touch memory
+__host__ __device__ constexpr int pos4(int sl, int h) {
+  return int(((h ? 0x150d11235cfull : 0xc4c166380a2ull) >> (5 * sl)) & 31u);
+}
+__host__ __device__ constexpr int soff4(int sl, int j) { return 2 * pos4(sl, j >> 1) + (j & 1); }
+// lane -> off-diagonal pair of the C warps' pair stage (same search)
+__host__ __device__ constexpr int pair4(int lane) {
+  constexpr int P[28] = {47, 24, 27, 7, 6, 2, 23, 57, 13, 15, 26, 36, 16, 14,
+                         17, 56, 46, 37, 45, 4, 67, 12, 35, 25, 3, 1, 5, 34};
+  return P[lane];
+}
 
 // off-diagonal pair p (0..27) -> (a, b), a < b
 __device__ __forceinline__ void offdiag_ab(int p, int& a, int& b) {
@@ -277,12 +296,25 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
   // pair lane
   const bool plane_lane = lane < S4::NOFF;
   int pa = 0, pb = 1;
-  if (plane_lane) offdiag_ab(lane, pa, pb);
+  if (plane_lane) {
+#pragma unroll
+    for (int k = 0; k < S4::NOFF; ++k)
+      if (lane == k) {
+        pa = pair4(k) / 10;
+        pb = pair4(k) % 10;
+      }
+  }
   int oax, oay, oaz, obx, oby, obz;
   node_off<3>(pa, oax, oay, oaz);
   node_off<3>(pb, obx, oby, obz);
   const int psAB = plane_slot<3>(obx - oax, oby - oay), psBA = plane_slot<3>(oax - obx, oay - oby);
   const int dzAB = obz - oaz;
+  int qAB0 = 0, qAB1 = 0, qBA0 = 0, qBA1 = 0;   // pos4 of this lane's two slots
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+    if (psAB == k) { qAB0 = pos4(k, 0); qAB1 = pos4(k, 1); }
+    if (psBA == k) { qBA0 = pos4(k, 0); qBA1 = pos4(k, 1); }
+  }
   double* myrec = recs + cw * S4::RWARP;
   auto col_of = [&](int x, int y) { return acc + ((x - ix0) + cols_x * (y - iy0)) * S4::COL; };
   auto plane_of = [&](double* colp, int zpar, bool zs, int dz) -> double* {
@@ -291,6 +323,10 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
   };
 
   __shared__ int64_t sbase[2][S4::NCOLS];   // CSR offsets of node layers (by parity)
+  int lane_pos = 0;   // smem chunk position of CSR chunk `lane` (lanes 0..17) of a plane row
+#pragma unroll
+  for (int k = 0; k < 18; ++k)
+    if (lane == k) lane_pos = pos4(k >> 1, k & 1);
   // ---- flush helpers (one warp per column) ----
   // copy plane P ([row 4][9 slots][4]) of node (x, y, z) to its compacted CSR position
   auto write_plane = [&](int x, int y, int64_t z, int dz, const double* P, bool inner) {
@@ -301,7 +337,7 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
       const double2* src = reinterpret_cast<const double2*>(P);
 #pragma unroll
       for (int r = 0; r < 4; ++r)
-        if (lane < 18) __stcs(out + r * W2 + lane, src[r * 18 + (lane ^ ((lane >> 3) & 1))]);
+        if (lane < 18) __stcs(out + r * W2 + lane, src[r * 18 + lane_pos]);
       return;
     }
     const int xlo = x > 0 ? -1 : 0, xhi = x < G.nx ? 1 : 0;
@@ -315,8 +351,12 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
       if (dx < xlo || dx > xhi || dy < ylo || dy > yhi) continue;
       const double2* src = reinterpret_cast<const double2*>(P + i * 36);
       double2* dst = reinterpret_cast<double2*>(out + i * W + 4 * ((dy - ylo) * wx + (dx - xlo)));
-      __stcs(dst, src[swz(sl, 0)]);
-      __stcs(dst + 1, src[swz(sl, 1)]);
+      int q0 = 0, q1 = 0;
+#pragma unroll
+      for (int k = 0; k < 9; ++k)
+        if (sl == k) { q0 = pos4(k, 0); q1 = pos4(k, 1); }
+      __stcs(dst, src[q0]);
+      __stcs(dst + 1, src[q1]);
     }
   };
   // lanes 0..15: entry (i, j) = (lane / 4, lane % 4) of the 4x4 blocks, summed over slots
@@ -326,7 +366,7 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
     const int j = lane & 3;
 #pragma unroll
     for (int sl = 0; sl < 9; ++sl)
-      if (!(skip_self && sl == 4)) s += p[soff(sl, j)];
+      if (!(skip_self && sl == 4)) s += p[soff4(sl, j)];
     return s;
   };
   // finish node (x, y, z): diagonal block = -sum(plane -1) [kept in the self slot]
@@ -336,7 +376,7 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
     const double* ns = colp + S4::NS + (z & 1) * 8;
     if (lane < 16) {
       const int i = lane >> 2, j = lane & 3;
-      double* self = Zp + i * 36 + soff(4, j);
+      double* self = Zp + i * 36 + soff4(4, j);
       double d = *self - plane_sum(Zp, true);
       if (has_up) d -= plane_sum(colp + S4::UP, false);
       if (j == 3) d += (i < 3) ? ns[4 + i] : ns[7];
@@ -489,32 +529,46 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
           const bool own_b = bx >= ix0 && bx < ix1 && by >= iy0 && by < iy1 && bzr >= 0 && s + obz < z1;
           if (own_a) {
             double* Pp = plane_of(col_of(ax, ay), (zpar_s ^ oaz) & 1, oaz == 0, dzAB);
+            // all 8 loads of the block first: the compiler cannot prove the rows distinct and
+            // would otherwise serialise 8 read-modify-write round trips
+            double2 lo[4], hi[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              const double2* q = reinterpret_cast<const double2*>(Pp + r * 36);
+              lo[r] = q[qAB0];
+              hi[r] = q[qAB1];
+            }
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
               double2* q = reinterpret_cast<double2*>(Pp + r * 36);
-              double2 lo = q[swz(psAB, 0)], hi = q[swz(psAB, 1)];
               if (r < 3) {
-                lo.x += P.Kuu[r][0]; lo.y += P.Kuu[r][1]; hi.x += P.Kuu[r][2]; hi.y += P.Kue_ab[r];
+                lo[r].x += P.Kuu[r][0]; lo[r].y += P.Kuu[r][1]; hi[r].x += P.Kuu[r][2]; hi[r].y += P.Kue_ab[r];
               } else {
-                lo.x += P.Keu_ab[0]; lo.y += P.Keu_ab[1]; hi.x += P.Keu_ab[2]; hi.y += P.Kee_ab;
+                lo[r].x += P.Keu_ab[0]; lo[r].y += P.Keu_ab[1]; hi[r].x += P.Keu_ab[2]; hi[r].y += P.Kee_ab;
               }
-              q[swz(psAB, 0)] = lo;
-              q[swz(psAB, 1)] = hi;
+              q[qAB0] = lo[r];
+              q[qAB1] = hi[r];
             }
           }
           if (own_b) {
             double* Pp = plane_of(col_of(bx, by), (zpar_s ^ obz) & 1, obz == 0, -dzAB);
+            double2 lo[4], hi[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              const double2* q = reinterpret_cast<const double2*>(Pp + r * 36);
+              lo[r] = q[qBA0];
+              hi[r] = q[qBA1];
+            }
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
               double2* q = reinterpret_cast<double2*>(Pp + r * 36);
-              double2 lo = q[swz(psBA, 0)], hi = q[swz(psBA, 1)];
               if (r < 3) {
-                lo.x += P.Kuu[0][r]; lo.y += P.Kuu[1][r]; hi.x += P.Kuu[2][r]; hi.y += P.Kue_ba[r];
+                lo[r].x += P.Kuu[0][r]; lo[r].y += P.Kuu[1][r]; hi[r].x += P.Kuu[2][r]; hi[r].y += P.Kue_ba[r];
               } else {
-                lo.x += P.Keu_ba[0]; lo.y += P.Keu_ba[1]; hi.x += P.Keu_ba[2]; hi.y += P.Kee_ba;
+                lo[r].x += P.Keu_ba[0]; lo[r].y += P.Keu_ba[1]; hi[r].x += P.Keu_ba[2]; hi[r].y += P.Kee_ba;
               }
-              q[swz(psBA, 0)] = lo;
-              q[swz(psBA, 1)] = hi;
+              q[qBA0] = lo[r];
+              q[qBA1] = hi[r];
             }
           }
         }
@@ -535,7 +589,7 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
             // plane -1 of node layer s+1 is complete: out, and minus its row sums go to the
             // self slot of that node's plane 0 (never accumulated by pair adds)
             if (lane < 16)
-              colp[(((s + 1) & 1) ? S4::Z1 : S4::Z0) + (lane >> 2) * 36 + soff(4, lane & 3)] =
+              colp[(((s + 1) & 1) ? S4::Z1 : S4::Z0) + (lane >> 2) * 36 + soff4(4, lane & 3)] =
                   -plane_sum(colp + S4::DN, false);
             write_plane(x, y, s + 1, -1, colp + S4::DN, inner);
           }
@@ -547,8 +601,10 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
           double2* z2 = reinterpret_cast<double2*>(colp + ((s & 1) ? S4::Z1 : S4::Z0));
           double2* ud = reinterpret_cast<double2*>(colp + S4::UP);
           const double2 zero = make_double2(0.0, 0.0);
-          for (int k2 = lane; k2 < S4::PL / 2; k2 += 32) z2[k2] = zero;
-          for (int k2 = lane; k2 < S4::PL; k2 += 32) ud[k2] = zero;
+          for (int k2 = lane; k2 < S4::PLD / 2; k2 += 32) z2[k2] = zero;
+          for (int k2 = lane; k2 < S4::PLD / 2; k2 += 32) ud[k2] = zero;
+          double2* dn2 = reinterpret_cast<double2*>(colp + S4::DN);
+          for (int k2 = lane; k2 < S4::PLD / 2; k2 += 32) dn2[k2] = zero;
           if (lane < 4) reinterpret_cast<double2*>(colp + S4::NS + (s & 1) * 8)[lane] = zero;
         }
         PT_MARK(7, ptc);

@@ -24,8 +24,9 @@ struct S5 {
   // GP fall in distinct bank groups); per (element, GP): 8 records + (mu*, ghc) = 210 doubles
   // (105 x 16 B, odd: the 8 GP lanes of an element write distinct bank groups)
   static constexpr int RS = 26, RGP = NEN * RS + 2, REL = NGP * RGP, SLOT = E * REL;
-  static constexpr int PL = S4::PL, Z0 = S4::Z0, Z1 = S4::Z1, UP = S4::UP, DN = S4::DN,
-                       NS = S4::NS, COL = S4::COL, NCOLS = S4::NCOLS;
+  // accumulator column (k_sweep4's round-1 layout): planes Z0, Z1, UP, DN of 146 doubles, NS
+  static constexpr int PL = 146, Z0 = 0, Z1 = PL, UP = 2 * PL, DN = 3 * PL, NS = 4 * PL,
+                       COL = NS + 16 + 2, NCOLS = S4::NCOLS;
   static constexpr size_t SMEM = sizeof(double) * (size_t(SHT) + size_t(SLOT) + size_t(NCOLS) * COL);
   // The slot is split by Gauss point into halves h (GPs 4h .. 4h+3) written by PC warp (pair
   // p, half h) and released by C half by half, so the next batch's first half is written
