@@ -30,6 +30,8 @@
 //                              off-diagonal pairs; adds into the block-row planes; flush
 #pragma once
 
+#include <type_traits>
+
 namespace lgdm {
 
 struct S4 {
@@ -71,9 +73,19 @@ struct C4 {
 };
 
 // record of (element, GP, node), doubles:
-//   [g0 g1][g2 E][s0 s1][s2 w0][w1 w2][d0 d1][d2 N][t1_0 t1_1][t1_2 t2_0][t2_1 t2_2]
-//   g = grad N, s = S grad N, w = W' grad N (Kue), d = Dt' grad N (Keu), E (Kee), N,
-//   t1 = lam* g + Ams s, t2 = Ams g + Ass s (Kuu)
+//   [g0 g1][g2 s0][s1 s2][g2 t1_0][t1_1 t1_2][t2_0 t2_1][t2_2 E][w0 w1][w2 d0][d1 d2]
+//   g = grad N, s = S grad N, t1 = lam* g + Ams s, t2 = Ams g + Ass s (Kuu), w = W' grad N
+//   (Kue), d = Dt' grad N (Keu), E (Kee).  The pair lanes read only the Kuu fields (A side:
+//   chunks 0-2, B side: chunks 0, 3-6); the coupling blocks come from moments (below).
+// coupling moments: for node n and component c of (w0 w1 w2 d0 d1 d2 E),
+//   M[n][m][c] = sum_g N_m(g) c_n(g), so that Kue_ab = M[a][b][w], Kue_ba = M[b][a][w],
+//   Keu_ab = M[b][a][d], Keu_ba = M[a][b][d], Kee_ab = M[a][b][E] + sum_g ghc gA.gB
+//   (Eqs. 11b-d with N_b evaluated at the Gauss points: constants)
+__host__ __device__ constexpr int mom_off(int c) { return c < 6 ? 14 + c : 13; }   // record offset of component c
+// moment M[n][m][c] at m * 63 + n * 7 + c: conflict-free stores of the (n, c) lanes and
+// 42 (ideal 28) wavefronts for the pair lanes' 14 loads (bank search over linear layouts)
+__host__ __device__ constexpr int mom_idx(int n, int m, int c) { return m * 63 + n * 7 + c; }
+static_assert(mom_idx(7, 7, 6) < S4::RWARP, "moments fit the warp's record buffer");
 
 __device__ __forceinline__ void bsync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -155,16 +167,16 @@ __device__ __forceinline__ void expand4(const double* __restrict__ co, const dou
   const double Ea = fma(c[C4::HN], Na, gvd);
   const double fe = fma(c[C4::FE0], Na, fvd);
   double2* r2 = reinterpret_cast<double2*>(r);
-  r2[0] = make_double2(gn[0], gn[1]);
-  r2[1] = make_double2(gn[2], Ea);
-  r2[2] = make_double2(SgN[0], SgN[1]);
-  r2[3] = make_double2(SgN[2], WgN[0]);
-  r2[4] = make_double2(WgN[1], WgN[2]);
-  r2[5] = make_double2(DgN[0], DgN[1]);
-  r2[6] = make_double2(DgN[2], Na);
-  r2[7] = make_double2(t1[0], t1[1]);
-  r2[8] = make_double2(t1[2], t2[0]);
-  r2[9] = make_double2(t2[1], t2[2]);
+  r2[0] = make_double2(gn[0], gn[1]);     // Kuu, row side (A): chunks 0-2
+  r2[1] = make_double2(gn[2], SgN[0]);
+  r2[2] = make_double2(SgN[1], SgN[2]);
+  r2[3] = make_double2(gn[2], t1[0]);     // Kuu, column side (B): chunks 0, 3-6
+  r2[4] = make_double2(t1[1], t1[2]);
+  r2[5] = make_double2(t2[0], t2[1]);
+  r2[6] = make_double2(t2[2], Ea);        // coupling moments read E, W' grad N, Dt' grad N
+  r2[7] = make_double2(WgN[0], WgN[1]);
+  r2[8] = make_double2(WgN[2], DgN[0]);
+  r2[9] = make_double2(DgN[1], DgN[2]);
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     ns[i] += fu[i];
@@ -420,17 +432,42 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
         const int i = ifst + 2 * (k % ni), j = jfst + 2 * (k / ni);
         const int sz = int(s - z0);   // layer of node z relative to the chunk
         const double* ce = cores + cslot * S4::CSLOT + cw * S4::CEL;
-        Pair4 P;
+        // pair lanes: Kuu_ab and sum_g ghc gA.gB; moment lanes: two (node, component)
+        // tasks t = lane, lane + 32 (t < 56: n = t / 7, c = t % 7), 8 moments each
+        double Kuu[3][3], Gd = 0.0;
 #pragma unroll
-        for (int r = 0; r < 3; ++r) {
+        for (int r = 0; r < 3; ++r)
 #pragma unroll
-          for (int u = 0; u < 3; ++u) P.Kuu[r][u] = 0.0;
-          P.Kue_ab[r] = P.Kue_ba[r] = P.Keu_ab[r] = P.Keu_ba[r] = 0.0;
-        }
-        P.Kee_ab = P.Kee_ba = 0.0;
+          for (int u = 0; u < 3; ++u) Kuu[r][u] = 0.0;
+        double M1[8], M2[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) M1[q] = M2[q] = 0.0;
+        const int mt1 = lane, mt2 = lane + 32;
+        const int mn1 = mt1 / 7, mc1 = mt1 - 7 * mn1;
+        const int mn2 = mt2 < 56 ? mt2 / 7 : 0, mc2 = mt2 < 56 ? mt2 - 7 * (mt2 / 7) : 0;
+        int mo1 = 0, mo2 = 0;
+        mo1 = mom_off(mc1);
+        mo2 = mom_off(mc2);
+        const double* mrec1 = myrec + mn1 * S4::RS + mo1;
+        const double* mrec2 = myrec + mn2 * S4::RS + mo2;
         double ns[8];
 #pragma unroll
         for (int k2 = 0; k2 < 8; ++k2) ns[k2] = 0.0;
+        // moments of the records of round R (GPs 4R .. 4R + 3); N_m(g) compile-time constants
+        auto moments = [&](auto rc) {
+          constexpr int R = decltype(rc)::value;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const double v1 = mrec1[k * S4::RGP];
+            const double v2 = mt2 < 56 ? mrec2[k * S4::RGP] : 0.0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const double nq = shapeN<3>(q, 4 * R + k);
+              M1[q] = fma(nq, v1, M1[q]);
+              M2[q] = fma(nq, v2, M2[q]);
+            }
+          }
+        };
 #pragma unroll 1
         for (int rnd = 0; rnd < 2; ++rnd) {
           // expansions of the 8 nodes at GPs 4 rnd .. 4 rnd + 3
@@ -445,30 +482,24 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
           if (rnd == 1) barrive(S4::B_CE + cslot, NPC_T + NC_T);   // core slot no longer read
           __syncwarp();
           PT_MARK(1, ptc);
+          if (rnd == 0) moments(std::integral_constant<int, 0>{});
+          else moments(std::integral_constant<int, 1>{});
 #pragma unroll 1
           for (int gg = 0; gg < 4; ++gg) {
             const double* blk = myrec + gg * S4::RGP;
             const double2* A2 = reinterpret_cast<const double2*>(blk + pa * S4::RS);
             const double2* B2 = reinterpret_cast<const double2*>(blk + pb * S4::RS);
             const double2 hdr = *reinterpret_cast<const double2*>(blk + NEN * S4::RS);
-            double gA[3], sA[3], wA[3], dA[3], EA, NA, gB[3], t1[3], t2[3], wB[3], dB[3], EB, NB;
+            double gA[3], sA[3], gB[3], t1[3], t2[3];
             double2 v;
             v = A2[0]; gA[0] = v.x; gA[1] = v.y;
-            v = A2[1]; gA[2] = v.x; EA = v.y;
-            v = A2[2]; sA[0] = v.x; sA[1] = v.y;
-            v = A2[3]; sA[2] = v.x; wA[0] = v.y;
-            v = A2[4]; wA[1] = v.x; wA[2] = v.y;
-            v = A2[5]; dA[0] = v.x; dA[1] = v.y;
-            v = A2[6]; dA[2] = v.x; NA = v.y;
+            v = A2[1]; gA[2] = v.x; sA[0] = v.y;
+            v = A2[2]; sA[1] = v.x; sA[2] = v.y;
             v = B2[0]; gB[0] = v.x; gB[1] = v.y;
-            v = B2[1]; gB[2] = v.x; EB = v.y;
-            v = B2[3]; wB[0] = v.y;
-            v = B2[4]; wB[1] = v.x; wB[2] = v.y;
-            v = B2[5]; dB[0] = v.x; dB[1] = v.y;
-            v = B2[6]; dB[2] = v.x; NB = v.y;
-            v = B2[7]; t1[0] = v.x; t1[1] = v.y;
-            v = B2[8]; t1[2] = v.x; t2[0] = v.y;
-            v = B2[9]; t2[1] = v.x; t2[2] = v.y;
+            v = B2[3]; gB[2] = v.x; t1[0] = v.y;
+            v = B2[4]; t1[1] = v.x; t1[2] = v.y;
+            v = B2[5]; t2[0] = v.x; t2[1] = v.y;
+            t2[2] = B2[6].x;
             const double mu = hdr.x, ghc = hdr.y;
             double dot = gA[0] * gB[0];
             dot = fma(gA[1], gB[1], dot);
@@ -478,23 +509,42 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
               const double ub = mu * gB[r];
 #pragma unroll
               for (int u = 0; u < 3; ++u) {
-                double x = P.Kuu[r][u];
+                double x = Kuu[r][u];
                 x = fma(gA[r], t1[u], x);
                 x = fma(sA[r], t2[u], x);
                 x = fma(gA[u], ub, x);
-                P.Kuu[r][u] = x;
+                Kuu[r][u] = x;
               }
-              P.Kuu[r][r] = fma(mu, dot, P.Kuu[r][r]);
-              P.Kue_ab[r] = fma(NB, wA[r], P.Kue_ab[r]);
-              P.Kue_ba[r] = fma(NA, wB[r], P.Kue_ba[r]);
-              P.Keu_ab[r] = fma(NA, dB[r], P.Keu_ab[r]);
-              P.Keu_ba[r] = fma(NB, dA[r], P.Keu_ba[r]);
+              Kuu[r][r] = fma(mu, dot, Kuu[r][r]);
             }
-            P.Kee_ab = fma(NB, EA, fma(ghc, dot, P.Kee_ab));
-            P.Kee_ba = fma(NA, EB, fma(ghc, dot, P.Kee_ba));
+            Gd = fma(ghc, dot, Gd);
           }
           __syncwarp();
           PT_MARK(2, ptc);
+        }
+        // moments out (the record buffer is free now), then each pair lane picks its 14
+        double* mom = myrec;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          mom[mom_idx(mn1, q, mc1)] = M1[q];
+          if (mt2 < 56) mom[mom_idx(mn2, q, mc2)] = M2[q];
+        }
+        __syncwarp();
+        Pair4 P;
+        {
+          const double* mab = mom + mom_idx(pa, pb, 0);   // M[a][b][.]
+          const double* mba = mom + mom_idx(pb, pa, 0);
+#pragma unroll
+          for (int r = 0; r < 3; ++r) {
+#pragma unroll
+            for (int u = 0; u < 3; ++u) P.Kuu[r][u] = Kuu[r][u];
+            P.Kue_ab[r] = mab[r];
+            P.Kue_ba[r] = mba[r];
+            P.Keu_ab[r] = mba[3 + r];
+            P.Keu_ba[r] = mab[3 + r];
+          }
+          P.Kee_ab = mab[6] + Gd;
+          P.Kee_ba = mba[6] + Gd;
         }
         // node sums: reduce the four Gauss-point lanes of each node (lanes xa + 8 xg)
 #pragma unroll
