@@ -40,7 +40,7 @@ struct S4 {
   static constexpr int NPC = 4, NC = E;                          // warps per role
   static constexpr int T = 32 * (NPC + NC);
   // shape table [NGP][NEN][4] = (dN/dxi, N) at the Gauss points
-  static constexpr int SHT = NGP * NEN * 4;
+  static constexpr int SHT = NGP * NEN * 6;   // stride 3 x 16 B per (g, a): conflict-free reads
   // core ring [3][E][NGP][CSP]: core = Core<3> values with a pad after J^-1 so every field
   // group is 16-byte aligned (48 doubles); CSP = 50 (25 x 16 B) puts the 4 cores a C warp
   // reads at once into distinct bank groups
@@ -196,7 +196,7 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
          const int64_t* __restrict__ base, double* __restrict__ val, double* __restrict__ Rv) {
   constexpr int E = S4::E, NGP = 8, NEN = 8;
   extern __shared__ double sm[];
-  double* shtab = sm;                              // [NGP][NEN][4]
+  double* shtab = sm;                              // [NGP][NEN][6] = (dN/dxi, N, pad)
   double* cores = shtab + S4::SHT;                 // [3][E][CEL]
   double* recs = cores + S4::NCSLOT * S4::CSLOT;   // [NC][RWARP]
   double* acc = recs + S4::NC * S4::RWARP;         // [NCOLS][COL]
@@ -226,8 +226,8 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
   for (int k = tid; k < NGP * NEN; k += S4::T) {
     const int g = k >> 3, a = k & 7;
 #pragma unroll
-    for (int j = 0; j < 3; ++j) shtab[k * 4 + j] = shape_dxi<3>(a, g, j);
-    shtab[k * 4 + 3] = shapeN<3>(a, g);
+    for (int j = 0; j < 3; ++j) shtab[k * 6 + j] = shape_dxi<3>(a, g, j);
+    shtab[k * 6 + 3] = shapeN<3>(a, g);
   }
   for (int k = tid; k < S4::NCOLS * S4::COL; k += S4::T) acc[k] = 0.0;
   __syncthreads();
@@ -335,10 +335,10 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
   };
 
   __shared__ int64_t sbase[2][S4::NCOLS];   // CSR offsets of node layers (by parity)
-  int lane_pos = 0;   // smem chunk position of CSR chunk `lane` (lanes 0..17) of a plane row
-#pragma unroll
+  int lane_csr = 0;   // CSR chunk of smem chunk position `lane` (lanes 0..17) of a plane row:
+#pragma unroll        // contiguous (conflict-free) smem reads, permuted 16-byte global stores
   for (int k = 0; k < 18; ++k)
-    if (lane == k) lane_pos = pos4(k >> 1, k & 1);
+    if (pos4(k >> 1, k & 1) == lane) lane_csr = k;
   // ---- flush helpers (one warp per column) ----
   // copy plane P ([row 4][9 slots][4]) of node (x, y, z) to its compacted CSR position
   auto write_plane = [&](int x, int y, int64_t z, int dz, const double* P, bool inner) {
@@ -349,7 +349,7 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
       const double2* src = reinterpret_cast<const double2*>(P);
 #pragma unroll
       for (int r = 0; r < 4; ++r)
-        if (lane < 18) __stcs(out + r * W2 + lane, src[r * 18 + lane_pos]);
+        if (lane < 18) __stcs(out + r * W2 + lane_csr, src[r * 18 + lane]);
       return;
     }
     const int xlo = x > 0 ? -1 : 0, xhi = x < G.nx ? 1 : 0;
@@ -475,7 +475,7 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
             const int g = 4 * rnd + xg;
             const double* co = ce + g * S4::CSP;
             double* blk = myrec + xg * S4::RGP;
-            expand4(co, shtab + (g * NEN + xa) * 4, blk + xa * S4::RS, ns);
+            expand4(co, shtab + (g * NEN + xa) * 6, blk + xa * S4::RS, ns);
             if (xa == 0)
               *reinterpret_cast<double2*>(blk + NEN * S4::RS) = make_double2(co[C4::MU], co[C4::GHC]);
           }
