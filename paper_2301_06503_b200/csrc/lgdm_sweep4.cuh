@@ -17,17 +17,25 @@
 //     (Exact in exact arithmetic; the rounding difference is ~26 eps x row max.)
 //  2. One C warp per element does the node expansions of its element itself (lane =
 //     node x 4 Gauss points, two rounds) into a warp-private record buffer, then the 28
-//     pair lanes read the records with broadcast 16-byte loads -- no inter-warp hand-off per
-//     Gauss point, only one per batch (the core ring).
-//  3. Node sums (R = F, U, V) accumulate in registers and are reduced with shuffles.
+//     pair lanes read the Kuu fields of the records with 16-byte loads -- no inter-warp
+//     hand-off per Gauss point, only one per batch (the core ring).
+//  3. Coupling blocks by shape-function moments: Kue, Keu and the N E part of Kee of pair
+//     (a, b) are sum_g N_b(g) x_a(g) with N_b(g) a constant (Eqs. 11b-d), so 56 (node,
+//     component) lanes form M[n][m] = sum_g N_m(g) x_n(g) once per element and each pair
+//     lane reads its 14 values; the pair Gauss sums keep only Kuu and sum ghc gA.gB.
+//     Node sums (R = F, U, V) accumulate in registers and are reduced with shuffles.
+//  6. Shared-memory layouts (pair lane order, plane-row chunk positions, plane / column
+//     offsets, moment buffer, shape table) from quarter-warp bank-conflict searches
+//     (tools/bank_search4.py).
 //  4. The Appendix A core (exp, sqrt, divide: a long FP64 dependency chain) runs in two PC
 //     warp pairs on alternate batches, one core slot each, 16-byte core stores/loads.
 //  5. Flush: vectorised row copies, the -sum of plane -1 kept in the (never accumulated)
 //     self slot of plane 0.
 //
 //   PC warps (element x GP)   gpCore -> core slots [2][E][NGP][CSP] (one per PC pair)
-//   C  warps (one per element) expansions -> records [4 GP][8 node]; Gauss sums of the 28
-//                              off-diagonal pairs; adds into the block-row planes; flush
+//   C  warps (one per element) expansions -> records [4 GP][8 node]; Kuu Gauss sums of the
+//                              28 off-diagonal pairs; coupling moments; adds into the
+//                              block-row planes; flush
 #pragma once
 
 #include <type_traits>
@@ -39,7 +47,7 @@ struct S4 {
   static constexpr int NGP = 8, NEN = 8, NDPN = 4, NOFF = 28;
   static constexpr int NPC = 4, NC = E;                          // warps per role
   static constexpr int T = 32 * (NPC + NC);
-  // shape table [NGP][NEN][4] = (dN/dxi, N) at the Gauss points
+  // shape table [NGP][NEN][6] = (dN/dxi, N, pad) at the Gauss points
   static constexpr int SHT = NGP * NEN * 6;   // stride 3 x 16 B per (g, a): conflict-free reads
   // core ring [3][E][NGP][CSP]: core = Core<3> values with a pad after J^-1 so every field
   // group is 16-byte aligned (48 doubles); CSP = 50 (25 x 16 B) puts the 4 cores a C warp
