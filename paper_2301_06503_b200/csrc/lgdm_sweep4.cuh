@@ -380,14 +380,14 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
     }
   };
   // lanes 0..15: entry (i, j) = (lane / 4, lane % 4) of the 4x4 blocks, summed over slots
-  auto plane_sum = [&](const double* P, bool skip_self) {
-    double s = 0.0;
+  auto plane_sum = [&](const double* P, bool skip_self) {   // pairwise: short add chains
     const double* p = P + (lane >> 2) * 36;
     const int j = lane & 3;
+    double v[9];
 #pragma unroll
-    for (int sl = 0; sl < 9; ++sl)
-      if (!(skip_self && sl == 4)) s += p[soff4(sl, j)];
-    return s;
+    for (int sl = 0; sl < 9; ++sl) v[sl] = p[soff4(sl, j)];
+    if (skip_self) v[4] = 0.0;
+    return ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + ((v[6] + v[7]) + v[8]));
   };
   // finish node (x, y, z): diagonal block = -sum(plane -1) [kept in the self slot]
   // - sum(plane 0 off-diagonal) - sum(plane +1) + (U, V); then plane 0, +1 and R go out
