@@ -67,7 +67,7 @@ struct S4 {
   static constexpr size_t SMEM = sizeof(double) * (size_t(SHT) + size_t(NCSLOT) * CSLOT +
                                                    size_t(NC) * RWARP + size_t(NCOLS) * COL);
   // named barriers: core full 1-2, core empty 3-4 (slot = PC pair), C warps 5
-  static constexpr int B_CF = 1, B_CE = 3, B_C = 5;
+  static constexpr int B_CF = 1, B_CE = 3, B_C = 5, B_AD = 6, B_FL = 7;
 };
 
 // shifted Core<3> offsets in the ring (J^-1 at 0..8, pad, then the rest +1)
@@ -238,6 +238,14 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
     shtab[k * 6 + 3] = shapeN<3>(a, g);
   }
   for (int k = tid; k < S4::NCOLS * S4::COL; k += S4::T) acc[k] = 0.0;
+  __shared__ int64_t sbase[3][S4::NCOLS];   // CSR offsets of node layers (by z % 3)
+  for (int q = tid; q < 2 * cols; q += S4::T) {
+    const int cc = q % cols;
+    const int64_t zq = s_first + q / cols;
+    const int cy = cc / cols_x;
+    if (zq >= z0 && zq < z1)
+      sbase[zq % 3][cc] = base[node_id(ix0 + (cc - cy * cols_x), iy0 + cy, zq) - G.own_node_b];
+  }
   __syncthreads();
 
   // batch schedule, identical in every role: layer s, colour c (parity of i, j), batches of
@@ -250,99 +258,17 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
         const int jfst = jlo + ((jlo & 1) != (c >> 1) ? 1 : 0);
         const int nj = jfst < jhi ? (jhi - jfst + 1) / 2 : 0;
         const int nc = ni * nj;
-        for (int b0 = 0; b0 < nc; b0 += E) body(s, c, b0, ifst, ni, jfst, nc);
+        body(s, c, 0, ifst, ni, jfst, nc);   // nc <= E: one batch per colour
       }
       end_of_layer(s);
     }
   };
 
   constexpr int NPC_T = 64, NC_T = 32 * S4::NC;
+  static_assert(((S4::TX + 2) / 2) * ((S4::TY + 2) / 2) <= S4::E, "one batch per colour");
+  constexpr int FL_T = S4::T;   // layer adds done (C -> PC) / PC flush part done (PC -> C)
 
-  if (warp < S4::NPC) {
-    // ---------------------------- PC: Gauss-point cores ----------------------------
-    const int pair = warp >> 1;                       // batches t with t % 2 == pair
-    const int lid = (warp & 1) * 32 + lane;
-    const int el = lid >> 3, g = lid & 7;
-    int t = 0;
-    PT_DECL
-    schedule(
-        [&](int64_t s, int, int b0, int ifst, int ni, int jfst, int nc) {
-          if ((t & 1) == pair) {
-            const int slot = pair;   // each PC pair owns one core slot (fixed producer)
-            PT_MARK(12, tid == 0);
-            if (t >= 2) bsync(S4::B_CE + slot, NPC_T + NC_T);
-            PT_MARK(10, tid == 0);
-            const int k = b0 + el;
-            if (k < nc) {
-              const int i = ifst + 2 * (k % ni), j = jfst + 2 * (k / ni);
-              const int64_t n0 = node_id(i, j, s);
-              auto nid = [&](int a) {
-                int ox, oy, oz;
-                node_off<3>(a, ox, oy, oz);
-                return n0 + ox + nxN * (oy + G.nyN * oz);
-              };
-              auto X = [&](int a, int q) { return __ldg(coords + nid(a) * 3 + q); };
-              auto U = [&](int a, int q) { return __ldg(dofs + nid(a) * 4 + q); };
-              const int64_t e = i + G.nx * (j + G.nyE * s);
-              double core[Core<3>::STRIDE];
-              gpCore<3>(m, X, U, __ldg(kappa + e * NGP + g), g, core);
-              double2* dst = reinterpret_cast<double2*>(cores + slot * S4::CSLOT + el * S4::CEL + g * S4::CSP);
-#pragma unroll
-              for (int k2 = 0; k2 < 4; ++k2) dst[k2] = make_double2(core[2 * k2], core[2 * k2 + 1]);
-              dst[4] = make_double2(core[8], 0.0);
-#pragma unroll
-              for (int k2 = 5; k2 < 23; ++k2) dst[k2] = make_double2(core[2 * k2 - 1], core[2 * k2]);
-              dst[23] = make_double2(core[45], 0.0);
-            }
-            PT_MARK(11, tid == 0);
-            barrive(S4::B_CF + slot, NPC_T + NC_T);
-          }
-          ++t;
-        },
-        [](int64_t) {});
-    // drain: the core-empty arrival of this pair's last batch
-    for (int tt = max(t - 2, 0); tt < t; ++tt)
-      if ((tt & 1) == pair) bsync(S4::B_CE + pair, NPC_T + NC_T);
-    return;
-  }
-
-  // ------------------------- C: one warp per element of the batch -------------------------
-  const int cw = warp - S4::NPC;                     // element slot of this warp
-  const int ct = tid - 32 * S4::NPC;
-  // expansion lane: node xa, Gauss point 4 * round + xg
-  const int xa = lane & 7, xg = lane >> 3;
-  int xox, xoy, xoz;
-  node_off<3>(xa, xox, xoy, xoz);
-  // pair lane
-  const bool plane_lane = lane < S4::NOFF;
-  int pa = 0, pb = 1;
-  if (plane_lane) {
-#pragma unroll
-    for (int k = 0; k < S4::NOFF; ++k)
-      if (lane == k) {
-        pa = pair4(k) / 10;
-        pb = pair4(k) % 10;
-      }
-  }
-  int oax, oay, oaz, obx, oby, obz;
-  node_off<3>(pa, oax, oay, oaz);
-  node_off<3>(pb, obx, oby, obz);
-  const int psAB = plane_slot<3>(obx - oax, oby - oay), psBA = plane_slot<3>(oax - obx, oay - oby);
-  const int dzAB = obz - oaz;
-  int qAB0 = 0, qAB1 = 0, qBA0 = 0, qBA1 = 0;   // pos4 of this lane's two slots
-#pragma unroll
-  for (int k = 0; k < 9; ++k) {
-    if (psAB == k) { qAB0 = pos4(k, 0); qAB1 = pos4(k, 1); }
-    if (psBA == k) { qBA0 = pos4(k, 0); qBA1 = pos4(k, 1); }
-  }
-  double* myrec = recs + cw * S4::RWARP;
   auto col_of = [&](int x, int y) { return acc + ((x - ix0) + cols_x * (y - iy0)) * S4::COL; };
-  auto plane_of = [&](double* colp, int zpar, bool zs, int dz) -> double* {
-    if (dz == 0) return colp + (zpar ? S4::Z1 : S4::Z0);
-    return colp + (zs ? S4::UP : S4::DN);
-  };
-
-  __shared__ int64_t sbase[2][S4::NCOLS];   // CSR offsets of node layers (by parity)
   int lane_csr = 0;   // CSR chunk of smem chunk position `lane` (lanes 0..17) of a plane row:
 #pragma unroll        // contiguous (conflict-free) smem reads, permuted 16-byte global stores
   for (int k = 0; k < 18; ++k)
@@ -353,7 +279,7 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
     const int zlo = z > 0 ? -1 : 0, zhi = z < G.nl ? 1 : 0;
     if (inner) {
       const int W2 = 18 * (zhi - zlo + 1);   // row width in double2
-      double2* out = reinterpret_cast<double2*>(val + sbase[z & 1][(x - ix0) + cols_x * (y - iy0)]) + (dz - zlo) * 18;
+      double2* out = reinterpret_cast<double2*>(val + sbase[z % 3][(x - ix0) + cols_x * (y - iy0)]) + (dz - zlo) * 18;
       const double2* src = reinterpret_cast<const double2*>(P);
 #pragma unroll
       for (int r = 0; r < 4; ++r)
@@ -364,7 +290,7 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
     const int ylo = y > 0 ? -1 : 0, yhi = y < G.nyN - 1 ? 1 : 0;
     const int wx = xhi - xlo + 1, wy = yhi - ylo + 1, wz = zhi - zlo + 1;
     const int W = 4 * wx * wy * wz;
-    double* out = val + sbase[z & 1][(x - ix0) + cols_x * (y - iy0)] + (dz - zlo) * (4 * wx * wy);
+    double* out = val + sbase[z % 3][(x - ix0) + cols_x * (y - iy0)] + (dz - zlo) * (4 * wx * wy);
     for (int it = lane; it < 36; it += 32) {
       const int i = it / 9, sl = it - 9 * i;
       const int dy = sl / 3 - 1, dx = sl - 3 * (dy + 1) - 1;
@@ -408,6 +334,131 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
     if (lane < 4) __stcs(Rv + (node_id(x, y, z) - G.own_node_b) * 4 + lane, ns[lane]);
   };
 
+  // flush of element layer s for one node column cc: plane -1 of node layer s+1 out (its minus
+  // row sums parked in the self slot of that node's plane 0), node layer s finished (and s+1
+  // if s is the chunk's last layer), planes and node sums reset
+  auto flush_col = [&](int64_t s, int cc) {
+    const bool own_s = s >= z0 && s < z1, own_s1 = s + 1 >= z0 && s + 1 < z1;
+    const bool top = s == s_last && own_s1;   // node layer s+1 has no element layer above
+    const int cy = cc / cols_x;
+    const int x = ix0 + (cc - cy * cols_x), y = iy0 + cy;
+    const bool inner = x > 0 && x < G.nx && y > 0 && y < G.nyN - 1;
+    double* colp = col_of(x, y);
+    if (own_s1) {
+      if (lane < 16)
+        colp[(((s + 1) & 1) ? S4::Z1 : S4::Z0) + (lane >> 2) * 36 + soff4(4, lane & 3)] =
+            -plane_sum(colp + S4::DN, false);
+      write_plane(x, y, s + 1, -1, colp + S4::DN, inner);
+    }
+    __syncwarp();
+    if (own_s) finish_node(x, y, s, colp, s < G.nl, inner);
+    if (top) finish_node(x, y, s + 1, colp, false, inner);
+    __syncwarp();
+    double2* z2 = reinterpret_cast<double2*>(colp + ((s & 1) ? S4::Z1 : S4::Z0));
+    double2* ud = reinterpret_cast<double2*>(colp + S4::UP);
+    double2* dn2 = reinterpret_cast<double2*>(colp + S4::DN);
+    const double2 zero = make_double2(0.0, 0.0);
+    for (int k2 = lane; k2 < S4::PLD / 2; k2 += 32) z2[k2] = zero;
+    for (int k2 = lane; k2 < S4::PLD / 2; k2 += 32) ud[k2] = zero;
+    for (int k2 = lane; k2 < S4::PLD / 2; k2 += 32) dn2[k2] = zero;
+    if (lane < 4) reinterpret_cast<double2*>(colp + S4::NS + (s & 1) * 8)[lane] = zero;
+  };
+  // the layer flush is split: the C warps take columns 0 .. NC-1 right after the layer's adds,
+  // the PC warps (idle ~70 %) the rest while the C warps compute the next layer's first batch
+  constexpr int NCC = S4::NC;
+
+  if (warp < S4::NPC) {
+    // ---------------------------- PC: Gauss-point cores ----------------------------
+    const int pair = warp >> 1;                       // batches t with t % 2 == pair
+    const int lid = (warp & 1) * 32 + lane;
+    const int el = lid >> 3, g = lid & 7;
+    int t = 0;
+    PT_DECL
+    schedule(
+        [&](int64_t s, int c, int b0, int ifst, int ni, int jfst, int nc) {
+          if ((t & 1) == pair) {
+            const int slot = pair;   // each PC pair owns one core slot (fixed producer)
+            PT_MARK(12, tid == 0);
+            if (t >= 2) bsync(S4::B_CE + slot, NPC_T + NC_T);
+            PT_MARK(10, tid == 0);
+            const int k = b0 + el;
+            if (k < nc) {
+              const int i = ifst + 2 * (k % ni), j = jfst + 2 * (k / ni);
+              const int64_t n0 = node_id(i, j, s);
+              auto nid = [&](int a) {
+                int ox, oy, oz;
+                node_off<3>(a, ox, oy, oz);
+                return n0 + ox + nxN * (oy + G.nyN * oz);
+              };
+              auto X = [&](int a, int q) { return __ldg(coords + nid(a) * 3 + q); };
+              auto U = [&](int a, int q) { return __ldg(dofs + nid(a) * 4 + q); };
+              const int64_t e = i + G.nx * (j + G.nyE * s);
+              double core[Core<3>::STRIDE];
+              gpCore<3>(m, X, U, __ldg(kappa + e * NGP + g), g, core);
+              double2* dst = reinterpret_cast<double2*>(cores + slot * S4::CSLOT + el * S4::CEL + g * S4::CSP);
+#pragma unroll
+              for (int k2 = 0; k2 < 4; ++k2) dst[k2] = make_double2(core[2 * k2], core[2 * k2 + 1]);
+              dst[4] = make_double2(core[8], 0.0);
+#pragma unroll
+              for (int k2 = 5; k2 < 23; ++k2) dst[k2] = make_double2(core[2 * k2 - 1], core[2 * k2]);
+              dst[23] = make_double2(core[45], 0.0);
+            }
+            PT_MARK(11, tid == 0);
+            barrive(S4::B_CF + slot, NPC_T + NC_T);
+            if (c == pair && s > s_first) {   // PC part of the flush of layer s - 1
+              bsync(S4::B_AD, FL_T);
+              PT_MARK(15, tid == 0);
+              for (int cc = NCC + warp; cc < cols; cc += S4::NPC) flush_col(s - 1, cc);
+              barrive(S4::B_FL, FL_T);
+              PT_MARK(14, tid == 0);
+            }
+          }
+          ++t;
+        },
+        [](int64_t) {});
+    bsync(S4::B_AD, FL_T);   // the last layer
+    for (int cc = NCC + warp; cc < cols; cc += S4::NPC) flush_col(s_last, cc);
+    // drain: the core-empty arrival of this pair's last batch
+    for (int tt = max(t - 2, 0); tt < t; ++tt)
+      if ((tt & 1) == pair) bsync(S4::B_CE + pair, NPC_T + NC_T);
+    return;
+  }
+
+  // ------------------------- C: one warp per element of the batch -------------------------
+  const int cw = warp - S4::NPC;                     // element slot of this warp
+  const int ct = tid - 32 * S4::NPC;
+  // expansion lane: node xa, Gauss point 4 * round + xg
+  const int xa = lane & 7, xg = lane >> 3;
+  int xox, xoy, xoz;
+  node_off<3>(xa, xox, xoy, xoz);
+  // pair lane
+  const bool plane_lane = lane < S4::NOFF;
+  int pa = 0, pb = 1;
+  if (plane_lane) {
+#pragma unroll
+    for (int k = 0; k < S4::NOFF; ++k)
+      if (lane == k) {
+        pa = pair4(k) / 10;
+        pb = pair4(k) % 10;
+      }
+  }
+  int oax, oay, oaz, obx, oby, obz;
+  node_off<3>(pa, oax, oay, oaz);
+  node_off<3>(pb, obx, oby, obz);
+  const int psAB = plane_slot<3>(obx - oax, oby - oay), psBA = plane_slot<3>(oax - obx, oay - oby);
+  const int dzAB = obz - oaz;
+  int qAB0 = 0, qAB1 = 0, qBA0 = 0, qBA1 = 0;   // pos4 of this lane's two slots
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+    if (psAB == k) { qAB0 = pos4(k, 0); qAB1 = pos4(k, 1); }
+    if (psBA == k) { qBA0 = pos4(k, 0); qBA1 = pos4(k, 1); }
+  }
+  double* myrec = recs + cw * S4::RWARP;
+  auto plane_of = [&](double* colp, int zpar, bool zs, int dz) -> double* {
+    if (dz == 0) return colp + (zpar ? S4::Z1 : S4::Z0);
+    return colp + (zs ? S4::UP : S4::DN);
+  };
+
   int prev_c = -1, t = 0;
   const bool ptc = ct == 0;
   PT_DECL
@@ -417,15 +468,14 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
         const bool live = k < nc;   // warp-uniform
         const int cslot = t & 1;
         ++t;
-        if (prev_c < 0) {
-          // first batch of element layer s: fetch the CSR offsets of the block-rows of node
-          // layers s and s+1 for this layer's flush (the loads overlap the batch)
-          for (int q = ct; q < 2 * cols; q += NC_T) {
-            const int cc = q % cols;
-            const int64_t zq = s + q / cols;
+        const bool wait_flush = prev_c < 0 && s > s_first;   // PC part of flush(s - 1)
+        if (prev_c < 0 && s > s_first) {
+          // first batch of element layer s: CSR offsets of node layer s+1 (for flush(s); slot
+          // (s+1) % 3 was last read by flush(s-2), finished before the adds of layer s-1)
+          for (int cc = ct; cc < cols; cc += NC_T) {
             const int cy = cc / cols_x;
-            if (zq >= z0 && zq < z1)
-              sbase[zq & 1][cc] = base[node_id(ix0 + (cc - cy * cols_x), iy0 + cy, zq) - G.own_node_b];
+            if (s + 1 >= z0 && s + 1 < z1)
+              sbase[(s + 1) % 3][cc] = base[node_id(ix0 + (cc - cy * cols_x), iy0 + cy, s + 1) - G.own_node_b];
           }
         }
         PT_MARK(9, ptc);
@@ -433,6 +483,7 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
         PT_MARK(0, ptc);
         if (!live) {
           barrive(S4::B_CE + cslot, NPC_T + NC_T);
+          if (wait_flush) bsync(S4::B_FL, FL_T);
           if (c != prev_c) bsync(S4::B_C, NC_T);
           prev_c = c;
           return;
@@ -562,6 +613,7 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
         }
         PT_MARK(3, ptc);
         // batches of one colour share no node; a new colour waits for the previous adds
+        if (wait_flush) bsync(S4::B_FL, FL_T);
         if (c != prev_c) bsync(S4::B_C, NC_T);
         prev_c = c;
         PT_MARK(4, ptc);
@@ -633,38 +685,11 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
       },
       [&](int64_t s) {
         PT_MARK(5, ptc);
-        bsync(S4::B_C, NC_T);   // all adds of layer s are in
+        bsync(S4::B_C, NC_T);      // all adds of layer s are in
+        barrive(S4::B_AD, FL_T);   // the PC warps may flush their columns
         PT_MARK(6, ptc);
         prev_c = -1;
-        const bool own_s = s >= z0 && s < z1, own_s1 = s + 1 >= z0 && s + 1 < z1;
-        const bool top = s == s_last && own_s1;   // node layer s+1 has no element layer above
-        for (int cc = cw; cc < cols; cc += S4::NC) {
-          const int cy = cc / cols_x;
-          const int x = ix0 + (cc - cy * cols_x), y = iy0 + cy;
-          const bool inner = x > 0 && x < G.nx && y > 0 && y < G.nyN - 1;
-          double* colp = col_of(x, y);
-          if (own_s1) {
-            // plane -1 of node layer s+1 is complete: out, and minus its row sums go to the
-            // self slot of that node's plane 0 (never accumulated by pair adds)
-            if (lane < 16)
-              colp[(((s + 1) & 1) ? S4::Z1 : S4::Z0) + (lane >> 2) * 36 + soff4(4, lane & 3)] =
-                  -plane_sum(colp + S4::DN, false);
-            write_plane(x, y, s + 1, -1, colp + S4::DN, inner);
-          }
-          __syncwarp();
-          if (own_s) finish_node(x, y, s, colp, s < G.nl, inner);
-          if (top) finish_node(x, y, s + 1, colp, false, inner);
-          __syncwarp();
-          // reset plane 0 and node sums of node layer s (reused for layer s+2), UP, DN
-          double2* z2 = reinterpret_cast<double2*>(colp + ((s & 1) ? S4::Z1 : S4::Z0));
-          double2* ud = reinterpret_cast<double2*>(colp + S4::UP);
-          const double2 zero = make_double2(0.0, 0.0);
-          for (int k2 = lane; k2 < S4::PLD / 2; k2 += 32) z2[k2] = zero;
-          for (int k2 = lane; k2 < S4::PLD / 2; k2 += 32) ud[k2] = zero;
-          double2* dn2 = reinterpret_cast<double2*>(colp + S4::DN);
-          for (int k2 = lane; k2 < S4::PLD / 2; k2 += 32) dn2[k2] = zero;
-          if (lane < 4) reinterpret_cast<double2*>(colp + S4::NS + (s & 1) * 8)[lane] = zero;
-        }
+        if (cw < NCC && cw < cols) flush_col(s, cw);
         PT_MARK(7, ptc);
         bsync(S4::B_C, NC_T);
         PT_MARK(8, ptc);
