@@ -689,7 +689,7 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
         barrive(S4::B_AD, FL_T);   // the PC warps may flush their columns
         PT_MARK(6, ptc);
         prev_c = -1;
-        if (cw < NCC && cw < cols) flush_col(s, cw);
+        for (int cc = cw; cc < NCC && cc < cols; cc += S4::NC) flush_col(s, cc);
         PT_MARK(7, ptc);
         bsync(S4::B_C, NC_T);
         PT_MARK(8, ptc);
