@@ -72,6 +72,11 @@ def lib():
         L.oracle_pattern.argtypes = [C.c_int, C.c_int64, C.c_int64, i64p, i64p, i32p]
         L.oracle_assemble.argtypes = [C.c_int, mp, C.c_int64, dp, C.c_int64, i64p, dp, dp,
                                       i64p, i32p, dp, dp, dp, i64p]
+        L.oracle_assemble_d.argtypes = [C.c_int, mp, C.c_int64, dp, C.c_int64, i64p, dp, dp,
+                                        dp, dp, i64p, i32p, dp, dp, dp, i64p]
+        L.oracle_sdv_width.argtypes = [C.c_int]
+        L.oracle_update_state.argtypes = [C.c_int, mp, C.c_int64, dp, C.c_int64, i64p, dp, dp,
+                                          dp, dp, dp]
         L.oracle_rows_nnz.argtypes = [C.c_int, C.c_int64, C.c_int64, i64p, C.c_int64, i64p]
         L.oracle_rows_nnz.restype = C.c_int64
         L.oracle_assemble_rows.argtypes = [C.c_int, mp, C.c_int64, dp, C.c_int64, i64p, dp, dp,
@@ -170,8 +175,20 @@ def pattern(etype: int, n_nodes: int, conn):
     return rp, ci
 
 
-def assemble(etype: int, m: Material, coords, conn, dofs, kappa, row_ptr=None, col_idx=None):
-    """Alg. 1 assembly.  Returns dict(row_ptr, col_idx, val, R, S, n_guard)."""
+def _opt(a, n):
+    """optional per-GP array -> (keep-alive array or None, pointer or None)"""
+    if a is None:
+        return None, None
+    a = np.ascontiguousarray(a, dtype=np.float64).reshape(-1)
+    if a.size != n:
+        raise ValueError(f"per-GP array of {a.size} values, expected {n}")
+    return a, _d(a)
+
+
+def assemble(etype: int, m: Material, coords, conn, dofs, kappa, row_ptr=None, col_idx=None,
+             kappa0_gp=None, alpha_gp=None):
+    """Alg. 1 assembly.  Returns dict(row_ptr, col_idx, val, R, S, n_guard).
+    kappa0_gp / alpha_gp: optional per-GP damage threshold and alpha (defect regions)."""
     dim, nen, ndpn, nv, ngp, nd = FAMILY[etype]
     coords = np.ascontiguousarray(coords, dtype=np.float64)
     conn = np.ascontiguousarray(conn, dtype=np.int64)
@@ -185,9 +202,11 @@ def assemble(etype: int, m: Material, coords, conn, dofs, kappa, row_ptr=None, c
     R = np.zeros(nn * ndpn)
     S = np.zeros(nn * ndpn)
     ng = C.c_int64()
-    rc = lib().oracle_assemble(etype, C.byref(m), nn, _d(coords), ne, _i64(conn), _d(dofs),
-                               _d(kappa), _i64(row_ptr), _i32(col_idx), _d(val), _d(R), _d(S),
-                               C.byref(ng))
+    k0a, k0p = _opt(kappa0_gp, ne * ngp)
+    ala, alp = _opt(alpha_gp, ne * ngp)
+    rc = lib().oracle_assemble_d(etype, C.byref(m), nn, _d(coords), ne, _i64(conn), _d(dofs),
+                                 _d(kappa), k0p, alp, _i64(row_ptr), _i32(col_idx), _d(val),
+                                 _d(R), _d(S), C.byref(ng))
     if rc != 0:
         raise ValueError(f"oracle_assemble failed rc={rc}")
     return dict(row_ptr=row_ptr, col_idx=col_idx, val=val, R=R, S=S, n_guard=ng.value)
@@ -231,3 +250,29 @@ def residual_norms(etype: int, R):
     out = np.zeros(2)
     lib().oracle_residual_norms(etype, R.size, _d(R), _d(out))
     return out
+
+
+def sdv_width(etype: int) -> int:
+    """doubles per (element, GP) state record: 3 nv + 5"""
+    return lib().oracle_sdv_width(etype)
+
+
+def update_state(etype: int, m: Material, coords, conn, dofs, kappa, kappa0_gp=None,
+                 alpha_gp=None):
+    """State-variable update (Alg. 2 l.8-14, Fig. 9a).  Returns (sdv [ne, ngp, W], kappa_new);
+    record = [eps_v (nv), d eeq/d eps_v (nv), sigma (nv), eeq, ebar, kappa, D, g]."""
+    dim, nen, ndpn, nv, ngp, nd = FAMILY[etype]
+    coords = np.ascontiguousarray(coords, dtype=np.float64)
+    conn = np.ascontiguousarray(conn, dtype=np.int64)
+    dofs = np.ascontiguousarray(dofs, dtype=np.float64)
+    k = np.array(kappa, dtype=np.float64, copy=True).reshape(-1)
+    ne = conn.shape[0]
+    W = sdv_width(etype)
+    sdv = np.zeros(ne * ngp * W)
+    k0a, k0p = _opt(kappa0_gp, ne * ngp)
+    ala, alp = _opt(alpha_gp, ne * ngp)
+    rc = lib().oracle_update_state(etype, C.byref(m), coords.shape[0], _d(coords), ne, _i64(conn),
+                                   _d(dofs), _d(k), k0p, alp, _d(sdv))
+    if rc != 0:
+        raise ValueError(f"oracle_update_state failed rc={rc}")
+    return sdv.reshape(ne, ngp, W), k

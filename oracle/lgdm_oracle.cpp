@@ -225,6 +225,16 @@ void oracle_shape(int type, const double* xi, double* N, double* dNdxi) {
 int oracle_element(int type, const oracle_material* m, const double* Xe, const double* Ue,
                    const double* kap, double* Ke, double* Fe, double* Fabs, double* sig,
                    int32_t* guard) {
+  return oracle_element_d(type, m, Xe, Ue, kap, nullptr, nullptr, Ke, Fe, Fabs, sig, guard);
+}
+
+// Same, with per-GP damage threshold kappa0 and alpha (defect regions; the code's
+// per-GP `ki` and `alpha_var`, Fig. 9a l.3-4 / P:380-389).  NULL = the material's value.
+int oracle_element_d(int type, const oracle_material* m0, const double* Xe, const double* Ue,
+                     const double* kap, const double* k0g, const double* alg, double* Ke,
+                     double* Fe, double* Fabs, double* sig, int32_t* guard) {
+  oracle_material mg = *m0;   // per-GP damage parameters (defect fields) set in the GP loop
+  const oracle_material* m = &mg;
   Fam f;
   if (!family(type, &f)) return -1000;
   const int dim = f.dim, nen = f.nen, ndpn = f.ndpn, nv = f.nv, nd = f.ndofe;
@@ -309,6 +319,8 @@ int oracle_element(int type, const oracle_material* m, const double* Xe, const d
     }
 
     // ---- constitutive (Appendix A; Fig. 8b condition vectors) ----
+    mg.kappa0 = k0g ? k0g[g] : m0->kappa0;
+    mg.alpha = alg ? alg[g] : m0->alpha;
     double eeq, dv[6], H[36];
     oracle_eqstrain(m, dim, ev, &eeq, dv, H);
     const double kh = kap[g];
@@ -451,6 +463,15 @@ int oracle_assemble(int type, const oracle_material* m, int64_t n_nodes, const d
                     int64_t n_elems, const int64_t* conn, const double* dofs, const double* kappa,
                     const int64_t* row_ptr, const int32_t* col_idx, double* val, double* R,
                     double* S, int64_t* n_guard) {
+  return oracle_assemble_d(type, m, n_nodes, coords, n_elems, conn, dofs, kappa, nullptr, nullptr,
+                           row_ptr, col_idx, val, R, S, n_guard);
+}
+
+int oracle_assemble_d(int type, const oracle_material* m, int64_t n_nodes, const double* coords,
+                      int64_t n_elems, const int64_t* conn, const double* dofs,
+                      const double* kappa, const double* kappa0_gp, const double* alpha_gp,
+                      const int64_t* row_ptr, const int32_t* col_idx, double* val, double* R,
+                      double* S, int64_t* n_guard) {
   Fam f;
   if (!family(type, &f)) return -1;
   const int nd = f.ndofe;
@@ -464,8 +485,10 @@ int oracle_assemble(int type, const oracle_material* m, int64_t n_nodes, const d
   int64_t ng = 0;
   for (int64_t e = 0; e < n_elems; ++e) {
     gather(f, e, conn, coords, dofs, Xe, Ue);
-    const int rc = oracle_element(type, m, Xe, Ue, kappa + e * f.ngp, Ke.data(), Fe.data(),
-                                  Fa.data(), nullptr, guard);
+    const int rc = oracle_element_d(type, m, Xe, Ue, kappa + e * f.ngp,
+                                    kappa0_gp ? kappa0_gp + e * f.ngp : nullptr,
+                                    alpha_gp ? alpha_gp + e * f.ngp : nullptr, Ke.data(),
+                                    Fe.data(), Fa.data(), nullptr, guard);
     if (rc != 0) return -2;  // det J <= 0
     for (int g = 0; g < f.ngp; ++g) ng += guard[g];
     for (int a = 0; a < f.nen; ++a)
@@ -592,6 +615,120 @@ int oracle_update_history(int type, int64_t n_nodes, int64_t n_elems, const int6
       double& k = kappa[e * f.ngp + g];
       if ((ebar - k) > kTolHist) k = ebar;
     }
+  return 0;
+}
+
+// J^-1 by cofactors (as in oracle_element); false if det J <= 0.
+static bool invert(int dim, const double (&J)[3][3], double (&Ji)[3][3]) {
+  double detJ;
+  if (dim == 1) {
+    detJ = J[0][0];
+    Ji[0][0] = 1.0 / detJ;
+  } else if (dim == 2) {
+    detJ = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+    Ji[0][0] = J[1][1] / detJ;
+    Ji[0][1] = -J[0][1] / detJ;
+    Ji[1][0] = -J[1][0] / detJ;
+    Ji[1][1] = J[0][0] / detJ;
+  } else {
+    detJ = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) -
+           J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+           J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+    Ji[0][0] = (J[1][1] * J[2][2] - J[1][2] * J[2][1]) / detJ;
+    Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) / detJ;
+    Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) / detJ;
+    Ji[1][0] = (J[1][2] * J[2][0] - J[1][0] * J[2][2]) / detJ;
+    Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) / detJ;
+    Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) / detJ;
+    Ji[2][0] = (J[1][0] * J[2][1] - J[1][1] * J[2][0]) / detJ;
+    Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) / detJ;
+    Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) / detJ;
+  }
+  return detJ > 0.0;
+}
+
+// State-variable update (Alg. 2 l.8-14, Fig. 9a `update_variables`),
+// one record of oracle_sdv_width(type) doubles per (element, GP):
+//   [strain eps_v (nv, Voigt, engineering shear; Fig. 9a l.7 `B_mat_u*udof`)]
+//   [d eeq / d eps_v (nv; Alg. 2 l.11, Eq. A.3)]
+//   [sigma (nv; Eq. 2 with the reading-R-11a term h_sigma (eeq - ebar) d)]
+//   [eeq (Eq. A.3, Fig. 9a l.11-16), ebar (Fig. 9a l.19), kappa (history, l.22-24),
+//    D (Eq. A.1, l.27-31), g (Eq. A.4, Alg. 2 l.12)]
+// and commits the history kappa <- kappa (as oracle_update_history).  kappa0_gp / alpha_gp:
+// per-GP damage threshold and alpha (defect regions), NULL = material value.
+int oracle_sdv_width(int type) {
+  Fam f;
+  if (!family(type, &f)) return -1;
+  return 3 * f.nv + 5;
+}
+
+int oracle_update_state(int type, const oracle_material* m, int64_t n_nodes, const double* coords,
+                        int64_t n_elems, const int64_t* conn, const double* dofs, double* kappa,
+                        const double* kappa0_gp, const double* alpha_gp, double* sdv) {
+  Fam f;
+  if (!family(type, &f)) return -1;
+  (void)n_nodes;
+  const int dim = f.dim, nen = f.nen, ndpn = f.ndpn, nv = f.nv;
+  const int W = 3 * nv + 5;
+  double xi[24], w[8], C[36];
+  oracle_gauss(type, xi, w);
+  elasticity(m, dim, C);
+  double Xe[24], Ue[32];
+  for (int64_t e = 0; e < n_elems; ++e) {
+    gather(f, e, conn, coords, dofs, Xe, Ue);
+    for (int g = 0; g < f.ngp; ++g) {
+      double N[8], dNdxi[24];
+      oracle_shape(type, xi + g * dim, N, dNdxi);
+      // J_ij = sum_a X_ai dN_a/dxi_j; grad_x N = J^-T grad_xi N (as oracle_element)
+      double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}}, Ji[3][3];
+      for (int a = 0; a < nen; ++a)
+        for (int i = 0; i < dim; ++i)
+          for (int j = 0; j < dim; ++j) J[i][j] += Xe[a * dim + i] * dNdxi[a * dim + j];
+      if (!invert(dim, J, Ji)) return -2;
+      double gradN[8][3];
+      for (int a = 0; a < nen; ++a)
+        for (int i = 0; i < dim; ++i) {
+          double s = 0.0;
+          for (int j = 0; j < dim; ++j) s += Ji[j][i] * dNdxi[a * dim + j];
+          gradN[a][i] = s;
+        }
+      // strain (Voigt, engineering shear) and ebar at the GP
+      double ev[6] = {0, 0, 0, 0, 0, 0}, ebar = 0.0;
+      for (int a = 0; a < nen; ++a) {
+        for (int V = 0; V < nv; ++V) {
+          int p, q;
+          voigt_pair(dim, V, &p, &q);
+          if (p == q) ev[V] += gradN[a][p] * Ue[a * ndpn + p];
+          else ev[V] += gradN[a][q] * Ue[a * ndpn + p] + gradN[a][p] * Ue[a * ndpn + q];
+        }
+        ebar += N[a] * Ue[a * ndpn + dim];
+      }
+      oracle_material mg = *m;
+      if (kappa0_gp) mg.kappa0 = kappa0_gp[e * f.ngp + g];
+      if (alpha_gp) mg.alpha = alpha_gp[e * f.ngp + g];
+      double eeq, dv[6], H[36];
+      oracle_eqstrain(&mg, dim, ev, &eeq, dv, H);
+      double& kh = kappa[e * f.ngp + g];
+      const double kap = (ebar - kh) > kTolHist ? ebar : kh;   // Fig. 9a l.22-24
+      double D, dD, gI, dg;
+      oracle_damage(&mg, kap, &D, &dD);
+      oracle_interaction(&mg, D, &gI, &dg);
+      double* out = sdv + (e * f.ngp + g) * W;
+      for (int V = 0; V < nv; ++V) {
+        double ce = 0.0;
+        for (int U = 0; U < nv; ++U) ce += C[V * nv + U] * ev[U];
+        out[V] = ev[V];
+        out[nv + V] = dv[V];
+        out[2 * nv + V] = (1.0 - D) * ce + m->h_sigma * (eeq - ebar) * dv[V];   // Eq. 2
+      }
+      out[3 * nv + 0] = eeq;
+      out[3 * nv + 1] = ebar;
+      out[3 * nv + 2] = kap;
+      out[3 * nv + 3] = D;
+      out[3 * nv + 4] = gI;
+      kh = kap;
+    }
+  }
   return 0;
 }
 

@@ -54,6 +54,11 @@ void oracle_shape(int type, const double* xi, double* N /*[nen]*/, double* dNdxi
 int oracle_element(int type, const oracle_material* m, const double* Xe, const double* Ue,
                    const double* kap, double* Ke, double* Fe, double* Fabs,
                    double* sig, int32_t* guard);
+/* Same with per-GP damage threshold k0g [ngp] and alpha alg [ngp] (defect regions);
+ * NULL = the material's kappa0 / alpha. */
+int oracle_element_d(int type, const oracle_material* m, const double* Xe, const double* Ue,
+                     const double* kap, const double* k0g, const double* alg, double* Ke,
+                     double* Fe, double* Fabs, double* sig, int32_t* guard);
 
 /* ---- pattern (reading R-PAT) ---- */
 int64_t oracle_pattern_nnz(int type, int64_t n_nodes, int64_t n_elems, const int64_t* conn);
@@ -65,6 +70,13 @@ int oracle_assemble(int type, const oracle_material* m, int64_t n_nodes, const d
                     int64_t n_elems, const int64_t* conn, const double* dofs, const double* kappa,
                     const int64_t* row_ptr, const int32_t* col_idx,
                     double* val, double* R, double* S, int64_t* n_guard);
+
+/* With per-GP defect fields kappa0_gp, alpha_gp [n_elems*ngp] (NULL = material). */
+int oracle_assemble_d(int type, const oracle_material* m, int64_t n_nodes, const double* coords,
+                      int64_t n_elems, const int64_t* conn, const double* dofs,
+                      const double* kappa, const double* kappa0_gp, const double* alpha_gp,
+                      const int64_t* row_ptr, const int32_t* col_idx,
+                      double* val, double* R, double* S, int64_t* n_guard);
 
 /* Sampled rows: the block-rows of the n_sel listed nodes only, each computed from the
  * elements adjacent to that node (ascending element id).  Output per selected node s is
@@ -81,6 +93,14 @@ int oracle_assemble_rows(int type, const oracle_material* m, int64_t n_nodes, co
 int oracle_update_history(int type, int64_t n_nodes, int64_t n_elems, const int64_t* conn,
                           const double* dofs, double* kappa);
 void oracle_residual_norms(int type, int64_t n_rows, const double* R, double* out2);
+
+/* ---- state-variable update (Alg. 2 l.8-14, Fig. 9a) ----
+ * sdv [n_elems*ngp*oracle_sdv_width(type)]: per GP [eps_v (nv), d eeq/d eps_v (nv),
+ * sigma (nv), eeq, ebar, kappa, D, g]; commits kappa.  kappa0_gp / alpha_gp nullable. */
+int oracle_sdv_width(int type);
+int oracle_update_state(int type, const oracle_material* m, int64_t n_nodes, const double* coords,
+                        int64_t n_elems, const int64_t* conn, const double* dofs, double* kappa,
+                        const double* kappa0_gp, const double* alpha_gp, double* sdv);
 
 #ifdef __cplusplus
 }

@@ -313,6 +313,38 @@ def test_tangent_finite_difference(etype, n, hs):
         assert np.linalg.norm(Kv - fd) <= 1e-6 * np.linalg.norm(Kv)
 
 
+@pytest.mark.parametrize("etype,n", [(2, (3, 3)), (3, (2, 2, 1))])
+def test_tangent_finite_difference_defects(etype, n):
+    """per-GP kappa0 / alpha (defect regions): K = -dR/dx still holds,
+    with GPs both below (damaging) and above (undamaged) their own threshold"""
+    dim, nen, ndpn, nv, ngp, nd = oracle.FAMILY[etype]
+    cfg, mesh, X = small_mesh(etype, n, distort=0.15)
+    rng = np.random.default_rng(29 + etype)
+    dofs, kap = _state_away_from_switches(etype, cfg, mesh, rng)
+    k0 = kap * np.where(rng.uniform(size=kap.shape) < 0.7, rng.uniform(0.4, 0.8, kap.shape), 1.6)
+    al = rng.uniform(0.5, 0.99, kap.shape)
+    m = mat()
+    res = oracle.assemble(etype, m, X, mesh.conn, dofs, kap, kappa0_gp=k0, alpha_gp=al)
+    K = dense(res, dofs.size)
+    plain = oracle.assemble(etype, m, X, mesh.conn, dofs, kap)
+    assert not np.allclose(res["val"], plain["val"])          # the fields do change K
+    scale = np.abs(dofs).reshape(-1, ndpn).max(axis=0)
+    for _ in range(10):
+        v = (rng.normal(size=dofs.shape) * scale).ravel()
+        d = 1e-4
+        Rp = oracle.assemble(etype, m, X, mesh.conn, dofs + d * v.reshape(dofs.shape), kap,
+                             kappa0_gp=k0, alpha_gp=al)["R"]
+        Rm = oracle.assemble(etype, m, X, mesh.conn, dofs - d * v.reshape(dofs.shape), kap,
+                             kappa0_gp=k0, alpha_gp=al)["R"]
+        Kv = K @ v
+        fd = -(Rp - Rm) / (2 * d)
+        assert np.linalg.norm(Kv - fd) <= 1e-6 * np.linalg.norm(Kv)
+    uni = oracle.assemble(etype, m, X, mesh.conn, dofs, kap,
+                          kappa0_gp=np.full(kap.size, MAT["kappa0"]),
+                          alpha_gp=np.full(kap.size, MAT["alpha"]))
+    assert np.array_equal(uni["val"], plain["val"]) and np.array_equal(uni["R"], plain["R"])
+
+
 def test_tangent_fd_detects_printed_11f_sign():
     """The printed sign of Eq. 11f's gradient term is not consistent with 11d: with it,
     the FD test fails (reading R-11f).  We emulate it by flipping c in Fe only via c -> -c ...
