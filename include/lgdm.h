@@ -122,6 +122,35 @@ lgdm_status lgdm_assemble(lgdm_mesh mesh, lgdm_csr* K, double** R);
  * every local GP (owned and ghost), Eq. A.2 with Fig. 8b lines 22-24. */
 lgdm_status lgdm_update_history(lgdm_mesh mesh);
 
+/* ---- state-variable update and defect fields ----
+ *
+ * Doubles per (element, GP) record of lgdm_update_state: 3 nv + 5 with nv = 1 / 3 / 6 Voigt
+ * components (bar / Q4 / Hex8): 8 / 14 / 23; -1 for an unknown type. */
+int lgdm_sdv_width(lgdm_elem_type type);
+
+/* Per-GP damage threshold kappa0 and damage parameter alpha of Eq. A.1 (defect regions,
+ * PAPER.md P:418; the code's per-GP `ki` and `alpha_var`, Fig. 9a l.3-4 / P:380-389), each an
+ * array [n_elems][ngp] (n = n_elems * ngp) or NULL = the material's value (NULL clears a
+ * previously set field).  src_on_device: 1 device pointers (async D2D copy on the mesh stream),
+ * 0 host (copied before return).  Values are not validated (kappa0 > 0, 0 <= alpha <= 1 are
+ * the caller's responsibility).  With a field set, lgdm_assemble uses the general kernel
+ * (kernel 0 or 1; an explicit sweep kernel 2-5 returns LGDM_ERR_INVALID_ARGUMENT) and
+ * lgdm_update_state uses the field.  n mismatch -> LGDM_ERR_INVALID_STATE. */
+lgdm_status lgdm_set_defects(lgdm_mesh mesh, const double* kappa0_gp, const double* alpha_gp,
+                             int64_t n, int src_on_device);
+
+/* State-variable update of Alg. 2 lines 8-14 (Fig. 9a update_variables,
+ * P:359-390) for the current state: per (element, GP), in element-major order, the record
+ *   [eps_v (nv, Voigt, engineering shear: bar [e]; Q4 [xx, yy, xy]; Hex8 [xx, yy, zz, xy, yz, xz]),
+ *    d eeq / d eps_v (nv, Eq. A.3 with reading R-A3 / R-SQ),
+ *    sigma (nv, Eq. 2 with the h_sigma (eeq - ebar) d term of reading R-11a),
+ *    eeq (Eq. A.3), ebar (Fig. 9a l.19), kappa (history, l.22-24), D (Eq. A.1), g (Eq. A.4)]
+ * and commits the history kappa_hist <- kappa (as lgdm_update_history).  sdv: n_sdv =
+ * n_elems * ngp * lgdm_sdv_width doubles, device (dst_on_device = 1, async on the mesh stream)
+ * or host (synchronises the stream), or NULL to commit the history only.
+ * Before set_state -> LGDM_ERR_INVALID_STATE; n_sdv mismatch -> LGDM_ERR_INVALID_STATE. */
+lgdm_status lgdm_update_state(lgdm_mesh mesh, double* sdv, int64_t n_sdv, int dst_on_device);
+
 /* Sums of squares of the last assembled R over owned rows: out2 = {sum Fu^2, sum Fe^2}.
  * out2 is a device pointer (2 doubles) when on_device = 1 (stream-ordered, no sync; for a
  * caller-side allreduce), else a host pointer (synchronises). */

@@ -102,6 +102,8 @@ struct lgdm_mesh_s {
   int32_t* conn = nullptr;
   double* dofs = nullptr;
   double* kappa = nullptr;
+  double* k0g = nullptr;        // per-GP kappa0 / alpha (defect fields), NULL = material value
+  double* alg = nullptr;
   int64_t* row_ptr = nullptr;
   int32_t* col_idx = nullptr;
   double* val = nullptr;
@@ -115,6 +117,7 @@ struct lgdm_mesh_s {
   double* sumsq_part = nullptr; // [kSumBlocks*2]
   double* sumsq_out = nullptr;  // [2]
   double* host_pinned = nullptr;  // [2]
+  double* sdv_dev = nullptr;      // staging for lgdm_update_state with a host destination
   int64_t device_bytes = 0;
   bool have_state = false, have_kappa = false, assembled = false;
   int kernel = 0;  // 0 auto, 1 general, 2 sweep
@@ -502,7 +505,8 @@ template <int D> lgdm_status assemble_general(lgdm_mesh m) {
   const int64_t batches = (m->n_elems + EPB - 1) / EPB;
   const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(batches, int64_t(nsm) * std::max(per_sm, 1))));
   k_elem_blocks<D, EPB><<<grid, EPB * F::NPAIR, smem, m->stream>>>(
-      m->dm, m->n_elems, m->conn, m->coords, m->dofs, m->kappa, m->scratchK, m->scratchF);
+      m->dm, m->n_elems, m->conn, m->coords, m->dofs, m->kappa, m->k0g, m->alg, m->scratchK,
+      m->scratchF);
   lgdm_status s = check_launch(m, "k_elem_blocks");
   if (s != LGDM_OK) return s;
   constexpr int WPB = 8;
@@ -520,7 +524,10 @@ lgdm_status lgdm_assemble(lgdm_mesh m, lgdm_csr* K, double** R) {
   if (!m->have_state || !m->have_kappa) return fail(LGDM_ERR_INVALID_STATE, "assemble before set_state");
   CU(cudaSetDevice(m->device));
   lgdm_status s;
-  const bool sweep = m->kernel >= 2 || (m->kernel == 0 && m->structured && sweep_supported(m));
+  const bool defects = m->k0g || m->alg;   // per-GP fields: general path only
+  const bool sweep = !defects && (m->kernel >= 2 || (m->kernel == 0 && m->structured && sweep_supported(m)));
+  if (m->kernel >= 2 && defects)
+    return fail(LGDM_ERR_INVALID_ARGUMENT, "sweep kernels do not take per-GP defect fields (kernel 0 or 1)");
   if (m->kernel >= 2 && !(m->structured && sweep_supported(m)))
     return fail(LGDM_ERR_INVALID_ARGUMENT, "sweep kernel requested but mesh is not structured");
   if (sweep) s = assemble_sweep(m);
@@ -552,6 +559,79 @@ lgdm_status lgdm_update_history(lgdm_mesh m) {
   else if (m->f.dim == 2) k_update_history<2><<<blocks, 256, 0, m->stream>>>(m->n_elems, m->conn, m->dofs, m->kappa);
   else k_update_history<3><<<blocks, 256, 0, m->stream>>>(m->n_elems, m->conn, m->dofs, m->kappa);
   return check_launch(m, "k_update_history");
+}
+
+int lgdm_sdv_width(lgdm_elem_type type) {
+  switch (type) {
+    case LGDM_BAR2: return StateW<1>::W;
+    case LGDM_QUAD4: return StateW<2>::W;
+    case LGDM_HEX8: return StateW<3>::W;
+    default: return -1;
+  }
+}
+
+lgdm_status lgdm_set_defects(lgdm_mesh m, const double* kappa0_gp, const double* alpha_gp,
+                             int64_t n, int src_on_device) {
+  if (!m) return fail(LGDM_ERR_INVALID_ARGUMENT, "mesh is NULL");
+  const int64_t ngp = m->n_elems * m->f.ngp;
+  if ((kappa0_gp || alpha_gp) && n != ngp)
+    return fail(LGDM_ERR_INVALID_STATE, "n = %lld, expected n_elems * ngp = %lld", (long long)n,
+                (long long)ngp);
+  CU(cudaSetDevice(m->device));
+  const cudaMemcpyKind kind = src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  struct { const double* src; double** dst; } f[2] = {{kappa0_gp, &m->k0g}, {alpha_gp, &m->alg}};
+  for (auto& x : f) {
+    if (!x.src) {
+      if (*x.dst) {
+        CU(cudaStreamSynchronize(m->stream));
+        CU(cudaFree(*x.dst));
+        m->device_bytes -= ngp * 8;
+        *x.dst = nullptr;
+      }
+      continue;
+    }
+    if (!*x.dst) {
+      CU(dalloc(x.dst, size_t(ngp)));
+      m->device_bytes += ngp * 8;
+    }
+    CU(cudaMemcpyAsync(*x.dst, x.src, size_t(ngp) * 8, kind, m->stream));
+  }
+  if (!src_on_device) CU(cudaStreamSynchronize(m->stream));   // host arrays may be pageable
+  return LGDM_OK;
+}
+
+lgdm_status lgdm_update_state(lgdm_mesh m, double* sdv, int64_t n_sdv, int dst_on_device) {
+  if (!m) return fail(LGDM_ERR_INVALID_ARGUMENT, "mesh is NULL");
+  if (!m->have_state || !m->have_kappa) return fail(LGDM_ERR_INVALID_STATE, "update_state before set_state");
+  const int W = lgdm_sdv_width(lgdm_elem_type(m->type));
+  const int64_t ngp = m->n_elems * m->f.ngp;
+  if (sdv && n_sdv != ngp * W)
+    return fail(LGDM_ERR_INVALID_STATE, "n_sdv = %lld, expected %lld", (long long)n_sdv,
+                (long long)(ngp * W));
+  CU(cudaSetDevice(m->device));
+  double* out = nullptr;
+  if (sdv && dst_on_device) out = sdv;
+  if (sdv && !dst_on_device) {
+    if (!m->sdv_dev) {
+      CU(dalloc(&m->sdv_dev, size_t(ngp) * W));
+      m->device_bytes += ngp * W * 8;
+    }
+    out = m->sdv_dev;
+  }
+  const unsigned blocks = unsigned((ngp + 255) / 256);
+  if (m->f.dim == 1)
+    k_update_state<1><<<blocks, 256, 0, m->stream>>>(m->dm, m->n_elems, m->conn, m->coords, m->dofs, m->kappa, m->k0g, m->alg, out);
+  else if (m->f.dim == 2)
+    k_update_state<2><<<blocks, 256, 0, m->stream>>>(m->dm, m->n_elems, m->conn, m->coords, m->dofs, m->kappa, m->k0g, m->alg, out);
+  else
+    k_update_state<3><<<blocks, 256, 0, m->stream>>>(m->dm, m->n_elems, m->conn, m->coords, m->dofs, m->kappa, m->k0g, m->alg, out);
+  lgdm_status s = check_launch(m, "k_update_state");
+  if (s != LGDM_OK) return s;
+  if (sdv && !dst_on_device) {
+    CU(cudaMemcpyAsync(sdv, out, size_t(ngp) * W * 8, cudaMemcpyDeviceToHost, m->stream));
+    CU(cudaStreamSynchronize(m->stream));
+  }
+  return LGDM_OK;
 }
 
 lgdm_status lgdm_residual_sumsq(lgdm_mesh m, double* out2, int on_device) {
@@ -671,7 +751,7 @@ void lgdm_destroy(lgdm_mesh m) {
   if (m->comm && g_nccl.loaded) g_nccl.commDestroy(m->comm);
   void* ptrs[] = {m->coords, m->conn, m->dofs, m->kappa, m->row_ptr, m->col_idx, m->val, m->R,
                   m->nbr_ptr, m->base, m->adj_ptr, m->adj, m->scratchK, m->scratchF,
-                  m->sumsq_part, m->sumsq_out};
+                  m->sumsq_part, m->sumsq_out, m->k0g, m->alg, m->sdv_dev};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (m->host_pinned) cudaFreeHost(m->host_pinned);

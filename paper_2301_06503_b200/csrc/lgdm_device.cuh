@@ -152,9 +152,11 @@ template <int D> struct Core {
 // ---------------------------------------------------------------------------------------
 // Shape values are supplied by SHD(a, j) = dN_a/dxi_j and SHN(a) = N_a at the Gauss point
 // (gpCore below passes the closed forms; kernels may pass register copies of a table).
+// k0 / al: the GP's damage threshold kappa0 and alpha (defect regions; the material's
+// values unless per-GP fields are set, lgdm_set_defects).
 template <int D, class XF, class UF, class SD, class SN>
-__device__ __forceinline__ double gpCoreS(const DevMat& m, XF&& X, UF&& U, double kh, SD&& SHD,
-                                          SN&& SHN, double* __restrict__ core) {
+__device__ __forceinline__ double gpCoreSK(const DevMat& m, XF&& X, UF&& U, double kh, double k0,
+                                           double al, SD&& SHD, SN&& SHN, double* __restrict__ core) {
   using Co = Core<D>;
   using F = Fam<D>;
   constexpr int NEN = F::NEN, NS = F::NS;
@@ -299,12 +301,12 @@ __device__ __forceinline__ double gpCoreS(const DevMat& m, XF&& X, UF&& U, doubl
   const bool L = (ebar - kh) > 1e-10;                  // Fig. 8b l.22 cond1
   const double kap = L ? ebar : kh;
   double Dm = 0.0, dD = 0.0;
-  if (!((kap - m.kappa0) < 1e-10)) {                   // Fig. 8b l.27 cond2 (negated)
-    const double ex = exp(-m.beta * (kap - m.kappa0));
-    const double br = 1.0 - m.alpha + m.alpha * ex;
-    const double r = m.kappa0 / kap;
+  if (!((kap - k0) < 1e-10)) {                         // Fig. 8b l.27 cond2 (negated)
+    const double ex = exp(-m.beta * (kap - k0));
+    const double br = 1.0 - al + al * ex;
+    const double r = k0 / kap;
     Dm = 1.0 - r * br;                                 // Eq. A.1
-    dD = (r / kap) * br + r * m.alpha * m.beta * ex;
+    dD = (r / kap) * br + r * al * m.beta * ex;
   }
   const double enD = exp(-m.n * Dm);
   const double gI = m.ga * enD + m.gb;                 // Eq. A.4
@@ -378,6 +380,12 @@ __device__ __forceinline__ double gpCoreS(const DevMat& m, XF&& X, UF&& U, doubl
 }
 
 
+template <int D, class XF, class UF, class SD, class SN>
+__device__ __forceinline__ double gpCoreS(const DevMat& m, XF&& X, UF&& U, double kh, SD&& SHD,
+                                          SN&& SHN, double* __restrict__ core) {
+  return gpCoreSK<D>(m, X, U, kh, m.kappa0, m.alpha, SHD, SHN, core);
+}
+
 // Core of one GP with the closed-form shape functions at Gauss point g.
 template <int D, class XF, class UF>
 __device__ __forceinline__ double gpCore(const DevMat& m, XF&& X, UF&& U, double kh, int g,
@@ -427,12 +435,15 @@ __device__ __forceinline__ void gpExpand(const double* __restrict__ core, int a,
 // Phase A for one GP, all nodes (general path): core into registers, then expansions.
 template <int D>
 __device__ __forceinline__ double phaseA(const DevMat& m, const double* __restrict__ X,
-                                         const double* __restrict__ U, double kh, int g,
-                                         double* __restrict__ rec, double* __restrict__ scal) {
+                                         const double* __restrict__ U, double kh, double k0,
+                                         double al, int g, double* __restrict__ rec,
+                                         double* __restrict__ scal) {
   double core[Core<D>::STRIDE];
-  const double detJ = gpCore<D>(
+  const double detJ = gpCoreSK<D>(
       m, [&](int a, int i) { return X[a * D + i]; },
-      [&](int a, int i) { return U[a * Fam<D>::NDPN + i]; }, kh, g, core);
+      [&](int a, int i) { return U[a * Fam<D>::NDPN + i]; }, kh, k0, al,
+      [&](int a, int j) { return shape_dxi<D>(a, g, j); }, [&](int a) { return shapeN<D>(a, g); },
+      core);
 #pragma unroll
   for (int a = 0; a < Fam<D>::NEN; ++a) gpExpand<D>(core, a, g, rec + a * Rec<D>::STRIDE);
   scal[0] = core[Core<D>::MU];

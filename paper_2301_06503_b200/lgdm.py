@@ -28,7 +28,8 @@ EXPORTS = ["lgdm_create_mesh", "lgdm_set_state", "lgdm_assemble", "lgdm_update_h
            "lgdm_residual_sumsq", "lgdm_residual_norms", "lgdm_set_comm", "lgdm_nccl_unique_id",
            "lgdm_get_kappa",
            "lgdm_scale_dofs", "lgdm_set_kernel", "lgdm_get_info", "lgdm_launch_count",
-           "lgdm_last_error", "lgdm_destroy"]
+           "lgdm_last_error", "lgdm_destroy", "lgdm_sdv_width", "lgdm_set_defects",
+           "lgdm_update_state"]
 
 
 class LGDMError(RuntimeError):
@@ -89,6 +90,9 @@ def load() -> C.CDLL:
     L.lgdm_launch_count.restype = C.c_int64
     L.lgdm_last_error.restype = C.c_char_p
     L.lgdm_destroy.argtypes = [vp]
+    L.lgdm_sdv_width.argtypes = [C.c_int]
+    L.lgdm_set_defects.argtypes = [vp, vp, vp, i64, C.c_int]
+    L.lgdm_update_state.argtypes = [vp, vp, i64, C.c_int]
     for name in EXPORTS:
         if name not in ("lgdm_launch_count", "lgdm_last_error", "lgdm_destroy"):
             getattr(L, name).restype = C.c_int
@@ -196,6 +200,36 @@ class Mesh:
                     R=DeviceArray(r.value, csr.n_rows, "<f8", self),
                     first_row=csr.first_row, n_cols=csr.n_cols, n_rows=csr.n_rows, nnz=csr.nnz)
 
+    def set_defects(self, kappa0_gp=None, alpha_gp=None):
+        """Per-GP kappa0 / alpha ([n_elems, ngp] or flat; None = material value)."""
+        n = self.n_elems * self.ngp
+        ptrs, keep, dev = [], [], None
+        for a in (kappa0_gp, alpha_gp):
+            if a is None:
+                ptrs.append(None)
+                continue
+            p, on_dev, k = _ptr_and_kind(a)
+            if dev is not None and dev != on_dev:
+                raise ValueError("kappa0_gp and alpha_gp must both be host or both be device")
+            dev = on_dev
+            ptrs.append(p)
+            keep.append(k)
+        _check(load().lgdm_set_defects(self._h, ptrs[0], ptrs[1], n, dev or 0))
+        self._keep_defects = keep
+
+    def update_state(self, out=None):
+        """State-variable update (Alg. 2 l.8-14) + history commit.  Returns a device tensor
+        [n_elems, ngp, sdv_width] (or fills `out`, a float64 tensor / numpy array)."""
+        import torch
+        W = load().lgdm_sdv_width(self.etype)
+        n = self.n_elems * self.ngp * W
+        if out is None:
+            out = torch.empty((self.n_elems, self.ngp, W), dtype=torch.float64,
+                              device=f"cuda:{self.device}")
+        p, on_dev, _ = _ptr_and_kind(out)
+        _check(load().lgdm_update_state(self._h, p, n, on_dev))
+        return out
+
     def update_history(self):
         _check(load().lgdm_update_history(self._h))
 
@@ -246,3 +280,8 @@ class Mesh:
             self.close()
         except Exception:
             pass
+
+
+def sdv_width(etype: int) -> int:
+    """doubles per (element, GP) record of Mesh.update_state (include/lgdm.h)"""
+    return load().lgdm_sdv_width(etype)

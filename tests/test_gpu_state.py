@@ -1,0 +1,154 @@
+"""GPU parity of the state-variable update (lgdm_update_state; Alg. 2
+l.8-14, Fig. 9a) and of the per-GP defect fields (lgdm_set_defects) against the CPU
+oracle, through the C ABI.
+
+Tolerances: every record component within 1e-12 of that component's largest magnitude over
+the mesh (the FP64 evaluation orders differ); the committed history within 1e-13 relative
+(a copy of ebar -- interpolated in a different FMA order -- or of kappa_hist; both sides take
+the same threshold decision on inputs kept away from it); K / R of the defect-field assembly
+as in parity.py.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from paper_2301_06503_b200 import lgdm
+
+from parity import compare
+
+pytestmark = pytest.mark.gpu
+
+CASES = [(lgdm.BAR2, (7,)), (lgdm.QUAD4, (5, 4)), (lgdm.QUAD4, (37, 29)),
+         (lgdm.HEX8, (3, 4, 5)), (lgdm.HEX8, (9, 6, 2))]
+
+
+def _case(etype, n, distort=0.1):
+    cfg = synth.small_config(etype, n)
+    mesh = synth.structured_mesh(cfg)
+    coords = synth.distort(mesh, distort) if etype != lgdm.BAR2 else mesh.coords
+    dofs, kappa = synth.fields(cfg, mesh)
+    return cfg, mesh, coords, dofs, kappa
+
+
+def _defects(kappa, seed):
+    rng = np.random.default_rng(seed)
+    k = kappa.reshape(-1)
+    # thresholds well away from the state's kappa (both damaging and undamaged GPs)
+    k0 = np.where(rng.uniform(size=k.shape) < 0.7, k * rng.uniform(0.3, 0.8, k.shape), k * 1.7)
+    al = rng.uniform(0.3, 1.0, k.shape)
+    return k0, al
+
+
+def _check_records(etype, got, ref):
+    W = oracle.sdv_width(etype)
+    got = got.reshape(-1, W)
+    ref = ref.reshape(-1, W)
+    scale = np.maximum(np.abs(ref).max(axis=0), 1e-300)
+    err = np.abs(got - ref) / scale
+    assert err.max() <= 1e-12, f"worst {err.max():.3e} in component {np.unravel_index(err.argmax(), err.shape)[1]}"
+
+
+@pytest.mark.parametrize("etype,n", CASES)
+@pytest.mark.parametrize("defects", [False, True])
+def test_update_state_parity(etype, n, defects):
+    import torch
+    cfg, mesh, coords, dofs, kappa = _case(etype, n)
+    k0, al = _defects(kappa, 3 + etype) if defects else (None, None)
+    ref, kref = oracle.update_state(etype, oracle.material(**synth.MATERIAL), coords, mesh.conn,
+                                    dofs, kappa, kappa0_gp=k0, alpha_gp=al)
+    m = lgdm.Mesh(etype, coords, mesh.conn, lgdm.material(**synth.MATERIAL))
+    m.set_state(dofs, kappa)
+    if defects:
+        m.set_defects(k0, al)
+    got = m.update_state()
+    torch.cuda.synchronize()
+    _check_records(etype, got.cpu().numpy(), ref)
+    np.testing.assert_allclose(m.get_kappa().reshape(-1), kref.reshape(-1), rtol=1e-13, atol=0)
+    # the record's kappa is the committed history
+    W = oracle.sdv_width(etype)
+    nv = oracle.FAMILY[etype][3]
+    assert np.array_equal(got.cpu().numpy().reshape(-1, W)[:, 3 * nv + 2],
+                          m.get_kappa().reshape(-1))
+    m.close()
+
+
+def test_update_state_host_destination_and_history_only():
+    import torch
+    etype, n = lgdm.QUAD4, (6, 5)
+    cfg, mesh, coords, dofs, kappa = _case(etype, n)
+    m = lgdm.Mesh(etype, coords, mesh.conn, lgdm.material(**synth.MATERIAL))
+    m.set_state(dofs, kappa)
+    dev = m.update_state().cpu().numpy()
+    m.set_state(dofs, kappa)
+    host = np.zeros_like(dev)
+    m.update_state(out=host)
+    assert np.array_equal(dev, host)
+    # NULL destination: history commit only, equal to lgdm_update_history
+    m.set_state(dofs, kappa)
+    lgdm._check(lgdm.load().lgdm_update_state(m._h, None, 0, 1))
+    k1 = m.get_kappa()
+    m.set_state(dofs, kappa)
+    m.update_history()
+    assert np.array_equal(k1, m.get_kappa())
+    m.close()
+
+
+def test_update_state_errors():
+    etype, n = lgdm.HEX8, (2, 2, 2)
+    cfg, mesh, coords, dofs, kappa = _case(etype, n)
+    m = lgdm.Mesh(etype, coords, mesh.conn, lgdm.material(**synth.MATERIAL))
+    with pytest.raises(lgdm.LGDMError):
+        m.update_state()                       # before set_state
+    m.set_state(dofs, kappa)
+    L = lgdm.load()
+    buf = np.zeros(10)
+    assert L.lgdm_update_state(m._h, buf.ctypes.data, 10, 0) != 0   # wrong size
+    assert L.lgdm_set_defects(m._h, buf.ctypes.data, None, 10, 0) != 0
+    assert [lgdm.sdv_width(t) for t in (1, 2, 3)] == [8, 14, 23] and lgdm.sdv_width(9) == -1
+    m.close()
+
+
+@pytest.mark.parametrize("etype,n", [(lgdm.QUAD4, (11, 7)), (lgdm.HEX8, (5, 4, 3))])
+def test_defect_assembly_parity(etype, n):
+    import torch
+    cfg, mesh, coords, dofs, kappa = _case(etype, n)
+    k0, al = _defects(kappa, 11 + etype)
+    ref = oracle.assemble(etype, oracle.material(**synth.MATERIAL), coords, mesh.conn, dofs,
+                          kappa, kappa0_gp=k0, alpha_gp=al)
+    plain = oracle.assemble(etype, oracle.material(**synth.MATERIAL), coords, mesh.conn, dofs,
+                            kappa)
+    assert not np.allclose(ref["val"], plain["val"])
+    for kernel in (lgdm.KERNEL_AUTO, lgdm.KERNEL_GENERAL):
+        m = lgdm.Mesh(etype, coords, mesh.conn, lgdm.material(**synth.MATERIAL))
+        m.set_kernel(kernel)
+        m.set_state(dofs, kappa)
+        m.set_defects(k0, al)
+        out = m.assemble()
+        torch.cuda.synchronize()
+        got = dict(row_ptr=out["row_ptr"].torch().cpu().numpy(),
+                   col_idx=out["col_idx"].torch().cpu().numpy(),
+                   val=out["val"].torch().cpu().numpy(), R=out["R"].torch().cpu().numpy())
+        compare(ref, got, f"defects kernel {kernel}")
+        # clearing the fields returns to the uniform material (and to the sweep path)
+        m.set_defects(None, None)
+        out = m.assemble()
+        torch.cuda.synchronize()
+        got = dict(row_ptr=out["row_ptr"].torch().cpu().numpy(),
+                   col_idx=out["col_idx"].torch().cpu().numpy(),
+                   val=out["val"].torch().cpu().numpy(), R=out["R"].torch().cpu().numpy())
+        compare(plain, got, f"cleared kernel {kernel}")
+        m.close()
+
+
+def test_defects_refuse_sweep_kernels():
+    etype, n = lgdm.HEX8, (3, 3, 3)
+    cfg, mesh, coords, dofs, kappa = _case(etype, n, distort=0.0)
+    k0, al = _defects(kappa, 5)
+    m = lgdm.Mesh(etype, coords, mesh.conn, lgdm.material(**synth.MATERIAL))
+    m.set_kernel(lgdm.KERNEL_SWEEP4)
+    m.set_state(dofs, kappa)
+    m.set_defects(k0, al)
+    with pytest.raises(lgdm.LGDMError):
+        m.assemble()
+    m.close()
