@@ -151,7 +151,7 @@ def build_rank_mesh(cfg, rank, world):
 
 
 def run_lgdm(cfg, steps, warmup, rank, world, local, pg_barrier, allmax, comm_uid=None,
-             e2e=True, kernel=0):
+             e2e=True, kernel=0, state=False):
     import torch
     from paper_2301_06503_b200 import lgdm
     torch.cuda.set_device(local)
@@ -232,6 +232,28 @@ def run_lgdm(cfg, steps, warmup, rank, world, local, pg_barrier, allmax, comm_ui
         res["e2e_ms_per_step"] = allmax(s2.elapsed_time(e2)) / steps
         res["h2d_bytes"] = int(dofs_h.numel() * 8)
         res["d2h_bytes"] = 16
+    if state:
+        # lgdm_update_state: per-GP state records, device destination
+        W = lgdm.sdv_width(cfg.etype)
+        m.set_state(dofs_d, kappa_d)
+        buf = torch.empty((mesh.conn.shape[0], ngp, W), dtype=torch.float64,
+                          device=f"cuda:{local}")
+        for _ in range(max(1, warmup)):
+            m.update_state(out=buf)
+        torch.cuda.synchronize()
+        pg_barrier()
+        s3, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s3.record(stream)
+        for _ in range(steps):
+            m.update_state(out=buf)
+        e3.record(stream)
+        torch.cuda.synchronize()
+        res["state_ms"] = allmax(s3.elapsed_time(e3)) / steps
+        ne_l, nn_l = mesh.conn.shape[0], mesh.coords.shape[0]
+        res["state_bytes"] = (ne_l * nen * 4 + nn_l * (dim + ndpn) * 8 +
+                              ne_l * ngp * (16 + W * 8))
+        res["state_width"] = W
+        del buf
     m.close()
     return res
 
@@ -355,7 +377,7 @@ def main():
             return x
     peak, peak_src = peaks()
     r = run_lgdm(cfg, args.steps, args.warmup, rank, ws, local, barrier, allmax, comm_uid,
-                 kernel=args.kernel)
+                 kernel=args.kernel, state=not args.no_secondary)
     n_total = cfg.n_elems
     value = n_total / (r["ms_per_step"] * 1e-3)
     achieved = r["alg_bytes"] / (r["assemble_ms"] * 1e-3) / 1e9
@@ -381,6 +403,14 @@ def main():
                 "h2d_bytes_per_step": r["h2d_bytes"], "d2h_bytes_per_step": r["d2h_bytes"]},
         "setup_s": {"generate": r["t_gen"], "create_mesh": r["t_create"]},
     }
+    if "state_ms" in r:
+        sa = r["state_bytes"] / (r["state_ms"] * 1e-3) / 1e9
+        out["state_update"] = {
+            "what": "lgdm_update_state (SURVEY NEXT f1): per-GP state records of Alg. 2 l.8-14 "
+                    f"({r['state_width']} doubles per GP) + history commit, device destination",
+            "ms": r["state_ms"], "elements_per_s": n_total / (r["state_ms"] * 1e-3),
+            "roofline": {"bound": "hbm", "achieved": sa, "peak": peak, "unit": "GB/s",
+                         "frac": sa / peak, "algorithmic_bytes": r["state_bytes"]}}
     if ws == 1 and rank == 0:
         if not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(cfg)

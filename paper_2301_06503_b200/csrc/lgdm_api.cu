@@ -618,13 +618,20 @@ lgdm_status lgdm_update_state(lgdm_mesh m, double* sdv, int64_t n_sdv, int dst_o
     }
     out = m->sdv_dev;
   }
-  const unsigned blocks = unsigned((ngp + 255) / 256);
+  constexpr int TPB = 128;
+  const unsigned blocks = unsigned((ngp + TPB - 1) / TPB);
+  const size_t smem = out ? size_t(TPB) * W * sizeof(double) : 0;   // record staging
+  static bool attr = false;
+  if (!attr) {
+    CU(cudaFuncSetAttribute(k_update_state<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, TPB * StateW<3>::W * 8));
+    attr = true;
+  }
   if (m->f.dim == 1)
-    k_update_state<1><<<blocks, 256, 0, m->stream>>>(m->dm, m->n_elems, m->conn, m->coords, m->dofs, m->kappa, m->k0g, m->alg, out);
+    k_update_state<1><<<blocks, TPB, smem, m->stream>>>(m->dm, m->n_elems, m->conn, m->coords, m->dofs, m->kappa, m->k0g, m->alg, out);
   else if (m->f.dim == 2)
-    k_update_state<2><<<blocks, 256, 0, m->stream>>>(m->dm, m->n_elems, m->conn, m->coords, m->dofs, m->kappa, m->k0g, m->alg, out);
+    k_update_state<2><<<blocks, TPB, smem, m->stream>>>(m->dm, m->n_elems, m->conn, m->coords, m->dofs, m->kappa, m->k0g, m->alg, out);
   else
-    k_update_state<3><<<blocks, 256, 0, m->stream>>>(m->dm, m->n_elems, m->conn, m->coords, m->dofs, m->kappa, m->k0g, m->alg, out);
+    k_update_state<3><<<blocks, TPB, smem, m->stream>>>(m->dm, m->n_elems, m->conn, m->coords, m->dofs, m->kappa, m->k0g, m->alg, out);
   lgdm_status s = check_launch(m, "k_update_state");
   if (s != LGDM_OK) return s;
   if (sdv && !dst_on_device) {

@@ -187,155 +187,165 @@ template <int D> struct StateW {
   static constexpr int W = 3 * NV + 5;
 };
 template <int D>
-__global__ void k_update_state(DevMat m, int64_t ne, const int32_t* __restrict__ conn,
-                               const double* __restrict__ coords, const double* __restrict__ dofs,
-                               double* __restrict__ kappa, const double* __restrict__ k0g,
-                               const double* __restrict__ alg, double* __restrict__ sdv) {
+__global__ void __launch_bounds__(128, 4)
+k_update_state(DevMat m, int64_t ne, const int32_t* __restrict__ conn,
+               const double* __restrict__ coords, const double* __restrict__ dofs,
+               double* __restrict__ kappa, const double* __restrict__ k0g,
+               const double* __restrict__ alg, double* __restrict__ sdv) {
   using F = Fam<D>;
   constexpr int NV = StateW<D>::NV, W = StateW<D>::W;
-  const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (t >= ne * F::NGP) return;
-  const int64_t e = t / F::NGP;
-  const int g = int(t % F::NGP);
-  double X[F::NEN][D], U[F::NEN][F::NDPN];
-#pragma unroll
-  for (int a = 0; a < F::NEN; ++a) {
-    const int64_t n = conn[e * F::NEN + a];
-#pragma unroll
-    for (int i = 0; i < D; ++i) X[a][i] = coords[n * D + i];
-#pragma unroll
-    for (int i = 0; i < F::NDPN; ++i) U[a][i] = dofs[n * F::NDPN + i];
-  }
-  // geometry: J_ij = sum_a X_ai dN_a/dxi_j, grad N = J^-T grad_xi N
-  double J[D][D];
-#pragma unroll
-  for (int i = 0; i < D; ++i)
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-      double s = 0.0;
-#pragma unroll
-      for (int a = 0; a < F::NEN; ++a) s = fma(X[a][i], shape_dxi<D>(a, g, j), s);
-      J[i][j] = s;
-    }
-  double Ji[D][D];
-  if constexpr (D == 1) {
-    Ji[0][0] = 1.0 / J[0][0];
-  } else if constexpr (D == 2) {
-    const double r = 1.0 / (J[0][0] * J[1][1] - J[0][1] * J[1][0]);
-    Ji[0][0] = J[1][1] * r;
-    Ji[0][1] = -J[0][1] * r;
-    Ji[1][0] = -J[1][0] * r;
-    Ji[1][1] = J[0][0] * r;
-  } else {
-    const double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
-    const double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
-    const double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
-    const double r = 1.0 / (J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02);
-    Ji[0][0] = c00 * r;
-    Ji[1][0] = c01 * r;
-    Ji[2][0] = c02 * r;
-    Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * r;
-    Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * r;
-    Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * r;
-    Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * r;
-    Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * r;
-    Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * r;
-  }
-  // displacement gradient Gu_ij = sum_a u_ai dN_a/dx_j and ebar = sum_a N_a e_a
-  double Gu[D][D], ebar = 0.0;
-#pragma unroll
-  for (int i = 0; i < D; ++i)
-#pragma unroll
-    for (int j = 0; j < D; ++j) Gu[i][j] = 0.0;
-#pragma unroll
-  for (int a = 0; a < F::NEN; ++a) {
-    double gn[D];
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-      double s = 0.0;
-#pragma unroll
-      for (int k = 0; k < D; ++k) s = fma(Ji[k][j], shape_dxi<D>(a, g, k), s);
-      gn[j] = s;
-    }
+  extern __shared__ double stage[];   // [blockDim][W]: records, written out coalesced
+  const int64_t t0 = int64_t(blockIdx.x) * blockDim.x;
+  const int64_t t = t0 + threadIdx.x;
+  const int64_t ngp = ne * F::NGP;
+  if (t < ngp) {
+    const int64_t e = t / F::NGP;
+    const int g = int(t % F::NGP);
+    const int32_t* ce = conn + e * F::NEN;
+    // geometry: J_ij = sum_a X_ai dN_a/dxi_j (node data streamed; the element's GP threads
+    // share the loads through L1)
+    double J[D][D];
 #pragma unroll
     for (int i = 0; i < D; ++i)
 #pragma unroll
-      for (int j = 0; j < D; ++j) Gu[i][j] = fma(U[a][i], gn[j], Gu[i][j]);
-    ebar = fma(shapeN<D>(a, g), U[a][D], ebar);
-  }
-  // Voigt strain (engineering shear): 2D [xx, yy, xy], 3D [xx, yy, zz, xy, yz, xz]
-  double ev[NV], mv[NV], sv[NV];   // strain, d I1 / d eps_v, d J2 / d eps_v
-  double eeq, dv[NV];
-  if constexpr (D == 1) {
-    ev[0] = Gu[0][0];
-    eeq = ev[0];                                   // reading R-1D
-    dv[0] = 1.0;
-  } else {
-    constexpr int P[6] = {0, 1, 2, 0, 1, 0}, Q[6] = {0, 1, 2, 1, 2, 2};
-    const int nnorm = D;   // normal components first
+      for (int j = 0; j < D; ++j) J[i][j] = 0.0;
 #pragma unroll
-    for (int V = 0; V < NV; ++V) {
-      const int p = (D == 2 && V == 2) ? 0 : P[V], q = (D == 2 && V == 2) ? 1 : Q[V];
-      ev[V] = V < nnorm ? Gu[p][p] : Gu[p][q] + Gu[q][p];
-      mv[V] = V < nnorm ? 1.0 : 0.0;
-    }
-    double I1 = 0.0;
+    for (int a = 0; a < F::NEN; ++a) {
+      const int64_t n = ce[a];
 #pragma unroll
-    for (int V = 0; V < nnorm; ++V) I1 += ev[V];
-    // J2 = 1/2 dev:dev on the 3x3 tensor (plane strain eps33 = 0, reading R-PS; shear gamma/2)
-    double J2 = 0.0;
+      for (int i = 0; i < D; ++i) {
+        const double x = __ldg(coords + n * D + i);
 #pragma unroll
-    for (int p = 0; p < 3; ++p) {
-      const double dp = (p < nnorm ? ev[p] : 0.0) - I1 / 3.0;
-      J2 += 0.5 * dp * dp;
-      if (p < nnorm) sv[p] = dp;
-    }
-#pragma unroll
-    for (int V = nnorm; V < NV; ++V) {
-      J2 += 0.25 * ev[V] * ev[V];
-      sv[V] = 0.5 * ev[V];
-    }
-    const double Qv = m.c2 * I1 * I1 + m.c3 * J2;
-    const double sQ = sqrt(Qv);
-    eeq = m.c1 * I1 + sQ / (2.0 * m.k);
-#pragma unroll
-    for (int V = 0; V < NV; ++V)
-      dv[V] = Qv < 1e-30 ? m.c1 * mv[V]                                   // reading R-SQ
-                         : m.c1 * mv[V] + (2.0 * m.c2 * I1 * mv[V] + m.c3 * sv[V]) / (4.0 * m.k * sQ);
-  }
-  // history (Fig. 9a l.22-24), damage (Eq. A.1, l.27-31), interaction (Eq. A.4)
-  const double kh = kappa[t];
-  const double kap = (ebar - kh) > 1e-10 ? ebar : kh;
-  const double k0 = k0g ? k0g[t] : m.kappa0, al = alg ? alg[t] : m.alpha;
-  double Dm = 0.0;
-  if (!((kap - k0) < 1e-10)) Dm = 1.0 - (k0 / kap) * (1.0 - al + al * exp(-m.beta * (kap - k0)));
-  const double gI = m.ga * exp(-m.n * Dm) + m.gb;
-  // Eq. 2: sigma = (1 - D) C eps + h_sigma (eeq - ebar) d
-  double* out = sdv ? sdv + t * W : nullptr;
-  if (out) {
-    const double hr = m.hs * (eeq - ebar);
-#pragma unroll
-    for (int V = 0; V < NV; ++V) {
-      double ce;
-      if constexpr (D == 1) {
-        ce = m.E * ev[0];
-      } else {
-        double tr = 0.0;
-#pragma unroll
-        for (int U2 = 0; U2 < D; ++U2) tr += ev[U2];
-        ce = V < D ? m.lam * tr + 2.0 * m.mu * ev[V] : m.mu * ev[V];
+        for (int j = 0; j < D; ++j) J[i][j] = fma(x, shape_dxi<D>(a, g, j), J[i][j]);
       }
-      out[V] = ev[V];
-      out[NV + V] = dv[V];
-      out[2 * NV + V] = fma(1.0 - Dm, ce, hr * dv[V]);
     }
-    out[3 * NV + 0] = eeq;
-    out[3 * NV + 1] = ebar;
-    out[3 * NV + 2] = kap;
-    out[3 * NV + 3] = Dm;
-    out[3 * NV + 4] = gI;
+    double Ji[D][D];
+    if constexpr (D == 1) {
+      Ji[0][0] = 1.0 / J[0][0];
+    } else if constexpr (D == 2) {
+      const double r = 1.0 / (J[0][0] * J[1][1] - J[0][1] * J[1][0]);
+      Ji[0][0] = J[1][1] * r;
+      Ji[0][1] = -J[0][1] * r;
+      Ji[1][0] = -J[1][0] * r;
+      Ji[1][1] = J[0][0] * r;
+    } else {
+      const double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+      const double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+      const double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+      const double r = 1.0 / (J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02);
+      Ji[0][0] = c00 * r;
+      Ji[1][0] = c01 * r;
+      Ji[2][0] = c02 * r;
+      Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * r;
+      Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * r;
+      Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * r;
+      Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * r;
+      Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * r;
+      Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * r;
+    }
+    // displacement gradient Gu_ij = sum_a u_ai dN_a/dx_j and ebar = sum_a N_a e_a
+    double Gu[D][D], ebar = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+      for (int j = 0; j < D; ++j) Gu[i][j] = 0.0;
+#pragma unroll
+    for (int a = 0; a < F::NEN; ++a) {
+      const int64_t n = ce[a];
+      double gn[D];
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < D; ++k) s = fma(Ji[k][j], shape_dxi<D>(a, g, k), s);
+        gn[j] = s;
+      }
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        const double u = __ldg(dofs + n * F::NDPN + i);
+#pragma unroll
+        for (int j = 0; j < D; ++j) Gu[i][j] = fma(u, gn[j], Gu[i][j]);
+      }
+      ebar = fma(shapeN<D>(a, g), __ldg(dofs + n * F::NDPN + D), ebar);
+    }
+    // Voigt strain (engineering shear): 2D [xx, yy, xy], 3D [xx, yy, zz, xy, yz, xz]
+    double ev[NV], dv[NV], eeq;
+    if constexpr (D == 1) {
+      ev[0] = Gu[0][0];
+      eeq = ev[0];                                   // reading R-1D
+      dv[0] = 1.0;
+    } else {
+      constexpr int P[6] = {0, 1, 2, 0, 1, 0}, Q[6] = {0, 1, 2, 1, 2, 2};
+      double mv[NV], sv[NV];
+#pragma unroll
+      for (int V = 0; V < NV; ++V) {
+        const int p = (D == 2 && V == 2) ? 0 : P[V], q = (D == 2 && V == 2) ? 1 : Q[V];
+        ev[V] = V < D ? Gu[p][p] : Gu[p][q] + Gu[q][p];
+        mv[V] = V < D ? 1.0 : 0.0;
+      }
+      double I1 = 0.0;
+#pragma unroll
+      for (int V = 0; V < D; ++V) I1 += ev[V];
+      // J2 = 1/2 dev:dev on the 3x3 tensor (plane strain eps33 = 0, reading R-PS; shear gamma/2)
+      double J2 = 0.0;
+#pragma unroll
+      for (int p = 0; p < 3; ++p) {
+        const double dp = (p < D ? ev[p] : 0.0) - I1 / 3.0;
+        J2 += 0.5 * dp * dp;
+        if (p < D) sv[p] = dp;
+      }
+#pragma unroll
+      for (int V = D; V < NV; ++V) {
+        J2 += 0.25 * ev[V] * ev[V];
+        sv[V] = 0.5 * ev[V];
+      }
+      const double Qv = m.c2 * I1 * I1 + m.c3 * J2;
+      const double sQ = sqrt(Qv);
+      eeq = m.c1 * I1 + sQ / (2.0 * m.k);
+#pragma unroll
+      for (int V = 0; V < NV; ++V)
+        dv[V] = Qv < 1e-30 ? m.c1 * mv[V]                                   // reading R-SQ
+                           : m.c1 * mv[V] + (2.0 * m.c2 * I1 * mv[V] + m.c3 * sv[V]) / (4.0 * m.k * sQ);
+    }
+    // history (Fig. 9a l.22-24), damage (Eq. A.1, l.27-31), interaction (Eq. A.4)
+    const double kh = kappa[t];
+    const double kap = (ebar - kh) > 1e-10 ? ebar : kh;
+    const double k0 = k0g ? k0g[t] : m.kappa0, al = alg ? alg[t] : m.alpha;
+    double Dm = 0.0;
+    if (!((kap - k0) < 1e-10)) Dm = 1.0 - (k0 / kap) * (1.0 - al + al * exp(-m.beta * (kap - k0)));
+    const double gI = m.ga * exp(-m.n * Dm) + m.gb;
+    kappa[t] = kap;
+    if (sdv) {
+      // Eq. 2: sigma = (1 - D) C eps + h_sigma (eeq - ebar) d
+      double* out = stage + threadIdx.x * W;
+      const double hr = m.hs * (eeq - ebar);
+      double tr = 0.0;
+#pragma unroll
+      for (int U2 = 0; U2 < D; ++U2) tr += ev[U2];
+#pragma unroll
+      for (int V = 0; V < NV; ++V) {
+        const double ce = D == 1 ? m.E * ev[0] : (V < D ? m.lam * tr + 2.0 * m.mu * ev[V] : m.mu * ev[V]);
+        out[V] = ev[V];
+        out[NV + V] = dv[V];
+        out[2 * NV + V] = fma(1.0 - Dm, ce, hr * dv[V]);
+      }
+      out[3 * NV + 0] = eeq;
+      out[3 * NV + 1] = ebar;
+      out[3 * NV + 2] = kap;
+      out[3 * NV + 3] = Dm;
+      out[3 * NV + 4] = gI;
+    }
   }
-  kappa[t] = kap;
+  if (sdv) {   // the block's records are one contiguous range of the output: coalesced copy
+    __syncthreads();
+    const int64_t nrec = min(int64_t(blockDim.x), ngp - t0);
+    const int n = int(nrec) * W;
+    double* dst = sdv + t0 * W;   // 16-byte aligned: 128 W doubles per block, even
+    const int n2 = n >> 1;
+    for (int k = threadIdx.x; k < n2; k += blockDim.x)
+      __stcs(reinterpret_cast<double2*>(dst) + k, reinterpret_cast<const double2*>(stage)[k]);
+    if ((n & 1) && threadIdx.x == 0) __stcs(dst + n - 1, stage[n - 1]);
+  }
 }
 
 // ----------------------------------------------------------------------------------------
