@@ -276,3 +276,31 @@ def update_state(etype: int, m: Material, coords, conn, dofs, kappa, kappa0_gp=N
     if rc != 0:
         raise ValueError(f"oracle_update_state failed rc={rc}")
     return sdv.reshape(ne, ngp, W), k
+
+
+def blocked_perm(etype: int, n_nodes: int):
+    """Blocked DOF order of the paper's global vector [u; ebar] (`u(1:ndof_u)`
+    then the ebar dofs): blocked index -> node-interleaved index."""
+    dim, ndpn = FAMILY[etype][0], FAMILY[etype][2]
+    nu = n_nodes * dim
+    r = np.arange(n_nodes * ndpn)
+    return np.where(r < nu, (r // dim) * ndpn + r % dim, (r - nu) * ndpn + dim).astype(np.int64)
+
+
+def blocked(etype: int, res: dict, n_nodes: int):
+    """P K P^T and P R of an assembled (node-interleaved) result, columns ascending per row,
+    explicit zeros of the pattern kept (reading R-PAT).  Plain definition: a symmetric
+    permutation of the CSR, done on the matrix of 1-based source positions (scipy.sparse as
+    the primitive) so that every stored entry moves exactly once."""
+    import scipy.sparse as sp
+    p = blocked_perm(etype, n_nodes)
+    n = p.size
+    nnz = res["val"].size
+    pos = sp.csr_matrix((np.arange(1, nnz + 1, dtype=np.float64),
+                         res["col_idx"].astype(np.int64), res["row_ptr"]), shape=(n, n))
+    Pb = pos[p][:, p].tocsr()
+    Pb.sort_indices()
+    src = Pb.data.astype(np.int64) - 1
+    assert Pb.nnz == nnz and np.array_equal(np.sort(src), np.arange(nnz))
+    return dict(row_ptr=Pb.indptr.astype(np.int64), col_idx=Pb.indices.astype(np.int32),
+                val=np.asarray(res["val"])[src], R=np.asarray(res["R"])[p])
