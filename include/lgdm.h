@@ -151,6 +151,16 @@ lgdm_status lgdm_set_defects(lgdm_mesh mesh, const double* kappa0_gp, const doub
  * Before set_state -> LGDM_ERR_INVALID_STATE; n_sdv mismatch -> LGDM_ERR_INVALID_STATE. */
 lgdm_status lgdm_update_state(lgdm_mesh mesh, double* sdv, int64_t n_sdv, int dst_on_device);
 
+/* The last assembled K and R in the paper's blocked DOF order [u; ebar] (PAPER.md P:345-346,
+ * `u(1:ndof_u)` then the ebar dofs): rows and columns permuted by
+ * blocked r < n dim -> interleaved ndpn (r / dim) + r % dim, r >= n dim -> ndpn (r - n dim) + dim,
+ * i.e. P K P^T and P R, columns ascending per row, the same nnz (explicit zeros kept).  Mesh-
+ * owned device memory, valid until the next lgdm_get_blocked / lgdm_destroy; async on the
+ * mesh stream (a pure permutation of lgdm_assemble's output: bit-identical values).  Needs a
+ * single-rank whole mesh (no slab offset / ownership) -> else LGDM_ERR_INVALID_ARGUMENT;
+ * before lgdm_assemble -> LGDM_ERR_INVALID_STATE. */
+lgdm_status lgdm_get_blocked(lgdm_mesh mesh, lgdm_csr* K, double** R);
+
 /* Sums of squares of the last assembled R over owned rows: out2 = {sum Fu^2, sum Fe^2}.
  * out2 is a device pointer (2 doubles) when on_device = 1 (stream-ordered, no sync; for a
  * caller-side allreduce), else a host pointer (synchronises). */

@@ -118,6 +118,10 @@ struct lgdm_mesh_s {
   double* sumsq_out = nullptr;  // [2]
   double* host_pinned = nullptr;  // [2]
   double* sdv_dev = nullptr;      // staging for lgdm_update_state with a host destination
+  int64_t* rp_b = nullptr;        // blocked-order CSR (lgdm_get_blocked)
+  int32_t* ci_b = nullptr;
+  double* val_b = nullptr;
+  double* R_b = nullptr;
   int64_t device_bytes = 0;
   bool have_state = false, have_kappa = false, assembled = false;
   int kernel = 0;  // 0 auto, 1 general, 2 sweep
@@ -641,6 +645,42 @@ lgdm_status lgdm_update_state(lgdm_mesh m, double* sdv, int64_t n_sdv, int dst_o
   return LGDM_OK;
 }
 
+lgdm_status lgdm_get_blocked(lgdm_mesh m, lgdm_csr* K, double** R) {
+  if (!m) return fail(LGDM_ERR_INVALID_ARGUMENT, "mesh is NULL");
+  if (!m->assembled) return fail(LGDM_ERR_INVALID_STATE, "get_blocked before assemble");
+  if (m->own_b != 0 || m->own_e != m->n_nodes || m->gid0 != 0 || m->n_global_nodes != m->n_nodes)
+    return fail(LGDM_ERR_INVALID_ARGUMENT, "blocked order needs a single-rank whole mesh");
+  CU(cudaSetDevice(m->device));
+  if (!m->rp_b) {
+    CU(dalloc(&m->rp_b, size_t(m->n_rows) + 1));
+    CU(dalloc(&m->ci_b, size_t(m->nnz)));
+    CU(dalloc(&m->val_b, size_t(m->nnz)));
+    CU(dalloc(&m->R_b, size_t(m->n_rows)));
+    m->device_bytes += (m->n_rows + 1) * 8 + m->nnz * 12 + m->n_rows * 8;
+  }
+  const unsigned blocks = unsigned((m->n_rows * 32 + 255) / 256);
+  const int64_t no = m->n_owned;
+  if (m->f.dim == 1)
+    k_blocked<1, 2><<<blocks, 256, 0, m->stream>>>(no, m->nbr_ptr, m->base, m->col_idx, m->val, m->R, m->rp_b, m->ci_b, m->val_b, m->R_b);
+  else if (m->f.dim == 2)
+    k_blocked<2, 3><<<blocks, 256, 0, m->stream>>>(no, m->nbr_ptr, m->base, m->col_idx, m->val, m->R, m->rp_b, m->ci_b, m->val_b, m->R_b);
+  else
+    k_blocked<3, 4><<<blocks, 256, 0, m->stream>>>(no, m->nbr_ptr, m->base, m->col_idx, m->val, m->R, m->rp_b, m->ci_b, m->val_b, m->R_b);
+  lgdm_status s = check_launch(m, "k_blocked");
+  if (s != LGDM_OK) return s;
+  if (K) {
+    K->n_rows = m->n_rows;
+    K->n_cols = m->n_global_nodes * m->f.ndpn;
+    K->nnz = m->nnz;
+    K->first_row = 0;
+    K->row_ptr = m->rp_b;
+    K->col_idx = m->ci_b;
+    K->val = m->val_b;
+  }
+  if (R) *R = m->R_b;
+  return LGDM_OK;
+}
+
 lgdm_status lgdm_residual_sumsq(lgdm_mesh m, double* out2, int on_device) {
   if (!m || !out2) return fail(LGDM_ERR_INVALID_ARGUMENT, "NULL argument");
   if (!m->assembled) return fail(LGDM_ERR_INVALID_STATE, "residual before assemble");
@@ -758,7 +798,8 @@ void lgdm_destroy(lgdm_mesh m) {
   if (m->comm && g_nccl.loaded) g_nccl.commDestroy(m->comm);
   void* ptrs[] = {m->coords, m->conn, m->dofs, m->kappa, m->row_ptr, m->col_idx, m->val, m->R,
                   m->nbr_ptr, m->base, m->adj_ptr, m->adj, m->scratchK, m->scratchF,
-                  m->sumsq_part, m->sumsq_out, m->k0g, m->alg, m->sdv_dev};
+                  m->sumsq_part, m->sumsq_out, m->k0g, m->alg, m->sdv_dev, m->rp_b,
+                  m->ci_b, m->val_b, m->R_b};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (m->host_pinned) cudaFreeHost(m->host_pinned);

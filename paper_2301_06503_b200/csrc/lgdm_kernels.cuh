@@ -177,6 +177,45 @@ k_gather(int64_t n_owned, const int64_t* __restrict__ adj_ptr, const AdjEntry* _
 }
 
 // ----------------------------------------------------------------------------------------
+// Blocked DOF order [u; ebar]: P K P^T and P R of the
+// node-interleaved CSR, one warp per blocked row.  Interleaved row (o, i) of node o with deg
+// neighbours holds, from base[o] + i deg ndpn, the columns (neighbour k, comp) at k ndpn + comp;
+// blocked row (u rows first: r = o dim + i, then e rows: r = n dim + o) holds the u columns
+// (k, comp < dim) then the e columns (k, comp = dim) -- ascending blocked column ids.
+template <int DIM, int NDPN>
+__global__ void k_blocked(int64_t no, const int64_t* __restrict__ nbr_ptr,
+                          const int64_t* __restrict__ base, const int32_t* __restrict__ col_idx,
+                          const double* __restrict__ val, const double* __restrict__ R,
+                          int64_t* __restrict__ rp_b, int32_t* __restrict__ ci_b,
+                          double* __restrict__ val_b, double* __restrict__ R_b) {
+  const int64_t warp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nrows = no * NDPN;
+  if (warp >= nrows) return;
+  const bool urow = warp < no * DIM;
+  const int64_t o = urow ? warp / DIM : warp - no * DIM;
+  const int i = urow ? int(warp % DIM) : DIM;
+  const int64_t deg = nbr_ptr[o + 1] - nbr_ptr[o];
+  const int64_t start = urow ? nbr_ptr[o] * NDPN * DIM + i * deg * NDPN
+                             : nbr_ptr[no] * NDPN * DIM + nbr_ptr[o] * NDPN;
+  const int64_t src0 = base[o] + i * deg * NDPN;
+  for (int64_t j = lane; j < deg * NDPN; j += 32) {
+    const bool ucol = j < deg * DIM;
+    const int64_t k = ucol ? j / DIM : j - deg * DIM;
+    const int comp = ucol ? int(j % DIM) : DIM;
+    const int64_t src = src0 + k * NDPN + comp;
+    const int64_t mnode = col_idx[src] / NDPN;
+    ci_b[start + j] = int32_t(ucol ? mnode * DIM + comp : no * DIM + mnode);
+    val_b[start + j] = val[src];
+  }
+  if (lane == 0) {
+    rp_b[warp] = start;
+    R_b[warp] = R[o * NDPN + i];
+    if (warp == nrows - 1) rp_b[nrows] = nbr_ptr[no] * NDPN * NDPN;
+  }
+}
+
+// ----------------------------------------------------------------------------------------
 // State-variable update (Alg. 2 l.8-14, Fig. 9a update_variables, P:288-295,
 // P:359-390), one thread per (element, GP): record [eps_v (NV, Voigt, engineering shear),
 // d eeq / d eps_v (NV, Eq. A.3), sigma (NV, Eq. 2 with the h_sigma term of reading R-11a),

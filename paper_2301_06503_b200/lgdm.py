@@ -29,7 +29,7 @@ EXPORTS = ["lgdm_create_mesh", "lgdm_set_state", "lgdm_assemble", "lgdm_update_h
            "lgdm_get_kappa",
            "lgdm_scale_dofs", "lgdm_set_kernel", "lgdm_get_info", "lgdm_launch_count",
            "lgdm_last_error", "lgdm_destroy", "lgdm_sdv_width", "lgdm_set_defects",
-           "lgdm_update_state"]
+           "lgdm_update_state", "lgdm_get_blocked"]
 
 
 class LGDMError(RuntimeError):
@@ -93,6 +93,7 @@ def load() -> C.CDLL:
     L.lgdm_sdv_width.argtypes = [C.c_int]
     L.lgdm_set_defects.argtypes = [vp, vp, vp, i64, C.c_int]
     L.lgdm_update_state.argtypes = [vp, vp, i64, C.c_int]
+    L.lgdm_get_blocked.argtypes = [vp, C.POINTER(CSR), C.POINTER(vp)]
     for name in EXPORTS:
         if name not in ("lgdm_launch_count", "lgdm_last_error", "lgdm_destroy"):
             getattr(L, name).restype = C.c_int
@@ -199,6 +200,17 @@ class Mesh:
                     val=DeviceArray(csr.val, csr.nnz, "<f8", self),
                     R=DeviceArray(r.value, csr.n_rows, "<f8", self),
                     first_row=csr.first_row, n_cols=csr.n_cols, n_rows=csr.n_rows, nnz=csr.nnz)
+
+    def get_blocked(self):
+        """K, R of the last assemble in the blocked DOF order [u; ebar] (zero-copy views)."""
+        csr = CSR()
+        r = C.c_void_p()
+        _check(load().lgdm_get_blocked(self._h, C.byref(csr), C.byref(r)))
+        return dict(row_ptr=DeviceArray(csr.row_ptr, csr.n_rows + 1, "<i8", self),
+                    col_idx=DeviceArray(csr.col_idx, csr.nnz, "<i4", self),
+                    val=DeviceArray(csr.val, csr.nnz, "<f8", self),
+                    R=DeviceArray(r.value, csr.n_rows, "<f8", self),
+                    n_rows=csr.n_rows, nnz=csr.nnz)
 
     def set_defects(self, kappa0_gp=None, alpha_gp=None):
         """Per-GP kappa0 / alpha ([n_elems, ngp] or flat; None = material value)."""

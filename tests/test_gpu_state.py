@@ -152,3 +152,53 @@ def test_defects_refuse_sweep_kernels():
     with pytest.raises(lgdm.LGDMError):
         m.assemble()
     m.close()
+
+
+# ---------------- blocked DOF order [u; ebar] ----------------
+
+@pytest.mark.parametrize("etype,n,kernel", [(lgdm.BAR2, (9,), lgdm.KERNEL_AUTO),
+                                            (lgdm.QUAD4, (7, 5), lgdm.KERNEL_AUTO),
+                                            (lgdm.QUAD4, (7, 5), lgdm.KERNEL_GENERAL),
+                                            (lgdm.HEX8, (4, 3, 5), lgdm.KERNEL_AUTO),
+                                            (lgdm.HEX8, (3, 2, 2), lgdm.KERNEL_GENERAL)])
+def test_blocked_order(etype, n, kernel):
+    import torch
+    cfg, mesh, coords, dofs, kappa = _case(etype, n, distort=0.0)
+    m = lgdm.Mesh(etype, coords, mesh.conn, lgdm.material(**synth.MATERIAL))
+    m.set_kernel(kernel)
+    m.set_state(dofs, kappa)
+    out = m.assemble()
+    b = m.get_blocked()
+    torch.cuda.synchronize()
+    got = {k: out[k].torch().cpu().numpy() for k in ("row_ptr", "col_idx", "val", "R")}
+    gb = {k: b[k].torch().cpu().numpy() for k in ("row_ptr", "col_idx", "val", "R")}
+    nn = coords.shape[0]
+    # a pure permutation of the interleaved result: bit-identical to the oracle's permutation
+    # of the same CSR
+    ob = oracle.blocked(etype, got, nn)
+    for k in ("row_ptr", "col_idx", "val", "R"):
+        assert np.array_equal(gb[k], ob[k]), k
+    # and within parity of the oracle's own assembly, permuted
+    ref = oracle.assemble(etype, oracle.material(**synth.MATERIAL), coords, mesh.conn, dofs, kappa)
+    rb = oracle.blocked(etype, ref, nn)
+    rb["S"] = ref["S"][oracle.blocked_perm(etype, nn)]
+    compare(rb, gb, "blocked")
+    m.close()
+
+
+def test_blocked_errors():
+    etype, n = lgdm.QUAD4, (3, 3)
+    cfg, mesh, coords, dofs, kappa = _case(etype, n, distort=0.0)
+    m = lgdm.Mesh(etype, coords, mesh.conn, lgdm.material(**synth.MATERIAL))
+    m.set_state(dofs, kappa)
+    with pytest.raises(lgdm.LGDMError):
+        m.get_blocked()                       # before assemble
+    m.close()
+    nn = coords.shape[0]
+    m = lgdm.Mesh(etype, coords, mesh.conn, lgdm.material(**synth.MATERIAL),
+                  global_node_offset=0, n_global_nodes=nn, owned=(0, nn - 4))
+    m.set_state(dofs, kappa)
+    m.assemble()
+    with pytest.raises(lgdm.LGDMError):
+        m.get_blocked()                       # not a whole single-rank mesh
+    m.close()
