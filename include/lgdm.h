@@ -133,9 +133,9 @@ int lgdm_sdv_width(lgdm_elem_type type);
  * array [n_elems][ngp] (n = n_elems * ngp) or NULL = the material's value (NULL clears a
  * previously set field).  src_on_device: 1 device pointers (async D2D copy on the mesh stream),
  * 0 host (copied before return).  Values are not validated (kappa0 > 0, 0 <= alpha <= 1 are
- * the caller's responsibility).  With a field set, lgdm_assemble uses the general kernel
- * (kernel 0 or 1; an explicit sweep kernel 2-5 returns LGDM_ERR_INVALID_ARGUMENT) and
- * lgdm_update_state uses the field.  n mismatch -> LGDM_ERR_INVALID_STATE. */
+ * the caller's responsibility).  With a field set, lgdm_assemble uses it in the general
+ * kernel and the default sweeps (kernels 0, 1, 4; the experimental sweep kernels 2, 3, 5
+ * return LGDM_ERR_INVALID_ARGUMENT) and lgdm_update_state uses it.  n mismatch -> LGDM_ERR_INVALID_STATE. */
 lgdm_status lgdm_set_defects(lgdm_mesh mesh, const double* kappa0_gp, const double* alpha_gp,
                              int64_t n, int src_on_device);
 

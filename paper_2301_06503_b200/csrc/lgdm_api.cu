@@ -528,10 +528,11 @@ lgdm_status lgdm_assemble(lgdm_mesh m, lgdm_csr* K, double** R) {
   if (!m->have_state || !m->have_kappa) return fail(LGDM_ERR_INVALID_STATE, "assemble before set_state");
   CU(cudaSetDevice(m->device));
   lgdm_status s;
-  const bool defects = m->k0g || m->alg;   // per-GP fields: general path only
-  const bool sweep = !defects && (m->kernel >= 2 || (m->kernel == 0 && m->structured && sweep_supported(m)));
-  if (m->kernel >= 2 && defects)
-    return fail(LGDM_ERR_INVALID_ARGUMENT, "sweep kernels do not take per-GP defect fields (kernel 0 or 1)");
+  // per-GP defect fields: the general path and the default sweeps (k_sweep4, k_sweepq)
+  const bool defects = m->k0g || m->alg;
+  const bool sweep = m->kernel >= 2 || (m->kernel == 0 && m->structured && sweep_supported(m));
+  if (defects && (m->kernel == 2 || m->kernel == 3 || m->kernel == 5))
+    return fail(LGDM_ERR_INVALID_ARGUMENT, "kernels 2, 3, 5 do not take per-GP defect fields (use 0, 1 or 4)");
   if (m->kernel >= 2 && !(m->structured && sweep_supported(m)))
     return fail(LGDM_ERR_INVALID_ARGUMENT, "sweep kernel requested but mesh is not structured");
   if (sweep) s = assemble_sweep(m);

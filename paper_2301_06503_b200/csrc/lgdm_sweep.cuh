@@ -57,6 +57,8 @@ struct SweepGeom {
   int64_t own_node_b;              // local id of the first owned node
   int64_t chunk_len;               // owned node layers per CTA chunk
   int tiles_x, tiles_y, chunks;
+  const double* k0g;               // per-GP kappa0 / alpha (defect fields) or NULL
+  const double* alg;               //   (read by k_sweep4 / k_sweepq only)
 };
 
 template <int D> __device__ __forceinline__ void node_off(int a, int& ox, int& oy, int& oz) {
@@ -532,6 +534,8 @@ lgdm_status launch_sweep4(lgdm_mesh m) {
   G.lay_own_b = m->own_b / per_layer;
   G.lay_own_e = m->own_e / per_layer;
   G.own_node_b = m->own_b;
+  G.k0g = m->k0g;
+  G.alg = m->alg;
   G.tiles_x = int((G.nx + 1 + S4::TX - 1) / S4::TX);
   G.tiles_y = int((G.nyN + S4::TY - 1) / S4::TY);
   static bool attr = false;
@@ -592,6 +596,8 @@ lgdm_status launch_sweepq(lgdm_mesh m) {
   G.lay_own_b = m->own_b / per_layer;
   G.lay_own_e = m->own_e / per_layer;
   G.own_node_b = m->own_b;
+  G.k0g = m->k0g;
+  G.alg = m->alg;
   G.tiles_x = int((G.nx + 1 + SQ::TX - 1) / SQ::TX);
   G.tiles_y = 1;
   static bool attr = false;

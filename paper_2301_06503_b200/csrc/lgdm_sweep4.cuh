@@ -394,7 +394,11 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
               auto U = [&](int a, int q) { return __ldg(dofs + nid(a) * 4 + q); };
               const int64_t e = i + G.nx * (j + G.nyE * s);
               double core[Core<3>::STRIDE];
-              gpCore<3>(m, X, U, __ldg(kappa + e * NGP + g), g, core);
+              const int64_t q = e * NGP + g;   // defect fields if set
+              gpCoreSK<3>(m, X, U, __ldg(kappa + q), G.k0g ? __ldg(G.k0g + q) : m.kappa0,
+                          G.alg ? __ldg(G.alg + q) : m.alpha,
+                          [&](int a, int j) { return shape_dxi<3>(a, g, j); },
+                          [&](int a) { return shapeN<3>(a, g); }, core);
               double2* dst = reinterpret_cast<double2*>(cores + slot * S4::CSLOT + el * S4::CEL + g * S4::CSP);
 #pragma unroll
               for (int k2 = 0; k2 < 4; ++k2) dst[k2] = make_double2(core[2 * k2], core[2 * k2 + 1]);

@@ -155,8 +155,10 @@ k_sweepq(DevMat m, SweepGeom G, const double* __restrict__ coords,
               const int64_t e = i + G.nx * s;
               using Co = Core<2>;
               double c[Co::STRIDE];
-              gpCoreS<2>(m, X, U, __ldg(kappa + e * NGP + g), [&](int a, int j) { return sh[a][j]; },
-                         [&](int a) { return sh[a][2]; }, c);
+              const int64_t q = e * NGP + g;   // defect fields if set
+              gpCoreSK<2>(m, X, U, __ldg(kappa + q), G.k0g ? __ldg(G.k0g + q) : m.kappa0,
+                          G.alg ? __ldg(G.alg + q) : m.alpha, [&](int a, int j) { return sh[a][j]; },
+                          [&](int a) { return sh[a][2]; }, c);
 #pragma unroll
               for (int a = 0; a < NEN; ++a) {
                 double gn[2], SgN[2], WgN[2], DgN[2], fu[2];

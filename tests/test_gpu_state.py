@@ -119,7 +119,7 @@ def test_defect_assembly_parity(etype, n):
     plain = oracle.assemble(etype, oracle.material(**synth.MATERIAL), coords, mesh.conn, dofs,
                             kappa)
     assert not np.allclose(ref["val"], plain["val"])
-    for kernel in (lgdm.KERNEL_AUTO, lgdm.KERNEL_GENERAL):
+    for kernel in (lgdm.KERNEL_AUTO, lgdm.KERNEL_GENERAL, lgdm.KERNEL_SWEEP4):
         m = lgdm.Mesh(etype, coords, mesh.conn, lgdm.material(**synth.MATERIAL))
         m.set_kernel(kernel)
         m.set_state(dofs, kappa)
@@ -141,12 +141,13 @@ def test_defect_assembly_parity(etype, n):
         m.close()
 
 
-def test_defects_refuse_sweep_kernels():
+@pytest.mark.parametrize("kernel", [lgdm.KERNEL_SWEEP, lgdm.KERNEL_SWEEP3, lgdm.KERNEL_SWEEP5])
+def test_defects_refuse_experimental_sweeps(kernel):
     etype, n = lgdm.HEX8, (3, 3, 3)
     cfg, mesh, coords, dofs, kappa = _case(etype, n, distort=0.0)
     k0, al = _defects(kappa, 5)
     m = lgdm.Mesh(etype, coords, mesh.conn, lgdm.material(**synth.MATERIAL))
-    m.set_kernel(lgdm.KERNEL_SWEEP4)
+    m.set_kernel(kernel)
     m.set_state(dofs, kappa)
     m.set_defects(k0, al)
     with pytest.raises(lgdm.LGDMError):
