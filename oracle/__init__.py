@@ -304,3 +304,62 @@ def blocked(etype: int, res: dict, n_nodes: int):
     assert Pb.nnz == nnz and np.array_equal(np.sort(src), np.arange(nnz))
     return dict(row_ptr=Pb.indptr.astype(np.int64), col_idx=Pb.indices.astype(np.int32),
                 val=np.asarray(res["val"])[src], R=np.asarray(res["R"])[p])
+
+
+# ---------------- Newton loop pieces (Alg. 2 l.4-7, l.16) ----------------
+# The paper never states its elimination scheme or solver beyond `mldivide`; these are
+# the plain definitions of SPEC.md's apply_dirichlet / linear_solve / check_convergence.
+
+def apply_dirichlet(res: dict, fixed, incr):
+    """Symmetric elimination of the constrained dofs `fixed` (u dofs) with prescribed increments
+    `incr` (the step's displacement increment on the first iteration, 0 afterwards): for every
+    free row i, R_i -= sum_j K_ij incr_j over constrained j and K_ij = 0; constrained rows become
+    unit rows with R_j = incr_j.  Returns a new dict (row_ptr, col_idx, val, R)."""
+    rp, ci = res["row_ptr"], res["col_idx"].astype(np.int64)
+    val = np.array(res["val"], dtype=np.float64, copy=True)
+    R = np.array(res["R"], dtype=np.float64, copy=True)
+    n = R.size
+    fixed = np.asarray(fixed, dtype=np.int64)
+    inc = np.zeros(n)
+    isfix = np.zeros(n, dtype=bool)
+    isfix[fixed] = True
+    inc[fixed] = np.asarray(incr, dtype=np.float64)
+    for i in range(n):
+        lo, hi = rp[i], rp[i + 1]
+        if isfix[i]:
+            val[lo:hi] = np.where(ci[lo:hi] == i, 1.0, 0.0)
+            R[i] = inc[i]
+        else:
+            cols = ci[lo:hi]
+            m = isfix[cols]
+            R[i] -= float(np.dot(val[lo:hi][m], inc[cols[m]]))
+            val[lo:hi][m] = 0.0
+    return dict(row_ptr=rp, col_idx=res["col_idx"], val=val, R=R)
+
+
+def solve(res: dict):
+    """Direct sparse solve K delta = R (the paper's mldivide) -- scipy as the primitive."""
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spl
+    n = res["R"].size
+    K = sp.csr_matrix((res["val"], res["col_idx"].astype(np.int64), res["row_ptr"]), shape=(n, n))
+    return spl.spsolve(K.tocsc(), res["R"])
+
+
+def converged(etype: int, delta, dofs, tol: float, floor: float = 1e-16):
+    """Alg. 1 l.26 / Alg. 2 l.16: ||du|| / max(||u||, floor) <= tol and the same for ebar."""
+    dim, ndpn = FAMILY[etype][0], FAMILY[etype][2]
+    d = np.asarray(delta).reshape(-1, ndpn)
+    u = np.asarray(dofs).reshape(-1, ndpn)
+    ru = np.linalg.norm(d[:, :dim]) / max(np.linalg.norm(u[:, :dim]), floor)
+    re = np.linalg.norm(d[:, dim]) / max(np.linalg.norm(u[:, dim]), floor)
+    return bool(ru <= tol and re <= tol), ru, re
+
+
+def newton_iteration(etype: int, m: Material, coords, conn, dofs, kappa_hist, fixed, incr):
+    """One iteration of Alg. 2 l.4-7: assemble at (dofs, committed history), eliminate the
+    constraints, solve, return (delta, dofs + delta)."""
+    res = assemble(etype, m, coords, conn, dofs, kappa_hist)
+    sys_ = apply_dirichlet(res, fixed, incr)
+    delta = solve(sys_)
+    return delta, np.asarray(dofs, dtype=np.float64).reshape(-1) + delta
