@@ -47,7 +47,8 @@ typedef enum {
   LGDM_ERR_OUT_OF_MEMORY = 4,
   LGDM_ERR_CUDA = 5,
   LGDM_ERR_NCCL = 6,
-  LGDM_ERR_UNSUPPORTED = 7        /* e.g. NCCL not loadable                                 */
+  LGDM_ERR_UNSUPPORTED = 7,       /* e.g. NCCL not loadable                                 */
+  LGDM_ERR_NOT_CONVERGED = 8      /* lgdm_solve: residual above tolerance after max_iter    */
 } lgdm_status;
 
 typedef enum { LGDM_BAR2 = 1, LGDM_QUAD4 = 2, LGDM_HEX8 = 3 } lgdm_elem_type;
@@ -160,6 +161,34 @@ lgdm_status lgdm_update_state(lgdm_mesh mesh, double* sdv, int64_t n_sdv, int ds
  * single-rank whole mesh (no slab offset / ownership) -> else LGDM_ERR_INVALID_ARGUMENT;
  * before lgdm_assemble -> LGDM_ERR_INVALID_STATE. */
 lgdm_status lgdm_get_blocked(lgdm_mesh mesh, lgdm_csr* K, double** R);
+
+/* ---- Newton loop pieces (Alg. 2 lines 4-7 and 16) ----
+ * Single-rank whole meshes only (else LGDM_ERR_UNSUPPORTED).  All work runs on the mesh
+ * stream; the calls below synchronise it where they return host values.
+ *
+ * Symmetric Dirichlet elimination on the last assembled K, R (in place; the paper does not
+ * state its scheme -- SPEC.md apply_dirichlet): constrained u dofs dof_ids[n_fixed] (host,
+ * node-interleaved ids) get unit rows and R = increments[k] (the step's prescribed increment
+ * on the first iteration, 0 afterwards, since Eq. 11 solves for increments); every free row
+ * moves K_ij increments_j to its RHS and zeroes K_ij.  An ebar dof or an id out of range ->
+ * LGDM_ERR_INVALID_ARGUMENT; before lgdm_assemble -> LGDM_ERR_INVALID_STATE. */
+lgdm_status lgdm_apply_dirichlet(lgdm_mesh mesh, int64_t n_fixed, const int64_t* dof_ids,
+                                 const double* increments);
+
+/* Solve K delta = R (Alg. 2 l.6; the paper uses a direct `mldivide`) with
+ * Jacobi-preconditioned BiCGSTAB on the GPU: delta (device, n_rows doubles) from 0 until
+ * ||R - K delta|| <= tol ||R||; iters / relres (host, nullable) report the iterations and the
+ * true relative residual.  Not within 10 tol after max_iter -> LGDM_ERR_NOT_CONVERGED (delta
+ * holds the last iterate).  Reductions are fixed-order: bitwise reproducible. */
+lgdm_status lgdm_solve(lgdm_mesh mesh, double* delta, double tol, int max_iter, int* iters,
+                       double* relres);
+
+/* dofs += alpha * delta (delta device, n_nodes * ndpn doubles; Alg. 2 l.7). */
+lgdm_status lgdm_add_dofs(lgdm_mesh mesh, const double* delta, double alpha);
+
+/* Convergence sums of Alg. 1 l.26 / Alg. 2 l.16 (host out4): {sum du^2, sum u^2, sum de^2,
+ * sum e^2} over the u and ebar dofs of delta (device) and of the current dofs. */
+lgdm_status lgdm_delta_norms(lgdm_mesh mesh, const double* delta, double out4[4]);
 
 /* Sums of squares of the last assembled R over owned rows: out2 = {sum Fu^2, sum Fe^2}.
  * out2 is a device pointer (2 doubles) when on_device = 1 (stream-ordered, no sync; for a

@@ -19,6 +19,7 @@
 
 #include "../../include/lgdm.h"
 #include "lgdm_kernels.cuh"
+#include "lgdm_solver.cuh"
 
 using namespace lgdm;
 
@@ -118,6 +119,10 @@ struct lgdm_mesh_s {
   double* sumsq_out = nullptr;  // [2]
   double* host_pinned = nullptr;  // [2]
   double* sdv_dev = nullptr;      // staging for lgdm_update_state with a host destination
+  double* sol = nullptr;          // solver work vectors [9][n_rows] + partial sums (lgdm_solve)
+  double* sol_part = nullptr;
+  uint8_t* fixed = nullptr;       // Dirichlet mask / increments (lgdm_apply_dirichlet)
+  double* fixinc = nullptr;
   int64_t* rp_b = nullptr;        // blocked-order CSR (lgdm_get_blocked)
   int32_t* ci_b = nullptr;
   double* val_b = nullptr;
@@ -682,6 +687,170 @@ lgdm_status lgdm_get_blocked(lgdm_mesh m, lgdm_csr* K, double** R) {
   return LGDM_OK;
 }
 
+static bool whole_single_rank(lgdm_mesh m) {
+  return m->own_b == 0 && m->own_e == m->n_nodes && m->gid0 == 0 && m->n_global_nodes == m->n_nodes;
+}
+
+lgdm_status lgdm_apply_dirichlet(lgdm_mesh m, int64_t n_fixed, const int64_t* dof_ids,
+                                 const double* increments) {
+  if (!m) return fail(LGDM_ERR_INVALID_ARGUMENT, "mesh is NULL");
+  if (!m->assembled) return fail(LGDM_ERR_INVALID_STATE, "apply_dirichlet before assemble");
+  if (!whole_single_rank(m)) return fail(LGDM_ERR_UNSUPPORTED, "Newton pieces need a single-rank whole mesh");
+  if (n_fixed < 0 || (n_fixed && (!dof_ids || !increments)))
+    return fail(LGDM_ERR_INVALID_ARGUMENT, "dof_ids / increments");
+  const int64_t n = m->n_rows;
+  std::vector<uint8_t> mask(n, 0);
+  std::vector<double> inc(n, 0.0);
+  for (int64_t k = 0; k < n_fixed; ++k) {
+    const int64_t d = dof_ids[k];
+    if (d < 0 || d >= n) return fail(LGDM_ERR_INVALID_ARGUMENT, "dof id %lld out of range", (long long)d);
+    if (d % m->f.ndpn == m->f.dim)
+      return fail(LGDM_ERR_INVALID_ARGUMENT, "dof %lld is an ebar dof (only u dofs can be constrained)", (long long)d);
+    mask[d] = 1;
+    inc[d] = increments[k];
+  }
+  CU(cudaSetDevice(m->device));
+  if (!m->fixed) {
+    CU(dalloc(&m->fixed, size_t(n)));
+    CU(dalloc(&m->fixinc, size_t(n)));
+    m->device_bytes += n * 9;
+  }
+  CU(cudaMemcpyAsync(m->fixed, mask.data(), size_t(n), cudaMemcpyHostToDevice, m->stream));
+  CU(cudaMemcpyAsync(m->fixinc, inc.data(), size_t(n) * 8, cudaMemcpyHostToDevice, m->stream));
+  k_dirichlet<<<unsigned((n * 32 + 255) / 256), 256, 0, m->stream>>>(n, m->row_ptr, m->col_idx, m->val, m->R, m->fixed, m->fixinc);
+  lgdm_status s = check_launch(m, "k_dirichlet");
+  if (s != LGDM_OK) return s;
+  CU(cudaStreamSynchronize(m->stream));   // host staging vectors go out of scope
+  return LGDM_OK;
+}
+
+lgdm_status lgdm_solve(lgdm_mesh m, double* delta, double tol, int max_iter, int* iters_out,
+                       double* relres_out) {
+  if (!m) return fail(LGDM_ERR_INVALID_ARGUMENT, "mesh is NULL");
+  if (!m->assembled) return fail(LGDM_ERR_INVALID_STATE, "solve before assemble");
+  if (!whole_single_rank(m)) return fail(LGDM_ERR_UNSUPPORTED, "Newton pieces need a single-rank whole mesh");
+  if (!delta || !(tol > 0) || max_iter < 1) return fail(LGDM_ERR_INVALID_ARGUMENT, "delta / tol / max_iter");
+  const int64_t n = m->n_rows;
+  CU(cudaSetDevice(m->device));
+  if (!m->sol) {
+    CU(dalloc(&m->sol, size_t(n) * 9));
+    CU(dalloc(&m->sol_part, size_t(kRedBlocks) * 4 + 4));
+    m->device_bytes += n * 72 + kRedBlocks * 32 + 32;
+  }
+  double *r = m->sol, *r0 = r + n, *p = r0 + n, *v = p + n, *sv = v + n, *t = sv + n,
+         *ph = t + n, *sh = ph + n, *dinv = sh + n;
+  double* part = m->sol_part;
+  double* fin = part + size_t(kRedBlocks) * 4;
+  cudaStream_t st = m->stream;
+  const unsigned gw = unsigned((n * 32 + 255) / 256), ge = unsigned((n + 255) / 256);
+  auto dots = [&](const double* a, const double* b, const double* c, const double* d, double* h) -> lgdm_status {
+    k_dot2<<<kRedBlocks, 256, 0, st>>>(n, a, b, c, d, part);
+    k_final<2><<<1, 256, 0, st>>>(kRedBlocks, part, fin);
+    CU(cudaMemcpyAsync(h, fin, 16, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    m->launches += 2;
+    return LGDM_OK;
+  };
+  // x = 0, r = r0 = b, p = v = 0, Jacobi M = diag(K)
+  CU(cudaMemsetAsync(delta, 0, size_t(n) * 8, st));
+  CU(cudaMemcpyAsync(r, m->R, size_t(n) * 8, cudaMemcpyDeviceToDevice, st));
+  CU(cudaMemcpyAsync(r0, m->R, size_t(n) * 8, cudaMemcpyDeviceToDevice, st));
+  CU(cudaMemsetAsync(p, 0, size_t(n) * 8, st));
+  CU(cudaMemsetAsync(v, 0, size_t(n) * 8, st));
+  k_invdiag<<<ge, 256, 0, st>>>(n, m->row_ptr, m->col_idx, m->val, dinv);
+  ++m->launches;
+  double h[2];
+  lgdm_status s = dots(r, r, nullptr, nullptr, h);
+  if (s != LGDM_OK) return s;
+  const double bnorm = std::sqrt(h[0]);
+  int it = 0;
+  double rel = 0.0;
+  if (bnorm == 0.0) {
+    if (iters_out) *iters_out = 0;
+    if (relres_out) *relres_out = 0.0;
+    return LGDM_OK;
+  }
+  double rho = 1.0, alpha = 1.0, omega = 1.0;
+  rel = 1.0;
+  for (it = 1; it <= max_iter; ++it) {
+    if ((s = dots(r0, r, nullptr, nullptr, h)) != LGDM_OK) return s;
+    const double rho_new = h[0];
+    if (rho_new == 0.0 || omega == 0.0) break;   // breakdown
+    const double beta = (rho_new / rho) * (alpha / omega);
+    k_p_update<<<ge, 256, 0, st>>>(n, beta, omega, r, v, p);
+    k_scale_mul<<<ge, 256, 0, st>>>(n, dinv, p, ph);
+    k_spmv<<<gw, 256, 0, st>>>(n, m->row_ptr, m->col_idx, m->val, ph, v);
+    m->launches += 3;
+    if ((s = dots(r0, v, nullptr, nullptr, h)) != LGDM_OK) return s;
+    if (h[0] == 0.0) break;
+    alpha = rho_new / h[0];
+    k_s_update<<<ge, 256, 0, st>>>(n, alpha, r, v, sv);
+    ++m->launches;
+    if ((s = dots(sv, sv, nullptr, nullptr, h)) != LGDM_OK) return s;
+    if (std::sqrt(h[0]) / bnorm <= tol) {
+      k_axpy<<<ge, 256, 0, st>>>(n, alpha, ph, delta);
+      ++m->launches;
+      rel = std::sqrt(h[0]) / bnorm;
+      break;
+    }
+    k_scale_mul<<<ge, 256, 0, st>>>(n, dinv, sv, sh);
+    k_spmv<<<gw, 256, 0, st>>>(n, m->row_ptr, m->col_idx, m->val, sh, t);
+    m->launches += 2;
+    if ((s = dots(t, sv, t, t, h)) != LGDM_OK) return s;
+    omega = h[1] != 0.0 ? h[0] / h[1] : 0.0;
+    k_x_update<<<ge, 256, 0, st>>>(n, alpha, omega, ph, sh, delta);
+    k_r_update<<<ge, 256, 0, st>>>(n, omega, sv, t, r);
+    m->launches += 2;
+    if ((s = dots(r, r, nullptr, nullptr, h)) != LGDM_OK) return s;
+    rel = std::sqrt(h[0]) / bnorm;
+    if (rel <= tol) break;
+    rho = rho_new;
+  }
+  // true residual of the returned delta (||b - K delta|| / ||b||)
+  k_spmv<<<gw, 256, 0, st>>>(n, m->row_ptr, m->col_idx, m->val, delta, t);
+  k_s_update<<<ge, 256, 0, st>>>(n, 1.0, m->R, t, sv);
+  m->launches += 2;
+  if ((s = dots(sv, sv, nullptr, nullptr, h)) != LGDM_OK) return s;
+  rel = std::sqrt(h[0]) / bnorm;
+  if (iters_out) *iters_out = std::min(it, max_iter);
+  if (relres_out) *relres_out = rel;
+  if (!(rel <= 10.0 * tol))
+    return fail(LGDM_ERR_NOT_CONVERGED, "BiCGSTAB: relative residual %.3e after %d iterations (tol %.1e)", rel, std::min(it, max_iter), tol);
+  return LGDM_OK;
+}
+
+lgdm_status lgdm_add_dofs(lgdm_mesh m, const double* delta, double alpha) {
+  if (!m || !delta) return fail(LGDM_ERR_INVALID_ARGUMENT, "mesh / delta is NULL");
+  if (!m->have_state) return fail(LGDM_ERR_INVALID_STATE, "add_dofs before set_state");
+  if (!whole_single_rank(m)) return fail(LGDM_ERR_UNSUPPORTED, "Newton pieces need a single-rank whole mesh");
+  CU(cudaSetDevice(m->device));
+  const int64_t n = m->n_nodes * m->f.ndpn;
+  k_axpy<<<unsigned((n + 255) / 256), 256, 0, m->stream>>>(n, alpha, delta, m->dofs);
+  return check_launch(m, "k_axpy");
+}
+
+lgdm_status lgdm_delta_norms(lgdm_mesh m, const double* delta, double out4[4]) {
+  if (!m || !delta || !out4) return fail(LGDM_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (!m->have_state) return fail(LGDM_ERR_INVALID_STATE, "delta_norms before set_state");
+  if (!whole_single_rank(m)) return fail(LGDM_ERR_UNSUPPORTED, "Newton pieces need a single-rank whole mesh");
+  CU(cudaSetDevice(m->device));
+  if (!m->sol_part) {
+    CU(dalloc(&m->sol_part, size_t(kRedBlocks) * 4 + 4));
+    m->device_bytes += kRedBlocks * 32 + 32;
+  }
+  const int64_t n = m->n_nodes * m->f.ndpn;
+  double* part = m->sol_part;
+  double* fin = part + size_t(kRedBlocks) * 4;
+  if (m->f.ndpn == 2) k_delta_sumsq<2><<<kRedBlocks, 256, 0, m->stream>>>(n, delta, m->dofs, part);
+  else if (m->f.ndpn == 3) k_delta_sumsq<3><<<kRedBlocks, 256, 0, m->stream>>>(n, delta, m->dofs, part);
+  else k_delta_sumsq<4><<<kRedBlocks, 256, 0, m->stream>>>(n, delta, m->dofs, part);
+  k_final<4><<<1, 256, 0, m->stream>>>(kRedBlocks, part, fin);
+  m->launches += 2;
+  CU(cudaMemcpyAsync(out4, fin, 32, cudaMemcpyDeviceToHost, m->stream));
+  CU(cudaStreamSynchronize(m->stream));
+  return LGDM_OK;
+}
+
 lgdm_status lgdm_residual_sumsq(lgdm_mesh m, double* out2, int on_device) {
   if (!m || !out2) return fail(LGDM_ERR_INVALID_ARGUMENT, "NULL argument");
   if (!m->assembled) return fail(LGDM_ERR_INVALID_STATE, "residual before assemble");
@@ -800,7 +969,7 @@ void lgdm_destroy(lgdm_mesh m) {
   void* ptrs[] = {m->coords, m->conn, m->dofs, m->kappa, m->row_ptr, m->col_idx, m->val, m->R,
                   m->nbr_ptr, m->base, m->adj_ptr, m->adj, m->scratchK, m->scratchF,
                   m->sumsq_part, m->sumsq_out, m->k0g, m->alg, m->sdv_dev, m->rp_b,
-                  m->ci_b, m->val_b, m->R_b};
+                  m->ci_b, m->val_b, m->R_b, m->sol, m->sol_part, m->fixed, m->fixinc};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (m->host_pinned) cudaFreeHost(m->host_pinned);

@@ -21,7 +21,7 @@ KERNEL_AUTO, KERNEL_GENERAL, KERNEL_SWEEP, KERNEL_SWEEP3, KERNEL_SWEEP4, KERNEL_
 
 STATUS = {0: "LGDM_OK", 1: "LGDM_ERR_INVALID_ARGUMENT", 2: "LGDM_ERR_INVERTED_ELEMENT",
           3: "LGDM_ERR_INVALID_STATE", 4: "LGDM_ERR_OUT_OF_MEMORY", 5: "LGDM_ERR_CUDA",
-          6: "LGDM_ERR_NCCL", 7: "LGDM_ERR_UNSUPPORTED"}
+          6: "LGDM_ERR_NCCL", 7: "LGDM_ERR_UNSUPPORTED", 8: "LGDM_ERR_NOT_CONVERGED"}
 
 # every symbol include/lgdm.h declares
 EXPORTS = ["lgdm_create_mesh", "lgdm_set_state", "lgdm_assemble", "lgdm_update_history",
@@ -29,7 +29,8 @@ EXPORTS = ["lgdm_create_mesh", "lgdm_set_state", "lgdm_assemble", "lgdm_update_h
            "lgdm_get_kappa",
            "lgdm_scale_dofs", "lgdm_set_kernel", "lgdm_get_info", "lgdm_launch_count",
            "lgdm_last_error", "lgdm_destroy", "lgdm_sdv_width", "lgdm_set_defects",
-           "lgdm_update_state", "lgdm_get_blocked"]
+           "lgdm_update_state", "lgdm_get_blocked", "lgdm_apply_dirichlet", "lgdm_solve",
+           "lgdm_add_dofs", "lgdm_delta_norms"]
 
 
 class LGDMError(RuntimeError):
@@ -94,6 +95,10 @@ def load() -> C.CDLL:
     L.lgdm_set_defects.argtypes = [vp, vp, vp, i64, C.c_int]
     L.lgdm_update_state.argtypes = [vp, vp, i64, C.c_int]
     L.lgdm_get_blocked.argtypes = [vp, C.POINTER(CSR), C.POINTER(vp)]
+    L.lgdm_apply_dirichlet.argtypes = [vp, i64, vp, vp]
+    L.lgdm_solve.argtypes = [vp, vp, C.c_double, C.c_int, C.POINTER(C.c_int), dp]
+    L.lgdm_add_dofs.argtypes = [vp, vp, C.c_double]
+    L.lgdm_delta_norms.argtypes = [vp, vp, dp]
     for name in EXPORTS:
         if name not in ("lgdm_launch_count", "lgdm_last_error", "lgdm_destroy"):
             getattr(L, name).restype = C.c_int
@@ -201,6 +206,33 @@ class Mesh:
                     R=DeviceArray(r.value, csr.n_rows, "<f8", self),
                     first_row=csr.first_row, n_cols=csr.n_cols, n_rows=csr.n_rows, nnz=csr.nnz)
 
+    # -- Newton loop pieces --------------------------------------------
+    def apply_dirichlet(self, dof_ids, increments):
+        ids = np.ascontiguousarray(dof_ids, dtype=np.int64)
+        inc = np.ascontiguousarray(increments, dtype=np.float64)
+        _check(load().lgdm_apply_dirichlet(self._h, ids.size, ids.ctypes.data if ids.size else None,
+                                           inc.ctypes.data if inc.size else None))
+
+    def solve(self, tol=1e-12, max_iter=10000, out=None):
+        """BiCGSTAB on the assembled (eliminated) system; returns (delta device tensor, iters,
+        relative residual)."""
+        import torch
+        n = self.n_nodes * self.ndpn
+        if out is None:
+            out = torch.empty(n, dtype=torch.float64, device=f"cuda:{self.device}")
+        it = C.c_int()
+        rr = C.c_double()
+        _check(load().lgdm_solve(self._h, out.data_ptr(), tol, max_iter, C.byref(it), C.byref(rr)))
+        return out, it.value, rr.value
+
+    def add_dofs(self, delta, alpha=1.0):
+        _check(load().lgdm_add_dofs(self._h, delta.data_ptr(), alpha))
+
+    def delta_norms(self, delta):
+        out = np.zeros(4)
+        _check(load().lgdm_delta_norms(self._h, delta.data_ptr(), out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
     def get_blocked(self):
         """K, R of the last assemble in the blocked DOF order [u; ebar] (zero-copy views)."""
         csr = CSR()
@@ -297,3 +329,36 @@ class Mesh:
 def sdv_width(etype: int) -> int:
     """doubles per (element, GP) record of Mesh.update_state (include/lgdm.h)"""
     return load().lgdm_sdv_width(etype)
+
+
+def newton(mesh: "Mesh", fixed_dofs, step_increment, n_steps: int, tol: float = 1e-4,
+           max_iter: int = 25, solver_tol: float = 1e-12):
+    """Incremental-iterative Newton driver of Alg. 2 (orchestration only --
+    every computation is a library call on the GPU): for each of n_steps load steps, iterate
+    assemble (trial kappa against the committed history) -> eliminate the constraints
+    (increment on the first iteration, 0 after) -> solve -> dofs += delta until
+    ||du||/||u|| and ||de||/||e|| <= tol (Alg. 2 l.16), then commit the history.  Returns one
+    dict per step (iterations, final ratios, solver iterations).  Raises LGDMError if a step does
+    not converge in max_iter iterations."""
+    fixed = np.ascontiguousarray(fixed_dofs, dtype=np.int64)
+    inc = np.broadcast_to(np.asarray(step_increment, dtype=np.float64), fixed.shape).copy()
+    zero = np.zeros_like(inc)
+    log = []
+    for step in range(n_steps):
+        for it in range(1, max_iter + 1):
+            mesh.assemble()
+            mesh.apply_dirichlet(fixed, inc if it == 1 else zero)
+            delta, sit, rr = mesh.solve(tol=solver_tol)
+            mesh.add_dofs(delta)
+            du2, u2, de2, e2 = mesh.delta_norms(delta)
+            ru = np.sqrt(du2) / max(np.sqrt(u2), 1e-16)
+            re = np.sqrt(de2) / max(np.sqrt(e2), 1e-16)
+            if ru <= tol and re <= tol:
+                break
+        else:
+            raise LGDMError(8, f"Newton step {step}: not converged in {max_iter} iterations "
+                               f"(|du|/|u| = {ru:.3e}, |de|/|e| = {re:.3e})")
+        mesh.update_history()
+        log.append(dict(step=step, iterations=it, ratio_u=ru, ratio_e=re, solver_iters=sit,
+                        solver_relres=rr))
+    return log
