@@ -414,6 +414,14 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
               PT_MARK(15, tid == 0);
               for (int cc = NCC + warp; cc < cols; cc += S4::NPC) flush_col(s - 1, cc);
               barrive(S4::B_FL, FL_T);
+              // CSR offsets of node layer s+1 for flush(s) (slot (s+1) % 3 was last read by
+              // flush(s-2), done); issued after the hand-off so the load latency stays off the
+              // C warps' path; visible to them through B_AD / B_FL of the next layer
+              if (pair == 0 && s + 1 >= z0 && s + 1 < z1)
+                for (int cc = (warp & 1) * 32 + lane; cc < cols; cc += NPC_T) {
+                  const int cy = cc / cols_x;
+                  sbase[(s + 1) % 3][cc] = base[node_id(ix0 + (cc - cy * cols_x), iy0 + cy, s + 1) - G.own_node_b];
+                }
               PT_MARK(14, tid == 0);
             }
           }
@@ -473,15 +481,6 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
         const int cslot = t & 1;
         ++t;
         const bool wait_flush = prev_c < 0 && s > s_first;   // PC part of flush(s - 1)
-        if (prev_c < 0 && s > s_first) {
-          // first batch of element layer s: CSR offsets of node layer s+1 (for flush(s); slot
-          // (s+1) % 3 was last read by flush(s-2), finished before the adds of layer s-1)
-          for (int cc = ct; cc < cols; cc += NC_T) {
-            const int cy = cc / cols_x;
-            if (s + 1 >= z0 && s + 1 < z1)
-              sbase[(s + 1) % 3][cc] = base[node_id(ix0 + (cc - cy * cols_x), iy0 + cy, s + 1) - G.own_node_b];
-          }
-        }
         PT_MARK(9, ptc);
         bsync(S4::B_CF + cslot, NPC_T + NC_T);
         PT_MARK(0, ptc);
