@@ -183,6 +183,11 @@ lgdm_status lgdm_apply_dirichlet(lgdm_mesh mesh, int64_t n_fixed, const int64_t*
 lgdm_status lgdm_solve(lgdm_mesh mesh, double* delta, double tol, int max_iter, int* iters,
                        double* relres);
 
+/* Reaction of a displacement-controlled problem (the load of the paper's load-displacement
+ * curves, Fig. 11 / P:418; SPEC reaction_force): -sum of the last assembled R over the listed
+ * dofs (host ids), to be called after lgdm_assemble and BEFORE lgdm_apply_dirichlet.  Host out. */
+lgdm_status lgdm_reaction(lgdm_mesh mesh, int64_t n, const int64_t* dof_ids, double* out);
+
 /* dofs += alpha * delta (delta device, n_nodes * ndpn doubles; Alg. 2 l.7). */
 lgdm_status lgdm_add_dofs(lgdm_mesh mesh, const double* delta, double alpha);
 

@@ -363,3 +363,11 @@ def newton_iteration(etype: int, m: Material, coords, conn, dofs, kappa_hist, fi
     sys_ = apply_dirichlet(res, fixed, incr)
     delta = solve(sys_)
     return delta, np.asarray(dofs, dtype=np.float64).reshape(-1) + delta
+
+
+def reaction(res: dict, dof_ids):
+    """Reaction at the driven dofs (SPEC reaction_force; the load of the paper's
+    load-displacement curves, Fig. 11 / P:418): the internal force sum_i int B^T sigma over the
+    listed u dofs of the UNCONSTRAINED assembled system, i.e. -sum R_i (R = F of Eq. 11 has no
+    external load in a displacement-controlled problem)."""
+    return -float(np.sum(np.asarray(res["R"])[np.asarray(dof_ids, dtype=np.int64)]))

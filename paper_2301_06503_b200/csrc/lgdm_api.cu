@@ -819,6 +819,25 @@ lgdm_status lgdm_solve(lgdm_mesh m, double* delta, double tol, int max_iter, int
   return LGDM_OK;
 }
 
+lgdm_status lgdm_reaction(lgdm_mesh m, int64_t n, const int64_t* dof_ids, double* out) {
+  if (!m || !out || (n > 0 && !dof_ids)) return fail(LGDM_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (!m->assembled) return fail(LGDM_ERR_INVALID_STATE, "reaction before assemble");
+  if (!whole_single_rank(m)) return fail(LGDM_ERR_UNSUPPORTED, "Newton pieces need a single-rank whole mesh");
+  for (int64_t k = 0; k < n; ++k)
+    if (dof_ids[k] < 0 || dof_ids[k] >= m->n_rows) return fail(LGDM_ERR_INVALID_ARGUMENT, "dof id out of range");
+  CU(cudaSetDevice(m->device));
+  int64_t* ids = nullptr;
+  CU(dalloc(&ids, size_t(std::max<int64_t>(n, 1)) + 1));   // + 1 double-sized slot for the sum
+  double* sum = reinterpret_cast<double*>(ids + std::max<int64_t>(n, 1));
+  if (n) CU(cudaMemcpyAsync(ids, dof_ids, size_t(n) * 8, cudaMemcpyHostToDevice, m->stream));
+  k_reaction<<<1, 256, 0, m->stream>>>(n, ids, m->R, sum);
+  ++m->launches;
+  CU(cudaMemcpyAsync(out, sum, 8, cudaMemcpyDeviceToHost, m->stream));
+  CU(cudaStreamSynchronize(m->stream));
+  cudaFree(ids);
+  return LGDM_OK;
+}
+
 lgdm_status lgdm_add_dofs(lgdm_mesh m, const double* delta, double alpha) {
   if (!m || !delta) return fail(LGDM_ERR_INVALID_ARGUMENT, "mesh / delta is NULL");
   if (!m->have_state) return fail(LGDM_ERR_INVALID_STATE, "add_dofs before set_state");

@@ -156,4 +156,12 @@ __global__ void k_delta_sumsq(int64_t n, const double* __restrict__ delta,
   block_sum_store<4>(v, part);
 }
 
+// reaction: -sum of R over listed dofs, one block, fixed order
+__global__ void k_reaction(int64_t n, const int64_t* __restrict__ ids, const double* __restrict__ R,
+                           double* __restrict__ out) {
+  double v[1] = {0.0};
+  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) v[0] -= R[ids[k]];
+  block_sum_store<1>(v, out);
+}
+
 }  // namespace lgdm

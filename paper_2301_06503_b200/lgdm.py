@@ -30,7 +30,7 @@ EXPORTS = ["lgdm_create_mesh", "lgdm_set_state", "lgdm_assemble", "lgdm_update_h
            "lgdm_scale_dofs", "lgdm_set_kernel", "lgdm_get_info", "lgdm_launch_count",
            "lgdm_last_error", "lgdm_destroy", "lgdm_sdv_width", "lgdm_set_defects",
            "lgdm_update_state", "lgdm_get_blocked", "lgdm_apply_dirichlet", "lgdm_solve",
-           "lgdm_add_dofs", "lgdm_delta_norms"]
+           "lgdm_add_dofs", "lgdm_delta_norms", "lgdm_reaction"]
 
 
 class LGDMError(RuntimeError):
@@ -99,6 +99,7 @@ def load() -> C.CDLL:
     L.lgdm_solve.argtypes = [vp, vp, C.c_double, C.c_int, C.POINTER(C.c_int), dp]
     L.lgdm_add_dofs.argtypes = [vp, vp, C.c_double]
     L.lgdm_delta_norms.argtypes = [vp, vp, dp]
+    L.lgdm_reaction.argtypes = [vp, i64, vp, dp]
     for name in EXPORTS:
         if name not in ("lgdm_launch_count", "lgdm_last_error", "lgdm_destroy"):
             getattr(L, name).restype = C.c_int
@@ -225,6 +226,13 @@ class Mesh:
         _check(load().lgdm_solve(self._h, out.data_ptr(), tol, max_iter, C.byref(it), C.byref(rr)))
         return out, it.value, rr.value
 
+    def reaction(self, dof_ids):
+        ids = np.ascontiguousarray(dof_ids, dtype=np.int64)
+        out = C.c_double()
+        _check(load().lgdm_reaction(self._h, ids.size, ids.ctypes.data if ids.size else None,
+                                    C.byref(out)))
+        return out.value
+
     def add_dofs(self, delta, alpha=1.0):
         _check(load().lgdm_add_dofs(self._h, delta.data_ptr(), alpha))
 
@@ -337,13 +345,15 @@ def newton(mesh: "Mesh", fixed_dofs, step_increment, n_steps: int, tol: float = 
     every computation is a library call on the GPU): for each of n_steps load steps, iterate
     assemble (trial kappa against the committed history) -> eliminate the constraints
     (increment on the first iteration, 0 after) -> solve -> dofs += delta until
-    ||du||/||u|| and ||de||/||e|| <= tol (Alg. 2 l.16), then commit the history.  Returns one
-    dict per step (iterations, final ratios, solver iterations).  Raises LGDMError if a step does
+    ||du||/||u|| and ||de||/||e|| <= tol (Alg. 2 l.16), then record the reaction at the driven
+    dofs (nonzero increments) and commit the history.  Returns one dict per step (iterations,
+    final ratios, solver iterations, reaction).  Raises LGDMError if a step does
     not converge in max_iter iterations."""
     fixed = np.ascontiguousarray(fixed_dofs, dtype=np.int64)
     inc = np.broadcast_to(np.asarray(step_increment, dtype=np.float64), fixed.shape).copy()
     zero = np.zeros_like(inc)
     log = []
+    driven = fixed[inc != 0.0]
     for step in range(n_steps):
         for it in range(1, max_iter + 1):
             mesh.assemble()
@@ -358,7 +368,9 @@ def newton(mesh: "Mesh", fixed_dofs, step_increment, n_steps: int, tol: float = 
         else:
             raise LGDMError(8, f"Newton step {step}: not converged in {max_iter} iterations "
                                f"(|du|/|u| = {ru:.3e}, |de|/|e| = {re:.3e})")
+        mesh.assemble()                       # converged state: reaction at the driven dofs
+        react = mesh.reaction(driven)
         mesh.update_history()
         log.append(dict(step=step, iterations=it, ratio_u=ru, ratio_e=re, solver_iters=sit,
-                        solver_relres=rr))
+                        solver_relres=rr, reaction=react))
     return log

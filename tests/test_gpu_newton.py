@@ -73,6 +73,11 @@ def test_elastic_bar_newton_exact():
     m.set_state(np.zeros(2 * (n + 1)), np.zeros(2 * n))
     log = lgdm.newton(m, ids, [0.0, 1e-4], n_steps=3, tol=1e-8)
     assert all(s["iterations"] <= 2 for s in log)
+    # SPEC: kappa0 huge -> reaction history exactly linear, R_n = E A u_n / L
+    Lb = mesh.coords[-1, 0] - mesh.coords[0, 0]
+    EA = synth.MATERIAL["E"] * synth.MATERIAL["t"]
+    for st, rec in enumerate(log):
+        assert rec["reaction"] == pytest.approx(EA * 1e-4 * (st + 1) / Lb, rel=1e-9)
     import torch
     torch.cuda.synchronize()
     # current dofs: from the mesh via update_state (ebar) -- read u through a fresh assemble
@@ -98,7 +103,7 @@ def test_damage_newton_matches_oracle():
     om = oracle.material(**mat)
     dofs = np.zeros(nd)
     kh = kap0.copy()
-    its_ref = []
+    its_ref, react_ref = [], []
     for step in range(2):
         for it in range(1, 26):
             delta, dofs = oracle.newton_iteration(etype, om, mesh.coords, mesh.conn, dofs, kh, ids,
@@ -107,10 +112,13 @@ def test_damage_newton_matches_oracle():
             if ok:
                 break
         its_ref.append(it)
+        react_ref.append(oracle.reaction(oracle.assemble(etype, om, mesh.coords, mesh.conn, dofs, kh),
+                                         ids[inc != 0]))
         kh = oracle.update_history(etype, mesh.conn, dofs, kh).reshape(-1)
     m = lgdm.Mesh(etype, mesh.coords, mesh.conn, lgdm.material(**mat))
     m.set_state(np.zeros(nd), kap0)
     log = lgdm.newton(m, ids, inc, n_steps=2, tol=1e-6)
     assert [s["iterations"] for s in log] == its_ref
+    np.testing.assert_allclose([s["reaction"] for s in log], react_ref, rtol=1e-7)
     np.testing.assert_allclose(m.get_kappa().reshape(-1), kh, rtol=1e-8, atol=1e-14)
     m.close()

@@ -86,3 +86,21 @@ def test_convergence_check_examples():
     d[0] = 2e-4 * np.linalg.norm(u.reshape(-1, 3)[:, :2])
     assert not oracle.converged(et, d, u, 1e-4)[0]
     assert oracle.converged(et, np.zeros(12), np.zeros(12), 1e-4)[0]     # floor guard
+
+
+def test_reaction_elastic_bar():
+    """SPEC reaction_force example: elastic 1D bar, applied end displacement u -> E A u / L"""
+    n = 10
+    cfg, mesh, m = _bar(n)
+    L = mesh.coords[-1, 0] - mesh.coords[0, 0]
+    dofs = np.zeros(2 * (n + 1))
+    kap = np.zeros(2 * n)
+    d = 2e-4
+    _, new = oracle.newton_iteration(oracle.BAR2, m, mesh.coords, mesh.conn, dofs, kap, [0, 2 * n],
+                                     [0.0, d])
+    res = oracle.assemble(oracle.BAR2, m, mesh.coords, mesh.conn, new, kap)
+    E, A = synth.MATERIAL["E"], synth.MATERIAL["t"]
+    assert oracle.reaction(res, [2 * n]) == pytest.approx(E * A * d / L, rel=1e-10)
+    assert oracle.reaction(res, [0]) == pytest.approx(-E * A * d / L, rel=1e-10)
+    assert oracle.reaction(oracle.assemble(oracle.BAR2, m, mesh.coords, mesh.conn, dofs, kap),
+                           [2 * n]) == 0.0
