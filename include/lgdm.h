@@ -183,6 +183,13 @@ lgdm_status lgdm_apply_dirichlet(lgdm_mesh mesh, int64_t n_fixed, const int64_t*
 lgdm_status lgdm_solve(lgdm_mesh mesh, double* delta, double tol, int max_iter, int* iters,
                        double* relres);
 
+/* Direct solve of K delta = R on the GPU (the paper's `mldivide`): sparse QR of
+ * cuSOLVER (cusolverSpDcsrlsvqr with symrcm reordering; libcusolver / libcusparse dlopen'ed,
+ * missing -> LGDM_ERR_UNSUPPORTED; nnz >= 2^31 -> LGDM_ERR_UNSUPPORTED).  delta device;
+ * singularity (host, nullable) = -1 or the first rank-deficient pivot, in which case
+ * LGDM_ERR_NOT_CONVERGED is returned.  Synchronises the mesh stream. */
+lgdm_status lgdm_solve_direct(lgdm_mesh mesh, double* delta, int* singularity);
+
 /* Reaction of a displacement-controlled problem (the load of the paper's load-displacement
  * curves, Fig. 11 / P:418; SPEC reaction_force): -sum of the last assembled R over the listed
  * dofs (host ids), to be called after lgdm_assemble and BEFORE lgdm_apply_dirichlet.  Host out. */

@@ -20,6 +20,7 @@
 #include "../../include/lgdm.h"
 #include "lgdm_kernels.cuh"
 #include "lgdm_solver.cuh"
+#include <cusolverSp.h>
 
 using namespace lgdm;
 
@@ -56,6 +57,41 @@ struct NcclApi {
   const char* (*getErrorString)(ncclResult_t) = nullptr;
 };
 NcclApi g_nccl;
+
+// cuSOLVER sparse QR (the direct solve of lgdm_solve_direct), dlopen'ed like NCCL: types from
+// the headers only, no link-time dependency
+struct SpSolverApi {
+  bool loaded = false;
+  cusolverStatus_t (*create)(cusolverSpHandle_t*);
+  cusolverStatus_t (*destroy)(cusolverSpHandle_t);
+  cusolverStatus_t (*setStream)(cusolverSpHandle_t, cudaStream_t);
+  cusolverStatus_t (*lsvqr)(cusolverSpHandle_t, int, int, const cusparseMatDescr_t, const double*,
+                            const int*, const int*, const double*, double, int, double*, int*);
+  cusparseStatus_t (*createDescr)(cusparseMatDescr_t*);
+  cusparseStatus_t (*destroyDescr)(cusparseMatDescr_t);
+  cusparseStatus_t (*setType)(cusparseMatDescr_t, cusparseMatrixType_t);
+  cusparseStatus_t (*setBase)(cusparseMatDescr_t, cusparseIndexBase_t);
+};
+SpSolverApi g_sps;
+bool load_spsolver() {
+  if (g_sps.loaded) return true;
+  void* hs = dlopen("libcusolver.so.11", RTLD_NOW | RTLD_GLOBAL);
+  if (!hs) hs = dlopen("libcusolver.so", RTLD_NOW | RTLD_GLOBAL);
+  void* hp = dlopen("libcusparse.so.12", RTLD_NOW | RTLD_GLOBAL);
+  if (!hp) hp = dlopen("libcusparse.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!hs || !hp) return false;
+  g_sps.create = (decltype(g_sps.create))dlsym(hs, "cusolverSpCreate");
+  g_sps.destroy = (decltype(g_sps.destroy))dlsym(hs, "cusolverSpDestroy");
+  g_sps.setStream = (decltype(g_sps.setStream))dlsym(hs, "cusolverSpSetStream");
+  g_sps.lsvqr = (decltype(g_sps.lsvqr))dlsym(hs, "cusolverSpDcsrlsvqr");
+  g_sps.createDescr = (decltype(g_sps.createDescr))dlsym(hp, "cusparseCreateMatDescr");
+  g_sps.destroyDescr = (decltype(g_sps.destroyDescr))dlsym(hp, "cusparseDestroyMatDescr");
+  g_sps.setType = (decltype(g_sps.setType))dlsym(hp, "cusparseSetMatType");
+  g_sps.setBase = (decltype(g_sps.setBase))dlsym(hp, "cusparseSetMatIndexBase");
+  g_sps.loaded = g_sps.create && g_sps.destroy && g_sps.setStream && g_sps.lsvqr && g_sps.createDescr &&
+                 g_sps.destroyDescr && g_sps.setType && g_sps.setBase;
+  return g_sps.loaded;
+}
 
 bool load_nccl() {
   if (g_nccl.loaded) return true;
@@ -835,6 +871,39 @@ lgdm_status lgdm_reaction(lgdm_mesh m, int64_t n, const int64_t* dof_ids, double
   CU(cudaMemcpyAsync(out, sum, 8, cudaMemcpyDeviceToHost, m->stream));
   CU(cudaStreamSynchronize(m->stream));
   cudaFree(ids);
+  return LGDM_OK;
+}
+
+lgdm_status lgdm_solve_direct(lgdm_mesh m, double* delta, int* singularity) {
+  if (!m || !delta) return fail(LGDM_ERR_INVALID_ARGUMENT, "mesh / delta is NULL");
+  if (!m->assembled) return fail(LGDM_ERR_INVALID_STATE, "solve before assemble");
+  if (!whole_single_rank(m)) return fail(LGDM_ERR_UNSUPPORTED, "Newton pieces need a single-rank whole mesh");
+  if (m->nnz > INT32_MAX || m->n_rows > INT32_MAX)
+    return fail(LGDM_ERR_UNSUPPORTED, "direct solve needs nnz < 2^31 (use lgdm_solve)");
+  if (!load_spsolver()) return fail(LGDM_ERR_UNSUPPORTED, "libcusolver / libcusparse not loadable");
+  CU(cudaSetDevice(m->device));
+  const int n = int(m->n_rows), nnz = int(m->nnz);
+  int32_t* rp32 = nullptr;
+  CU(dalloc(&rp32, size_t(n) + 1));
+  k_rowptr32<<<unsigned((n + 256) / 256), 256, 0, m->stream>>>(n + 1, m->row_ptr, rp32);
+  ++m->launches;
+  cusolverSpHandle_t h = nullptr;
+  cusparseMatDescr_t d = nullptr;
+  int sing = -1;
+  bool ok = g_sps.create(&h) == CUSOLVER_STATUS_SUCCESS && g_sps.setStream(h, m->stream) == CUSOLVER_STATUS_SUCCESS &&
+            g_sps.createDescr(&d) == CUSPARSE_STATUS_SUCCESS &&
+            g_sps.setType(d, CUSPARSE_MATRIX_TYPE_GENERAL) == CUSPARSE_STATUS_SUCCESS &&
+            g_sps.setBase(d, CUSPARSE_INDEX_BASE_ZERO) == CUSPARSE_STATUS_SUCCESS;
+  if (ok)
+    ok = g_sps.lsvqr(h, n, nnz, d, m->val, rp32, m->col_idx, m->R, 1e-14, 1, delta, &sing) ==
+         CUSOLVER_STATUS_SUCCESS;
+  if (d) g_sps.destroyDescr(d);
+  if (h) g_sps.destroy(h);
+  cudaStreamSynchronize(m->stream);
+  cudaFree(rp32);
+  if (singularity) *singularity = sing;
+  if (!ok) return fail(LGDM_ERR_CUDA, "cusolverSpDcsrlsvqr failed");
+  if (sing >= 0) return fail(LGDM_ERR_NOT_CONVERGED, "singular system (QR pivot %d)", sing);
   return LGDM_OK;
 }
 

@@ -164,4 +164,9 @@ __global__ void k_reaction(int64_t n, const int64_t* __restrict__ ids, const dou
   block_sum_store<1>(v, out);
 }
 
+__global__ void k_rowptr32(int64_t n, const int64_t* __restrict__ in, int32_t* __restrict__ out) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i < n) out[i] = int32_t(in[i]);
+}
+
 }  // namespace lgdm

@@ -30,7 +30,7 @@ EXPORTS = ["lgdm_create_mesh", "lgdm_set_state", "lgdm_assemble", "lgdm_update_h
            "lgdm_scale_dofs", "lgdm_set_kernel", "lgdm_get_info", "lgdm_launch_count",
            "lgdm_last_error", "lgdm_destroy", "lgdm_sdv_width", "lgdm_set_defects",
            "lgdm_update_state", "lgdm_get_blocked", "lgdm_apply_dirichlet", "lgdm_solve",
-           "lgdm_add_dofs", "lgdm_delta_norms", "lgdm_reaction"]
+           "lgdm_add_dofs", "lgdm_delta_norms", "lgdm_reaction", "lgdm_solve_direct"]
 
 
 class LGDMError(RuntimeError):
@@ -100,6 +100,7 @@ def load() -> C.CDLL:
     L.lgdm_add_dofs.argtypes = [vp, vp, C.c_double]
     L.lgdm_delta_norms.argtypes = [vp, vp, dp]
     L.lgdm_reaction.argtypes = [vp, i64, vp, dp]
+    L.lgdm_solve_direct.argtypes = [vp, vp, C.POINTER(C.c_int)]
     for name in EXPORTS:
         if name not in ("lgdm_launch_count", "lgdm_last_error", "lgdm_destroy"):
             getattr(L, name).restype = C.c_int
@@ -226,6 +227,16 @@ class Mesh:
         _check(load().lgdm_solve(self._h, out.data_ptr(), tol, max_iter, C.byref(it), C.byref(rr)))
         return out, it.value, rr.value
 
+    def solve_direct(self, out=None):
+        """Sparse QR on the GPU (cuSOLVER); returns the delta device tensor."""
+        import torch
+        n = self.n_nodes * self.ndpn
+        if out is None:
+            out = torch.empty(n, dtype=torch.float64, device=f"cuda:{self.device}")
+        sing = C.c_int()
+        _check(load().lgdm_solve_direct(self._h, out.data_ptr(), C.byref(sing)))
+        return out
+
     def reaction(self, dof_ids):
         ids = np.ascontiguousarray(dof_ids, dtype=np.int64)
         out = C.c_double()
@@ -340,11 +351,12 @@ def sdv_width(etype: int) -> int:
 
 
 def newton(mesh: "Mesh", fixed_dofs, step_increment, n_steps: int, tol: float = 1e-4,
-           max_iter: int = 25, solver_tol: float = 1e-12):
+           max_iter: int = 25, solver_tol: float = 1e-10, solver: str = "direct"):
     """Incremental-iterative Newton driver of Alg. 2 (orchestration only --
     every computation is a library call on the GPU): for each of n_steps load steps, iterate
     assemble (trial kappa against the committed history) -> eliminate the constraints
-    (increment on the first iteration, 0 after) -> solve -> dofs += delta until
+    (increment on the first iteration, 0 after) -> solve (sparse QR on the GPU as the paper's
+    mldivide, or solver="bicgstab") -> dofs += delta until
     ||du||/||u|| and ||de||/||e|| <= tol (Alg. 2 l.16), then record the reaction at the driven
     dofs (nonzero increments) and commit the history.  Returns one dict per step (iterations,
     final ratios, solver iterations, reaction).  Raises LGDMError if a step does
@@ -358,7 +370,10 @@ def newton(mesh: "Mesh", fixed_dofs, step_increment, n_steps: int, tol: float = 
         for it in range(1, max_iter + 1):
             mesh.assemble()
             mesh.apply_dirichlet(fixed, inc if it == 1 else zero)
-            delta, sit, rr = mesh.solve(tol=solver_tol)
+            if solver == "direct":
+                delta, sit, rr = mesh.solve_direct(), 0, 0.0
+            else:
+                delta, sit, rr = mesh.solve(tol=solver_tol)
             mesh.add_dofs(delta)
             du2, u2, de2, e2 = mesh.delta_norms(delta)
             ru = np.sqrt(du2) / max(np.sqrt(u2), 1e-16)

@@ -40,6 +40,24 @@ def _fixed_left_right(etype, mesh):
 
 
 @pytest.mark.parametrize("etype,n", [(lgdm.BAR2, (9,)), (lgdm.QUAD4, (6, 4)), (lgdm.HEX8, (3, 2, 2))])
+def test_direct_solve_parity(etype, n):
+    """sparse QR on the GPU (the paper's mldivide) against scipy's direct solve"""
+    cfg, mesh, d, k, mat = _problem(etype, n)
+    ids, inc = _fixed_left_right(etype, mesh)
+    inc = inc * 1e-4
+    ref = oracle.assemble(etype, oracle.material(**mat), mesh.coords, mesh.conn, d, k)
+    dref = oracle.solve(oracle.apply_dirichlet(ref, ids, inc))
+    m = lgdm.Mesh(etype, mesh.coords, mesh.conn, lgdm.material(**mat))
+    m.set_state(d, k)
+    m.assemble()
+    m.apply_dirichlet(ids, inc)
+    dg = m.solve_direct().cpu().numpy()
+    np.testing.assert_allclose(dg, dref, rtol=0, atol=1e-10 * np.abs(dref).max())
+    np.testing.assert_allclose(dg[ids], inc, rtol=0, atol=1e-12 * np.abs(inc).max())
+    m.close()
+
+
+@pytest.mark.parametrize("etype,n", [(lgdm.BAR2, (9,)), (lgdm.QUAD4, (6, 4)), (lgdm.HEX8, (3, 2, 2))])
 def test_dirichlet_and_solve_parity(etype, n):
     import torch
     cfg, mesh, d, k, mat = _problem(etype, n)
@@ -89,7 +107,8 @@ def test_elastic_bar_newton_exact():
     m.close()
 
 
-def test_damage_newton_matches_oracle():
+@pytest.mark.parametrize("solver", ["direct", "bicgstab"])
+def test_damage_newton_matches_oracle(solver):
     """two displacement steps into damage on a small Q4 strip: GPU Newton iterates equal the
     oracle's (direct solve) within the solver tolerance"""
     import torch
@@ -117,8 +136,63 @@ def test_damage_newton_matches_oracle():
         kh = oracle.update_history(etype, mesh.conn, dofs, kh).reshape(-1)
     m = lgdm.Mesh(etype, mesh.coords, mesh.conn, lgdm.material(**mat))
     m.set_state(np.zeros(nd), kap0)
-    log = lgdm.newton(m, ids, inc, n_steps=2, tol=1e-6)
+    log = lgdm.newton(m, ids, inc, n_steps=2, tol=1e-6, solver=solver)
     assert [s["iterations"] for s in log] == its_ref
     np.testing.assert_allclose([s["reaction"] for s in log], react_ref, rtol=1e-7)
     np.testing.assert_allclose(m.get_kappa().reshape(-1), kh, rtol=1e-8, atol=1e-14)
+    m.close()
+
+
+def test_softening_bar_matches_oracle():
+    """The paper's 1D bar setting (Sec. 3.1: displacement control, defect region in the
+    middle; equal-order elements here): load up to the peak and into softening.
+    Per step the GPU Newton loop (direct solve) takes the oracle's iteration count and reaches
+    its reaction; the history kappa agrees; the reaction peaks and then decays (softening) and
+    damage localises in the defect region."""
+    etype, n = lgdm.BAR2, 100
+    cfg = synth.small_config(etype, (n,))
+    mesh = synth.structured_mesh(cfg)
+    mat = dict(synth.MATERIAL)
+    L = mesh.coords[-1, 0] - mesh.coords[0, 0]
+    xc = mesh.coords[mesh.conn, 0].mean(axis=1)
+    defect = np.abs(xc - (mesh.coords[0, 0] + L / 2)) < 0.05 * L
+    k0g = np.repeat(np.where(defect, 0.9, 1.0) * mat["kappa0"], 2)
+    ids = np.array([0, 2 * n])
+    # 8 steps of 1e-3 (elastic: below the defect's damage threshold), 30 of 1e-4
+    schedule = [(8, 1e-3), (30, 1e-4)]
+    om = oracle.material(**mat)
+    nd = 2 * (n + 1)
+    dofs, kh = np.zeros(nd), np.zeros(2 * n)
+    its_ref, react_ref = [], []
+    for nst, du in schedule:
+        inc = np.array([0.0, du])
+        for _ in range(nst):
+            for it in range(1, 41):
+                res = oracle.assemble(etype, om, mesh.coords, mesh.conn, dofs, kh, kappa0_gp=k0g)
+                delta = oracle.solve(oracle.apply_dirichlet(res, ids, inc if it == 1 else 0 * inc))
+                dofs = dofs + delta
+                ok, _, _ = oracle.converged(etype, delta, dofs, 1e-6)
+                if ok:
+                    break
+            assert ok
+            its_ref.append(it)
+            res = oracle.assemble(etype, om, mesh.coords, mesh.conn, dofs, kh, kappa0_gp=k0g)
+            react_ref.append(oracle.reaction(res, [2 * n]))
+            kh = oracle.update_history(etype, mesh.conn, dofs, kh).reshape(-1)
+    m = lgdm.Mesh(etype, mesh.coords, mesh.conn, lgdm.material(**mat))
+    m.set_state(np.zeros(nd), np.zeros(2 * n))
+    m.set_defects(k0g, None)
+    log = []
+    for nst, du in schedule:
+        log += lgdm.newton(m, ids, [0.0, du], n_steps=nst, tol=1e-6, max_iter=40)
+    assert [s["iterations"] for s in log] == its_ref
+    r = np.array([s["reaction"] for s in log])
+    np.testing.assert_allclose(r, react_ref, rtol=1e-7)
+    kap = m.get_kappa().reshape(-1)
+    np.testing.assert_allclose(kap, kh, rtol=1e-7, atol=1e-14)
+    ip = int(r.argmax())
+    assert 8 <= ip < len(r) - 5                  # peak inside the fine steps, then softening
+    assert np.all(np.diff(r[ip:]) < 0)
+    kel = kap.reshape(n, 2).max(axis=1)
+    assert kel[defect].min() > kel[~defect].max()  # damage localises in the defect region
     m.close()
