@@ -83,6 +83,18 @@ def lib():
                                            C.c_int64, i64p, i64p, i32p, dp, dp, dp]
         L.oracle_update_history.argtypes = [C.c_int, C.c_int64, C.c_int64, i64p, dp, dp]
         L.oracle_residual_norms.argtypes = [C.c_int, C.c_int64, dp, dp]
+        L.oracle_mixed_family.argtypes = [C.c_int, i32p]
+        L.oracle_mixed_gauss.argtypes = [C.c_int, dp, dp]
+        L.oracle_mixed_shape_u.argtypes = [C.c_int, dp, dp, dp]
+        L.oracle_mixed_shape_e.argtypes = [C.c_int, dp, dp, dp]
+        L.oracle_mixed_element.argtypes = [C.c_int, mp, dp, dp, dp, dp, dp, dp, dp, dp, dp]
+        L.oracle_mixed_dofs.argtypes = [C.c_int, C.c_int64, C.c_int64, i64p, i64p]
+        L.oracle_mixed_dofs.restype = C.c_int64
+        L.oracle_mixed_pattern.argtypes = [C.c_int, C.c_int64, C.c_int64, i64p, i64p, i64p, i32p]
+        L.oracle_mixed_pattern.restype = C.c_int64
+        L.oracle_mixed_assemble.argtypes = [C.c_int, mp, C.c_int64, dp, C.c_int64, i64p, i64p,
+                                            dp, dp, dp, dp, i64p, i32p, dp, dp, dp]
+        L.oracle_mixed_update_history.argtypes = [C.c_int, C.c_int64, i64p, i64p, dp, dp]
         _lib = L
     return _lib
 
@@ -371,3 +383,117 @@ def reaction(res: dict, dof_ids):
     listed u dofs of the UNCONSTRAINED assembled system, i.e. -sum R_i (R = F of Eq. 11 has no
     external load in a displacement-controlled problem)."""
     return -float(np.sum(np.asarray(res["R"])[np.asarray(dof_ids, dtype=np.int64)]))
+
+
+# ---------------------------------------------------------------------------------------
+# Mixed-order elements (SURVEY NEXT f2; lgdm_oracle.cpp "Mixed-order elements")
+# ---------------------------------------------------------------------------------------
+BAR3, QUAD8 = 4, 5
+
+
+def mixed_family(etype: int):
+    """(dim, nenu, nene, nv, ngp, ndofe)"""
+    out = np.zeros(6, dtype=np.int32)
+    assert lib().oracle_mixed_family(etype, _i32(out)) == 0
+    return tuple(int(v) for v in out)
+
+
+def mixed_gauss(etype: int):
+    dim, _, _, _, ngp, _ = mixed_family(etype)
+    xi, w = np.zeros(ngp * dim), np.zeros(ngp)
+    lib().oracle_mixed_gauss(etype, _d(xi), _d(w))
+    return xi.reshape(ngp, dim), w
+
+
+def mixed_shape(etype: int, xi, field: str = "u"):
+    dim, nenu, nene, _, _, _ = mixed_family(etype)
+    nen = nenu if field == "u" else nene
+    x = np.ascontiguousarray(xi, dtype=np.float64)
+    N, dN = np.zeros(nen), np.zeros(nen * dim)
+    fn = lib().oracle_mixed_shape_u if field == "u" else lib().oracle_mixed_shape_e
+    fn(etype, _d(x), _d(N), _d(dN))
+    return N, dN.reshape(nen, dim)
+
+
+def mixed_element(etype: int, m: Material, Xe, Ue, kap, k0g=None, alg=None):
+    dim, nenu, nene, nv, ngp, nd = mixed_family(etype)
+    Xe = np.ascontiguousarray(Xe, dtype=np.float64).reshape(-1)
+    Ue = np.ascontiguousarray(Ue, dtype=np.float64).reshape(-1)
+    kap = np.ascontiguousarray(kap, dtype=np.float64).reshape(-1)
+    Ke, Fe, Fa, sig = np.zeros(nd * nd), np.zeros(nd), np.zeros(nd), np.zeros(ngp * nv)
+    k0k, k0p = _opt(k0g, ngp)
+    alk, alp = _opt(alg, ngp)
+    rc = lib().oracle_mixed_element(etype, C.byref(m), _d(Xe), _d(Ue), _d(kap), k0p, alp,
+                                    _d(Ke), _d(Fe), _d(Fa), _d(sig))
+    if rc != 0:
+        raise ValueError(f"oracle_mixed_element rc={rc}")
+    return Ke.reshape(nd, nd), Fe, Fa, sig.reshape(ngp, nv)
+
+
+def mixed_dofs(etype: int, n_nodes: int, conn):
+    conn = np.ascontiguousarray(conn, dtype=np.int64)
+    doff = np.zeros(n_nodes + 1, dtype=np.int64)
+    nd = lib().oracle_mixed_dofs(etype, n_nodes, conn.shape[0], _i64(conn), _i64(doff))
+    if nd < 0:
+        raise ValueError("inconsistent mixed mesh")
+    return doff
+
+
+def dof_kind(doff, dim: int):
+    """component index per global dof: 0..dim-1 displacement, dim = ebar"""
+    cnt = np.diff(doff)
+    kind = np.concatenate([np.arange(c) for c in cnt]).astype(np.int64)
+    return kind
+
+
+def mixed_pattern(etype: int, n_nodes: int, conn, doff):
+    conn = np.ascontiguousarray(conn, dtype=np.int64)
+    null = C.POINTER(C.c_int64)()
+    nnz = lib().oracle_mixed_pattern(etype, n_nodes, conn.shape[0], _i64(conn), _i64(doff), null,
+                                     C.POINTER(C.c_int32)())
+    rp = np.zeros(doff[-1] + 1, dtype=np.int64)
+    ci = np.zeros(nnz, dtype=np.int32)
+    lib().oracle_mixed_pattern(etype, n_nodes, conn.shape[0], _i64(conn), _i64(doff), _i64(rp),
+                               _i32(ci))
+    return rp, ci
+
+
+def mixed_assemble(etype: int, m: Material, coords, conn, dofs, kappa, kappa0_gp=None,
+                   alpha_gp=None):
+    """Alg. 1 assembly for mixed elements.  Returns dict(row_ptr, col_idx, val, R, S, doff)."""
+    dim, nenu, nene, nv, ngp, nd = mixed_family(etype)
+    coords = np.ascontiguousarray(coords, dtype=np.float64)
+    conn = np.ascontiguousarray(conn, dtype=np.int64)
+    dofs = np.ascontiguousarray(dofs, dtype=np.float64)
+    kappa = np.ascontiguousarray(kappa, dtype=np.float64)
+    nn, ne = coords.shape[0], conn.shape[0]
+    doff = mixed_dofs(etype, nn, conn)
+    rp, ci = mixed_pattern(etype, nn, conn, doff)
+    val = np.zeros(ci.size)
+    R, S = np.zeros(doff[-1]), np.zeros(doff[-1])
+    k0k, k0p = _opt(kappa0_gp, ne * ngp)
+    alk, alp = _opt(alpha_gp, ne * ngp)
+    rc = lib().oracle_mixed_assemble(etype, C.byref(m), nn, _d(coords), ne, _i64(conn),
+                                     _i64(doff), _d(dofs), _d(kappa), k0p, alp, _i64(rp),
+                                     _i32(ci), _d(val), _d(R), _d(S))
+    if rc != 0:
+        raise ValueError(f"oracle_mixed_assemble rc={rc}")
+    return dict(row_ptr=rp, col_idx=ci, val=val, R=R, S=S, doff=doff)
+
+
+def mixed_update_history(etype: int, conn, doff, dofs, kappa):
+    conn = np.ascontiguousarray(conn, dtype=np.int64)
+    dofs = np.ascontiguousarray(dofs, dtype=np.float64)
+    k = np.array(kappa, dtype=np.float64, copy=True)
+    lib().oracle_mixed_update_history(etype, conn.shape[0], _i64(conn), _i64(doff), _d(dofs),
+                                      _d(k))
+    return k
+
+
+def converged_kind(delta, dofs, kind, dim: int, tol: float, floor: float = 1e-16):
+    """Alg. 2 l.16 ratios with the dof kinds of a mixed mesh."""
+    d, u = np.asarray(delta), np.asarray(dofs)
+    e = kind == dim
+    ru = np.linalg.norm(d[~e]) / max(np.linalg.norm(u[~e]), floor)
+    re = np.linalg.norm(d[e]) / max(np.linalg.norm(u[e]), floor)
+    return bool(ru <= tol and re <= tol), ru, re

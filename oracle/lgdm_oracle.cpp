@@ -746,3 +746,385 @@ void oracle_residual_norms(int type, int64_t n_rows, const double* R, double* ou
 }
 
 }  // extern "C"
+
+// =========================================================================================
+// Mixed-order elements: quadratic u with linear ebar, the paper's own
+// discretisation ("shape functions for displacement (u) are taken as quadratic, and for
+// micro-equivalent strain as linear"; 1D bar P:418; 2D SEN P:466).
+//   type 4 = BAR3:  3-node quadratic bar for u (local nodes xi = -1, +1, 0), ebar on the two
+//                   end nodes (linear), 3-point Gauss.
+//   type 5 = QUAD8: 8-node serendipity quad for u (corners counter-clockwise, then midsides
+//                   (0,-1), (1,0), (0,1), (-1,0)), ebar bilinear on the 4 corners, 3x3 Gauss
+//                   (reading R-Q8: the paper's "biquadratic" with Fig. 6's 8 shape rows).
+// Geometry is isoparametric on the u nodes (reading R-GEO).  The corner ("ebar") nodes are
+// the first nene local nodes.  Local element dofs are node-major: corner node a has
+// (u_0..u_{d-1}, ebar) at a*(d+1); midside node a >= nene has (u_0..u_{d-1}) at
+// nene*(d+1) + (a-nene)*d.  Global dofs are node-interleaved with a variable count per node:
+// dof = doff[node] + comp, doff the prefix sum of (d+1 for ebar-carrying nodes, d otherwise)
+// (reading R-ORD extended).
+// =========================================================================================
+namespace {
+
+struct MFam {
+  int dim, nenu, nene, nv, ngp, ndofe;
+};
+
+bool mfamily(int type, MFam* f) {
+  switch (type) {
+    case 4: *f = {1, 3, 2, 1, 3, 5}; return true;      // 3 u + 2 ebar dofs
+    case 5: *f = {2, 8, 4, 3, 9, 20}; return true;     // 16 u + 4 ebar dofs
+    default: return false;
+  }
+}
+
+int mldof(const MFam& f, int a) {
+  return a < f.nene ? a * (f.dim + 1) : f.nene * (f.dim + 1) + (a - f.nene) * f.dim;
+}
+
+// reference coordinates of the u nodes
+void mref_node(int type, int a, double* xa) {
+  static const double q8[8][2] = {{-1, -1}, {1, -1}, {1, 1}, {-1, 1},
+                                  {0, -1},  {1, 0},  {0, 1}, {-1, 0}};
+  if (type == 4) xa[0] = a == 0 ? -1.0 : (a == 1 ? 1.0 : 0.0);
+  else { xa[0] = q8[a][0]; xa[1] = q8[a][1]; }
+}
+
+}  // namespace
+
+extern "C" {
+
+int oracle_mixed_family(int type, int32_t* out6) {
+  MFam f;
+  if (!mfamily(type, &f)) return -1;
+  out6[0] = f.dim; out6[1] = f.nenu; out6[2] = f.nene; out6[3] = f.nv; out6[4] = f.ngp;
+  out6[5] = f.ndofe;
+  return 0;
+}
+
+// 3-point Gauss-Legendre per direction: xi = -sqrt(3/5), 0, +sqrt(3/5); w = 5/9, 8/9, 5/9
+// (xi fastest in 2D).
+int oracle_mixed_gauss(int type, double* xi, double* w) {
+  MFam f;
+  if (!mfamily(type, &f)) return -1;
+  const double p[3] = {-std::sqrt(3.0 / 5.0), 0.0, std::sqrt(3.0 / 5.0)};
+  const double q[3] = {5.0 / 9.0, 8.0 / 9.0, 5.0 / 9.0};
+  for (int g = 0; g < f.ngp; ++g) {
+    const int gx = g % 3, gy = g / 3;
+    xi[g * f.dim] = p[gx];
+    w[g] = q[gx];
+    if (f.dim == 2) {
+      xi[g * f.dim + 1] = p[gy];
+      w[g] *= q[gy];
+    }
+  }
+  return f.ngp;
+}
+
+// u shape functions.  BAR3: N = xi(xi-1)/2, xi(xi+1)/2, 1-xi^2.  QUAD8 serendipity:
+// corner  N = 1/4 (1+xi xa)(1+eta ea)(xi xa + eta ea - 1);
+// midside xa = 0: N = 1/2 (1-xi^2)(1+eta ea);  ea = 0: N = 1/2 (1+xi xa)(1-eta^2).
+void oracle_mixed_shape_u(int type, const double* xi, double* N, double* dNdxi) {
+  if (type == 4) {
+    const double x = xi[0];
+    N[0] = 0.5 * x * (x - 1.0);
+    N[1] = 0.5 * x * (x + 1.0);
+    N[2] = 1.0 - x * x;
+    dNdxi[0] = x - 0.5;
+    dNdxi[1] = x + 0.5;
+    dNdxi[2] = -2.0 * x;
+    return;
+  }
+  const double x = xi[0], y = xi[1];
+  for (int a = 0; a < 8; ++a) {
+    double r[2];
+    mref_node(type, a, r);
+    const double xa = r[0], ea = r[1];
+    if (a < 4) {
+      N[a] = 0.25 * (1.0 + x * xa) * (1.0 + y * ea) * (x * xa + y * ea - 1.0);
+      dNdxi[a * 2 + 0] = 0.25 * xa * (1.0 + y * ea) * (2.0 * x * xa + y * ea);
+      dNdxi[a * 2 + 1] = 0.25 * ea * (1.0 + x * xa) * (x * xa + 2.0 * y * ea);
+    } else if (xa == 0.0) {
+      N[a] = 0.5 * (1.0 - x * x) * (1.0 + y * ea);
+      dNdxi[a * 2 + 0] = -x * (1.0 + y * ea);
+      dNdxi[a * 2 + 1] = 0.5 * ea * (1.0 - x * x);
+    } else {
+      N[a] = 0.5 * (1.0 + x * xa) * (1.0 - y * y);
+      dNdxi[a * 2 + 0] = 0.5 * xa * (1.0 - y * y);
+      dNdxi[a * 2 + 1] = -y * (1.0 + x * xa);
+    }
+  }
+}
+
+// ebar shape functions: linear on the corners (BAR2 / Q4 of the corner nodes).
+void oracle_mixed_shape_e(int type, const double* xi, double* N, double* dNdxi) {
+  MFam f;
+  if (!mfamily(type, &f)) return;
+  for (int a = 0; a < f.nene; ++a) {
+    double r[2];
+    mref_node(type, a, r);
+    if (f.dim == 1) {
+      N[a] = 0.5 * (1.0 + r[0] * xi[0]);
+      dNdxi[a] = 0.5 * r[0];
+    } else {
+      N[a] = 0.25 * (1.0 + r[0] * xi[0]) * (1.0 + r[1] * xi[1]);
+      dNdxi[a * 2 + 0] = 0.25 * r[0] * (1.0 + r[1] * xi[1]);
+      dNdxi[a * 2 + 1] = 0.25 * r[1] * (1.0 + r[0] * xi[0]);
+    }
+  }
+}
+
+// Element blocks of Eqs. 11a-f for a mixed element: identical integrands to
+// oracle_element_d; B_u from the u shape functions over the u dofs, N_e / B_e from the ebar
+// shape functions over the ebar dofs; dV = w_g det J t.
+int oracle_mixed_element(int type, const oracle_material* m0, const double* Xe, const double* Ue,
+                         const double* kap, const double* k0g, const double* alg, double* Ke,
+                         double* Fe, double* Fabs, double* sig) {
+  oracle_material mg = *m0;
+  const oracle_material* m = &mg;
+  MFam f;
+  if (!mfamily(type, &f)) return -1000;
+  const int dim = f.dim, nv = f.nv, nd = f.ndofe;
+  double xi[18], w[9];
+  oracle_mixed_gauss(type, xi, w);
+  double C[36];
+  elasticity(m, dim, C);
+  for (int r = 0; r < nd * nd; ++r) Ke[r] = 0.0;
+  for (int r = 0; r < nd; ++r) Fe[r] = 0.0, Fabs[r] = 0.0;
+
+  for (int g = 0; g < f.ngp; ++g) {
+    double Nu[8], dNu[16], Nn[4], dNe[8];
+    oracle_mixed_shape_u(type, xi + g * dim, Nu, dNu);
+    oracle_mixed_shape_e(type, xi + g * dim, Nn, dNe);
+    double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}}, Ji[3][3];
+    for (int a = 0; a < f.nenu; ++a)
+      for (int i = 0; i < dim; ++i)
+        for (int j = 0; j < dim; ++j) J[i][j] += Xe[a * dim + i] * dNu[a * dim + j];
+    const double detJ = dim == 1 ? J[0][0] : J[0][0] * J[1][1] - J[0][1] * J[1][0];
+    if (!invert(dim, J, Ji)) return -(g + 1);
+    double gNu[8][3], gNe[4][3];
+    for (int a = 0; a < f.nenu; ++a)
+      for (int i = 0; i < dim; ++i) {
+        double s = 0.0;
+        for (int j = 0; j < dim; ++j) s += Ji[j][i] * dNu[a * dim + j];
+        gNu[a][i] = s;
+      }
+    for (int a = 0; a < f.nene; ++a)
+      for (int i = 0; i < dim; ++i) {
+        double s = 0.0;
+        for (int j = 0; j < dim; ++j) s += Ji[j][i] * dNe[a * dim + j];
+        gNe[a][i] = s;
+      }
+    const double dV = w[g] * detJ * m->t;
+
+    // full-width operators over the element dof vector
+    double Bu[6][20], Ne[20], Be[3][20];
+    for (int r = 0; r < nd; ++r) {
+      Ne[r] = 0.0;
+      for (int V = 0; V < 6; ++V) Bu[V][r] = 0.0;
+      for (int i = 0; i < 3; ++i) Be[i][r] = 0.0;
+    }
+    for (int a = 0; a < f.nenu; ++a) {
+      const int o = mldof(f, a);
+      for (int V = 0; V < nv; ++V) {
+        int p, q;
+        voigt_pair(dim, V, &p, &q);
+        if (p == q) {
+          Bu[V][o + p] = gNu[a][p];
+        } else {
+          Bu[V][o + p] = gNu[a][q];
+          Bu[V][o + q] = gNu[a][p];
+        }
+      }
+    }
+    for (int a = 0; a < f.nene; ++a) {
+      const int o = mldof(f, a) + dim;
+      Ne[o] = Nn[a];
+      for (int i = 0; i < dim; ++i) Be[i][o] = gNe[a][i];
+    }
+
+    double ev[6] = {0, 0, 0, 0, 0, 0}, ebar = 0.0, gbar[3] = {0, 0, 0};
+    for (int r = 0; r < nd; ++r) {
+      for (int V = 0; V < nv; ++V) ev[V] += Bu[V][r] * Ue[r];
+      ebar += Ne[r] * Ue[r];
+      for (int i = 0; i < dim; ++i) gbar[i] += Be[i][r] * Ue[r];
+    }
+
+    mg.kappa0 = k0g ? k0g[g] : m0->kappa0;
+    mg.alpha = alg ? alg[g] : m0->alpha;
+    double eeq, dv[6], H[36];
+    oracle_eqstrain(m, dim, ev, &eeq, dv, H);
+    const double kh = kap[g];
+    const bool L = (ebar - kh) > kTolHist;
+    const double kappa = L ? ebar : kh;
+    double D, dD;
+    oracle_damage(m, kappa, &D, &dD);
+    double gI, dgdD;
+    oracle_interaction(m, D, &gI, &dgdD);
+    const double gprime = dgdD * dD;
+    const double Lf = L ? 1.0 : 0.0;
+
+    double Ceps[6], sv[6];
+    for (int V = 0; V < nv; ++V) {
+      double s = 0.0;
+      for (int W = 0; W < nv; ++W) s += C[V * nv + W] * ev[W];
+      Ceps[V] = s;
+      sv[V] = (1.0 - D) * Ceps[V] + m->h_sigma * (eeq - ebar) * dv[V];
+    }
+    if (sig)
+      for (int V = 0; V < nv; ++V) sig[g * nv + V] = sv[V];
+    double X[36];
+    for (int V = 0; V < nv; ++V)
+      for (int W = 0; W < nv; ++W)
+        X[V * nv + W] = (1.0 - D) * C[V * nv + W] +
+                        m->h_sigma * (dv[V] * dv[W] + (eeq - ebar) * H[V * nv + W]);
+    double wv[6];
+    for (int V = 0; V < nv; ++V) wv[V] = Ceps[V] * dD * Lf + m->h_sigma * dv[V];
+    double XB[6][20];
+    for (int V = 0; V < nv; ++V)
+      for (int c = 0; c < nd; ++c) {
+        double s = 0.0;
+        for (int W = 0; W < nv; ++W) s += X[V * nv + W] * Bu[W][c];
+        XB[V][c] = s;
+      }
+    for (int r = 0; r < nd; ++r) {
+      double btw = 0.0, btsig = 0.0, btsig_abs = 0.0, bg = 0.0, bg_abs = 0.0;
+      for (int V = 0; V < nv; ++V) {
+        btw += Bu[V][r] * wv[V];
+        btsig += Bu[V][r] * sv[V];
+        btsig_abs += std::fabs(Bu[V][r]) * (std::fabs((1.0 - D) * Ceps[V]) +
+                                            std::fabs(m->h_sigma * (eeq - ebar) * dv[V]));
+      }
+      for (int i = 0; i < dim; ++i) {
+        bg += Be[i][r] * gbar[i];
+        bg_abs += std::fabs(Be[i][r]) * std::fabs(gbar[i]);
+      }
+      for (int c = 0; c < nd; ++c) {
+        double kuu = 0.0, bb = 0.0;
+        for (int V = 0; V < nv; ++V) kuu += Bu[V][r] * XB[V][c];       // 11a
+        for (int i = 0; i < dim; ++i) bb += Be[i][r] * Be[i][c];
+        double kue = -btw * Ne[c];                                     // 11b
+        double keu = 0.0;                                              // 11c
+        for (int V = 0; V < nv; ++V) keu += -Ne[r] * m->h * dv[V] * Bu[V][c];
+        double kee = m->h * Ne[r] * Ne[c] + m->h * m->c * gprime * Lf * bg * Ne[c] +
+                     gI * m->h * m->c * bb;                            // 11d
+        Ke[r * nd + c] += dV * (kuu + kue + keu + kee);
+      }
+      Fe[r] += dV * (-btsig + m->h * Ne[r] * (eeq - ebar) - gI * m->h * m->c * bg);   // 11e, 11f
+      Fabs[r] += dV * (btsig_abs + m->h * std::fabs(Ne[r] * (eeq - ebar)) +
+                       gI * m->h * m->c * bg_abs);
+    }
+  }
+  return 0;
+}
+
+// Global dof offsets: doff[n] = first dof of node n, doff[n_nodes] = ndof.  A node carries
+// ebar iff it is a corner (local index < nene) of its elements.  Returns ndof, or -1 when a
+// node is a corner of one element and a midside node of another, or is referenced by none.
+int64_t oracle_mixed_dofs(int type, int64_t n_nodes, int64_t n_elems, const int64_t* conn,
+                          int64_t* doff) {
+  MFam f;
+  if (!mfamily(type, &f)) return -1;
+  std::vector<int> kind(n_nodes, 0);   // 0 unused, 1 corner, 2 midside
+  for (int64_t e = 0; e < n_elems; ++e)
+    for (int a = 0; a < f.nenu; ++a) {
+      const int k = a < f.nene ? 1 : 2;
+      int& s = kind[conn[e * f.nenu + a]];
+      if (s != 0 && s != k) return -1;
+      s = k;
+    }
+  doff[0] = 0;
+  for (int64_t n = 0; n < n_nodes; ++n) {
+    if (kind[n] == 0) return -1;
+    doff[n + 1] = doff[n] + (kind[n] == 1 ? f.dim + 1 : f.dim);
+  }
+  return doff[n_nodes];
+}
+
+// Pattern (reading R-PAT): every dof pair of two nodes sharing an element (explicit zeros
+// kept); rows in dof order, ascending global columns.
+int64_t oracle_mixed_pattern(int type, int64_t n_nodes, int64_t n_elems, const int64_t* conn,
+                             const int64_t* doff, int64_t* row_ptr, int32_t* col_idx) {
+  MFam f;
+  if (!mfamily(type, &f)) return -1;
+  std::vector<std::set<int64_t>> nb(n_nodes);
+  for (int64_t e = 0; e < n_elems; ++e)
+    for (int a = 0; a < f.nenu; ++a)
+      for (int b = 0; b < f.nenu; ++b) nb[conn[e * f.nenu + a]].insert(conn[e * f.nenu + b]);
+  int64_t pos = 0;
+  if (row_ptr) row_ptr[0] = 0;
+  for (int64_t a = 0; a < n_nodes; ++a)
+    for (int64_t r = doff[a]; r < doff[a + 1]; ++r) {
+      for (int64_t b : nb[a])
+        for (int64_t c = doff[b]; c < doff[b + 1]; ++c) {
+          if (col_idx) col_idx[pos] = int32_t(c);
+          ++pos;
+        }
+      if (row_ptr) row_ptr[r + 1] = pos;
+    }
+  return pos;
+}
+
+// Alg. 1 l.4-11 for mixed elements: element loop, K_local, scatter into the pattern.
+int oracle_mixed_assemble(int type, const oracle_material* m, int64_t n_nodes,
+                          const double* coords, int64_t n_elems, const int64_t* conn,
+                          const int64_t* doff, const double* dofs, const double* kappa,
+                          const double* kappa0_gp, const double* alpha_gp,
+                          const int64_t* row_ptr, const int32_t* col_idx, double* val, double* R,
+                          double* S) {
+  MFam f;
+  if (!mfamily(type, &f)) return -1;
+  const int nd = f.ndofe;
+  const int64_t ndof = doff[n_nodes];
+  std::fill(val, val + row_ptr[ndof], 0.0);
+  std::fill(R, R + ndof, 0.0);
+  std::fill(S, S + ndof, 0.0);
+  std::vector<double> Ke(nd * nd), Fe(nd), Fa(nd);
+  double Xe[16], Ue[20];
+  int64_t gdof[20];
+  for (int64_t e = 0; e < n_elems; ++e) {
+    for (int a = 0; a < f.nenu; ++a) {
+      const int64_t n = conn[e * f.nenu + a];
+      for (int i = 0; i < f.dim; ++i) Xe[a * f.dim + i] = coords[n * f.dim + i];
+      const int nda = a < f.nene ? f.dim + 1 : f.dim;
+      for (int i = 0; i < nda; ++i) {
+        gdof[mldof(f, a) + i] = doff[n] + i;
+        Ue[mldof(f, a) + i] = dofs[doff[n] + i];
+      }
+    }
+    if (oracle_mixed_element(type, m, Xe, Ue, kappa + e * f.ngp,
+                             kappa0_gp ? kappa0_gp + e * f.ngp : nullptr,
+                             alpha_gp ? alpha_gp + e * f.ngp : nullptr, Ke.data(), Fe.data(),
+                             Fa.data(), nullptr) != 0)
+      return -2;
+    for (int r = 0; r < nd; ++r) {
+      R[gdof[r]] += Fe[r];
+      S[gdof[r]] += Fa[r];
+      for (int c = 0; c < nd; ++c) {
+        const int64_t p = find_col(row_ptr, col_idx, gdof[r], gdof[c]);
+        if (p < 0) return -3;
+        val[p] += Ke[r * nd + c];
+      }
+    }
+  }
+  return 0;
+}
+
+// Eq. A.2 with Fig. 8b l.19-24 for mixed elements: ebar_gp from the linear ebar field.
+int oracle_mixed_update_history(int type, int64_t n_elems, const int64_t* conn,
+                                const int64_t* doff, const double* dofs, double* kappa) {
+  MFam f;
+  if (!mfamily(type, &f)) return -1;
+  double xi[18], w[9], N[4], dN[8];
+  oracle_mixed_gauss(type, xi, w);
+  for (int64_t e = 0; e < n_elems; ++e)
+    for (int g = 0; g < f.ngp; ++g) {
+      oracle_mixed_shape_e(type, xi + g * f.dim, N, dN);
+      double ebar = 0.0;
+      for (int a = 0; a < f.nene; ++a) ebar += N[a] * dofs[doff[conn[e * f.nenu + a]] + f.dim];
+      double& k = kappa[e * f.ngp + g];
+      if ((ebar - k) > kTolHist) k = ebar;
+    }
+  return 0;
+}
+
+}  // extern "C"

@@ -102,6 +102,31 @@ int oracle_update_state(int type, const oracle_material* m, int64_t n_nodes, con
                         int64_t n_elems, const int64_t* conn, const double* dofs, double* kappa,
                         const double* kappa0_gp, const double* alpha_gp, double* sdv);
 
+/* ---- mixed-order elements ----
+ * type 4 = BAR3 (quadratic u on 3 nodes [xi=-1, +1, 0], linear ebar on the 2 end nodes,
+ * 3-point Gauss); type 5 = QUAD8 (8-node serendipity u [corners ccw, midsides (0,-1), (1,0),
+ * (0,1), (-1,0)], bilinear ebar on the corners, 3x3 Gauss).  Local dofs node-major, corners
+ * (u..., ebar) first, then midsides (u...).  Global dof = doff[node] + comp. */
+int oracle_mixed_family(int type, int32_t* out6 /* dim, nenu, nene, nv, ngp, ndofe */);
+int oracle_mixed_gauss(int type, double* xi, double* w);
+void oracle_mixed_shape_u(int type, const double* xi, double* N, double* dNdxi);
+void oracle_mixed_shape_e(int type, const double* xi, double* N, double* dNdxi);
+int oracle_mixed_element(int type, const oracle_material* m, const double* Xe, const double* Ue,
+                         const double* kap, const double* k0g, const double* alg, double* Ke,
+                         double* Fe, double* Fabs, double* sig);
+int64_t oracle_mixed_dofs(int type, int64_t n_nodes, int64_t n_elems, const int64_t* conn,
+                          int64_t* doff /*[n_nodes+1]*/);
+/* row_ptr / col_idx may be NULL (count only); returns nnz */
+int64_t oracle_mixed_pattern(int type, int64_t n_nodes, int64_t n_elems, const int64_t* conn,
+                             const int64_t* doff, int64_t* row_ptr, int32_t* col_idx);
+int oracle_mixed_assemble(int type, const oracle_material* m, int64_t n_nodes,
+                          const double* coords, int64_t n_elems, const int64_t* conn,
+                          const int64_t* doff, const double* dofs, const double* kappa,
+                          const double* kappa0_gp, const double* alpha_gp,
+                          const int64_t* row_ptr, const int32_t* col_idx, double* val, double* R,
+                          double* S);
+int oracle_mixed_update_history(int type, int64_t n_elems, const int64_t* conn,
+                                const int64_t* doff, const double* dofs, double* kappa);
 #ifdef __cplusplus
 }
 #endif

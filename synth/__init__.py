@@ -253,3 +253,72 @@ def sample_nodes(n_nodes: int, count: int, seed: int) -> np.ndarray:
     u = uniform(seed, 30, np.arange(count * 2, dtype=np.uint64))
     ids = np.unique((u * n_nodes).astype(np.int64))[:count]
     return np.sort(ids)
+
+
+# ---------------------------------------------------------------------------------------
+# Mixed-order meshes: BAR3 (quadratic u, linear ebar) and QUAD8
+# (serendipity u, bilinear ebar).  Local node order: corners first (bar: x-, x+; quad:
+# counter-clockwise), then midsides (bar: centre; quad: (0,-1), (1,0), (0,1), (-1,0)).
+# Global nodes are the points of the half-spacing lattice that belong to an element
+# (QUAD8 has no element-centre node), numbered x-fastest.  The flat dof vector lists, per
+# node in id order, its displacement components and then, for corner nodes only, ebar.
+# ---------------------------------------------------------------------------------------
+BAR3, QUAD8 = 4, 5
+# type -> (dim, nenu, nene, ngp)
+MFAM = {4: (1, 3, 2, 3), 5: (2, 8, 4, 9)}
+
+
+@dataclass
+class MixedMesh:
+    etype: int
+    coords: np.ndarray      # [nn, dim]
+    conn: np.ndarray        # [ne, nenu]
+    corner: np.ndarray      # [nn] bool: node carries ebar
+    shape: tuple
+
+
+def mixed_mesh(etype: int, n: tuple, extent: float = 100.0) -> MixedMesh:
+    h = extent / n[0]
+    if etype == BAR3:
+        ne = n[0]
+        coords = (np.arange(2 * ne + 1, dtype=np.float64) * (h / 2.0))[:, None]
+        e = np.arange(ne, dtype=np.int64)
+        conn = np.stack([2 * e, 2 * e + 2, 2 * e + 1], axis=1)
+        corner = np.arange(2 * ne + 1) % 2 == 0
+        return MixedMesh(etype, coords, conn, corner, tuple(n))
+    nx, ny = n
+    I, J = np.meshgrid(np.arange(2 * nx + 1), np.arange(2 * ny + 1), indexing="xy")
+    I, J = I.ravel(), J.ravel()                       # x fastest
+    keep = ~((I % 2 == 1) & (J % 2 == 1))
+    ids = -np.ones(I.size, dtype=np.int64)
+    ids[keep] = np.arange(int(keep.sum()))
+    lat = lambda i, j: ids[i + (2 * nx + 1) * j]      # noqa: E731
+    coords = np.stack([I[keep] * (h / 2.0), J[keep] * (h / 2.0)], axis=1).astype(np.float64)
+    corner = (I[keep] % 2 == 0) & (J[keep] % 2 == 0)
+    EJ, EI = np.meshgrid(np.arange(ny), np.arange(nx), indexing="ij")
+    i0, j0 = 2 * EI.ravel(), 2 * EJ.ravel()
+    conn = np.stack([lat(i0, j0), lat(i0 + 2, j0), lat(i0 + 2, j0 + 2), lat(i0, j0 + 2),
+                     lat(i0 + 1, j0), lat(i0 + 2, j0 + 1), lat(i0 + 1, j0 + 2),
+                     lat(i0, j0 + 1)], axis=1).astype(np.int64)
+    return MixedMesh(etype, coords, conn, corner, tuple(n))
+
+
+def mixed_fields(mesh: MixedMesh, cid: int = 200):
+    """Flat dof vector (per node: u comps, then ebar for corner nodes) and kappa_hist
+    [ne, ngp], drawn with the recipe of ``fields`` for the equal-order family of the same
+    dimension (evaluated at the mixed mesh's nodes)."""
+    dim, nenu, nene, ngp = MFAM[mesh.etype]
+    eq = BAR2 if dim == 1 else QUAD4
+    ext = float(mesh.coords[:, 0].max() - mesh.coords[:, 0].min())
+    cfg = Config(cid, eq, tuple(mesh.shape), ext, "mixed")
+    ne = mesh.conn.shape[0]
+    proxy = Mesh(eq, mesh.coords, mesh.conn[:, :nene], 0, np.arange(ne, dtype=np.int64),
+                 mesh.coords.shape[0], ne, mesh.shape)
+    nodal, _ = fields(cfg, proxy)
+    parts = [np.concatenate([nodal[i, :dim], nodal[i, dim:dim + 1] if mesh.corner[i] else []])
+             for i in range(nodal.shape[0])]
+    dofs = np.concatenate(parts).astype(np.float64)
+    gp = (np.arange(ne, dtype=np.uint64)[:, None] * np.uint64(ngp) +
+          np.arange(ngp, dtype=np.uint64)[None, :])
+    kappa = np.maximum(MATERIAL["kappa0"], 4e-4 * uniform(cfg.seed, S_KAPPA, gp))
+    return dofs, kappa
