@@ -51,7 +51,23 @@ typedef enum {
   LGDM_ERR_NOT_CONVERGED = 8      /* lgdm_solve: residual above tolerance after max_iter    */
 } lgdm_status;
 
-typedef enum { LGDM_BAR2 = 1, LGDM_QUAD4 = 2, LGDM_HEX8 = 3 } lgdm_elem_type;
+/* Equal-order families (u and ebar on the same nodes; node-interleaved dofs, ndpn = d + 1) and
+ * the paper's mixed-order families ("shape functions for displacement
+ * (u) are taken as quadratic, and for micro-equivalent strain as linear"):
+ *   LGDM_BAR3  = 4: 3-node quadratic bar for u, local nodes (xi = -1, +1, 0); linear ebar on
+ *                   the two end nodes; 3-point Gauss.
+ *   LGDM_QUAD8 = 5: 8-node serendipity quad for u (corners counter-clockwise, then midsides
+ *                   (0,-1), (1,0), (0,1), (-1,0)); bilinear ebar on the corners; 3x3 Gauss;
+ *                   plane strain.
+ * Mixed meshes: a node carries ebar iff it is a corner (local index < 2 / < 4) of its
+ * elements (a node that is a corner of one element and a midside node of another, or no
+ * element's node, is INVALID_ARGUMENT).  Dofs stay node-interleaved with a variable count
+ * per node: dof = doff[node] + comp, comp = (u_x[, u_y][, ebar]), doff = prefix sum of
+ * (d + 1 for corner nodes, d for midside nodes), see lgdm_dof_offsets.  Single-rank whole
+ * meshes only (global_node_offset 0, owned range = all nodes); assemble uses the element-block
+ * + gather kernels (lgdm_set_kernel 0 or 1); lgdm_update_state / lgdm_get_blocked return
+ * LGDM_ERR_UNSUPPORTED. */
+typedef enum { LGDM_BAR2 = 1, LGDM_QUAD4 = 2, LGDM_HEX8 = 3, LGDM_BAR3 = 4, LGDM_QUAD8 = 5 } lgdm_elem_type;
 
 /* Material (Eq. 1 4C, Eqs. 2-4, Appendix A).  Validated at create:
  * E > 0, 0 <= nu < 0.5, k >= 1, kappa0 > 0, 0 < alpha <= 1, beta > 0, h > 0,
@@ -189,6 +205,11 @@ lgdm_status lgdm_solve(lgdm_mesh mesh, double* delta, double tol, int max_iter, 
  * singularity (host, nullable) = -1 or the first rank-deficient pivot, in which case
  * LGDM_ERR_NOT_CONVERGED is returned.  Synchronises the mesh stream. */
 lgdm_status lgdm_solve_direct(lgdm_mesh mesh, double* delta, int* singularity);
+
+/* First global dof of every node (mixed-order meshes: variable dofs per node; equal-order:
+ * ndpn * node): host_out [n_nodes + 1], the last entry = number of dofs.  n must equal
+ * n_nodes + 1, else LGDM_ERR_INVALID_ARGUMENT. */
+lgdm_status lgdm_dof_offsets(lgdm_mesh mesh, int64_t* host_out, int64_t n);
 
 /* Reaction of a displacement-controlled problem (the load of the paper's load-displacement
  * curves, Fig. 11 / P:418; SPEC reaction_force): -sum of the last assembled R over the listed

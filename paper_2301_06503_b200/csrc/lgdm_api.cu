@@ -20,6 +20,7 @@
 #include "../../include/lgdm.h"
 #include "lgdm_kernels.cuh"
 #include "lgdm_solver.cuh"
+#include "lgdm_mixed.cuh"
 #include <cusolverSp.h>
 
 using namespace lgdm;
@@ -114,6 +115,8 @@ FamInfo fam_info(int type) {
   switch (type) {
     case LGDM_BAR2: return {1, 2, 2, 2, 4, 3};
     case LGDM_QUAD4: return {2, 4, 3, 4, 12, 9};
+    case LGDM_BAR3: return {1, 3, 2, 3, 5, 5};      // mixed: nen = u nodes, ndpn = max dofs per node
+    case LGDM_QUAD8: return {2, 8, 3, 9, 20, 21};
     default: return {3, 8, 4, 8, 32, 27};
   }
 }
@@ -173,6 +176,16 @@ struct lgdm_mesh_s {
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
   void* sweep = nullptr;  // sweep-path state (lgdm_sweep.cuh)
+  // mixed-order meshes (lgdm_mixed.cuh)
+  bool mixed = false;
+  int64_t n_dofs_local = 0;       // length of the dof vector (n_nodes * ndpn, or doff[n_nodes])
+  std::vector<int64_t> hdoff;     // host copy of doff
+  std::vector<uint8_t> hkind;     // host component index per dof
+  int64_t* doff = nullptr;        // device [n_nodes+1]
+  uint8_t* dkind = nullptr;       // device [ndof]
+  int64_t* madj_ptr = nullptr;    // device [n_nodes+1]
+  MixAdj* madj = nullptr;         // device node -> element map of k_mixed_gather
+  int max_row = 0;                // largest block-row (rows x width) in doubles
 };
 
 namespace {
@@ -303,6 +316,271 @@ template <int D> void launch_detj(lgdm_mesh m, unsigned long long* bad) {
   k_detj<D><<<unsigned((n + 255) / 256), 256, 0, m->stream>>>(m->n_elems, m->conn, m->coords, bad);
 }
 
+// ---- mixed-order elements (lgdm_mixed.cuh) ----
+// Gauss points and shape functions of the two mixed families (closed forms, 3-point
+// Gauss-Legendre per axis), tabulated once per mesh into constant memory.
+template <int T> void mixed_tables(MShape<T>& S) {
+  using F = MFam<T>;
+  const double p[3] = {-std::sqrt(0.6), 0.0, std::sqrt(0.6)};
+  const double q[3] = {5.0 / 9.0, 8.0 / 9.0, 5.0 / 9.0};
+  for (int g = 0; g < F::NGP; ++g) {
+    const int gx = g % 3, gy = g / 3;
+    const double x = p[gx];
+    if constexpr (F::DIM == 1) {
+      S.w[g] = q[gx];
+      S.Nu[g][0] = 0.5 * x * (x - 1.0);
+      S.Nu[g][1] = 0.5 * x * (x + 1.0);
+      S.Nu[g][2] = (1.0 - x) * (1.0 + x);
+      S.dNu[g][0][0] = x - 0.5;
+      S.dNu[g][1][0] = x + 0.5;
+      S.dNu[g][2][0] = -2.0 * x;
+      S.Ne[g][0] = 0.5 * (1.0 - x);
+      S.Ne[g][1] = 0.5 * (1.0 + x);
+      S.dNe[g][0][0] = -0.5;
+      S.dNe[g][1][0] = 0.5;
+    } else {
+      const double y = p[gy];
+      S.w[g] = q[gx] * q[gy];
+      static const int cx[4] = {-1, 1, 1, -1}, cy[4] = {-1, -1, 1, 1};
+      for (int a = 0; a < 4; ++a) {   // serendipity corners and bilinear ebar
+        const double sx = cx[a], sy = cy[a];
+        const double fx = 1.0 + sx * x, fy = 1.0 + sy * y;
+        S.Nu[g][a] = 0.25 * fx * fy * (sx * x + sy * y - 1.0);
+        S.dNu[g][a][0] = 0.25 * sx * fy * (2.0 * sx * x + sy * y);
+        S.dNu[g][a][1] = 0.25 * sy * fx * (sx * x + 2.0 * sy * y);
+        S.Ne[g][a] = 0.25 * fx * fy;
+        S.dNe[g][a][0] = 0.25 * sx * fy;
+        S.dNe[g][a][1] = 0.25 * sy * fx;
+      }
+      // midsides: (0,-1), (1,0), (0,1), (-1,0)
+      const double bx = (1.0 - x) * (1.0 + x), by = (1.0 - y) * (1.0 + y);
+      S.Nu[g][4] = 0.5 * bx * (1.0 - y);  S.dNu[g][4][0] = -x * (1.0 - y);  S.dNu[g][4][1] = -0.5 * bx;
+      S.Nu[g][5] = 0.5 * (1.0 + x) * by;  S.dNu[g][5][0] = 0.5 * by;        S.dNu[g][5][1] = -y * (1.0 + x);
+      S.Nu[g][6] = 0.5 * bx * (1.0 + y);  S.dNu[g][6][0] = -x * (1.0 + y);  S.dNu[g][6][1] = 0.5 * bx;
+      S.Nu[g][7] = 0.5 * (1.0 - x) * by;  S.dNu[g][7][0] = -0.5 * by;       S.dNu[g][7][1] = -y * (1.0 - x);
+    }
+  }
+}
+
+template <int T> lgdm_status upload_tables(lgdm_mesh m) {
+  MShape<T> S{};
+  mixed_tables<T>(S);
+  if constexpr (T == 4) CU(cudaMemcpyToSymbolAsync(c_shape4, &S, sizeof(S), 0, cudaMemcpyHostToDevice, m->stream));
+  else CU(cudaMemcpyToSymbolAsync(c_shape5, &S, sizeof(S), 0, cudaMemcpyHostToDevice, m->stream));
+  CU(cudaStreamSynchronize(m->stream));   // S is on the host stack
+  return LGDM_OK;
+}
+
+lgdm_status create_mixed(lgdm_elem_type type, int64_t n_nodes, const double* coords, int64_t n_elems,
+                         const int64_t* conn, const lgdm_material* mat, int64_t gid0, int64_t n_global,
+                         int64_t own_b, int64_t own_e, int device, void* stream, lgdm_mesh* out) {
+  const FamInfo f = fam_info(type);
+  const int T = int(type);
+  const int nene = T == LGDM_BAR3 ? 2 : 4;
+  if (!coords || !conn || !mat) return fail(LGDM_ERR_INVALID_ARGUMENT, "NULL input pointer");
+  if (n_nodes < 2 || n_elems < 1 || n_nodes >= (int64_t(1) << 30))
+    return fail(LGDM_ERR_INVALID_ARGUMENT, "bad sizes n_nodes=%lld n_elems=%lld", (long long)n_nodes,
+                (long long)n_elems);
+  if (gid0 != 0 || n_global != n_nodes || own_b != 0 || own_e != n_nodes)
+    return fail(LGDM_ERR_INVALID_ARGUMENT, "mixed-order meshes: single-rank whole mesh only");
+  std::string why;
+  if (!validate_material(mat, &why)) return fail(LGDM_ERR_INVALID_ARGUMENT, "material: %s", why.c_str());
+  std::vector<uint8_t> kind(n_nodes, 0);   // 1 corner (ebar), 2 midside
+  for (int64_t e = 0; e < n_elems; ++e)
+    for (int a = 0; a < f.nen; ++a) {
+      const int64_t n = conn[e * f.nen + a];
+      if (n < 0 || n >= n_nodes)
+        return fail(LGDM_ERR_INVALID_ARGUMENT, "conn[%lld] = %lld out of range", (long long)(e * f.nen + a), (long long)n);
+      const uint8_t k = a < nene ? 1 : 2;
+      if (kind[n] && kind[n] != k)
+        return fail(LGDM_ERR_INVALID_ARGUMENT, "node %lld is a corner of one element and a midside node of another", (long long)n);
+      kind[n] = k;
+    }
+  std::vector<int64_t> doff(n_nodes + 1, 0);
+  for (int64_t n = 0; n < n_nodes; ++n) {
+    if (!kind[n]) return fail(LGDM_ERR_INVALID_ARGUMENT, "node %lld belongs to no element", (long long)n);
+    doff[n + 1] = doff[n] + (kind[n] == 1 ? f.dim + 1 : f.dim);
+  }
+  const int64_t ndof = doff[n_nodes];
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(LGDM_ERR_CUDA, "no CUDA device available (liblgdm has no CPU path)");
+  if (device < 0 || device >= ndev) return fail(LGDM_ERR_INVALID_ARGUMENT, "bad device %d", device);
+  CU(cudaSetDevice(device));
+  lgdm_mesh m = new lgdm_mesh_s();
+  m->type = type;
+  m->f = f;
+  m->mixed = true;
+  m->n_nodes = n_nodes;
+  m->n_elems = n_elems;
+  m->gid0 = 0;
+  m->n_global_nodes = n_nodes;
+  m->own_b = 0;
+  m->own_e = n_nodes;
+  m->n_owned = n_nodes;
+  m->n_rows = ndof;
+  m->n_dofs_local = ndof;
+  m->device = device;
+  m->stream = (cudaStream_t)stream;
+  m->dm = derive(*mat, f.dim);
+  m->hdoff = doff;
+  m->hkind.resize(ndof);
+  for (int64_t n = 0; n < n_nodes; ++n)
+    for (int64_t r = doff[n]; r < doff[n + 1]; ++r) m->hkind[r] = uint8_t(r - doff[n]);
+  auto bail = [&](lgdm_status s) {
+    std::string keep = g_err;
+    lgdm_destroy(m);
+    g_err = keep;
+    return s;
+  };
+  lgdm_status s;
+  std::vector<int32_t> conn32(size_t(n_elems) * f.nen);
+  for (size_t i = 0; i < conn32.size(); ++i) conn32[i] = int32_t(conn[i]);
+  if ((s = upload(m, &m->coords, coords, size_t(n_nodes) * f.dim)) != LGDM_OK) return bail(s);
+  if ((s = upload(m, &m->conn, conn32.data(), conn32.size())) != LGDM_OK) return bail(s);
+  if ((s = upload(m, &m->doff, doff.data(), doff.size())) != LGDM_OK) return bail(s);
+  if ((s = upload(m, &m->dkind, m->hkind.data(), m->hkind.size())) != LGDM_OK) return bail(s);
+  if ((s = (T == 4 ? upload_tables<4>(m) : upload_tables<5>(m))) != LGDM_OK) return bail(s);
+  // det J > 0 at every GP
+  unsigned long long* bad = nullptr;
+  if (cudaMalloc(&bad, sizeof(unsigned long long)) != cudaSuccess)
+    return bail(fail(LGDM_ERR_OUT_OF_MEMORY, "cudaMalloc"));
+  cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), m->stream);
+  const unsigned gb = unsigned((n_elems * f.ngp + 255) / 256);
+  if (T == 4) k_mixed_detj<4><<<gb, 256, 0, m->stream>>>(n_elems, m->conn, m->coords, bad);
+  else k_mixed_detj<5><<<gb, 256, 0, m->stream>>>(n_elems, m->conn, m->coords, bad);
+  if ((s = check_launch(m, "k_mixed_detj")) != LGDM_OK) { cudaFree(bad); return bail(s); }
+  unsigned long long hbad = 0;
+  cudaMemcpyAsync(&hbad, bad, sizeof(hbad), cudaMemcpyDeviceToHost, m->stream);
+  cudaError_t ce = cudaStreamSynchronize(m->stream);
+  cudaFree(bad);
+  if (ce != cudaSuccess) return bail(fail(LGDM_ERR_CUDA, "det J check: %s", cudaGetErrorString(ce)));
+  if (hbad != ~0ull)
+    return bail(fail(LGDM_ERR_INVERTED_ELEMENT, "det J <= 0 in element %lld at Gauss point %d",
+                     (long long)(hbad / f.ngp), int(hbad % f.ngp)));
+  // pattern (reading R-PAT): node adjacency, block-rows of variable width
+  std::vector<int64_t> nadj(n_nodes + 1, 0);
+  for (int64_t i = 0; i < n_elems * f.nen; ++i) ++nadj[conn[i] + 1];
+  for (int64_t n = 0; n < n_nodes; ++n) nadj[n + 1] += nadj[n];
+  std::vector<int32_t> adj_e(nadj[n_nodes]);
+  std::vector<uint8_t> adj_a(nadj[n_nodes]);
+  {
+    std::vector<int64_t> fillp(nadj.begin(), nadj.end() - 1);
+    for (int64_t e = 0; e < n_elems; ++e)
+      for (int a = 0; a < f.nen; ++a) {
+        const int64_t n = conn[e * f.nen + a];
+        adj_e[fillp[n]] = int32_t(e);
+        adj_a[fillp[n]] = uint8_t(a);
+        ++fillp[n];
+      }
+  }
+  std::vector<int32_t> width(n_nodes);
+  std::vector<std::vector<int32_t>> nbs(n_nodes);
+#pragma omp parallel for schedule(static)
+  for (int64_t n = 0; n < n_nodes; ++n) {
+    std::vector<int32_t>& nb = nbs[n];
+    for (int64_t k = nadj[n]; k < nadj[n + 1]; ++k)
+      for (int b = 0; b < f.nen; ++b) nb.push_back(int32_t(conn[int64_t(adj_e[k]) * f.nen + b]));
+    std::sort(nb.begin(), nb.end());
+    nb.erase(std::unique(nb.begin(), nb.end()), nb.end());
+    int32_t w = 0;
+    for (int32_t b : nb) w += int32_t(doff[b + 1] - doff[b]);
+    width[n] = w;
+  }
+  std::vector<int64_t> row_ptr(ndof + 1, 0);
+  int64_t pos = 0;
+  int max_row = 0;
+  for (int64_t n = 0; n < n_nodes; ++n) {
+    const int nr = int(doff[n + 1] - doff[n]);
+    for (int i = 0; i < nr; ++i) {
+      row_ptr[doff[n] + i] = pos;
+      pos += width[n];
+    }
+    max_row = std::max(max_row, nr * width[n]);
+  }
+  row_ptr[ndof] = pos;
+  m->nnz = pos;
+  m->max_row = max_row;
+  if (pos >= (int64_t(1) << 40)) return bail(fail(LGDM_ERR_INVALID_ARGUMENT, "pattern too large"));
+  std::vector<int32_t> col(pos);
+  std::vector<int64_t> madj_ptr(n_nodes + 1);
+  for (int64_t n = 0; n < n_nodes; ++n) madj_ptr[n + 1] = madj_ptr[n] + (nadj[n + 1] - nadj[n]);
+  std::vector<MixAdj> madj(madj_ptr[n_nodes]);
+#pragma omp parallel for schedule(static)
+  for (int64_t n = 0; n < n_nodes; ++n) {
+    const std::vector<int32_t>& nb = nbs[n];
+    std::vector<int32_t> coff(nb.size());
+    int32_t c = 0;
+    for (size_t s2 = 0; s2 < nb.size(); ++s2) {
+      coff[s2] = c;
+      c += int32_t(doff[nb[s2] + 1] - doff[nb[s2]]);
+    }
+    const int nr = int(doff[n + 1] - doff[n]);
+    for (int i = 0; i < nr; ++i) {
+      int64_t p = row_ptr[doff[n] + i];
+      for (int32_t b : nb)
+        for (int64_t d = doff[b]; d < doff[b + 1]; ++d) col[p++] = int32_t(d);
+    }
+    for (int64_t k = nadj[n]; k < nadj[n + 1]; ++k) {
+      MixAdj en{};
+      en.e = adj_e[k];
+      en.aloc = adj_a[k];
+      for (int b = 0; b < f.nen; ++b) {
+        const int32_t nbn = int32_t(conn[int64_t(en.e) * f.nen + b]);
+        en.coff[b] = coff[std::lower_bound(nb.begin(), nb.end(), nbn) - nb.begin()];
+      }
+      madj[madj_ptr[n] + (k - nadj[n])] = en;
+    }
+  }
+  if ((s = upload(m, &m->row_ptr, row_ptr.data(), row_ptr.size())) != LGDM_OK) return bail(s);
+  if ((s = upload(m, &m->col_idx, col.data(), col.size())) != LGDM_OK) return bail(s);
+  if ((s = upload(m, &m->madj_ptr, madj_ptr.data(), madj_ptr.size())) != LGDM_OK) return bail(s);
+  if ((s = upload(m, &m->madj, madj.data(), madj.size())) != LGDM_OK) return bail(s);
+  if (dalloc(&m->val, size_t(m->nnz)) != cudaSuccess || dalloc(&m->R, size_t(ndof)) != cudaSuccess ||
+      dalloc(&m->dofs, size_t(ndof)) != cudaSuccess || dalloc(&m->kappa, size_t(n_elems) * f.ngp) != cudaSuccess ||
+      dalloc(&m->sumsq_part, size_t(2 * kSumBlocks)) != cudaSuccess || dalloc(&m->sumsq_out, 2) != cudaSuccess ||
+      cudaMallocHost(&m->host_pinned, 2 * sizeof(double)) != cudaSuccess)
+    return bail(fail(LGDM_ERR_OUT_OF_MEMORY, "cudaMalloc (nnz=%lld)", (long long)m->nnz));
+  m->device_bytes += m->nnz * 8 + ndof * 16 + n_elems * f.ngp * 8;
+  ce = cudaStreamSynchronize(m->stream);   // host staging vectors go out of scope
+  if (ce != cudaSuccess) return bail(fail(LGDM_ERR_CUDA, "create: %s", cudaGetErrorString(ce)));
+  *out = m;
+  return LGDM_OK;
+}
+
+template <int T> lgdm_status assemble_mixed(lgdm_mesh m) {
+  using F = MFam<T>;
+  constexpr int WPB = 4, GW = 8;
+  if (!m->scratchK) {
+    CU(dalloc(&m->scratchK, size_t(m->n_elems) * F::NDOFE * F::NDOFE));
+    CU(dalloc(&m->scratchF, size_t(m->n_elems) * F::NDOFE));
+    m->device_bytes += m->n_elems * (F::NDOFE * F::NDOFE + F::NDOFE) * 8;
+  }
+  const size_t smem = sizeof(double) * size_t(WPB) * MSmem<T>::SIZE;
+  static bool attr = false;
+  if (!attr) {
+    CU(cudaFuncSetAttribute(k_mixed_blocks<T, WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr = true;
+  }
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mixed_blocks<T, WPB>, WPB * 32, smem);
+  const int64_t nb = (m->n_elems + WPB - 1) / WPB;
+  const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(nb, int64_t(nsm) * std::max(per_sm, 1))));
+  k_mixed_blocks<T, WPB><<<grid, WPB * 32, smem, m->stream>>>(m->dm, m->n_elems, m->conn, m->coords, m->doff,
+                                                              m->dofs, m->kappa, m->k0g, m->alg,
+                                                              m->scratchK, m->scratchF);
+  lgdm_status s = check_launch(m, "k_mixed_blocks");
+  if (s != LGDM_OK) return s;
+  const size_t gsm = sizeof(double) * size_t(GW) * m->max_row;
+  if (gsm > 48 * 1024) CU(cudaFuncSetAttribute(k_mixed_gather<T, GW>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gsm)));
+  const int64_t gn = (m->n_nodes + GW - 1) / GW;
+  k_mixed_gather<T, GW><<<unsigned(std::min<int64_t>(gn, int64_t(nsm) * 16)), GW * 32, gsm, m->stream>>>(
+      m->n_nodes, m->madj_ptr, m->madj, m->doff, m->row_ptr, m->scratchK, m->scratchF, m->max_row, m->val, m->R);
+  return check_launch(m, "k_mixed_gather");
+}
+
 }  // namespace
 
 #include "lgdm_sweep.cuh"
@@ -318,6 +596,9 @@ lgdm_status lgdm_create_mesh(lgdm_elem_type type, int64_t n_nodes, const double*
                              void* cuda_stream, lgdm_mesh* out) {
   if (!out) return fail(LGDM_ERR_INVALID_ARGUMENT, "out is NULL");
   *out = nullptr;
+  if (type == LGDM_BAR3 || type == LGDM_QUAD8)
+    return create_mixed(type, n_nodes, coords, n_elems, conn, mat, global_node_offset,
+                        n_global_nodes, owned_node_begin, owned_node_end, device, cuda_stream, out);
   if (type != LGDM_BAR2 && type != LGDM_QUAD4 && type != LGDM_HEX8)
     return fail(LGDM_ERR_INVALID_ARGUMENT, "unknown element type %d", int(type));
   if (!coords || !conn || !mat) return fail(LGDM_ERR_INVALID_ARGUMENT, "NULL input pointer");
@@ -356,6 +637,7 @@ lgdm_status lgdm_create_mesh(lgdm_elem_type type, int64_t n_nodes, const double*
   m->own_e = owned_node_end;
   m->n_owned = owned_node_end - owned_node_begin;
   m->n_rows = m->n_owned * f.ndpn;
+  m->n_dofs_local = n_nodes * f.ndpn;
   m->device = device;
   m->stream = (cudaStream_t)cuda_stream;
   m->dm = derive(*mat, f.dim);
@@ -508,9 +790,9 @@ lgdm_status lgdm_set_state(lgdm_mesh m, const double* dofs, int64_t n_dofs, cons
                            int64_t n_kappa, int src_on_device) {
   if (!m) return fail(LGDM_ERR_INVALID_ARGUMENT, "mesh is NULL");
   if (!dofs) return fail(LGDM_ERR_INVALID_ARGUMENT, "dofs is NULL");
-  if (n_dofs != m->n_nodes * m->f.ndpn)
+  if (n_dofs != m->n_dofs_local)
     return fail(LGDM_ERR_INVALID_STATE, "n_dofs = %lld, expected %lld", (long long)n_dofs,
-                (long long)(m->n_nodes * m->f.ndpn));
+                (long long)m->n_dofs_local);
   if (kappa && n_kappa != m->n_elems * m->f.ngp)
     return fail(LGDM_ERR_INVALID_STATE, "n_kappa = %lld, expected %lld", (long long)n_kappa,
                 (long long)(m->n_elems * m->f.ngp));
@@ -571,12 +853,13 @@ lgdm_status lgdm_assemble(lgdm_mesh m, lgdm_csr* K, double** R) {
   lgdm_status s;
   // per-GP defect fields: the general path and the default sweeps (k_sweep4, k_sweepq)
   const bool defects = m->k0g || m->alg;
-  const bool sweep = m->kernel >= 2 || (m->kernel == 0 && m->structured && sweep_supported(m));
+  const bool sweep = !m->mixed && (m->kernel >= 2 || (m->kernel == 0 && m->structured && sweep_supported(m)));
   if (defects && (m->kernel == 2 || m->kernel == 3 || m->kernel == 5))
     return fail(LGDM_ERR_INVALID_ARGUMENT, "kernels 2, 3, 5 do not take per-GP defect fields (use 0, 1 or 4)");
   if (m->kernel >= 2 && !(m->structured && sweep_supported(m)))
     return fail(LGDM_ERR_INVALID_ARGUMENT, "sweep kernel requested but mesh is not structured");
-  if (sweep) s = assemble_sweep(m);
+  if (m->mixed) s = m->type == LGDM_BAR3 ? assemble_mixed<4>(m) : assemble_mixed<5>(m);
+  else if (sweep) s = assemble_sweep(m);
   else if (m->f.dim == 1) s = assemble_general<1>(m);
   else if (m->f.dim == 2) s = assemble_general<2>(m);
   else s = assemble_general<3>(m);
@@ -584,9 +867,9 @@ lgdm_status lgdm_assemble(lgdm_mesh m, lgdm_csr* K, double** R) {
   m->assembled = true;
   if (K) {
     K->n_rows = m->n_rows;
-    K->n_cols = m->n_global_nodes * m->f.ndpn;
+    K->n_cols = m->mixed ? m->n_rows : m->n_global_nodes * m->f.ndpn;
     K->nnz = m->nnz;
-    K->first_row = (m->gid0 + m->own_b) * m->f.ndpn;
+    K->first_row = m->mixed ? 0 : (m->gid0 + m->own_b) * m->f.ndpn;
     K->row_ptr = m->row_ptr;
     K->col_idx = m->col_idx;
     K->val = m->val;
@@ -601,7 +884,9 @@ lgdm_status lgdm_update_history(lgdm_mesh m) {
   CU(cudaSetDevice(m->device));
   const int64_t n = m->n_elems * m->f.ngp;
   const unsigned blocks = unsigned((n + 255) / 256);
-  if (m->f.dim == 1) k_update_history<1><<<blocks, 256, 0, m->stream>>>(m->n_elems, m->conn, m->dofs, m->kappa);
+  if (m->type == LGDM_BAR3) k_mixed_history<4><<<blocks, 256, 0, m->stream>>>(m->n_elems, m->conn, m->doff, m->dofs, m->kappa);
+  else if (m->type == LGDM_QUAD8) k_mixed_history<5><<<blocks, 256, 0, m->stream>>>(m->n_elems, m->conn, m->doff, m->dofs, m->kappa);
+  else if (m->f.dim == 1) k_update_history<1><<<blocks, 256, 0, m->stream>>>(m->n_elems, m->conn, m->dofs, m->kappa);
   else if (m->f.dim == 2) k_update_history<2><<<blocks, 256, 0, m->stream>>>(m->n_elems, m->conn, m->dofs, m->kappa);
   else k_update_history<3><<<blocks, 256, 0, m->stream>>>(m->n_elems, m->conn, m->dofs, m->kappa);
   return check_launch(m, "k_update_history");
@@ -649,6 +934,7 @@ lgdm_status lgdm_set_defects(lgdm_mesh m, const double* kappa0_gp, const double*
 lgdm_status lgdm_update_state(lgdm_mesh m, double* sdv, int64_t n_sdv, int dst_on_device) {
   if (!m) return fail(LGDM_ERR_INVALID_ARGUMENT, "mesh is NULL");
   if (!m->have_state || !m->have_kappa) return fail(LGDM_ERR_INVALID_STATE, "update_state before set_state");
+  if (m->mixed) return fail(LGDM_ERR_UNSUPPORTED, "update_state: mixed-order meshes not supported");
   const int W = lgdm_sdv_width(lgdm_elem_type(m->type));
   const int64_t ngp = m->n_elems * m->f.ngp;
   if (sdv && n_sdv != ngp * W)
@@ -690,6 +976,7 @@ lgdm_status lgdm_update_state(lgdm_mesh m, double* sdv, int64_t n_sdv, int dst_o
 lgdm_status lgdm_get_blocked(lgdm_mesh m, lgdm_csr* K, double** R) {
   if (!m) return fail(LGDM_ERR_INVALID_ARGUMENT, "mesh is NULL");
   if (!m->assembled) return fail(LGDM_ERR_INVALID_STATE, "get_blocked before assemble");
+  if (m->mixed) return fail(LGDM_ERR_UNSUPPORTED, "get_blocked: mixed-order meshes not supported");
   if (m->own_b != 0 || m->own_e != m->n_nodes || m->gid0 != 0 || m->n_global_nodes != m->n_nodes)
     return fail(LGDM_ERR_INVALID_ARGUMENT, "blocked order needs a single-rank whole mesh");
   CU(cudaSetDevice(m->device));
@@ -740,7 +1027,7 @@ lgdm_status lgdm_apply_dirichlet(lgdm_mesh m, int64_t n_fixed, const int64_t* do
   for (int64_t k = 0; k < n_fixed; ++k) {
     const int64_t d = dof_ids[k];
     if (d < 0 || d >= n) return fail(LGDM_ERR_INVALID_ARGUMENT, "dof id %lld out of range", (long long)d);
-    if (d % m->f.ndpn == m->f.dim)
+    if (m->mixed ? m->hkind[d] == m->f.dim : d % m->f.ndpn == m->f.dim)
       return fail(LGDM_ERR_INVALID_ARGUMENT, "dof %lld is an ebar dof (only u dofs can be constrained)", (long long)d);
     mask[d] = 1;
     inc[d] = increments[k];
@@ -855,6 +1142,13 @@ lgdm_status lgdm_solve(lgdm_mesh m, double* delta, double tol, int max_iter, int
   return LGDM_OK;
 }
 
+lgdm_status lgdm_dof_offsets(lgdm_mesh m, int64_t* host_out, int64_t n) {
+  if (!m || !host_out) return fail(LGDM_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (n != m->n_nodes + 1) return fail(LGDM_ERR_INVALID_ARGUMENT, "n = %lld, expected n_nodes + 1", (long long)n);
+  for (int64_t i = 0; i <= m->n_nodes; ++i) host_out[i] = m->mixed ? m->hdoff[i] : i * m->f.ndpn;
+  return LGDM_OK;
+}
+
 lgdm_status lgdm_reaction(lgdm_mesh m, int64_t n, const int64_t* dof_ids, double* out) {
   if (!m || !out || (n > 0 && !dof_ids)) return fail(LGDM_ERR_INVALID_ARGUMENT, "NULL argument");
   if (!m->assembled) return fail(LGDM_ERR_INVALID_STATE, "reaction before assemble");
@@ -912,7 +1206,7 @@ lgdm_status lgdm_add_dofs(lgdm_mesh m, const double* delta, double alpha) {
   if (!m->have_state) return fail(LGDM_ERR_INVALID_STATE, "add_dofs before set_state");
   if (!whole_single_rank(m)) return fail(LGDM_ERR_UNSUPPORTED, "Newton pieces need a single-rank whole mesh");
   CU(cudaSetDevice(m->device));
-  const int64_t n = m->n_nodes * m->f.ndpn;
+  const int64_t n = m->n_dofs_local;
   k_axpy<<<unsigned((n + 255) / 256), 256, 0, m->stream>>>(n, alpha, delta, m->dofs);
   return check_launch(m, "k_axpy");
 }
@@ -926,10 +1220,11 @@ lgdm_status lgdm_delta_norms(lgdm_mesh m, const double* delta, double out4[4]) {
     CU(dalloc(&m->sol_part, size_t(kRedBlocks) * 4 + 4));
     m->device_bytes += kRedBlocks * 32 + 32;
   }
-  const int64_t n = m->n_nodes * m->f.ndpn;
+  const int64_t n = m->n_dofs_local;
   double* part = m->sol_part;
   double* fin = part + size_t(kRedBlocks) * 4;
-  if (m->f.ndpn == 2) k_delta_sumsq<2><<<kRedBlocks, 256, 0, m->stream>>>(n, delta, m->dofs, part);
+  if (m->mixed) k_delta_sumsq_kind<<<kRedBlocks, 256, 0, m->stream>>>(n, m->f.dim, m->dkind, delta, m->dofs, part);
+  else if (m->f.ndpn == 2) k_delta_sumsq<2><<<kRedBlocks, 256, 0, m->stream>>>(n, delta, m->dofs, part);
   else if (m->f.ndpn == 3) k_delta_sumsq<3><<<kRedBlocks, 256, 0, m->stream>>>(n, delta, m->dofs, part);
   else k_delta_sumsq<4><<<kRedBlocks, 256, 0, m->stream>>>(n, delta, m->dofs, part);
   k_final<4><<<1, 256, 0, m->stream>>>(kRedBlocks, part, fin);
@@ -943,7 +1238,8 @@ lgdm_status lgdm_residual_sumsq(lgdm_mesh m, double* out2, int on_device) {
   if (!m || !out2) return fail(LGDM_ERR_INVALID_ARGUMENT, "NULL argument");
   if (!m->assembled) return fail(LGDM_ERR_INVALID_STATE, "residual before assemble");
   CU(cudaSetDevice(m->device));
-  k_sumsq_partial<<<kSumBlocks, kSumThreads, 0, m->stream>>>(m->n_rows, m->f.ndpn, m->f.dim, m->R, m->sumsq_part);
+  if (m->mixed) k_sumsq_kind<<<kSumBlocks, kSumThreads, 0, m->stream>>>(m->n_rows, m->f.dim, m->dkind, m->R, m->sumsq_part);
+  else k_sumsq_partial<<<kSumBlocks, kSumThreads, 0, m->stream>>>(m->n_rows, m->f.ndpn, m->f.dim, m->R, m->sumsq_part);
   lgdm_status s = check_launch(m, "k_sumsq_partial");
   if (s != LGDM_OK) return s;
   double* dst = on_device ? out2 : m->sumsq_out;
@@ -1014,13 +1310,14 @@ lgdm_status lgdm_scale_dofs(lgdm_mesh m, double sc) {
   if (!m) return fail(LGDM_ERR_INVALID_ARGUMENT, "mesh is NULL");
   if (!m->have_state) return fail(LGDM_ERR_INVALID_STATE, "scale before set_state");
   CU(cudaSetDevice(m->device));
-  const int64_t n = m->n_nodes * m->f.ndpn;
+  const int64_t n = m->n_dofs_local;
   k_scale<<<unsigned((n + 255) / 256), 256, 0, m->stream>>>(n, sc, m->dofs);
   return check_launch(m, "k_scale");
 }
 
 lgdm_status lgdm_set_kernel(lgdm_mesh m, int kernel) {
   if (!m || kernel < 0 || kernel > 5) return fail(LGDM_ERR_INVALID_ARGUMENT, "bad kernel selector");
+  if (m->mixed && kernel > 1) return fail(LGDM_ERR_INVALID_ARGUMENT, "mixed-order meshes: kernels 0 and 1 only");
   if (kernel >= 2 && !(m->structured && sweep_supported(m)))
     return fail(LGDM_ERR_INVALID_ARGUMENT, "sweep kernel needs a structured mesh with whole owned layers");
   m->kernel = kernel;
@@ -1057,7 +1354,8 @@ void lgdm_destroy(lgdm_mesh m) {
   void* ptrs[] = {m->coords, m->conn, m->dofs, m->kappa, m->row_ptr, m->col_idx, m->val, m->R,
                   m->nbr_ptr, m->base, m->adj_ptr, m->adj, m->scratchK, m->scratchF,
                   m->sumsq_part, m->sumsq_out, m->k0g, m->alg, m->sdv_dev, m->rp_b,
-                  m->ci_b, m->val_b, m->R_b, m->sol, m->sol_part, m->fixed, m->fixinc};
+                  m->ci_b, m->val_b, m->R_b, m->sol, m->sol_part, m->fixed, m->fixinc,
+                  m->doff, m->dkind, m->madj_ptr, m->madj};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (m->host_pinned) cudaFreeHost(m->host_pinned);

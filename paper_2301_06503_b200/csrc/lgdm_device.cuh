@@ -145,115 +145,16 @@ template <int D> struct Core {
   static constexpr int STRIDE = (USED % 2 == 1) ? USED : USED + 1;
 };
 
-// ---------------------------------------------------------------------------------------
-// Phase A, part 1 ("core"): one Gauss point g of one element.  X [NEN][D] coords,
-// U [NEN][NDPN] dofs, kh = kappa_hist.  Writes the compact GP state (Core<D> layout) to core.
-// Returns det J (caller treats <= 0 as an inverted element).
-// ---------------------------------------------------------------------------------------
-// Shape values are supplied by SHD(a, j) = dN_a/dxi_j and SHN(a) = N_a at the Gauss point
-// (gpCore below passes the closed forms; kernels may pass register copies of a table).
-// k0 / al: the GP's damage threshold kappa0 and alpha (defect regions, P:418; the material's
-// values unless per-GP fields are set, lgdm_set_defects).
-template <int D, class XF, class UF, class SD, class SN>
-__device__ __forceinline__ double gpCoreSK(const DevMat& m, XF&& X, UF&& U, double kh, double k0,
-                                           double al, SD&& SHD, SN&& SHN, double* __restrict__ core) {
+// Constitutive part of the GP core (Appendix A, Eqs. 2-4, 11a-f coefficients): from the
+// Voigt-tensor strain es (tensor shear), ebar, grad ebar, the history kh, the GP's kappa0 /
+// alpha, dV and J^-1 to the compact GP state (Core<D> layout).  Shared by the equal-order
+// core below and the mixed-order elements (lgdm_mixed.cuh).
+template <int D>
+__device__ __forceinline__ void gpLaw(const DevMat& m, const double (&Ji)[D][D], double dV,
+                                      const double* es, double ebar, const double* gb, double kh,
+                                      double k0, double al, double* __restrict__ core) {
   using Co = Core<D>;
-  using F = Fam<D>;
-  constexpr int NEN = F::NEN, NS = F::NS;
-
-  // geometry: J_ij = sum_a X_ai dN_a/dxi_j
-  double J[D][D];
-#pragma unroll
-  for (int i = 0; i < D; ++i)
-#pragma unroll
-    for (int j = 0; j < D; ++j) J[i][j] = 0.0;
-#pragma unroll
-  for (int a = 0; a < NEN; ++a)
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-      const double dn = SHD(a, j);
-#pragma unroll
-      for (int i = 0; i < D; ++i) J[i][j] = fma(X(a, i), dn, J[i][j]);
-    }
-  double detJ, Ji[D][D];
-  if constexpr (D == 1) {
-    detJ = J[0][0];
-    Ji[0][0] = 1.0 / detJ;
-  } else if constexpr (D == 2) {
-    detJ = J[0][0] * J[1][1] - J[0][1] * J[1][0];
-    const double r = 1.0 / detJ;
-    Ji[0][0] = J[1][1] * r;
-    Ji[0][1] = -J[0][1] * r;
-    Ji[1][0] = -J[1][0] * r;
-    Ji[1][1] = J[0][0] * r;
-  } else {
-    const double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
-    const double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
-    const double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
-    detJ = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
-    const double r = 1.0 / detJ;
-    Ji[0][0] = c00 * r;
-    Ji[1][0] = c01 * r;
-    Ji[2][0] = c02 * r;
-    Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * r;
-    Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * r;
-    Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * r;
-    Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * r;
-    Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * r;
-    Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * r;
-  }
-  const double dV = detJ * m.t;  // Gauss weights are 1
-
-  // grad N_a = J^-T dN/dxi (recomputed where needed instead of kept live); kinematics
-  auto gradN = [&](int a, double* gn) {
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-      double s = 0.0;
-#pragma unroll
-      for (int j = 0; j < D; ++j) s = fma(Ji[j][i], SHD(a, j), s);
-      gn[i] = s;
-    }
-  };
-  double eps[D][D], ebar = 0.0, gb[D];
-#pragma unroll
-  for (int i = 0; i < D; ++i) {
-    gb[i] = 0.0;
-#pragma unroll
-    for (int j = 0; j < D; ++j) eps[i][j] = 0.0;
-  }
-#pragma unroll
-  for (int a = 0; a < NEN; ++a) {
-    double gn[D];
-    gradN(a, gn);
-    const double ea = U(a, D);
-    ebar = fma(SHN(a), ea, ebar);
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-      gb[i] = fma(gn[i], ea, gb[i]);
-      {
-        const double ua = U(a, i);
-#pragma unroll
-        for (int j = 0; j < D; ++j) eps[i][j] = fma(ua, gn[j], eps[i][j]);
-      }
-    }
-  }
-  // symmetrise: eps_ij = (du_i/dx_j + du_j/dx_i)/2
-  double es[NS];
-  if constexpr (D == 1) {
-    es[0] = eps[0][0];
-  } else if constexpr (D == 2) {
-    es[0] = eps[0][0];
-    es[1] = eps[1][1];
-    es[2] = 0.5 * (eps[0][1] + eps[1][0]);
-  } else {
-    es[0] = eps[0][0];
-    es[1] = eps[1][1];
-    es[2] = eps[2][2];
-    es[3] = 0.5 * (eps[0][1] + eps[1][0]);
-    es[4] = 0.5 * (eps[1][2] + eps[2][1]);
-    es[5] = 0.5 * (eps[0][2] + eps[2][0]);
-  }
-
+  constexpr int NS = Fam<D>::NS;
   // ---- Appendix A: equivalent strain, history, damage, interaction ----
   double I1, eeq, dm, ds;  // d = dm * m + ds * s
   double S[NS];            // deviatoric strain tensor (in-plane part in 2D)
@@ -376,6 +277,117 @@ __device__ __forceinline__ double gpCoreSK(const DevMat& m, XF&& X, UF&& U, doub
     core[Co::GV + i] = gv[i];
     core[Co::FV + i] = fv[i];
   }
+}
+
+// ---------------------------------------------------------------------------------------
+// Phase A, part 1 ("core"): one Gauss point g of one element.  X [NEN][D] coords,
+// U [NEN][NDPN] dofs, kh = kappa_hist.  Writes the compact GP state (Core<D> layout) to core.
+// Returns det J (caller treats <= 0 as an inverted element).
+// ---------------------------------------------------------------------------------------
+// Shape values are supplied by SHD(a, j) = dN_a/dxi_j and SHN(a) = N_a at the Gauss point
+// (gpCore below passes the closed forms; kernels may pass register copies of a table).
+// k0 / al: the GP's damage threshold kappa0 and alpha (defect regions, P:418; the material's
+// values unless per-GP fields are set, lgdm_set_defects).
+template <int D, class XF, class UF, class SD, class SN>
+__device__ __forceinline__ double gpCoreSK(const DevMat& m, XF&& X, UF&& U, double kh, double k0,
+                                           double al, SD&& SHD, SN&& SHN, double* __restrict__ core) {
+  using F = Fam<D>;
+  constexpr int NEN = F::NEN, NS = F::NS;
+
+  // geometry: J_ij = sum_a X_ai dN_a/dxi_j
+  double J[D][D];
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) J[i][j] = 0.0;
+#pragma unroll
+  for (int a = 0; a < NEN; ++a)
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const double dn = SHD(a, j);
+#pragma unroll
+      for (int i = 0; i < D; ++i) J[i][j] = fma(X(a, i), dn, J[i][j]);
+    }
+  double detJ, Ji[D][D];
+  if constexpr (D == 1) {
+    detJ = J[0][0];
+    Ji[0][0] = 1.0 / detJ;
+  } else if constexpr (D == 2) {
+    detJ = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+    const double r = 1.0 / detJ;
+    Ji[0][0] = J[1][1] * r;
+    Ji[0][1] = -J[0][1] * r;
+    Ji[1][0] = -J[1][0] * r;
+    Ji[1][1] = J[0][0] * r;
+  } else {
+    const double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+    const double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+    const double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+    detJ = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
+    const double r = 1.0 / detJ;
+    Ji[0][0] = c00 * r;
+    Ji[1][0] = c01 * r;
+    Ji[2][0] = c02 * r;
+    Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * r;
+    Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * r;
+    Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * r;
+    Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * r;
+    Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * r;
+    Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * r;
+  }
+  const double dV = detJ * m.t;  // Gauss weights are 1
+
+  // grad N_a = J^-T dN/dxi (recomputed where needed instead of kept live); kinematics
+  auto gradN = [&](int a, double* gn) {
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) s = fma(Ji[j][i], SHD(a, j), s);
+      gn[i] = s;
+    }
+  };
+  double eps[D][D], ebar = 0.0, gb[D];
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    gb[i] = 0.0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) eps[i][j] = 0.0;
+  }
+#pragma unroll
+  for (int a = 0; a < NEN; ++a) {
+    double gn[D];
+    gradN(a, gn);
+    const double ea = U(a, D);
+    ebar = fma(SHN(a), ea, ebar);
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      gb[i] = fma(gn[i], ea, gb[i]);
+      {
+        const double ua = U(a, i);
+#pragma unroll
+        for (int j = 0; j < D; ++j) eps[i][j] = fma(ua, gn[j], eps[i][j]);
+      }
+    }
+  }
+  // symmetrise: eps_ij = (du_i/dx_j + du_j/dx_i)/2
+  double es[NS];
+  if constexpr (D == 1) {
+    es[0] = eps[0][0];
+  } else if constexpr (D == 2) {
+    es[0] = eps[0][0];
+    es[1] = eps[1][1];
+    es[2] = 0.5 * (eps[0][1] + eps[1][0]);
+  } else {
+    es[0] = eps[0][0];
+    es[1] = eps[1][1];
+    es[2] = eps[2][2];
+    es[3] = 0.5 * (eps[0][1] + eps[1][0]);
+    es[4] = 0.5 * (eps[1][2] + eps[2][1]);
+    es[5] = 0.5 * (eps[0][2] + eps[2][0]);
+  }
+
+  gpLaw<D>(m, Ji, dV, es, ebar, gb, kh, k0, al, core);
   return detJ;
 }
 

@@ -1,0 +1,422 @@
+// lgdm_mixed.cuh -- mixed-order elements: quadratic u with linear ebar, the
+// paper's own discretisation ("shape functions for displacement (u) are taken as
+// quadratic, and for micro-equivalent strain as linear"; 1D bar P:418; 2D SEN P:466).
+//   LGDM_BAR3  (4): 3-node quadratic bar for u (local nodes xi = -1, +1, 0), linear ebar on
+//                   the two end nodes, 3-point Gauss.
+//   LGDM_QUAD8 (5): 8-node serendipity quad for u (corners counter-clockwise, then midsides
+//                   (0,-1), (1,0), (0,1), (-1,0)), bilinear ebar on the corners, 3x3 Gauss
+//                   (readings R-Q8, R-GEO, R-GP3, R-ORDM).
+// Local element dofs are node-major: corner a < NENE holds (u_0..u_{D-1}, ebar) at a (D+1);
+// midside a >= NENE holds (u_0..u_{D-1}) at NENE (D+1) + (a - NENE) D.  Global dof of node n,
+// component c = doff[n] + c.
+//
+// Two kernels, as the general equal-order path (k_elem_blocks + k_gather):
+//   k_mixed_blocks  one warp per element: GP cores (lanes g < NGP; the constitutive part is
+//                   gpLaw of lgdm_device.cuh), per-(GP, node) records in shared memory, then
+//                   node-pair Gauss sums (lanes over the NENU^2 ordered pairs) -> element
+//                   blocks Ke [NDOFE][NDOFE], Fe [NDOFE] in HBM;
+//   k_mixed_gather  one warp per node: the node's CSR block-row accumulated in shared memory
+//                   over its adjacent elements in ascending element id (atomic-free, bitwise
+//                   reproducible), then written once, coalesced.
+#pragma once
+#include <cstdint>
+
+namespace lgdm {
+
+template <int T> struct MFam;
+template <> struct MFam<4> {
+  static constexpr int DIM = 1, NENU = 3, NENE = 2, NGP = 3, NS = 1, NDOFE = 5;
+};
+template <> struct MFam<5> {
+  static constexpr int DIM = 2, NENU = 8, NENE = 4, NGP = 9, NS = 3, NDOFE = 20;
+};
+
+template <int T> __host__ __device__ constexpr int mldof(int a) {
+  using F = MFam<T>;
+  return a < F::NENE ? a * (F::DIM + 1) : F::NENE * (F::DIM + 1) + (a - F::NENE) * F::DIM;
+}
+// local dof -> (node, component)
+template <int T> __host__ __device__ constexpr int mdof_node(int c) {
+  using F = MFam<T>;
+  return c < F::NENE * (F::DIM + 1) ? c / (F::DIM + 1) : F::NENE + (c - F::NENE * (F::DIM + 1)) / F::DIM;
+}
+template <int T> __host__ __device__ constexpr int mdof_comp(int c) {
+  using F = MFam<T>;
+  return c < F::NENE * (F::DIM + 1) ? c % (F::DIM + 1) : (c - F::NENE * (F::DIM + 1)) % F::DIM;
+}
+
+// Shape-function values at the Gauss points, tabulated once on the host (lgdm_api.cu,
+// mixed_tables) into constant memory: every lane of a warp reads the same GP row.
+template <int T> struct MShape {
+  using F = MFam<T>;
+  double w[F::NGP];
+  double Nu[F::NGP][F::NENU], dNu[F::NGP][F::NENU][F::DIM];
+  double Ne[F::NGP][F::NENE], dNe[F::NGP][F::NENE][F::DIM];
+};
+__constant__ MShape<4> c_shape4;
+__constant__ MShape<5> c_shape5;
+template <int T> __device__ __forceinline__ const MShape<T>& mshape();
+template <> __device__ __forceinline__ const MShape<4>& mshape<4>() { return c_shape4; }
+template <> __device__ __forceinline__ const MShape<5>& mshape<5>() { return c_shape5; }
+
+// per-(GP, u node) record: grad N, S grad N, t1, t2, W' grad N, Dt' grad N, Sigma' grad N
+template <int D> struct MURec {
+  static constexpr int GN = 0, SGN = D, T1 = 2 * D, T2 = 3 * D, WGN = 4 * D, DGN = 5 * D,
+                       FU = 6 * D, STRIDE = 7 * D + 1;   // odd: spreads banks
+};
+// per-(GP, ebar node) record: N, grad N, hN N + gvec . grad N (Kee), fe0 N + fvec . grad N (Fe)
+template <int D> struct MERec {
+  static constexpr int N = 0, GN = 1, E = 1 + D, FE = 2 + D, STRIDE = 3 + D + ((3 + D) % 2 == 0);
+};
+
+template <int T> struct MSmem {   // doubles per warp (one element)
+  using F = MFam<T>;
+  static constexpr int D = F::DIM;
+  static constexpr int X = 0, U = X + F::NENU * D, CORE = U + F::NDOFE,
+                       UR = CORE + F::NGP * Core<D>::STRIDE,
+                       ER = UR + F::NGP * F::NENU * MURec<D>::STRIDE,
+                       SIZE = ER + F::NGP * F::NENE * MERec<D>::STRIDE;
+};
+
+template <int T, int WPB>
+__global__ void __launch_bounds__(WPB * 32)
+k_mixed_blocks(DevMat m, int64_t ne, const int32_t* __restrict__ conn, const double* __restrict__ coords,
+               const int64_t* __restrict__ doff, const double* __restrict__ dofs,
+               const double* __restrict__ kappa, const double* __restrict__ k0g,
+               const double* __restrict__ alg, double* __restrict__ EB, double* __restrict__ EF) {
+  using F = MFam<T>;
+  constexpr int D = F::DIM, NGP = F::NGP, NENU = F::NENU, NENE = F::NENE, ND = F::NDOFE;
+  using SM = MSmem<T>;
+  using UR = MURec<D>;
+  using ER = MERec<D>;
+  using Co = Core<D>;
+  extern __shared__ double smem_mx[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double* sm = smem_mx + w * SM::SIZE;
+  const MShape<T>& S = mshape<T>();
+  for (int64_t e = int64_t(blockIdx.x) * WPB + w; e < ne; e += int64_t(gridDim.x) * WPB) {
+    // gather coordinates and element dofs
+    for (int k = lane; k < NENU * D; k += 32) {
+      const int a = k / D, i = k % D;
+      sm[SM::X + k] = coords[int64_t(conn[e * NENU + a]) * D + i];
+    }
+    for (int c = lane; c < ND; c += 32)
+      sm[SM::U + c] = dofs[doff[conn[e * NENU + mdof_node<T>(c)]] + mdof_comp<T>(c)];
+    __syncwarp();
+    // GP cores: geometry on the u nodes (R-GEO), kinematics, Appendix A law
+    if (lane < NGP) {
+      const int g = lane;
+      double J[D][D];
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) J[i][j] = 0.0;
+#pragma unroll
+      for (int a = 0; a < NENU; ++a)
+#pragma unroll
+        for (int j = 0; j < D; ++j)
+#pragma unroll
+          for (int i = 0; i < D; ++i) J[i][j] = fma(sm[SM::X + a * D + i], S.dNu[g][a][j], J[i][j]);
+      double detJ, Ji[D][D];
+      if constexpr (D == 1) {
+        detJ = J[0][0];
+        Ji[0][0] = 1.0 / detJ;
+      } else {
+        detJ = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+        const double r = 1.0 / detJ;
+        Ji[0][0] = J[1][1] * r;
+        Ji[0][1] = -J[0][1] * r;
+        Ji[1][0] = -J[1][0] * r;
+        Ji[1][1] = J[0][0] * r;
+      }
+      const double dV = S.w[g] * detJ * m.t;
+      double eps[D][D], ebar = 0.0, gb[D];
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        gb[i] = 0.0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) eps[i][j] = 0.0;
+      }
+#pragma unroll
+      for (int a = 0; a < NENU; ++a) {
+        double gn[D];
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          double s = 0.0;
+#pragma unroll
+          for (int j = 0; j < D; ++j) s = fma(Ji[j][i], S.dNu[g][a][j], s);
+          gn[i] = s;
+        }
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          const double ua = sm[SM::U + mldof<T>(a) + i];
+#pragma unroll
+          for (int j = 0; j < D; ++j) eps[i][j] = fma(ua, gn[j], eps[i][j]);
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < NENE; ++a) {
+        const double ea = sm[SM::U + mldof<T>(a) + D];
+        ebar = fma(S.Ne[g][a], ea, ebar);
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          double s = 0.0;
+#pragma unroll
+          for (int j = 0; j < D; ++j) s = fma(Ji[j][i], S.dNe[g][a][j], s);
+          gb[i] = fma(s, ea, gb[i]);
+        }
+      }
+      double es[F::NS];
+      if constexpr (D == 1) {
+        es[0] = eps[0][0];
+      } else {
+        es[0] = eps[0][0];
+        es[1] = eps[1][1];
+        es[2] = 0.5 * (eps[0][1] + eps[1][0]);
+      }
+      const int64_t q = e * NGP + g;
+      gpLaw<D>(m, Ji, dV, es, ebar, gb, kappa[q], k0g ? k0g[q] : m.kappa0, alg ? alg[q] : m.alpha,
+               sm + SM::CORE + g * Co::STRIDE);
+    }
+    __syncwarp();
+    // per-(GP, node) records
+    for (int k = lane; k < NGP * NENU; k += 32) {
+      const int g = k / NENU, a = k % NENU;
+      const double* core = sm + SM::CORE + g * Co::STRIDE;
+      double* r = sm + SM::UR + k * UR::STRIDE;
+      double gn[D], SgN[D], WgN[D], DgN[D], fu[D];
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) s = fma(core[Co::JI + j * D + i], S.dNu[g][a][j], s);
+        gn[i] = s;
+      }
+      symv<D>(core + Co::S, gn, SgN);
+      symv<D>(core + Co::WT, gn, WgN);
+      symv<D>(core + Co::DT, gn, DgN);
+      symv<D>(core + Co::SG, gn, fu);
+      const double lamS = core[Co::LAM], Ams = core[Co::AMS], Ass = core[Co::ASS];
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        r[UR::GN + i] = gn[i];
+        r[UR::SGN + i] = SgN[i];
+        r[UR::T1 + i] = fma(lamS, gn[i], Ams * SgN[i]);
+        r[UR::T2 + i] = fma(Ams, gn[i], Ass * SgN[i]);
+        r[UR::WGN + i] = WgN[i];
+        r[UR::DGN + i] = DgN[i];
+        r[UR::FU + i] = fu[i];
+      }
+    }
+    for (int k = lane; k < NGP * NENE; k += 32) {
+      const int g = k / NENE, a = k % NENE;
+      const double* core = sm + SM::CORE + g * Co::STRIDE;
+      double* r = sm + SM::ER + k * ER::STRIDE;
+      double gvd = 0.0, fvd = 0.0;
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) s = fma(core[Co::JI + j * D + i], S.dNe[g][a][j], s);
+        r[ER::GN + i] = s;
+        gvd = fma(core[Co::GV + i], s, gvd);
+        fvd = fma(core[Co::FV + i], s, fvd);
+      }
+      const double Na = S.Ne[g][a];
+      r[ER::N] = Na;
+      r[ER::E] = fma(core[Co::HN], Na, gvd);
+      r[ER::FE] = fma(core[Co::FE0], Na, fvd);
+    }
+    __syncwarp();
+    // node-pair Gauss sums (Eqs. 11a-d), written in the local dof order
+    double* Ke = EB + e * (ND * ND);
+    for (int p = lane; p < NENU * NENU; p += 32) {
+      const int a = p / NENU, b = p % NENU;
+      const bool ea = a < NENE, eb = b < NENE;
+      double Kuu[D][D], Kue[D], Keu[D], Kee = 0.0;
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        Kue[i] = Keu[i] = 0.0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) Kuu[i][j] = 0.0;
+      }
+#pragma unroll 1
+      for (int g = 0; g < NGP; ++g) {
+        const double* A = sm + SM::UR + (g * NENU + a) * UR::STRIDE;
+        const double* B = sm + SM::UR + (g * NENU + b) * UR::STRIDE;
+        const double* core = sm + SM::CORE + g * Co::STRIDE;
+        const double mu = core[Co::MU];
+        double dot = 0.0;
+#pragma unroll
+        for (int i = 0; i < D; ++i) dot = fma(A[UR::GN + i], B[UR::GN + i], dot);
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          const double ub = mu * B[UR::GN + i];
+#pragma unroll
+          for (int j = 0; j < D; ++j) {
+            double v = Kuu[i][j];
+            v = fma(A[UR::GN + i], B[UR::T1 + j], v);
+            v = fma(A[UR::SGN + i], B[UR::T2 + j], v);
+            v = fma(A[UR::GN + j], ub, v);
+            Kuu[i][j] = v;
+          }
+          Kuu[i][i] = fma(mu, dot, Kuu[i][i]);
+        }
+        if (eb) {
+          const double NB = sm[SM::ER + (g * NENE + b) * ER::STRIDE + ER::N];
+#pragma unroll
+          for (int i = 0; i < D; ++i) Kue[i] = fma(NB, A[UR::WGN + i], Kue[i]);
+        }
+        if (ea) {
+          const double* EA = sm + SM::ER + (g * NENE + a) * ER::STRIDE;
+#pragma unroll
+          for (int i = 0; i < D; ++i) Keu[i] = fma(EA[ER::N], B[UR::DGN + i], Keu[i]);
+          if (eb) {
+            const double* EBr = sm + SM::ER + (g * NENE + b) * ER::STRIDE;
+            double dote = 0.0;
+#pragma unroll
+            for (int i = 0; i < D; ++i) dote = fma(EA[ER::GN + i], EBr[ER::GN + i], dote);
+            Kee = fma(EBr[ER::N], EA[ER::E], fma(core[Co::GHC], dote, Kee));
+          }
+        }
+      }
+      const int ra = mldof<T>(a), cb = mldof<T>(b);
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) Ke[(ra + i) * ND + cb + j] = Kuu[i][j];
+        if (eb) Ke[(ra + i) * ND + cb + D] = Kue[i];
+        if (ea) Ke[(ra + D) * ND + cb + i] = Keu[i];
+      }
+      if (ea && eb) Ke[(ra + D) * ND + cb + D] = Kee;
+    }
+    // residual (Eqs. 11e, 11f)
+    for (int c = lane; c < ND; c += 32) {
+      const int a = mdof_node<T>(c), i = mdof_comp<T>(c);
+      double f = 0.0;
+      if (i < D) {
+#pragma unroll 1
+        for (int g = 0; g < NGP; ++g) f += sm[SM::UR + (g * NENU + a) * UR::STRIDE + UR::FU + i];
+      } else {
+#pragma unroll 1
+        for (int g = 0; g < NGP; ++g) f += sm[SM::ER + (g * NENE + a) * ER::STRIDE + ER::FE];
+      }
+      EF[e * ND + c] = f;
+    }
+    __syncwarp();
+  }
+}
+
+// node -> adjacent element map of the gather: element, local index of the node, and the
+// column offset (within the node's block-row) of each local node's first dof
+struct MixAdj {
+  int32_t e;
+  int32_t aloc;
+  int32_t coff[8];
+};
+
+template <int T, int WPB>
+__global__ void __launch_bounds__(WPB * 32)
+k_mixed_gather(int64_t nn, const int64_t* __restrict__ adj_ptr, const MixAdj* __restrict__ adj,
+               const int64_t* __restrict__ doff, const int64_t* __restrict__ row_ptr,
+               const double* __restrict__ EB, const double* __restrict__ EF, int max_row,
+               double* __restrict__ val, double* __restrict__ R) {
+  using F = MFam<T>;
+  constexpr int ND = F::NDOFE;
+  extern __shared__ double smem_mg[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double* buf = smem_mg + w * max_row;
+  for (int64_t n = int64_t(blockIdx.x) * WPB + w; n < nn; n += int64_t(gridDim.x) * WPB) {
+    const int64_t r0 = doff[n];
+    const int nr = int(doff[n + 1] - r0);
+    const int64_t base = row_ptr[r0];
+    const int W = int(row_ptr[r0 + 1] - base);
+    const int tot = nr * W;
+    for (int k = lane; k < tot; k += 32) buf[k] = 0.0;
+    double rsum = 0.0;
+    __syncwarp();
+    for (int64_t k = adj_ptr[n]; k < adj_ptr[n + 1]; ++k) {
+      const MixAdj en = adj[k];
+      const int lr = mldof<T>(en.aloc);
+      const double* src = EB + int64_t(en.e) * (ND * ND) + lr * ND;
+      for (int q = lane; q < nr * ND; q += 32) {
+        const int i = q / ND, c = q % ND;
+        buf[i * W + en.coff[mdof_node<T>(c)] + mdof_comp<T>(c)] += src[q];
+      }
+      if (lane < nr) rsum += EF[int64_t(en.e) * ND + lr + lane];
+      __syncwarp();
+    }
+    for (int k = lane; k < tot; k += 32) val[base + k] = buf[k];
+    if (lane < nr) R[r0 + lane] = rsum;
+    __syncwarp();
+  }
+}
+
+template <int T>
+__global__ void k_mixed_detj(int64_t ne, const int32_t* __restrict__ conn,
+                             const double* __restrict__ coords, unsigned long long* bad) {
+  using F = MFam<T>;
+  constexpr int D = F::DIM;
+  const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (t >= ne * F::NGP) return;
+  const int64_t e = t / F::NGP;
+  const int g = int(t % F::NGP);
+  const MShape<T>& S = mshape<T>();
+  double J[D][D];
+  for (int i = 0; i < D; ++i)
+    for (int j = 0; j < D; ++j) J[i][j] = 0.0;
+  for (int a = 0; a < F::NENU; ++a) {
+    const int64_t n = conn[e * F::NENU + a];
+    for (int j = 0; j < D; ++j)
+      for (int i = 0; i < D; ++i) J[i][j] += coords[n * D + i] * S.dNu[g][a][j];
+  }
+  double det;
+  if constexpr (D == 1) det = J[0][0];
+  else det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+  if (!(det > 0.0)) atomicMin(bad, (unsigned long long)t);
+}
+
+// Eq. A.2 with Fig. 8b l.19-24: ebar at the GP from the linear ebar field
+template <int T>
+__global__ void k_mixed_history(int64_t ne, const int32_t* __restrict__ conn,
+                                const int64_t* __restrict__ doff, const double* __restrict__ dofs,
+                                double* __restrict__ kappa) {
+  using F = MFam<T>;
+  const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (t >= ne * F::NGP) return;
+  const int64_t e = t / F::NGP;
+  const int g = int(t % F::NGP);
+  const MShape<T>& S = mshape<T>();
+  double eb = 0.0;
+#pragma unroll
+  for (int a = 0; a < F::NENE; ++a) eb = fma(S.Ne[g][a], dofs[doff[conn[e * F::NENU + a]] + F::DIM], eb);
+  const double k = kappa[t];
+  if ((eb - k) > 1e-10) kappa[t] = eb;
+}
+
+// ||R_u||^2, ||R_e||^2 by dof kind (kind[i] = component; ebar = dim)
+__global__ void k_sumsq_kind(int64_t n, int dim, const uint8_t* __restrict__ kind,
+                             const double* __restrict__ R, double* __restrict__ part) {
+  double v[2] = {0.0, 0.0};
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const double x = R[i];
+    if (kind[i] == dim) v[1] = fma(x, x, v[1]);
+    else v[0] = fma(x, x, v[0]);
+  }
+  block_sum_store<2>(v, part);
+}
+
+__global__ void k_delta_sumsq_kind(int64_t n, int dim, const uint8_t* __restrict__ kind,
+                                   const double* __restrict__ delta, const double* __restrict__ dofs,
+                                   double* __restrict__ part) {
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const bool e = kind[i] == dim;
+    const double d = delta[i], u = dofs[i];
+    v[e ? 2 : 0] = fma(d, d, v[e ? 2 : 0]);
+    v[e ? 3 : 1] = fma(u, u, v[e ? 3 : 1]);
+  }
+  block_sum_store<4>(v, part);
+}
+
+}  // namespace lgdm

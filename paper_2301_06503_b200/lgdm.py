@@ -15,8 +15,10 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("LGDM_LIB") or os.path.join(_HERE, "liblgdm.so")   # override: experiments
 
 BAR2, QUAD4, HEX8 = 1, 2, 3
-# type -> (dim, nen, ndpn, ngp)
-FAMILY = {BAR2: (1, 2, 2, 2), QUAD4: (2, 4, 3, 4), HEX8: (3, 8, 4, 8)}
+BAR3, QUAD8 = 4, 5          # mixed order: quadratic u, linear ebar
+# type -> (dim, nen, ndpn, ngp); mixed families: nen = u nodes, ndpn = dofs of a corner node
+FAMILY = {BAR2: (1, 2, 2, 2), QUAD4: (2, 4, 3, 4), HEX8: (3, 8, 4, 8),
+          BAR3: (1, 3, 2, 3), QUAD8: (2, 8, 3, 9)}
 KERNEL_AUTO, KERNEL_GENERAL, KERNEL_SWEEP, KERNEL_SWEEP3, KERNEL_SWEEP4, KERNEL_SWEEP5 = 0, 1, 2, 3, 4, 5
 
 STATUS = {0: "LGDM_OK", 1: "LGDM_ERR_INVALID_ARGUMENT", 2: "LGDM_ERR_INVERTED_ELEMENT",
@@ -30,7 +32,8 @@ EXPORTS = ["lgdm_create_mesh", "lgdm_set_state", "lgdm_assemble", "lgdm_update_h
            "lgdm_scale_dofs", "lgdm_set_kernel", "lgdm_get_info", "lgdm_launch_count",
            "lgdm_last_error", "lgdm_destroy", "lgdm_sdv_width", "lgdm_set_defects",
            "lgdm_update_state", "lgdm_get_blocked", "lgdm_apply_dirichlet", "lgdm_solve",
-           "lgdm_add_dofs", "lgdm_delta_norms", "lgdm_reaction", "lgdm_solve_direct"]
+           "lgdm_add_dofs", "lgdm_delta_norms", "lgdm_reaction", "lgdm_solve_direct",
+           "lgdm_dof_offsets"]
 
 
 class LGDMError(RuntimeError):
@@ -101,6 +104,7 @@ def load() -> C.CDLL:
     L.lgdm_delta_norms.argtypes = [vp, vp, dp]
     L.lgdm_reaction.argtypes = [vp, i64, vp, dp]
     L.lgdm_solve_direct.argtypes = [vp, vp, C.POINTER(C.c_int)]
+    L.lgdm_dof_offsets.argtypes = [vp, vp, i64]
     for name in EXPORTS:
         if name not in ("lgdm_launch_count", "lgdm_last_error", "lgdm_destroy"):
             getattr(L, name).restype = C.c_int
@@ -180,11 +184,14 @@ class Mesh:
                                   n_global_nodes, owned[0], owned[1], device, stream,
                                   C.byref(self._h)))
         self._keep = []
+        self.doff = np.zeros(self.n_nodes + 1, dtype=np.int64)
+        _check(L.lgdm_dof_offsets(self._h, self.doff.ctypes.data, self.doff.size))
+        self.n_dofs = int(self.doff[-1])
 
     # -- state / assembly -------------------------------------------------------------
     def set_state(self, dofs, kappa=None):
         pd, on_dev, kd = _ptr_and_kind(dofs)
-        n_d = self.n_nodes * self.ndpn
+        n_d = self.n_dofs
         if kappa is None:
             _check(load().lgdm_set_state(self._h, pd, n_d, None, 0, on_dev))
             self._keep = [kd]
@@ -219,7 +226,7 @@ class Mesh:
         """BiCGSTAB on the assembled (eliminated) system; returns (delta device tensor, iters,
         relative residual)."""
         import torch
-        n = self.n_nodes * self.ndpn
+        n = self.n_dofs
         if out is None:
             out = torch.empty(n, dtype=torch.float64, device=f"cuda:{self.device}")
         it = C.c_int()
@@ -230,7 +237,7 @@ class Mesh:
     def solve_direct(self, out=None):
         """Sparse QR on the GPU (cuSOLVER); returns the delta device tensor."""
         import torch
-        n = self.n_nodes * self.ndpn
+        n = self.n_dofs
         if out is None:
             out = torch.empty(n, dtype=torch.float64, device=f"cuda:{self.device}")
         sing = C.c_int()
@@ -285,6 +292,8 @@ class Mesh:
         [n_elems, ngp, sdv_width] (or fills `out`, a float64 tensor / numpy array)."""
         import torch
         W = load().lgdm_sdv_width(self.etype)
+        if W < 0:                                   # family without an SDV record (mixed)
+            _check(load().lgdm_update_state(self._h, None, 0, 0))
         n = self.n_elems * self.ngp * W
         if out is None:
             out = torch.empty((self.n_elems, self.ngp, W), dtype=torch.float64,

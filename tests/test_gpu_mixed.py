@@ -1,0 +1,206 @@
+"""GPU parity of the mixed-order elements (BAR3 quadratic u / linear ebar,
+QUAD8 serendipity u / bilinear ebar) against the CPU oracle, through the
+C ABI: assembly (CSR structure bit-exact, K and R within the north_star tolerances of
+tests/parity.py), defect fields, bitwise run-to-run reproducibility, history, residual norms,
+errors, and the paper's 1D bar run with its own discretisation through the GPU Newton loop."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from paper_2301_06503_b200 import lgdm
+
+from parity import compare
+
+pytestmark = pytest.mark.gpu
+
+MAT = dict(synth.MATERIAL)
+
+
+def _mesh(etype, n, distort=0.0, seed=3):
+    mesh = synth.mixed_mesh(etype, n, 10.0 * n[0] / 8 if etype == lgdm.QUAD8 else 100.0)
+    X = mesh.coords.copy()
+    if distort and etype == lgdm.QUAD8:
+        h = X[:, 0].max() / n[0]
+        corner_ids = np.nonzero(mesh.corner)[0]
+        lo, hi = X.min(axis=0), X.max(axis=0)
+        inner = np.all((X[corner_ids] > lo + 1e-9) & (X[corner_ids] < hi - 1e-9), axis=1)
+        rng = np.random.default_rng(seed)
+        X[corner_ids[inner]] += rng.uniform(-1, 1, size=(inner.sum(), 2)) * distort * h
+        for c in mesh.conn:
+            for k in range(4):
+                X[c[4 + k]] = 0.5 * (X[c[k]] + X[c[(k + 1) % 4]])
+    return mesh, X
+
+
+def _gpu(etype, X, conn, dofs, kappa, k0g=None, alg=None, kernel=0, mat_kw=None):
+    import torch
+    m = lgdm.Mesh(etype, X, conn, lgdm.material(**(mat_kw or MAT)))
+    m.set_kernel(kernel)
+    m.set_state(dofs, kappa)
+    if k0g is not None or alg is not None:
+        m.set_defects(k0g, alg)
+    out = m.assemble()
+    torch.cuda.synchronize()
+    got = {q: out[q].torch().cpu().numpy() for q in ("row_ptr", "col_idx", "val", "R")}
+    return m, got
+
+
+CASES = [(lgdm.BAR3, (7,), 0.0), (lgdm.BAR3, (61,), 0.0), (lgdm.QUAD8, (5, 3), 0.0),
+         (lgdm.QUAD8, (16, 11), 0.2), (lgdm.QUAD8, (40, 33), 0.1)]
+
+
+@pytest.mark.parametrize("etype,n,distort", CASES)
+@pytest.mark.parametrize("kernel", [0, 1])
+def test_mixed_parity(etype, n, distort, kernel):
+    mesh, X = _mesh(etype, n, distort)
+    dofs, kap = synth.mixed_fields(mesh)
+    ref = oracle.mixed_assemble(etype, oracle.material(**MAT), X, mesh.conn, dofs, kap)
+    m, got = _gpu(etype, X, mesh.conn, dofs, kap, kernel=kernel)
+    assert np.array_equal(m.doff, ref["doff"])
+    compare(ref, got, f"mixed {etype} {n}")
+    m.close()
+
+
+@pytest.mark.parametrize("hs,eqv", [(0.0, 0), (30000.0, 1)])
+def test_mixed_parity_readings(hs, eqv):
+    """reading R2 (h_sigma = 0) and the literal A.3 constants"""
+    mesh, X = _mesh(lgdm.QUAD8, (9, 7), 0.15)
+    dofs, kap = synth.mixed_fields(mesh)
+    kw = dict(MAT, h_sigma=hs, eq_variant=eqv)
+    ref = oracle.mixed_assemble(lgdm.QUAD8, oracle.material(**kw), X, mesh.conn, dofs, kap)
+    m, got = _gpu(lgdm.QUAD8, X, mesh.conn, dofs, kap, mat_kw=kw)
+    compare(ref, got, "readings")
+    m.close()
+
+
+@pytest.mark.parametrize("etype,n", [(lgdm.BAR3, (20,)), (lgdm.QUAD8, (8, 6))])
+def test_mixed_parity_defects(etype, n):
+    mesh, X = _mesh(etype, n)
+    dofs, kap = synth.mixed_fields(mesh)
+    ngp = synth.MFAM[etype][3]
+    rng = np.random.default_rng(9)
+    k0g = MAT["kappa0"] * rng.uniform(0.8, 1.2, size=kap.size)
+    alg = rng.uniform(0.9, 0.99, size=kap.size)
+    ref = oracle.mixed_assemble(etype, oracle.material(**MAT), X, mesh.conn, dofs, kap,
+                                kappa0_gp=k0g, alpha_gp=alg)
+    m, got = _gpu(etype, X, mesh.conn, dofs, kap, k0g=k0g, alg=alg)
+    compare(ref, got, "defects")
+    assert kap.shape[1] == ngp
+    m.close()
+
+
+def test_mixed_bitwise_reproducible():
+    mesh, X = _mesh(lgdm.QUAD8, (24, 19), 0.1)
+    dofs, kap = synth.mixed_fields(mesh)
+    m, a = _gpu(lgdm.QUAD8, X, mesh.conn, dofs, kap)
+    import torch
+    out = m.assemble()
+    torch.cuda.synchronize()
+    assert np.array_equal(out["val"].torch().cpu().numpy(), a["val"])
+    assert np.array_equal(out["R"].torch().cpu().numpy(), a["R"])
+    m.close()
+
+
+@pytest.mark.parametrize("etype,n", [(lgdm.BAR3, (33,)), (lgdm.QUAD8, (11, 9))])
+def test_mixed_history_and_norms(etype, n):
+    mesh, X = _mesh(etype, n)
+    dofs, kap = synth.mixed_fields(mesh)
+    dim = synth.MFAM[etype][0]
+    m, got = _gpu(etype, X, mesh.conn, dofs, kap)
+    ref = oracle.mixed_assemble(etype, oracle.material(**MAT), X, mesh.conn, dofs, kap)
+    kind = oracle.dof_kind(ref["doff"], dim)
+    nu, ne = m.residual_norms()
+    assert nu == pytest.approx(np.linalg.norm(ref["R"][kind < dim]), rel=1e-10)
+    assert ne == pytest.approx(np.linalg.norm(ref["R"][kind == dim]), rel=1e-10)
+    m.update_history()
+    k_ref = oracle.mixed_update_history(etype, mesh.conn, ref["doff"], dofs, kap)
+    # ebar_gp = sum N_a e_a: fused multiply-adds on the GPU, plain products in the oracle
+    np.testing.assert_allclose(m.get_kappa().reshape(k_ref.shape), k_ref, rtol=1e-15, atol=0)
+    m.close()
+
+
+def test_mixed_errors():
+    mesh, X = _mesh(lgdm.QUAD8, (3, 2))
+    bad = mesh.conn.copy()
+    bad[0, [1, 4]] = bad[0, [4, 1]]
+    with pytest.raises(lgdm.LGDMError) as ei:
+        lgdm.Mesh(lgdm.QUAD8, X, bad, lgdm.material(**MAT))
+    assert ei.value.status == 1
+    inv = mesh.conn.copy()
+    inv[0, :4] = inv[0, [1, 0, 3, 2]]                      # clockwise corners
+    inv[0, 4:] = inv[0, [4, 7, 6, 5]]
+    with pytest.raises(lgdm.LGDMError) as ei:
+        lgdm.Mesh(lgdm.QUAD8, X, inv, lgdm.material(**MAT))
+    assert ei.value.status == 2
+    with pytest.raises(lgdm.LGDMError) as ei:            # slabs: whole mesh only
+        lgdm.Mesh(lgdm.QUAD8, X, mesh.conn, lgdm.material(**MAT), owned=(0, 5))
+    assert ei.value.status == 1
+    dofs, kap = synth.mixed_fields(mesh)
+    m, _ = _gpu(lgdm.QUAD8, X, mesh.conn, dofs, kap)
+    with pytest.raises(lgdm.LGDMError) as ei:
+        m.set_kernel(2)
+    assert ei.value.status == 1
+    with pytest.raises(lgdm.LGDMError) as ei:
+        m.update_state()
+    assert ei.value.status == 7
+    with pytest.raises(lgdm.LGDMError) as ei:
+        m.get_blocked()
+    assert ei.value.status == 7
+    with pytest.raises(lgdm.LGDMError):                   # ebar dof of a corner node
+        m.apply_dirichlet([int(m.doff[0]) + 2], [0.0])
+    m.close()
+
+
+def test_bar3_softening_newton_matches_oracle():
+    """The paper's 1D bar (Sec. 3.1) with its own discretisation -- quadratic u, linear
+    ebar -- and a weaker middle region, displacement-controlled into softening: the GPU
+    Newton loop (direct solve) takes the oracle's iteration counts and reaches its reactions and
+    history; the reaction peaks then decays and damage localises in the defect."""
+    etype, n = lgdm.BAR3, 80
+    mesh = synth.mixed_mesh(etype, (n,), 100.0)
+    X = mesh.coords
+    xc = X[mesh.conn[:, 2], 0]
+    L = X[:, 0].max()
+    defect = np.abs(xc - L / 2) < 0.05 * L
+    k0g = np.repeat(np.where(defect, 0.9, 1.0) * MAT["kappa0"], 3)
+    om = oracle.material(**MAT)
+    doff = oracle.mixed_dofs(etype, X.shape[0], mesh.conn)
+    kind = oracle.dof_kind(doff, 1)
+    ids = np.array([doff[0], doff[2 * n]])
+    schedule = [(8, 1e-3), (30, 1e-4)]
+    nd = int(doff[-1])
+    dofs, kh = np.zeros(nd), np.zeros((n, 3))
+    its_ref, react_ref = [], []
+    for nst, du in schedule:
+        inc = np.array([0.0, du])
+        for _ in range(nst):
+            for it in range(1, 41):
+                res = oracle.mixed_assemble(etype, om, X, mesh.conn, dofs, kh, kappa0_gp=k0g)
+                delta = oracle.solve(oracle.apply_dirichlet(res, ids, inc if it == 1 else 0 * inc))
+                dofs = dofs + delta
+                ok, _, _ = oracle.converged_kind(delta, dofs, kind, 1, 1e-6)
+                if ok:
+                    break
+            assert ok
+            its_ref.append(it)
+            res = oracle.mixed_assemble(etype, om, X, mesh.conn, dofs, kh, kappa0_gp=k0g)
+            react_ref.append(oracle.reaction(res, [ids[1]]))
+            kh = oracle.mixed_update_history(etype, mesh.conn, doff, dofs, kh)
+    m = lgdm.Mesh(etype, X, mesh.conn, lgdm.material(**MAT))
+    m.set_state(np.zeros(nd), np.zeros((n, 3)))
+    m.set_defects(k0g, None)
+    log = []
+    for nst, du in schedule:
+        log += lgdm.newton(m, ids, [0.0, du], n_steps=nst, tol=1e-6, max_iter=40)
+    assert [s["iterations"] for s in log] == its_ref
+    r = np.array([s["reaction"] for s in log])
+    np.testing.assert_allclose(r, react_ref, rtol=1e-7)
+    kap = m.get_kappa().reshape(n, 3)
+    np.testing.assert_allclose(kap, kh, rtol=1e-7, atol=1e-14)
+    ip = int(r.argmax())
+    assert 8 <= ip < len(r) - 5
+    assert np.all(np.diff(r[ip:]) < 0)
+    kel = kap.max(axis=1)
+    assert kel[defect].min() > kel[~defect].max()
+    m.close()
