@@ -315,9 +315,12 @@ def mixed_fields(mesh: MixedMesh, cid: int = 200):
     proxy = Mesh(eq, mesh.coords, mesh.conn[:, :nene], 0, np.arange(ne, dtype=np.int64),
                  mesh.coords.shape[0], ne, mesh.shape)
     nodal, _ = fields(cfg, proxy)
-    parts = [np.concatenate([nodal[i, :dim], nodal[i, dim:dim + 1] if mesh.corner[i] else []])
-             for i in range(nodal.shape[0])]
-    dofs = np.concatenate(parts).astype(np.float64)
+    cnt = dim + mesh.corner.astype(np.int64)            # dofs per node
+    start = np.concatenate([[0], np.cumsum(cnt)[:-1]])
+    dofs = np.zeros(int(cnt.sum()))
+    for c in range(dim):
+        dofs[start + c] = nodal[:, c]
+    dofs[start[mesh.corner] + dim] = nodal[mesh.corner, dim]
     gp = (np.arange(ne, dtype=np.uint64)[:, None] * np.uint64(ngp) +
           np.arange(ngp, dtype=np.uint64)[None, :])
     kappa = np.maximum(MATERIAL["kappa0"], 4e-4 * uniform(cfg.seed, S_KAPPA, gp))
