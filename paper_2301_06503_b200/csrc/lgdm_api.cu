@@ -183,7 +183,7 @@ struct lgdm_mesh_s {
   std::vector<uint8_t> hkind;     // host component index per dof
   int64_t* doff = nullptr;        // device [n_nodes+1]
   uint8_t* dkind = nullptr;       // device [ndof]
-  int64_t* madj_ptr = nullptr;    // device [n_nodes+1]
+  NodeMeta* madj_ptr = nullptr;   // device [n_nodes] gather metadata
   MixAdj* madj = nullptr;         // device node -> element map of k_mixed_gather
   int max_row = 0;                // largest block-row (rows x width) in doubles
 };
@@ -534,7 +534,14 @@ lgdm_status create_mixed(lgdm_elem_type type, int64_t n_nodes, const double* coo
   }
   if ((s = upload(m, &m->row_ptr, row_ptr.data(), row_ptr.size())) != LGDM_OK) return bail(s);
   if ((s = upload(m, &m->col_idx, col.data(), col.size())) != LGDM_OK) return bail(s);
-  if ((s = upload(m, &m->madj_ptr, madj_ptr.data(), madj_ptr.size())) != LGDM_OK) return bail(s);
+  std::vector<NodeMeta> meta(n_nodes);
+  for (int64_t n = 0; n < n_nodes; ++n) {
+    const int nr = int(doff[n + 1] - doff[n]);
+    meta[n] = NodeMeta{row_ptr[doff[n]], doff[n], madj_ptr[n], width[n], int16_t(nr),
+                       int16_t(madj_ptr[n + 1] - madj_ptr[n])};
+    if (madj_ptr[n + 1] - madj_ptr[n] > 32767) return bail(fail(LGDM_ERR_INVALID_ARGUMENT, "node %lld has too many elements", (long long)n));
+  }
+  if ((s = upload(m, &m->madj_ptr, meta.data(), meta.size())) != LGDM_OK) return bail(s);
   if ((s = upload(m, &m->madj, madj.data(), madj.size())) != LGDM_OK) return bail(s);
   if (dalloc(&m->val, size_t(m->nnz)) != cudaSuccess || dalloc(&m->R, size_t(ndof)) != cudaSuccess ||
       dalloc(&m->dofs, size_t(ndof)) != cudaSuccess || dalloc(&m->kappa, size_t(n_elems) * f.ngp) != cudaSuccess ||
@@ -556,7 +563,7 @@ template <int T> lgdm_status assemble_mixed(lgdm_mesh m) {
     CU(dalloc(&m->scratchF, size_t(m->n_elems) * F::NDOFE));
     m->device_bytes += m->n_elems * (F::NDOFE * F::NDOFE + F::NDOFE) * 8;
   }
-  const size_t smem = sizeof(double) * size_t(WPB) * MSmem<T>::SIZE;
+  const size_t smem = sizeof(double) * (size_t(WPB) * MSmem<T>::SIZE + ((sizeof(MShape<T>) / 8 + 1) & ~size_t(1)));
   static bool attr = false;
   if (!attr) {
     CU(cudaFuncSetAttribute(k_mixed_blocks<T, WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -577,7 +584,7 @@ template <int T> lgdm_status assemble_mixed(lgdm_mesh m) {
   if (gsm > 48 * 1024) CU(cudaFuncSetAttribute(k_mixed_gather<T, GW>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gsm)));
   const int64_t gn = (m->n_nodes + GW - 1) / GW;
   k_mixed_gather<T, GW><<<unsigned(std::min<int64_t>(gn, int64_t(nsm) * 16)), GW * 32, gsm, m->stream>>>(
-      m->n_nodes, m->madj_ptr, m->madj, m->doff, m->row_ptr, m->scratchK, m->scratchF, m->max_row, m->val, m->R);
+      m->n_nodes, m->madj_ptr, m->madj, m->scratchK, m->scratchF, m->max_row, m->val, m->R);
   return check_launch(m, "k_mixed_gather");
 }
 

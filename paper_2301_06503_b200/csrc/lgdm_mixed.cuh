@@ -59,10 +59,12 @@ template <int T> __device__ __forceinline__ const MShape<T>& mshape();
 template <> __device__ __forceinline__ const MShape<4>& mshape<4>() { return c_shape4; }
 template <> __device__ __forceinline__ const MShape<5>& mshape<5>() { return c_shape5; }
 
-// per-(GP, u node) record: grad N, S grad N, t1, t2, W' grad N, Dt' grad N, Sigma' grad N
+// per-(GP, u node) record: grad N, S grad N, W' grad N, Dt' grad N, Sigma' grad N (the Kuu
+// column factors t1 = lam* gN + Ams SgN, t2 = Ams gN + Ass SgN are formed in the pair loop:
+// 4 D fewer doubles of shared memory per record -> more resident elements)
 template <int D> struct MURec {
-  static constexpr int GN = 0, SGN = D, T1 = 2 * D, T2 = 3 * D, WGN = 4 * D, DGN = 5 * D,
-                       FU = 6 * D, STRIDE = 7 * D + 1;   // odd: spreads banks
+  static constexpr int GN = 0, SGN = D, WGN = 2 * D, DGN = 3 * D, FU = 4 * D,
+                       STRIDE = 5 * D + 1;   // odd: spreads banks
 };
 // per-(GP, ebar node) record: N, grad N, hN N + gvec . grad N (Kee), fe0 N + fvec . grad N (Fe)
 template <int D> struct MERec {
@@ -92,8 +94,14 @@ k_mixed_blocks(DevMat m, int64_t ne, const int32_t* __restrict__ conn, const dou
   using Co = Core<D>;
   extern __shared__ double smem_mx[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  double* sm = smem_mx + w * SM::SIZE;
-  const MShape<T>& S = mshape<T>();
+  // the shape table in shared memory: lanes read different Gauss points (divergent constant
+  // cache reads would serialise)
+  MShape<T>& S = *reinterpret_cast<MShape<T>*>(smem_mx);
+  constexpr int TBL = (int(sizeof(MShape<T>)) / 8 + 1) & ~1;
+  for (int k = threadIdx.x; k < int(sizeof(MShape<T>)) / 8; k += blockDim.x)
+    smem_mx[k] = reinterpret_cast<const double*>(&mshape<T>())[k];
+  __syncthreads();
+  double* sm = smem_mx + TBL + w * SM::SIZE;
   for (int64_t e = int64_t(blockIdx.x) * WPB + w; e < ne; e += int64_t(gridDim.x) * WPB) {
     // gather coordinates and element dofs
     for (int k = lane; k < NENU * D; k += 32) {
@@ -196,13 +204,10 @@ k_mixed_blocks(DevMat m, int64_t ne, const int32_t* __restrict__ conn, const dou
       symv<D>(core + Co::WT, gn, WgN);
       symv<D>(core + Co::DT, gn, DgN);
       symv<D>(core + Co::SG, gn, fu);
-      const double lamS = core[Co::LAM], Ams = core[Co::AMS], Ass = core[Co::ASS];
 #pragma unroll
       for (int i = 0; i < D; ++i) {
         r[UR::GN + i] = gn[i];
         r[UR::SGN + i] = SgN[i];
-        r[UR::T1 + i] = fma(lamS, gn[i], Ams * SgN[i]);
-        r[UR::T2 + i] = fma(Ams, gn[i], Ass * SgN[i]);
         r[UR::WGN + i] = WgN[i];
         r[UR::DGN + i] = DgN[i];
         r[UR::FU + i] = fu[i];
@@ -246,6 +251,13 @@ k_mixed_blocks(DevMat m, int64_t ne, const int32_t* __restrict__ conn, const dou
         const double* B = sm + SM::UR + (g * NENU + b) * UR::STRIDE;
         const double* core = sm + SM::CORE + g * Co::STRIDE;
         const double mu = core[Co::MU];
+        const double lamS = core[Co::LAM], Ams = core[Co::AMS], Ass = core[Co::ASS];
+        double t1[D], t2[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          t1[j] = fma(lamS, B[UR::GN + j], Ams * B[UR::SGN + j]);
+          t2[j] = fma(Ams, B[UR::GN + j], Ass * B[UR::SGN + j]);
+        }
         double dot = 0.0;
 #pragma unroll
         for (int i = 0; i < D; ++i) dot = fma(A[UR::GN + i], B[UR::GN + i], dot);
@@ -255,8 +267,8 @@ k_mixed_blocks(DevMat m, int64_t ne, const int32_t* __restrict__ conn, const dou
 #pragma unroll
           for (int j = 0; j < D; ++j) {
             double v = Kuu[i][j];
-            v = fma(A[UR::GN + i], B[UR::T1 + j], v);
-            v = fma(A[UR::SGN + i], B[UR::T2 + j], v);
+            v = fma(A[UR::GN + i], t1[j], v);
+            v = fma(A[UR::SGN + i], t2[j], v);
             v = fma(A[UR::GN + j], ub, v);
             Kuu[i][j] = v;
           }
@@ -314,37 +326,81 @@ struct MixAdj {
   int32_t aloc;
   int32_t coff[8];
 };
+// per-node gather metadata, one 32-byte load: first value of the block-row, first row,
+// first adjacency entry, block-row width, rows, adjacent elements
+struct NodeMeta {
+  int64_t base, r0, k0;
+  int32_t W;
+  int16_t nr, nk;
+};
 
 template <int T, int WPB>
-__global__ void __launch_bounds__(WPB * 32)
-k_mixed_gather(int64_t nn, const int64_t* __restrict__ adj_ptr, const MixAdj* __restrict__ adj,
-               const int64_t* __restrict__ doff, const int64_t* __restrict__ row_ptr,
+__global__ void __launch_bounds__(WPB * 32, 5)
+k_mixed_gather(int64_t nn, const NodeMeta* __restrict__ meta, const MixAdj* __restrict__ adj,
                const double* __restrict__ EB, const double* __restrict__ EF, int max_row,
                double* __restrict__ val, double* __restrict__ R) {
   using F = MFam<T>;
   constexpr int ND = F::NDOFE;
+  constexpr int NQ = ((F::DIM + 1) * ND + 31) / 32;   // entries of one element's rows per lane
+  constexpr int CH = 1;                               // adjacent elements loaded per round
   extern __shared__ double smem_mg[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   double* buf = smem_mg + w * max_row;
-  for (int64_t n = int64_t(blockIdx.x) * WPB + w; n < nn; n += int64_t(gridDim.x) * WPB) {
-    const int64_t r0 = doff[n];
-    const int nr = int(doff[n + 1] - r0);
-    const int64_t base = row_ptr[r0];
-    const int W = int(row_ptr[r0 + 1] - base);
+  const int64_t stride = int64_t(gridDim.x) * WPB;
+  int64_t n = int64_t(blockIdx.x) * WPB + w;
+  NodeMeta nx{};
+  if (n < nn) nx = meta[n];
+  for (; n < nn; n += stride) {
+    const NodeMeta md = nx;
+    if (n + stride < nn) nx = meta[n + stride];      // prefetch the next node's metadata
+    const int64_t r0 = md.r0, base = md.base;
+    const int nr = md.nr, W = md.W;
     const int tot = nr * W;
     for (int k = lane; k < tot; k += 32) buf[k] = 0.0;
+    // this lane's entries (row i, element dof c) of an element block: fixed for the node
+    int qb[NQ], qoff[NQ];   // local node of the column; row * W + component (-1: no entry)
+#pragma unroll
+    for (int t = 0; t < NQ; ++t) {
+      const int q = lane + 32 * t;
+      const int c = q % ND;
+      qb[t] = mdof_node<T>(c);
+      qoff[t] = q < nr * ND ? (q / ND) * W + mdof_comp<T>(c) : -1;
+    }
     double rsum = 0.0;
     __syncwarp();
-    for (int64_t k = adj_ptr[n]; k < adj_ptr[n + 1]; ++k) {
-      const MixAdj en = adj[k];
-      const int lr = mldof<T>(en.aloc);
-      const double* src = EB + int64_t(en.e) * (ND * ND) + lr * ND;
-      for (int q = lane; q < nr * ND; q += 32) {
-        const int i = q / ND, c = q % ND;
-        buf[i * W + en.coff[mdof_node<T>(c)] + mdof_comp<T>(c)] += src[q];
+    const int64_t k0 = md.k0, k1 = md.k0 + md.nk;
+    for (int64_t k = k0; k < k1; k += CH) {
+      const int kk = int(k1 - k < CH ? k1 - k : CH);
+      double v[CH][NQ], fr[CH];
+      int pos[CH][NQ];
+      // issue every load of the round first (one memory latency per round, not per element)
+#pragma unroll
+      for (int u = 0; u < CH; ++u) {
+        fr[u] = 0.0;
+        if (u < kk) {
+          const MixAdj* en = adj + k + u;
+          const int64_t e = en->e;
+          const int lr = mldof<T>(en->aloc);
+          const double* src = EB + e * (ND * ND) + lr * ND;
+#pragma unroll
+          for (int t = 0; t < NQ; ++t) {       // row i, column c of the element's rows: q = i ND + c
+            v[u][t] = qoff[t] >= 0 ? src[lane + 32 * t] : 0.0;
+            pos[u][t] = qoff[t] + en->coff[qb[t]];
+          }
+          if (lane < nr) fr[u] = EF[e * ND + lr + lane];
+        }
       }
-      if (lane < nr) rsum += EF[int64_t(en.e) * ND + lr + lane];
-      __syncwarp();
+      // accumulate in ascending element order
+#pragma unroll
+      for (int u = 0; u < CH; ++u) {
+        if (u < kk) {
+#pragma unroll
+          for (int t = 0; t < NQ; ++t)
+            if (qoff[t] >= 0) buf[pos[u][t]] += v[u][t];
+          rsum += fr[u];
+        }
+        __syncwarp();
+      }
     }
     for (int k = lane; k < tot; k += 32) val[base + k] = buf[k];
     if (lane < nr) R[r0 + lane] = rsum;
