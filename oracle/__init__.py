@@ -95,6 +95,8 @@ def lib():
         L.oracle_mixed_assemble.argtypes = [C.c_int, mp, C.c_int64, dp, C.c_int64, i64p, i64p,
                                             dp, dp, dp, dp, i64p, i32p, dp, dp, dp]
         L.oracle_mixed_update_history.argtypes = [C.c_int, C.c_int64, i64p, i64p, dp, dp]
+        L.oracle_mixed_update_state.argtypes = [C.c_int, mp, C.c_int64, dp, C.c_int64, i64p,
+                                                i64p, dp, dp, dp, dp, dp]
         _lib = L
     return _lib
 
@@ -497,3 +499,23 @@ def converged_kind(delta, dofs, kind, dim: int, tol: float, floor: float = 1e-16
     ru = np.linalg.norm(d[~e]) / max(np.linalg.norm(u[~e]), floor)
     re = np.linalg.norm(d[e]) / max(np.linalg.norm(u[e]), floor)
     return bool(ru <= tol and re <= tol), ru, re
+
+
+def mixed_update_state(etype: int, m: Material, coords, conn, doff, dofs, kappa, kappa0_gp=None,
+                       alpha_gp=None):
+    """State records [ne, ngp, 3 nv + 5] and the committed kappa (Alg. 2 l.8-14)."""
+    dim, nenu, nene, nv, ngp, nd = mixed_family(etype)
+    coords = np.ascontiguousarray(coords, dtype=np.float64)
+    conn = np.ascontiguousarray(conn, dtype=np.int64)
+    dofs = np.ascontiguousarray(dofs, dtype=np.float64)
+    k = np.array(kappa, dtype=np.float64, copy=True)
+    ne = conn.shape[0]
+    sdv = np.zeros((ne, ngp, 3 * nv + 5))
+    k0k, k0p = _opt(kappa0_gp, ne * ngp)
+    alk, alp = _opt(alpha_gp, ne * ngp)
+    rc = lib().oracle_mixed_update_state(etype, C.byref(m), coords.shape[0], _d(coords), ne,
+                                         _i64(conn), _i64(np.ascontiguousarray(doff)), _d(dofs),
+                                         _d(k), k0p, alp, _d(sdv))
+    if rc != 0:
+        raise ValueError(f"oracle_mixed_update_state rc={rc}")
+    return sdv, k

@@ -895,10 +895,13 @@ int oracle_mixed_element(int type, const oracle_material* m0, const double* Xe, 
     double Nu[8], dNu[16], Nn[4], dNe[8];
     oracle_mixed_shape_u(type, xi + g * dim, Nu, dNu);
     oracle_mixed_shape_e(type, xi + g * dim, Nn, dNe);
+    // J = sum_a X_a dN_a/dxi, with the coordinates taken relative to node 0 (reading R-REL:
+    // the same sum since sum_a dN_a/dxi = 0; exact differences instead of the cancellation of
+    // |X| >> element size)
     double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}}, Ji[3][3];
     for (int a = 0; a < f.nenu; ++a)
       for (int i = 0; i < dim; ++i)
-        for (int j = 0; j < dim; ++j) J[i][j] += Xe[a * dim + i] * dNu[a * dim + j];
+        for (int j = 0; j < dim; ++j) J[i][j] += (Xe[a * dim + i] - Xe[i]) * dNu[a * dim + j];
     const double detJ = dim == 1 ? J[0][0] : J[0][0] * J[1][1] - J[0][1] * J[1][0];
     if (!invert(dim, J, Ji)) return -(g + 1);
     double gNu[8][3], gNe[4][3];
@@ -942,11 +945,19 @@ int oracle_mixed_element(int type, const oracle_material* m0, const double* Xe, 
       for (int i = 0; i < dim; ++i) Be[i][o] = gNe[a][i];
     }
 
+    // eps = B_u u, grad ebar = B_e e on the dofs relative to node 0's (R-REL: B annihilates
+    // constants); ebar = N_e e on the absolute values
+    double Ur[20];
+    for (int r = 0; r < nd; ++r) {
+      const int a = r < f.nene * (dim + 1) ? r / (dim + 1) : f.nene + (r - f.nene * (dim + 1)) / dim;
+      const int comp = r - mldof(f, a);
+      Ur[r] = Ue[r] - Ue[comp];   // node 0 is a corner: (u_0.., ebar_0) at local dofs 0..dim
+    }
     double ev[6] = {0, 0, 0, 0, 0, 0}, ebar = 0.0, gbar[3] = {0, 0, 0};
     for (int r = 0; r < nd; ++r) {
-      for (int V = 0; V < nv; ++V) ev[V] += Bu[V][r] * Ue[r];
+      for (int V = 0; V < nv; ++V) ev[V] += Bu[V][r] * Ur[r];
       ebar += Ne[r] * Ue[r];
-      for (int i = 0; i < dim; ++i) gbar[i] += Be[i][r] * Ue[r];
+      for (int i = 0; i < dim; ++i) gbar[i] += Be[i][r] * Ur[r];
     }
 
     mg.kappa0 = k0g ? k0g[g] : m0->kappa0;
@@ -1124,6 +1135,84 @@ int oracle_mixed_update_history(int type, int64_t n_elems, const int64_t* conn,
       double& k = kappa[e * f.ngp + g];
       if ((ebar - k) > kTolHist) k = ebar;
     }
+  return 0;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+// State-variable update (Alg. 2 l.8-14, Fig. 9a) for mixed elements: the record of
+// oracle_update_state ([eps_v, d eeq/d eps_v, sigma, eeq, ebar, kappa, D, g], oracle_sdv_width
+// of the equal-order family of the same dimension) with eps from the quadratic u field and
+// ebar from the linear field; commits kappa.
+int oracle_mixed_update_state(int type, const oracle_material* m, int64_t n_nodes,
+                              const double* coords, int64_t n_elems, const int64_t* conn,
+                              const int64_t* doff, const double* dofs, double* kappa,
+                              const double* kappa0_gp, const double* alpha_gp, double* sdv) {
+  MFam f;
+  if (!mfamily(type, &f)) return -1;
+  (void)n_nodes;
+  const int dim = f.dim, nv = f.nv, W = 3 * f.nv + 5;
+  double xi[18], w[9], C[36];
+  oracle_mixed_gauss(type, xi, w);
+  elasticity(m, dim, C);
+  for (int64_t e = 0; e < n_elems; ++e) {
+    const int64_t* c = conn + e * f.nenu;
+    for (int g = 0; g < f.ngp; ++g) {
+      double Nu[8], dNu[16], Ne[4], dNe[8];
+      oracle_mixed_shape_u(type, xi + g * dim, Nu, dNu);
+      oracle_mixed_shape_e(type, xi + g * dim, Ne, dNe);
+      double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}}, Ji[3][3];
+      for (int a = 0; a < f.nenu; ++a)
+        for (int i = 0; i < dim; ++i)   // relative to node 0 (R-REL)
+          for (int j = 0; j < dim; ++j)
+            J[i][j] += (coords[c[a] * dim + i] - coords[c[0] * dim + i]) * dNu[a * dim + j];
+      if (!invert(dim, J, Ji)) return -2;
+      double ev[6] = {0, 0, 0, 0, 0, 0}, ebar = 0.0;
+      for (int a = 0; a < f.nenu; ++a) {
+        double gN[3];
+        for (int i = 0; i < dim; ++i) {
+          double s = 0.0;
+          for (int j = 0; j < dim; ++j) s += Ji[j][i] * dNu[a * dim + j];
+          gN[i] = s;
+        }
+        const double* ua = dofs + doff[c[a]];
+        const double* u0 = dofs + doff[c[0]];
+        for (int V = 0; V < nv; ++V) {
+          int p, q;
+          voigt_pair(dim, V, &p, &q);
+          if (p == q) ev[V] += gN[p] * (ua[p] - u0[p]);
+          else ev[V] += gN[q] * (ua[p] - u0[p]) + gN[p] * (ua[q] - u0[q]);
+        }
+      }
+      for (int a = 0; a < f.nene; ++a) ebar += Ne[a] * dofs[doff[c[a]] + dim];
+      oracle_material mg = *m;
+      if (kappa0_gp) mg.kappa0 = kappa0_gp[e * f.ngp + g];
+      if (alpha_gp) mg.alpha = alpha_gp[e * f.ngp + g];
+      double eeq, dv[6], H[36];
+      oracle_eqstrain(&mg, dim, ev, &eeq, dv, H);
+      double& kh = kappa[e * f.ngp + g];
+      const double kap = (ebar - kh) > kTolHist ? ebar : kh;
+      double D, dD, gI, dg;
+      oracle_damage(&mg, kap, &D, &dD);
+      oracle_interaction(&mg, D, &gI, &dg);
+      double* out = sdv + (e * f.ngp + g) * W;
+      for (int V = 0; V < nv; ++V) {
+        double ce = 0.0;
+        for (int U = 0; U < nv; ++U) ce += C[V * nv + U] * ev[U];
+        out[V] = ev[V];
+        out[nv + V] = dv[V];
+        out[2 * nv + V] = (1.0 - D) * ce + m->h_sigma * (eeq - ebar) * dv[V];
+      }
+      out[3 * nv + 0] = eeq;
+      out[3 * nv + 1] = ebar;
+      out[3 * nv + 2] = kap;
+      out[3 * nv + 3] = D;
+      out[3 * nv + 4] = gI;
+      kh = kap;
+    }
+  }
   return 0;
 }
 

@@ -127,6 +127,11 @@ int oracle_mixed_assemble(int type, const oracle_material* m, int64_t n_nodes,
                           double* S);
 int oracle_mixed_update_history(int type, int64_t n_elems, const int64_t* conn,
                                 const int64_t* doff, const double* dofs, double* kappa);
+/* state records (layout of oracle_update_state, nv of the dimension) + history commit */
+int oracle_mixed_update_state(int type, const oracle_material* m, int64_t n_nodes,
+                              const double* coords, int64_t n_elems, const int64_t* conn,
+                              const int64_t* doff, const double* dofs, double* kappa,
+                              const double* kappa0_gp, const double* alpha_gp, double* sdv);
 #ifdef __cplusplus
 }
 #endif

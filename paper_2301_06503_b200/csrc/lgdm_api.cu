@@ -904,6 +904,8 @@ int lgdm_sdv_width(lgdm_elem_type type) {
     case LGDM_BAR2: return StateW<1>::W;
     case LGDM_QUAD4: return StateW<2>::W;
     case LGDM_HEX8: return StateW<3>::W;
+    case LGDM_BAR3: return StateW<1>::W;
+    case LGDM_QUAD8: return StateW<2>::W;
     default: return -1;
   }
 }
@@ -941,7 +943,6 @@ lgdm_status lgdm_set_defects(lgdm_mesh m, const double* kappa0_gp, const double*
 lgdm_status lgdm_update_state(lgdm_mesh m, double* sdv, int64_t n_sdv, int dst_on_device) {
   if (!m) return fail(LGDM_ERR_INVALID_ARGUMENT, "mesh is NULL");
   if (!m->have_state || !m->have_kappa) return fail(LGDM_ERR_INVALID_STATE, "update_state before set_state");
-  if (m->mixed) return fail(LGDM_ERR_UNSUPPORTED, "update_state: mixed-order meshes not supported");
   const int W = lgdm_sdv_width(lgdm_elem_type(m->type));
   const int64_t ngp = m->n_elems * m->f.ngp;
   if (sdv && n_sdv != ngp * W)
@@ -965,7 +966,15 @@ lgdm_status lgdm_update_state(lgdm_mesh m, double* sdv, int64_t n_sdv, int dst_o
     CU(cudaFuncSetAttribute(k_update_state<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, TPB * StateW<3>::W * 8));
     attr = true;
   }
-  if (m->f.dim == 1)
+  if (m->mixed) {
+    const size_t tbl = sizeof(double) * 400;   // >= the padded shape table of either family
+    static_assert(sizeof(MShape<5>) <= 400 * sizeof(double) && sizeof(MShape<4>) <= 400 * sizeof(double), "table");
+    const size_t sm2 = tbl + size_t(TPB) * W * sizeof(double);
+    if (m->type == LGDM_BAR3)
+      k_mixed_state<4><<<blocks, TPB, sm2, m->stream>>>(m->dm, m->n_elems, m->conn, m->coords, m->doff, m->dofs, m->kappa, m->k0g, m->alg, out);
+    else
+      k_mixed_state<5><<<blocks, TPB, sm2, m->stream>>>(m->dm, m->n_elems, m->conn, m->coords, m->doff, m->dofs, m->kappa, m->k0g, m->alg, out);
+  } else if (m->f.dim == 1)
     k_update_state<1><<<blocks, TPB, smem, m->stream>>>(m->dm, m->n_elems, m->conn, m->coords, m->dofs, m->kappa, m->k0g, m->alg, out);
   else if (m->f.dim == 2)
     k_update_state<2><<<blocks, TPB, smem, m->stream>>>(m->dm, m->n_elems, m->conn, m->coords, m->dofs, m->kappa, m->k0g, m->alg, out);

@@ -225,6 +225,80 @@ template <int D> struct StateW {
   static constexpr int NV = D == 1 ? 1 : (D == 2 ? 3 : 6);
   static constexpr int W = 3 * NV + 5;
 };
+// State record of one GP from the displacement gradient Gu and ebar (shared by k_update_state
+// and the mixed-order k_mixed_state): [eps_v, d eeq/d eps_v, sigma (Eq. 2), eeq, ebar, kappa,
+// D (Eq. A.1), g (Eq. A.4)]; the trial kappa (Fig. 9a l.22-24) is returned in *kap_out.
+template <int D>
+__device__ __forceinline__ void state_record(const DevMat& m, const double (&Gu)[D][D], double ebar,
+                                             double kh, double k0, double al, double* out,
+                                             double* kap_out) {
+  constexpr int NV = StateW<D>::NV;
+  // Voigt strain (engineering shear): 2D [xx, yy, xy], 3D [xx, yy, zz, xy, yz, xz]
+  double ev[NV], dv[NV], eeq;
+  if constexpr (D == 1) {
+    ev[0] = Gu[0][0];
+    eeq = ev[0];                                   // reading R-1D
+    dv[0] = 1.0;
+  } else {
+    constexpr int P[6] = {0, 1, 2, 0, 1, 0}, Q[6] = {0, 1, 2, 1, 2, 2};
+    double mv[NV], sv[NV];
+#pragma unroll
+    for (int V = 0; V < NV; ++V) {
+      const int p = (D == 2 && V == 2) ? 0 : P[V], q = (D == 2 && V == 2) ? 1 : Q[V];
+      ev[V] = V < D ? Gu[p][p] : Gu[p][q] + Gu[q][p];
+      mv[V] = V < D ? 1.0 : 0.0;
+    }
+    double I1 = 0.0;
+#pragma unroll
+    for (int V = 0; V < D; ++V) I1 += ev[V];
+    // J2 = 1/2 dev:dev on the 3x3 tensor (plane strain eps33 = 0, reading R-PS; shear gamma/2)
+    double J2 = 0.0;
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+      const double dp = (p < D ? ev[p] : 0.0) - I1 / 3.0;
+      J2 += 0.5 * dp * dp;
+      if (p < D) sv[p] = dp;
+    }
+#pragma unroll
+    for (int V = D; V < NV; ++V) {
+      J2 += 0.25 * ev[V] * ev[V];
+      sv[V] = 0.5 * ev[V];
+    }
+    const double Qv = m.c2 * I1 * I1 + m.c3 * J2;
+    const double sQ = sqrt(Qv);
+    eeq = m.c1 * I1 + sQ / (2.0 * m.k);
+#pragma unroll
+    for (int V = 0; V < NV; ++V)
+      dv[V] = Qv < 1e-30 ? m.c1 * mv[V]                                   // reading R-SQ
+                         : m.c1 * mv[V] + (2.0 * m.c2 * I1 * mv[V] + m.c3 * sv[V]) / (4.0 * m.k * sQ);
+  }
+  // history (Fig. 9a l.22-24), damage (Eq. A.1, l.27-31), interaction (Eq. A.4)
+  const double kap = (ebar - kh) > 1e-10 ? ebar : kh;
+  double Dm = 0.0;
+  if (!((kap - k0) < 1e-10)) Dm = 1.0 - (k0 / kap) * (1.0 - al + al * exp(-m.beta * (kap - k0)));
+  const double gI = m.ga * exp(-m.n * Dm) + m.gb;
+  *kap_out = kap;
+  if (out) {
+    // Eq. 2: sigma = (1 - D) C eps + h_sigma (eeq - ebar) d
+    const double hr = m.hs * (eeq - ebar);
+    double tr = 0.0;
+#pragma unroll
+    for (int U2 = 0; U2 < D; ++U2) tr += ev[U2];
+#pragma unroll
+    for (int V = 0; V < NV; ++V) {
+      const double ce = D == 1 ? m.E * ev[0] : (V < D ? m.lam * tr + 2.0 * m.mu * ev[V] : m.mu * ev[V]);
+      out[V] = ev[V];
+      out[NV + V] = dv[V];
+      out[2 * NV + V] = fma(1.0 - Dm, ce, hr * dv[V]);
+    }
+    out[3 * NV + 0] = eeq;
+    out[3 * NV + 1] = ebar;
+    out[3 * NV + 2] = kap;
+    out[3 * NV + 3] = Dm;
+    out[3 * NV + 4] = gI;
+  }
+}
+
 template <int D>
 __global__ void __launch_bounds__(128, 4)
 k_update_state(DevMat m, int64_t ne, const int32_t* __restrict__ conn,
@@ -307,73 +381,10 @@ k_update_state(DevMat m, int64_t ne, const int32_t* __restrict__ conn,
       }
       ebar = fma(shapeN<D>(a, g), __ldg(dofs + n * F::NDPN + D), ebar);
     }
-    // Voigt strain (engineering shear): 2D [xx, yy, xy], 3D [xx, yy, zz, xy, yz, xz]
-    double ev[NV], dv[NV], eeq;
-    if constexpr (D == 1) {
-      ev[0] = Gu[0][0];
-      eeq = ev[0];                                   // reading R-1D
-      dv[0] = 1.0;
-    } else {
-      constexpr int P[6] = {0, 1, 2, 0, 1, 0}, Q[6] = {0, 1, 2, 1, 2, 2};
-      double mv[NV], sv[NV];
-#pragma unroll
-      for (int V = 0; V < NV; ++V) {
-        const int p = (D == 2 && V == 2) ? 0 : P[V], q = (D == 2 && V == 2) ? 1 : Q[V];
-        ev[V] = V < D ? Gu[p][p] : Gu[p][q] + Gu[q][p];
-        mv[V] = V < D ? 1.0 : 0.0;
-      }
-      double I1 = 0.0;
-#pragma unroll
-      for (int V = 0; V < D; ++V) I1 += ev[V];
-      // J2 = 1/2 dev:dev on the 3x3 tensor (plane strain eps33 = 0, reading R-PS; shear gamma/2)
-      double J2 = 0.0;
-#pragma unroll
-      for (int p = 0; p < 3; ++p) {
-        const double dp = (p < D ? ev[p] : 0.0) - I1 / 3.0;
-        J2 += 0.5 * dp * dp;
-        if (p < D) sv[p] = dp;
-      }
-#pragma unroll
-      for (int V = D; V < NV; ++V) {
-        J2 += 0.25 * ev[V] * ev[V];
-        sv[V] = 0.5 * ev[V];
-      }
-      const double Qv = m.c2 * I1 * I1 + m.c3 * J2;
-      const double sQ = sqrt(Qv);
-      eeq = m.c1 * I1 + sQ / (2.0 * m.k);
-#pragma unroll
-      for (int V = 0; V < NV; ++V)
-        dv[V] = Qv < 1e-30 ? m.c1 * mv[V]                                   // reading R-SQ
-                           : m.c1 * mv[V] + (2.0 * m.c2 * I1 * mv[V] + m.c3 * sv[V]) / (4.0 * m.k * sQ);
-    }
-    // history (Fig. 9a l.22-24), damage (Eq. A.1, l.27-31), interaction (Eq. A.4)
-    const double kh = kappa[t];
-    const double kap = (ebar - kh) > 1e-10 ? ebar : kh;
-    const double k0 = k0g ? k0g[t] : m.kappa0, al = alg ? alg[t] : m.alpha;
-    double Dm = 0.0;
-    if (!((kap - k0) < 1e-10)) Dm = 1.0 - (k0 / kap) * (1.0 - al + al * exp(-m.beta * (kap - k0)));
-    const double gI = m.ga * exp(-m.n * Dm) + m.gb;
+    double kap;
+    state_record<D>(m, Gu, ebar, kappa[t], k0g ? k0g[t] : m.kappa0, alg ? alg[t] : m.alpha,
+                    sdv ? stage + threadIdx.x * W : nullptr, &kap);
     kappa[t] = kap;
-    if (sdv) {
-      // Eq. 2: sigma = (1 - D) C eps + h_sigma (eeq - ebar) d
-      double* out = stage + threadIdx.x * W;
-      const double hr = m.hs * (eeq - ebar);
-      double tr = 0.0;
-#pragma unroll
-      for (int U2 = 0; U2 < D; ++U2) tr += ev[U2];
-#pragma unroll
-      for (int V = 0; V < NV; ++V) {
-        const double ce = D == 1 ? m.E * ev[0] : (V < D ? m.lam * tr + 2.0 * m.mu * ev[V] : m.mu * ev[V]);
-        out[V] = ev[V];
-        out[NV + V] = dv[V];
-        out[2 * NV + V] = fma(1.0 - Dm, ce, hr * dv[V]);
-      }
-      out[3 * NV + 0] = eeq;
-      out[3 * NV + 1] = ebar;
-      out[3 * NV + 2] = kap;
-      out[3 * NV + 3] = Dm;
-      out[3 * NV + 4] = gI;
-    }
   }
   if (sdv) {   // the block's records are one contiguous range of the output: coalesced copy
     __syncthreads();

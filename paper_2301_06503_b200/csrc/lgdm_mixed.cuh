@@ -119,12 +119,15 @@ k_mixed_blocks(DevMat m, int64_t ne, const int32_t* __restrict__ conn, const dou
       for (int i = 0; i < D; ++i)
 #pragma unroll
         for (int j = 0; j < D; ++j) J[i][j] = 0.0;
+      // J = sum_a X_a dN_a/dxi = sum_a (X_a - X_0) dN_a/dxi (sum_a dN_a = 0): node coordinates
+      // relative to node 0 (exact differences) remove the cancellation of |X| >> element size
 #pragma unroll
-      for (int a = 0; a < NENU; ++a)
+      for (int a = 1; a < NENU; ++a)
 #pragma unroll
         for (int j = 0; j < D; ++j)
 #pragma unroll
-          for (int i = 0; i < D; ++i) J[i][j] = fma(sm[SM::X + a * D + i], S.dNu[g][a][j], J[i][j]);
+          for (int i = 0; i < D; ++i)
+            J[i][j] = fma(sm[SM::X + a * D + i] - sm[SM::X + i], S.dNu[g][a][j], J[i][j]);
       double detJ, Ji[D][D];
       if constexpr (D == 1) {
         detJ = J[0][0];
@@ -146,7 +149,7 @@ k_mixed_blocks(DevMat m, int64_t ne, const int32_t* __restrict__ conn, const dou
         for (int j = 0; j < D; ++j) eps[i][j] = 0.0;
       }
 #pragma unroll
-      for (int a = 0; a < NENU; ++a) {
+      for (int a = 1; a < NENU; ++a) {       // gradients from differences to node 0, likewise
         double gn[D];
 #pragma unroll
         for (int i = 0; i < D; ++i) {
@@ -157,7 +160,7 @@ k_mixed_blocks(DevMat m, int64_t ne, const int32_t* __restrict__ conn, const dou
         }
 #pragma unroll
         for (int i = 0; i < D; ++i) {
-          const double ua = sm[SM::U + mldof<T>(a) + i];
+          const double ua = sm[SM::U + mldof<T>(a) + i] - sm[SM::U + i];
 #pragma unroll
           for (int j = 0; j < D; ++j) eps[i][j] = fma(ua, gn[j], eps[i][j]);
         }
@@ -166,12 +169,14 @@ k_mixed_blocks(DevMat m, int64_t ne, const int32_t* __restrict__ conn, const dou
       for (int a = 0; a < NENE; ++a) {
         const double ea = sm[SM::U + mldof<T>(a) + D];
         ebar = fma(S.Ne[g][a], ea, ebar);
+        if (a == 0) continue;
+        const double da = ea - sm[SM::U + D];
 #pragma unroll
         for (int i = 0; i < D; ++i) {
           double s = 0.0;
 #pragma unroll
           for (int j = 0; j < D; ++j) s = fma(Ji[j][i], S.dNe[g][a][j], s);
-          gb[i] = fma(s, ea, gb[i]);
+          gb[i] = fma(s, da, gb[i]);
         }
       }
       double es[F::NS];
@@ -448,6 +453,97 @@ __global__ void k_mixed_history(int64_t ne, const int32_t* __restrict__ conn,
   for (int a = 0; a < F::NENE; ++a) eb = fma(S.Ne[g][a], dofs[doff[conn[e * F::NENU + a]] + F::DIM], eb);
   const double k = kappa[t];
   if ((eb - k) > 1e-10) kappa[t] = eb;
+}
+
+// State-variable update (Alg. 2 l.8-14, Fig. 9a) for mixed elements: one thread per
+// (element, GP), u gradient from the quadratic field, ebar from the linear field, the record
+// of state_record (lgdm_kernels.cuh), history commit; records staged and written coalesced.
+template <int T>
+__global__ void __launch_bounds__(128)
+k_mixed_state(DevMat m, int64_t ne, const int32_t* __restrict__ conn,
+              const double* __restrict__ coords, const int64_t* __restrict__ doff,
+              const double* __restrict__ dofs, double* __restrict__ kappa,
+              const double* __restrict__ k0g, const double* __restrict__ alg,
+              double* __restrict__ sdv) {
+  using F = MFam<T>;
+  constexpr int D = F::DIM, W = StateW<D>::W;
+  extern __shared__ double smem_ms[];
+  MShape<T>& S = *reinterpret_cast<MShape<T>*>(smem_ms);
+  constexpr int TBL = (int(sizeof(MShape<T>)) / 8 + 1) & ~1;
+  for (int k = threadIdx.x; k < int(sizeof(MShape<T>)) / 8; k += blockDim.x)
+    smem_ms[k] = reinterpret_cast<const double*>(&mshape<T>())[k];
+  __syncthreads();
+  double* stage = smem_ms + TBL;
+  const int64_t t0 = int64_t(blockIdx.x) * blockDim.x;
+  const int64_t t = t0 + threadIdx.x;
+  const int64_t ngp = ne * F::NGP;
+  if (t < ngp) {
+    const int64_t e = t / F::NGP;
+    const int g = int(t % F::NGP);
+    const int32_t* ce = conn + e * F::NENU;
+    double J[D][D];
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+      for (int j = 0; j < D; ++j) J[i][j] = 0.0;
+    const int64_t n0 = ce[0];
+#pragma unroll
+    for (int a = 1; a < F::NENU; ++a) {      // relative to node 0 (see k_mixed_blocks)
+      const int64_t n = ce[a];
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        const double x = __ldg(coords + n * D + i) - __ldg(coords + n0 * D + i);
+#pragma unroll
+        for (int j = 0; j < D; ++j) J[i][j] = fma(x, S.dNu[g][a][j], J[i][j]);
+      }
+    }
+    double Ji[D][D];
+    if constexpr (D == 1) {
+      Ji[0][0] = 1.0 / J[0][0];
+    } else {
+      const double r = 1.0 / (J[0][0] * J[1][1] - J[0][1] * J[1][0]);
+      Ji[0][0] = J[1][1] * r;
+      Ji[0][1] = -J[0][1] * r;
+      Ji[1][0] = -J[1][0] * r;
+      Ji[1][1] = J[0][0] * r;
+    }
+    double Gu[D][D], ebar = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+      for (int j = 0; j < D; ++j) Gu[i][j] = 0.0;
+    const int64_t o0 = __ldg(doff + n0);
+#pragma unroll
+    for (int a = 0; a < F::NENU; ++a) {
+      const int64_t o = __ldg(doff + ce[a]);
+      double gn[D];
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < D; ++k) s = fma(Ji[k][j], S.dNu[g][a][k], s);
+        gn[j] = s;
+      }
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        const double u = __ldg(dofs + o + i) - __ldg(dofs + o0 + i);
+#pragma unroll
+        for (int j = 0; j < D; ++j) Gu[i][j] = fma(u, gn[j], Gu[i][j]);
+      }
+      if (a < F::NENE) ebar = fma(S.Ne[g][a], __ldg(dofs + o + D), ebar);
+    }
+    double kap;
+    state_record<D>(m, Gu, ebar, kappa[t], k0g ? k0g[t] : m.kappa0, alg ? alg[t] : m.alpha,
+                    sdv ? stage + threadIdx.x * W : nullptr, &kap);
+    kappa[t] = kap;
+  }
+  if (sdv) {
+    __syncthreads();
+    const int64_t nrec = min(int64_t(blockDim.x), ngp - t0);
+    const int n = int(nrec) * W;
+    double* dst = sdv + t0 * W;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) __stcs(dst + k, stage[k]);
+  }
 }
 
 // ||R_u||^2, ||R_e||^2 by dof kind (kind[i] = component; ebar = dim)

@@ -142,9 +142,6 @@ def test_mixed_errors():
         m.set_kernel(2)
     assert ei.value.status == 1
     with pytest.raises(lgdm.LGDMError) as ei:
-        m.update_state()
-    assert ei.value.status == 7
-    with pytest.raises(lgdm.LGDMError) as ei:
         m.get_blocked()
     assert ei.value.status == 7
     with pytest.raises(lgdm.LGDMError):                   # ebar dof of a corner node
@@ -203,4 +200,42 @@ def test_bar3_softening_newton_matches_oracle():
     assert np.all(np.diff(r[ip:]) < 0)
     kel = kap.max(axis=1)
     assert kel[defect].min() > kel[~defect].max()
+    m.close()
+
+
+def test_mixed_parity_bench_size():
+    """the bench.py mixed_order workload (QUAD8 500^2, 250 k elements, 70 M nnz) in full"""
+    mesh = synth.mixed_mesh(lgdm.QUAD8, (500, 500), 100.0)
+    dofs, kap = synth.mixed_fields(mesh)
+    ref = oracle.mixed_assemble(lgdm.QUAD8, oracle.material(**MAT), mesh.coords, mesh.conn,
+                                dofs, kap)
+    m, got = _gpu(lgdm.QUAD8, mesh.coords, mesh.conn, dofs, kap)
+    compare(ref, got, "QUAD8 500^2")
+    m.close()
+
+
+@pytest.mark.parametrize("etype,n,defects", [(lgdm.BAR3, (41,), False), (lgdm.QUAD8, (13, 9), False),
+                                             (lgdm.QUAD8, (9, 8), True)])
+def test_mixed_update_state(etype, n, defects):
+    """state records of Alg. 2 l.8-14 for mixed elements + history commit vs the oracle"""
+    mesh, X = _mesh(etype, n, 0.15 if etype == lgdm.QUAD8 else 0.0)
+    dofs, kap = synth.mixed_fields(mesh)
+    k0g = alg = None
+    if defects:
+        rng = np.random.default_rng(4)
+        k0g = MAT["kappa0"] * rng.uniform(0.8, 1.2, size=kap.size)
+        alg = rng.uniform(0.9, 0.99, size=kap.size)
+    om = oracle.material(**MAT)
+    doff = oracle.mixed_dofs(etype, X.shape[0], mesh.conn)
+    sdv_ref, k_ref = oracle.mixed_update_state(etype, om, X, mesh.conn, doff, dofs, kap, k0g, alg)
+    m = lgdm.Mesh(etype, X, mesh.conn, lgdm.material(**MAT))
+    m.set_state(dofs, kap)
+    if defects:
+        m.set_defects(k0g, alg)
+    out = m.update_state().cpu().numpy()
+    assert out.shape == sdv_ref.shape
+    scale = np.abs(sdv_ref).reshape(-1, sdv_ref.shape[-1]).max(axis=0)
+    err = np.abs(out - sdv_ref) / np.maximum(scale, 1e-300)
+    assert err.max() <= 1e-12, (err.max(), np.unravel_index(err.argmax(), err.shape))
+    np.testing.assert_allclose(m.get_kappa().reshape(k_ref.shape), k_ref, rtol=1e-15, atol=0)
     m.close()

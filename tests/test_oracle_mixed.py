@@ -450,3 +450,69 @@ def test_update_history(etype):
             want = eb if eb - kap[e, g] > 1e-10 else kap[e, g]
             assert k1[e, g] == pytest.approx(want, rel=1e-14)
     assert np.all(k1 >= kap)
+
+
+# ---------------- state update (Alg. 2 l.8-14) for mixed elements ----------------
+
+def test_bar3_state_closed_form():
+    """u = a x + b x^2 on a BAR3 mesh: eps at the physical Gauss points = a + 2 b x_g exactly
+    (the quadratic field is reproduced); eeq = eps (R-1D), d = 1; kappa by the history rule;
+    D, g from Eqs. A.1, A.4; sigma of Eq. 2."""
+    m = mat()
+    n = 6
+    mesh = synth.mixed_mesh(BAR3, (n,), 12.0)
+    X = mesh.coords
+    doff = oracle.mixed_dofs(BAR3, X.shape[0], mesh.conn)
+    a, b = 1e-4, 2e-5
+    dofs = np.zeros(doff[-1])
+    for k in range(X.shape[0]):
+        dofs[doff[k]] = a * X[k, 0] + b * X[k, 0] ** 2
+        if doff[k + 1] - doff[k] == 2:
+            dofs[doff[k] + 1] = 1.5e-4 + 1e-5 * X[k, 0]
+    kap0 = np.full((n, 3), 2.0e-4)
+    sdv, k1 = oracle.mixed_update_state(BAR3, m, X, mesh.conn, doff, dofs, kap0)
+    pts = np.array([-np.sqrt(0.6), 0.0, np.sqrt(0.6)])
+    for e, c in enumerate(mesh.conn):
+        x0, x1 = X[c[0], 0], X[c[1], 0]
+        for g in range(3):
+            xg = 0.5 * (x0 + x1) + 0.5 * (x1 - x0) * pts[g]
+            eps = a + 2 * b * xg
+            eb = 1.5e-4 + 1e-5 * xg
+            kap = eb if eb - kap0[e, g] > 1e-10 else kap0[e, g]
+            D, _ = oracle.damage(m, kap)
+            gI, _ = oracle.interaction(m, D)
+            want = [eps, 1.0, (1 - D) * MAT["E"] * eps + MAT["h_sigma"] * (eps - eb), eps, eb,
+                    kap, D, gI]
+            np.testing.assert_allclose(sdv[e, g], want, rtol=1e-12, atol=1e-20)
+    np.testing.assert_array_equal(k1, sdv[:, :, 5])
+
+
+def test_quad8_state_patch_and_consistency():
+    """linear u on a distorted QUAD8 patch: uniform strain, sigma = C eps (plane strain,
+    textbook Lame constants) while undamaged; the records' sigma equals the stress the element
+    routine reports at every GP"""
+    m = mat()
+    mesh, X = _q8_patch(3, 2, 0.2, 7)
+    doff = oracle.mixed_dofs(QUAD8, X.shape[0], mesh.conn)
+    G = np.array([[2e-5, 1e-5], [-0.5e-5, 3e-5]])
+    dofs = np.zeros(doff[-1])
+    for k in range(X.shape[0]):
+        dofs[doff[k]:doff[k] + 2] = G @ X[k]
+        if doff[k + 1] - doff[k] == 3:
+            dofs[doff[k] + 2] = 5e-5
+    ne = mesh.conn.shape[0]
+    sdv, _ = oracle.mixed_update_state(QUAD8, m, X, mesh.conn, doff, dofs, np.zeros((ne, 9)))
+    ev = np.array([G[0, 0], G[1, 1], G[0, 1] + G[1, 0]])
+    E, nu = MAT["E"], MAT["nu"]
+    lam, mu = E * nu / ((1 + nu) * (1 - 2 * nu)), E / (2 * (1 + nu))
+    eeq, dv, _ = oracle.eqstrain(m, 2, ev)
+    sig = np.array([(lam + 2 * mu) * ev[0] + lam * ev[1], lam * ev[0] + (lam + 2 * mu) * ev[1],
+                    mu * ev[2]]) + MAT["h_sigma"] * (eeq - 5e-5) * dv
+    for e in range(ne):
+        np.testing.assert_allclose(sdv[e, :, 0:3], np.tile(ev, (9, 1)), rtol=1e-11, atol=1e-18)
+        np.testing.assert_allclose(sdv[e, :, 6:9], np.tile(sig, (9, 1)), rtol=1e-10)
+        np.testing.assert_allclose(sdv[e, :, 12], 0.0, atol=0)            # D = 0
+        g = mesh.conn[e]
+        gd = np.concatenate([doff[g[a]] + np.arange(3 if a < 4 else 2) for a in range(8)])
+        _, _, _, s_el = oracle.mixed_element(QUAD8, m, X[g], dofs[gd], np.zeros(9))
+        np.testing.assert_allclose(sdv[e, :, 6:9], s_el, rtol=1e-13, atol=1e-13 * np.abs(s_el).max())
