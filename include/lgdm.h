@@ -66,8 +66,8 @@ typedef enum {
  * (d + 1 for corner nodes, d for midside nodes), see lgdm_dof_offsets.  Single-rank whole
  * meshes only (global_node_offset 0, owned range = all nodes); assemble uses the element-block
  * + gather kernels (lgdm_set_kernel 0 or 1); lgdm_update_state writes the records of the
- * equal-order family of the same dimension (lgdm_sdv_width); lgdm_get_blocked returns
- * LGDM_ERR_UNSUPPORTED.  Gradients are evaluated on coordinates / dofs relative to each
+ * equal-order family of the same dimension (lgdm_sdv_width); lgdm_get_blocked returns the
+ * u dofs (node order) then the ebar dofs (node order).  Gradients are evaluated on coordinates / dofs relative to each
  * element's node 0 (reading R-REL). */
 typedef enum { LGDM_BAR2 = 1, LGDM_QUAD4 = 2, LGDM_HEX8 = 3, LGDM_BAR3 = 4, LGDM_QUAD8 = 5 } lgdm_elem_type;
 

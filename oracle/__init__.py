@@ -306,8 +306,14 @@ def blocked(etype: int, res: dict, n_nodes: int):
     explicit zeros of the pattern kept (reading R-PAT).  Plain definition: a symmetric
     permutation of the CSR, done on the matrix of 1-based source positions (scipy.sparse as
     the primitive) so that every stored entry moves exactly once."""
+    return blocked_from_perm(res, blocked_perm(etype, n_nodes))
+
+
+def blocked_from_perm(res: dict, p):
+    """P K P^T and P R for a permutation p (new index -> old index), columns ascending, every
+    stored entry moved exactly once (see blocked)."""
     import scipy.sparse as sp
-    p = blocked_perm(etype, n_nodes)
+    p = np.asarray(p, dtype=np.int64)
     n = p.size
     nnz = res["val"].size
     pos = sp.csr_matrix((np.arange(1, nnz + 1, dtype=np.float64),
@@ -519,3 +525,12 @@ def mixed_update_state(etype: int, m: Material, coords, conn, doff, dofs, kappa,
     if rc != 0:
         raise ValueError(f"oracle_mixed_update_state rc={rc}")
     return sdv, k
+
+
+def mixed_blocked_perm(doff, dim: int):
+    """Blocked order [u; ebar] of a mixed-order mesh (SPEC DofMap "all displacement
+    DOFs, then all micro-strain DOFs"): the u dofs in node order, then the ebar dofs in node
+    order.  Returns new index -> node-interleaved index."""
+    kind = dof_kind(np.asarray(doff), dim)
+    r = np.arange(kind.size)
+    return np.concatenate([r[kind < dim], r[kind == dim]])

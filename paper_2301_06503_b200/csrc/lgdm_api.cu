@@ -186,6 +186,8 @@ struct lgdm_mesh_s {
   NodeMeta* madj_ptr = nullptr;   // device [n_nodes] gather metadata
   MixAdj* madj = nullptr;         // device node -> element map of k_mixed_gather
   int max_row = 0;                // largest block-row (rows x width) in doubles
+  int64_t* bperm = nullptr;       // blocked order of a mixed mesh: new -> old dof
+  int32_t* binv = nullptr;        // old -> new dof
 };
 
 namespace {
@@ -992,7 +994,6 @@ lgdm_status lgdm_update_state(lgdm_mesh m, double* sdv, int64_t n_sdv, int dst_o
 lgdm_status lgdm_get_blocked(lgdm_mesh m, lgdm_csr* K, double** R) {
   if (!m) return fail(LGDM_ERR_INVALID_ARGUMENT, "mesh is NULL");
   if (!m->assembled) return fail(LGDM_ERR_INVALID_STATE, "get_blocked before assemble");
-  if (m->mixed) return fail(LGDM_ERR_UNSUPPORTED, "get_blocked: mixed-order meshes not supported");
   if (m->own_b != 0 || m->own_e != m->n_nodes || m->gid0 != 0 || m->n_global_nodes != m->n_nodes)
     return fail(LGDM_ERR_INVALID_ARGUMENT, "blocked order needs a single-rank whole mesh");
   CU(cudaSetDevice(m->device));
@@ -1005,7 +1006,28 @@ lgdm_status lgdm_get_blocked(lgdm_mesh m, lgdm_csr* K, double** R) {
   }
   const unsigned blocks = unsigned((m->n_rows * 32 + 255) / 256);
   const int64_t no = m->n_owned;
-  if (m->f.dim == 1)
+  if (m->mixed) {
+    if (!m->bperm) {   // permutation and blocked row_ptr, once per mesh
+      const int64_t n = m->n_rows;
+      std::vector<int64_t> perm(n), rp(n + 1, 0), hrp(n + 1);
+      std::vector<int32_t> inv(n);
+      int64_t k = 0;
+      for (int pass = 0; pass < 2; ++pass)
+        for (int64_t d = 0; d < n; ++d)
+          if ((m->hkind[d] == m->f.dim) == (pass == 1)) { inv[d] = int32_t(k); perm[k++] = d; }
+      CU(cudaMemcpyAsync(hrp.data(), m->row_ptr, size_t(n + 1) * 8, cudaMemcpyDeviceToHost, m->stream));
+      CU(cudaStreamSynchronize(m->stream));
+      for (int64_t r = 0; r < n; ++r) rp[r + 1] = rp[r] + (hrp[perm[r] + 1] - hrp[perm[r]]);
+      CU(dalloc(&m->bperm, size_t(n)));
+      CU(dalloc(&m->binv, size_t(n)));
+      m->device_bytes += n * 12;
+      CU(cudaMemcpyAsync(m->bperm, perm.data(), size_t(n) * 8, cudaMemcpyHostToDevice, m->stream));
+      CU(cudaMemcpyAsync(m->binv, inv.data(), size_t(n) * 4, cudaMemcpyHostToDevice, m->stream));
+      CU(cudaMemcpyAsync(m->rp_b, rp.data(), size_t(n + 1) * 8, cudaMemcpyHostToDevice, m->stream));
+      CU(cudaStreamSynchronize(m->stream));   // host vectors go out of scope
+    }
+    k_blocked_mixed<<<blocks, 256, 0, m->stream>>>(m->n_rows, m->f.dim, m->bperm, m->binv, m->dkind, m->row_ptr, m->col_idx, m->val, m->R, m->rp_b, m->ci_b, m->val_b, m->R_b);
+  } else if (m->f.dim == 1)
     k_blocked<1, 2><<<blocks, 256, 0, m->stream>>>(no, m->nbr_ptr, m->base, m->col_idx, m->val, m->R, m->rp_b, m->ci_b, m->val_b, m->R_b);
   else if (m->f.dim == 2)
     k_blocked<2, 3><<<blocks, 256, 0, m->stream>>>(no, m->nbr_ptr, m->base, m->col_idx, m->val, m->R, m->rp_b, m->ci_b, m->val_b, m->R_b);
@@ -1015,7 +1037,7 @@ lgdm_status lgdm_get_blocked(lgdm_mesh m, lgdm_csr* K, double** R) {
   if (s != LGDM_OK) return s;
   if (K) {
     K->n_rows = m->n_rows;
-    K->n_cols = m->n_global_nodes * m->f.ndpn;
+    K->n_cols = m->mixed ? m->n_rows : m->n_global_nodes * m->f.ndpn;
     K->nnz = m->nnz;
     K->first_row = 0;
     K->row_ptr = m->rp_b;
@@ -1371,7 +1393,7 @@ void lgdm_destroy(lgdm_mesh m) {
                   m->nbr_ptr, m->base, m->adj_ptr, m->adj, m->scratchK, m->scratchF,
                   m->sumsq_part, m->sumsq_out, m->k0g, m->alg, m->sdv_dev, m->rp_b,
                   m->ci_b, m->val_b, m->R_b, m->sol, m->sol_part, m->fixed, m->fixinc,
-                  m->doff, m->dkind, m->madj_ptr, m->madj};
+                  m->doff, m->dkind, m->madj_ptr, m->madj, m->bperm, m->binv};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (m->host_pinned) cudaFreeHost(m->host_pinned);

@@ -546,6 +546,45 @@ k_mixed_state(DevMat m, int64_t ne, const int32_t* __restrict__ conn,
   }
 }
 
+// Blocked order [u; ebar] of a mixed-order system: one warp per
+// blocked row r' (source row perm[r']); the row's u columns first, then its ebar columns, each
+// group in source order -- ascending blocked ids, since inv preserves the order within a kind.
+// rp_b is built on the host (row lengths are permuted, not changed).  Values move unchanged.
+__global__ void k_blocked_mixed(int64_t n, int dim, const int64_t* __restrict__ perm,
+                                const int32_t* __restrict__ inv, const uint8_t* __restrict__ kind,
+                                const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
+                                const double* __restrict__ val, const double* __restrict__ R,
+                                const int64_t* __restrict__ rp_b, int32_t* __restrict__ ci_b,
+                                double* __restrict__ val_b, double* __restrict__ R_b) {
+  const int64_t r = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= n) return;
+  const int64_t src = perm[r];
+  const int64_t lo = row_ptr[src], hi = row_ptr[src + 1];
+  int nu = 0;   // u columns of the row
+  for (int64_t q = lo + lane; q - lane < hi; q += 32) {
+    const bool u = q < hi && kind[col_idx[q]] < dim;
+    nu += __popc(__ballot_sync(0xffffffffu, u));
+  }
+  const int64_t dst0 = rp_b[r];
+  int cu = 0, ce = 0;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t q = lo + lane; q - lane < hi; q += 32) {
+    const bool in = q < hi;
+    const int32_t c = in ? col_idx[q] : 0;
+    const bool u = in && kind[c] < dim;
+    const unsigned bu = __ballot_sync(0xffffffffu, u), be = __ballot_sync(0xffffffffu, in && !u);
+    if (in) {
+      const int64_t d = dst0 + (u ? cu + __popc(bu & lt) : nu + ce + __popc(be & lt));
+      ci_b[d] = inv[c];
+      val_b[d] = val[q];
+    }
+    cu += __popc(bu);
+    ce += __popc(be);
+  }
+  if (lane == 0) R_b[r] = R[src];
+}
+
 // ||R_u||^2, ||R_e||^2 by dof kind (kind[i] = component; ebar = dim)
 __global__ void k_sumsq_kind(int64_t n, int dim, const uint8_t* __restrict__ kind,
                              const double* __restrict__ R, double* __restrict__ part) {

@@ -141,9 +141,6 @@ def test_mixed_errors():
     with pytest.raises(lgdm.LGDMError) as ei:
         m.set_kernel(2)
     assert ei.value.status == 1
-    with pytest.raises(lgdm.LGDMError) as ei:
-        m.get_blocked()
-    assert ei.value.status == 7
     with pytest.raises(lgdm.LGDMError):                   # ebar dof of a corner node
         m.apply_dirichlet([int(m.doff[0]) + 2], [0.0])
     m.close()
@@ -238,4 +235,22 @@ def test_mixed_update_state(etype, n, defects):
     err = np.abs(out - sdv_ref) / np.maximum(scale, 1e-300)
     assert err.max() <= 1e-12, (err.max(), np.unravel_index(err.argmax(), err.shape))
     np.testing.assert_allclose(m.get_kappa().reshape(k_ref.shape), k_ref, rtol=1e-15, atol=0)
+    m.close()
+
+
+@pytest.mark.parametrize("etype,n", [(lgdm.BAR3, (9,)), (lgdm.QUAD8, (7, 5)), (lgdm.QUAD8, (40, 31))])
+def test_mixed_blocked_order(etype, n):
+    """the paper's [u; ebar] order of a mixed system: bit-identical values"""
+    import torch
+    mesh, X = _mesh(etype, n, 0.1 if etype == lgdm.QUAD8 else 0.0)
+    dofs, kap = synth.mixed_fields(mesh)
+    m, got = _gpu(etype, X, mesh.conn, dofs, kap)
+    b = m.get_blocked()
+    torch.cuda.synchronize()
+    gb = {q: b[q].torch().cpu().numpy() for q in ("row_ptr", "col_idx", "val", "R")}
+    dim = synth.MFAM[etype][0]
+    p = oracle.mixed_blocked_perm(m.doff, dim)
+    ref = oracle.blocked_from_perm(dict(got, col_idx=got["col_idx"].astype(np.int32)), p)
+    for q in ("row_ptr", "col_idx", "val", "R"):
+        assert np.array_equal(gb[q], ref[q]), q
     m.close()

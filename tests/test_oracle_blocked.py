@@ -53,3 +53,36 @@ def test_blocked_is_symmetric_permutation(etype, n):
     u = np.array([a * ndpn + c for a in range(nn) for c in range(dim)])
     nu = nn * dim
     assert np.array_equal(Kb[:nu, :nu], K[np.ix_(u, u)])
+
+
+# ---------------- mixed-order meshes (SURVEY NEXT f2 x f4) ----------------
+
+def test_mixed_perm_hand_example():
+    # one BAR3 element: nodes x = 0 (corner), h/2 (midside), h (corner)
+    # interleaved [u0 e0 u1 u2 e2] -> blocked [u0 u1 u2 e0 e2]
+    mesh = synth.mixed_mesh(synth.BAR3, (1,), 2.0)
+    doff = oracle.mixed_dofs(synth.BAR3, 3, mesh.conn)
+    assert list(doff) == [0, 2, 3, 5]
+    assert list(oracle.mixed_blocked_perm(doff, 1)) == [0, 2, 3, 1, 4]
+
+
+@pytest.mark.parametrize("etype,n", [(synth.BAR3, (4,)), (synth.QUAD8, (3, 2))])
+def test_mixed_blocked_is_symmetric_permutation(etype, n):
+    mesh = synth.mixed_mesh(etype, n, 10.0)
+    d, k = synth.mixed_fields(mesh)
+    res = oracle.mixed_assemble(etype, oracle.material(**synth.MATERIAL), mesh.coords, mesh.conn,
+                                d, k)
+    dim = synth.MFAM[etype][0]
+    p = oracle.mixed_blocked_perm(res["doff"], dim)
+    N = p.size
+    b = oracle.blocked_from_perm(res, p)
+    K, Kb = _dense(res, N), _dense(b, N)
+    assert np.array_equal(Kb, K[np.ix_(p, p)])
+    assert np.array_equal(b["R"], res["R"][p])
+    kind = oracle.dof_kind(res["doff"], dim)
+    nu = int((kind < dim).sum())
+    u = np.nonzero(kind < dim)[0]
+    assert np.array_equal(Kb[:nu, :nu], K[np.ix_(u, u)])
+    for r in range(N):
+        c = b["col_idx"][b["row_ptr"][r]:b["row_ptr"][r + 1]]
+        assert np.all(np.diff(c) > 0)
