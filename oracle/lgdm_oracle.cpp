@@ -249,10 +249,12 @@ int oracle_element_d(int type, const oracle_material* m0, const double* Xe, cons
     // ---- geometry (Fig. 3, gp_data): J, det J, grad N ----
     double N[8], dNdxi[24];
     oracle_shape(type, xi + g * dim, N, dNdxi);
+    // J = sum_a X_a dN_a/dxi with coordinates relative to node 0 (reading R-REL: the same sum,
+    // sum_a dN_a/dxi = 0; exact differences instead of the cancellation of |X| >> element size)
     double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
     for (int a = 0; a < nen; ++a)
       for (int i = 0; i < dim; ++i)
-        for (int j = 0; j < dim; ++j) J[i][j] += Xe[a * dim + i] * dNdxi[a * dim + j];
+        for (int j = 0; j < dim; ++j) J[i][j] += (Xe[a * dim + i] - Xe[i]) * dNdxi[a * dim + j];
     double detJ, Ji[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
     if (dim == 1) {
       detJ = J[0][0];
@@ -311,11 +313,15 @@ int oracle_element_d(int type, const oracle_material* m0, const double* Xe, cons
     }
 
     // ---- kinematics (Fig. 5b l.12, l.17): eps = B u, ebar = N e, grad ebar = B_e e ----
+    // (R-REL: B u and grad ebar on the dofs relative to node 0's -- B annihilates constants;
+    // ebar = N e on the absolute values)
+    double Ur[32];
+    for (int r = 0; r < nd; ++r) Ur[r] = Ue[r] - Ue[r % ndpn];
     double ev[6] = {0, 0, 0, 0, 0, 0}, ebar = 0.0, gbar[3] = {0, 0, 0};
     for (int r = 0; r < nd; ++r) {
-      for (int V = 0; V < nv; ++V) ev[V] += Bu[V][r] * Ue[r];
+      for (int V = 0; V < nv; ++V) ev[V] += Bu[V][r] * Ur[r];
       ebar += Ne[r] * Ue[r];
-      for (int i = 0; i < dim; ++i) gbar[i] += Be[i][r] * Ue[r];
+      for (int i = 0; i < dim; ++i) gbar[i] += Be[i][r] * Ur[r];
     }
 
     // ---- constitutive (Appendix A; Fig. 8b condition vectors) ----
@@ -681,9 +687,9 @@ int oracle_update_state(int type, const oracle_material* m, int64_t n_nodes, con
       oracle_shape(type, xi + g * dim, N, dNdxi);
       // J_ij = sum_a X_ai dN_a/dxi_j; grad_x N = J^-T grad_xi N (as oracle_element)
       double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}}, Ji[3][3];
-      for (int a = 0; a < nen; ++a)
+      for (int a = 0; a < nen; ++a)   // relative to node 0 (R-REL)
         for (int i = 0; i < dim; ++i)
-          for (int j = 0; j < dim; ++j) J[i][j] += Xe[a * dim + i] * dNdxi[a * dim + j];
+          for (int j = 0; j < dim; ++j) J[i][j] += (Xe[a * dim + i] - Xe[i]) * dNdxi[a * dim + j];
       if (!invert(dim, J, Ji)) return -2;
       double gradN[8][3];
       for (int a = 0; a < nen; ++a)
@@ -698,8 +704,8 @@ int oracle_update_state(int type, const oracle_material* m, int64_t n_nodes, con
         for (int V = 0; V < nv; ++V) {
           int p, q;
           voigt_pair(dim, V, &p, &q);
-          if (p == q) ev[V] += gradN[a][p] * Ue[a * ndpn + p];
-          else ev[V] += gradN[a][q] * Ue[a * ndpn + p] + gradN[a][p] * Ue[a * ndpn + q];
+          if (p == q) ev[V] += gradN[a][p] * (Ue[a * ndpn + p] - Ue[p]);
+          else ev[V] += gradN[a][q] * (Ue[a * ndpn + p] - Ue[p]) + gradN[a][p] * (Ue[a * ndpn + q] - Ue[q]);
         }
         ebar += N[a] * Ue[a * ndpn + dim];
       }

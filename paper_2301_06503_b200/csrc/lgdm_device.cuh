@@ -294,19 +294,20 @@ __device__ __forceinline__ double gpCoreSK(const DevMat& m, XF&& X, UF&& U, doub
   using F = Fam<D>;
   constexpr int NEN = F::NEN, NS = F::NS;
 
-  // geometry: J_ij = sum_a X_ai dN_a/dxi_j
+  // geometry: J_ij = sum_a X_ai dN_a/dxi_j = sum_{a>0} (X_ai - X_0i) dN_a/dxi_j (reading R-REL:
+  // sum_a dN_a = 0; exact differences instead of the cancellation of |X| >> element size)
   double J[D][D];
 #pragma unroll
   for (int i = 0; i < D; ++i)
 #pragma unroll
     for (int j = 0; j < D; ++j) J[i][j] = 0.0;
 #pragma unroll
-  for (int a = 0; a < NEN; ++a)
+  for (int a = 1; a < NEN; ++a)
 #pragma unroll
     for (int j = 0; j < D; ++j) {
       const double dn = SHD(a, j);
 #pragma unroll
-      for (int i = 0; i < D; ++i) J[i][j] = fma(X(a, i), dn, J[i][j]);
+      for (int i = 0; i < D; ++i) J[i][j] = fma(X(a, i) - X(0, i), dn, J[i][j]);
     }
   double detJ, Ji[D][D];
   if constexpr (D == 1) {
@@ -354,17 +355,19 @@ __device__ __forceinline__ double gpCoreSK(const DevMat& m, XF&& X, UF&& U, doub
 #pragma unroll
     for (int j = 0; j < D; ++j) eps[i][j] = 0.0;
   }
+  ebar = SHN(0) * U(0, D);
 #pragma unroll
-  for (int a = 0; a < NEN; ++a) {
+  for (int a = 1; a < NEN; ++a) {     // gradients from differences to node 0 (R-REL)
     double gn[D];
     gradN(a, gn);
     const double ea = U(a, D);
     ebar = fma(SHN(a), ea, ebar);
+    const double de = ea - U(0, D);
 #pragma unroll
     for (int i = 0; i < D; ++i) {
-      gb[i] = fma(gn[i], ea, gb[i]);
+      gb[i] = fma(gn[i], de, gb[i]);
       {
-        const double ua = U(a, i);
+        const double ua = U(a, i) - U(0, i);
 #pragma unroll
         for (int j = 0; j < D; ++j) eps[i][j] = fma(ua, gn[j], eps[i][j]);
       }

@@ -322,12 +322,13 @@ k_update_state(DevMat m, int64_t ne, const int32_t* __restrict__ conn,
     for (int i = 0; i < D; ++i)
 #pragma unroll
       for (int j = 0; j < D; ++j) J[i][j] = 0.0;
+    const int64_t n0 = ce[0];
 #pragma unroll
-    for (int a = 0; a < F::NEN; ++a) {
+    for (int a = 1; a < F::NEN; ++a) {        // relative to node 0 (reading R-REL)
       const int64_t n = ce[a];
 #pragma unroll
       for (int i = 0; i < D; ++i) {
-        const double x = __ldg(coords + n * D + i);
+        const double x = __ldg(coords + n * D + i) - __ldg(coords + n0 * D + i);
 #pragma unroll
         for (int j = 0; j < D; ++j) J[i][j] = fma(x, shape_dxi<D>(a, g, j), J[i][j]);
       }
@@ -375,7 +376,7 @@ k_update_state(DevMat m, int64_t ne, const int32_t* __restrict__ conn,
       }
 #pragma unroll
       for (int i = 0; i < D; ++i) {
-        const double u = __ldg(dofs + n * F::NDPN + i);
+        const double u = __ldg(dofs + n * F::NDPN + i) - __ldg(dofs + n0 * F::NDPN + i);
 #pragma unroll
         for (int j = 0; j < D; ++j) Gu[i][j] = fma(u, gn[j], Gu[i][j]);
       }
