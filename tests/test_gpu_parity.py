@@ -83,6 +83,17 @@ def test_parity_damage_edge_states():
                 compare(ref, got, "edge state")
 
 
+def test_parity_config2_full():
+    """BASELINE config 2 (Q4 1000^2, 1 M elements, 81 M entries) in full, default kernel"""
+    cfg = synth.CONFIGS[2]
+    mesh = synth.structured_mesh(cfg)
+    dofs, kappa = synth.fields(cfg, mesh)
+    ref = oracle_assemble(cfg.etype, mesh.coords, mesh.conn, dofs, kappa)
+    got = gpu_assemble(cfg.etype, mesh.coords, mesh.conn, dofs, kappa)
+    kerr, rerr = compare(ref, got, "config 2 full")
+    print(f"config 2 full: max K err/rowmax {kerr:.2e}, max R err/S {rerr:.2e}")
+
+
 @pytest.mark.parametrize("kernel", [lgdm.KERNEL_AUTO, lgdm.KERNEL_SWEEP3, lgdm.KERNEL_SWEEP4,
                                     lgdm.KERNEL_SWEEP5])
 @pytest.mark.parametrize("cid", [2, 3])
