@@ -306,7 +306,7 @@ k_update_state(DevMat m, int64_t ne, const int32_t* __restrict__ conn,
                double* __restrict__ kappa, const double* __restrict__ k0g,
                const double* __restrict__ alg, double* __restrict__ sdv) {
   using F = Fam<D>;
-  constexpr int NV = StateW<D>::NV, W = StateW<D>::W;
+  constexpr int W = StateW<D>::W;
   extern __shared__ double stage[];   // [blockDim][W]: records, written out coalesced
   const int64_t t0 = int64_t(blockIdx.x) * blockDim.x;
   const int64_t t = t0 + threadIdx.x;

@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(S4::T, 1)
 k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
          const double* __restrict__ dofs, const double* __restrict__ kappa,
          const int64_t* __restrict__ base, double* __restrict__ val, double* __restrict__ Rv) {
-  constexpr int E = S4::E, NGP = 8, NEN = 8;
+  constexpr int NGP = 8, NEN = 8;
   extern __shared__ double sm[];
   double* shtab = sm;                              // [NGP][NEN][6] = (dN/dxi, N, pad)
   double* cores = shtab + S4::SHT;                 // [3][E][CEL]
@@ -472,7 +472,7 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
   };
 
   int prev_c = -1, t = 0;
-  const bool ptc = ct == 0;
+  [[maybe_unused]] const bool ptc = ct == 0;   // phase-timing build (PT_MARK)
   PT_DECL
   schedule(
       [&](int64_t s, int c, int b0, int ifst, int ni, int jfst, int nc) {

@@ -89,7 +89,7 @@ k_sweep5(DevMat m, SweepGeom G, const double* __restrict__ coords,
     }
   };
 
-  constexpr int NPC_T = 64, NC_T = 32 * S5::NC;
+  [[maybe_unused]] constexpr int NPC_T = 64, NC_T = 32 * S5::NC;
 
   if (warp < S5::NPC) {
     // ---------- PC: core + 8 node expansions per lane (element, GP), straight to the slot ----------
@@ -251,7 +251,7 @@ k_sweep5(DevMat m, SweepGeom G, const double* __restrict__ coords,
   };
 
   int prev_c = -1, t = 0;
-  const bool ptc = ct == 0;
+  [[maybe_unused]] const bool ptc = ct == 0;
   PT_DECL
   schedule(
       [&](int64_t s, int c, int b0, int ifst, int ni, int jfst, int nc) {

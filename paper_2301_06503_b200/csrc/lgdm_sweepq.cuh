@@ -126,7 +126,7 @@ k_sweepq(DevMat m, SweepGeom G, const double* __restrict__ coords,
       sh[a][2] = shtab[(g * NEN + a) * 4 + 2];
     }
     int t = 0;
-    const bool ptp = tid == 0;
+    [[maybe_unused]] const bool ptp = tid == 0;
     PT_DECL
     schedule(
         [&](int64_t s, int, int b0, int ifst, int nc) {
@@ -230,7 +230,7 @@ k_sweepq(DevMat m, SweepGeom G, const double* __restrict__ coords,
     // consecutive interior nodes) and R stream out, and the row buffer is reset for s+2.
     const int ft = ctid - C_T;
     constexpr int F_T = 32 * SQ::NFW;
-    const bool ptf = ft == 0;
+    [[maybe_unused]] const bool ptf = ft == 0;
     PT_DECL
     // compact the block-row of an edge node (fewer than 9 neighbours) into its CSR slots
     auto flush_edge = [&](int x, int64_t zn) {
@@ -435,7 +435,7 @@ k_sweepq(DevMat m, SweepGeom G, const double* __restrict__ coords,
   auto owned = [&](int x, int64_t z) { return x >= ix0 && x < ix1 && z >= z0 && z < z1; };
 
   int t = 0;
-  const bool ptc = ct == 0;
+  [[maybe_unused]] const bool ptc = ct == 0;
   PT_DECL
   schedule(
       [&](int64_t s, int c, int, int ifst, int nc) {
