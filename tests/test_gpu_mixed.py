@@ -254,3 +254,52 @@ def test_mixed_blocked_order(etype, n):
     for q in ("row_ptr", "col_idx", "val", "R"):
         assert np.array_equal(gb[q], ref[q]), q
     m.close()
+
+
+def test_quad8_strip_newton_matches_oracle():
+    """2D with the paper's own discretisation (serendipity u, bilinear ebar): a plane
+    strain strip pulled at x = L with a weaker column of elements, three displacement steps
+    into damage; the GPU Newton loop (direct solve) matches the oracle's iteration counts,
+    reactions and committed history."""
+    etype, n = lgdm.QUAD8, (8, 3)
+    mesh = synth.mixed_mesh(etype, n, 8.0)
+    X = mesh.coords
+    ne = mesh.conn.shape[0]
+    ex = X[mesh.conn[:, :4], 0].mean(axis=1)
+    k0g = np.repeat(np.where(np.abs(ex - 4.0) < 0.6, 0.9, 1.0) * MAT["kappa0"], 9)
+    doff = oracle.mixed_dofs(etype, X.shape[0], mesh.conn)
+    kind = oracle.dof_kind(doff, 2)
+    left = np.nonzero(X[:, 0] == X[:, 0].min())[0]
+    right = np.nonzero(X[:, 0] == X[:, 0].max())[0]
+    ids = np.concatenate([doff[left], doff[left] + 1, doff[right]])
+    inc = np.concatenate([np.zeros(2 * left.size), np.full(right.size, 1.0)])
+    om = oracle.material(**MAT)
+    nd = int(doff[-1])
+    schedule = [(2, 3e-4), (3, 1e-4)]
+    dofs, kh = np.zeros(nd), np.zeros((ne, 9))
+    its_ref, react_ref = [], []
+    for nst, du in schedule:
+        for _ in range(nst):
+            for it in range(1, 41):
+                res = oracle.mixed_assemble(etype, om, X, mesh.conn, dofs, kh, kappa0_gp=k0g)
+                delta = oracle.solve(oracle.apply_dirichlet(res, ids, inc * du if it == 1 else 0 * inc))
+                dofs = dofs + delta
+                ok, _, _ = oracle.converged_kind(delta, dofs, kind, 2, 1e-6)
+                if ok:
+                    break
+            assert ok
+            its_ref.append(it)
+            res = oracle.mixed_assemble(etype, om, X, mesh.conn, dofs, kh, kappa0_gp=k0g)
+            react_ref.append(oracle.reaction(res, doff[right]))
+            kh = oracle.mixed_update_history(etype, mesh.conn, doff, dofs, kh)
+    assert kh.max() > MAT["kappa0"]                       # the run reaches damage
+    m = lgdm.Mesh(etype, X, mesh.conn, lgdm.material(**MAT))
+    m.set_state(np.zeros(nd), np.zeros((ne, 9)))
+    m.set_defects(k0g, None)
+    log = []
+    for nst, du in schedule:
+        log += lgdm.newton(m, ids, inc * du, n_steps=nst, tol=1e-6, max_iter=40)
+    assert [s["iterations"] for s in log] == its_ref
+    np.testing.assert_allclose([s["reaction"] for s in log], react_ref, rtol=1e-7)
+    np.testing.assert_allclose(m.get_kappa().reshape(kh.shape), kh, rtol=1e-7, atol=1e-14)
+    m.close()
