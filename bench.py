@@ -216,15 +216,20 @@ def run_lgdm(cfg, steps, warmup, rank, world, local, pg_barrier, allmax, comm_ui
     res["alg_bytes"] = algorithmic_bytes(ndpn, dim, nen, ngp, info["nnz"], info["n_rows"],
                                          info["n_nodes"], info["n_elems"])
     if e2e:
-        # end-to-end through the public API: H2D of this step's dofs from pinned host memory,
-        # the step, D2H of the residual norms (the convergence quantities).
+        # end-to-end through the public API: H2D of every step's dofs from pinned host memory,
+        # the step, D2H of the residual norms (the convergence quantities).  The copy of step
+        # t+1's dofs is started (lgdm_prefetch_dofs, own copy stream) before step t runs, so it
+        # overlaps the assembly; every copy is inside the timed region.
         m.set_state(dofs_h, None)
         torch.cuda.synchronize()
         pg_barrier()
         s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s2.record(stream)
+        m.prefetch_dofs(dofs_h)
         for t in range(steps):
-            m.set_state(dofs_h, None)
+            m.set_state_prefetched()
+            if t + 1 < steps:
+                m.prefetch_dofs(dofs_h)
             step(t)
         e2.record(stream)
         torch.cuda.synchronize()

@@ -132,6 +132,19 @@ lgdm_status lgdm_create_mesh(lgdm_elem_type type, int64_t n_nodes, const double*
 lgdm_status lgdm_set_state(lgdm_mesh mesh, const double* dofs, int64_t n_dofs,
                            const double* kappa, int64_t n_kappa, int src_on_device);
 
+/* Overlapped input transfer for a stream of iterates: lgdm_prefetch_dofs starts copying the
+ * NEXT iterate's dofs (host, pinned for asynchrony; n_dofs as in lgdm_set_state) into a second
+ * device buffer on an internal copy stream, concurrently with the work already enqueued on the
+ * mesh stream; lgdm_set_state_prefetched makes that buffer the current dofs (the mesh stream
+ * waits for the copy; the two buffers are swapped, nothing is copied again).  At most one
+ * prefetch may be pending: a second call before lgdm_set_state_prefetched, or
+ * lgdm_set_state_prefetched without a pending prefetch -> LGDM_ERR_INVALID_STATE.  The history
+ * kappa must have been set before (lgdm_set_state).  The host buffer must stay valid until the
+ * copy completes (next lgdm_set_state_prefetched returns after enqueuing the wait, so keep it
+ * until the following synchronisation of the mesh stream). */
+lgdm_status lgdm_prefetch_dofs(lgdm_mesh mesh, const double* host_dofs, int64_t n_dofs);
+lgdm_status lgdm_set_state_prefetched(lgdm_mesh mesh);
+
 /* Assemble K (owned rows) and R = F (owned rows) for the current state (Eqs. 11a-f with the
  * trial kappa = cond1 ? ebar : kappa_hist, Fig. 8b; history is NOT written, reading R-HIST).
  * K and *R point to mesh-owned device memory. */

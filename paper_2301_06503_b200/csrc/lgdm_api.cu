@@ -186,6 +186,11 @@ struct lgdm_mesh_s {
   NodeMeta* madj_ptr = nullptr;   // device [n_nodes] gather metadata
   MixAdj* madj = nullptr;         // device node -> element map of k_mixed_gather
   int max_row = 0;                // largest block-row (rows x width) in doubles
+  // overlapped input transfer (lgdm_prefetch_dofs)
+  double* dofs_back = nullptr;
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t copy_ev = nullptr, free_ev = nullptr;
+  bool prefetch_pending = false, free_ev_set = false;
   int64_t* bperm = nullptr;       // blocked order of a mixed mesh: new -> old dof
   int32_t* binv = nullptr;        // old -> new dof
 };
@@ -855,6 +860,41 @@ template <int D> lgdm_status assemble_general(lgdm_mesh m) {
 
 extern "C" {
 
+lgdm_status lgdm_prefetch_dofs(lgdm_mesh m, const double* host_dofs, int64_t n_dofs) {
+  if (!m || !host_dofs) return fail(LGDM_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (n_dofs != m->n_dofs_local)
+    return fail(LGDM_ERR_INVALID_STATE, "n_dofs = %lld, expected %lld", (long long)n_dofs, (long long)m->n_dofs_local);
+  if (m->prefetch_pending) return fail(LGDM_ERR_INVALID_STATE, "a prefetch is already pending");
+  CU(cudaSetDevice(m->device));
+  if (!m->dofs_back) {
+    CU(dalloc(&m->dofs_back, size_t(n_dofs)));
+    m->device_bytes += n_dofs * 8;
+    CU(cudaStreamCreateWithFlags(&m->cstream, cudaStreamNonBlocking));
+    CU(cudaEventCreateWithFlags(&m->copy_ev, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&m->free_ev, cudaEventDisableTiming));
+  }
+  // the back buffer was the current dofs until the last swap: wait for the work that used it
+  if (m->free_ev_set) CU(cudaStreamWaitEvent(m->cstream, m->free_ev, 0));
+  CU(cudaMemcpyAsync(m->dofs_back, host_dofs, size_t(n_dofs) * 8, cudaMemcpyHostToDevice, m->cstream));
+  CU(cudaEventRecord(m->copy_ev, m->cstream));
+  m->prefetch_pending = true;
+  return LGDM_OK;
+}
+
+lgdm_status lgdm_set_state_prefetched(lgdm_mesh m) {
+  if (!m) return fail(LGDM_ERR_INVALID_ARGUMENT, "mesh is NULL");
+  if (!m->prefetch_pending) return fail(LGDM_ERR_INVALID_STATE, "no pending prefetch");
+  if (!m->have_kappa) return fail(LGDM_ERR_INVALID_STATE, "kappa never set");
+  CU(cudaSetDevice(m->device));
+  CU(cudaStreamWaitEvent(m->stream, m->copy_ev, 0));
+  std::swap(m->dofs, m->dofs_back);
+  CU(cudaEventRecord(m->free_ev, m->stream));   // old buffer free once the work so far is done
+  m->free_ev_set = true;
+  m->prefetch_pending = false;
+  m->have_state = true;
+  return LGDM_OK;
+}
+
 lgdm_status lgdm_assemble(lgdm_mesh m, lgdm_csr* K, double** R) {
   if (!m) return fail(LGDM_ERR_INVALID_ARGUMENT, "mesh is NULL");
   if (!m->have_state || !m->have_kappa) return fail(LGDM_ERR_INVALID_STATE, "assemble before set_state");
@@ -1393,10 +1433,13 @@ void lgdm_destroy(lgdm_mesh m) {
                   m->nbr_ptr, m->base, m->adj_ptr, m->adj, m->scratchK, m->scratchF,
                   m->sumsq_part, m->sumsq_out, m->k0g, m->alg, m->sdv_dev, m->rp_b,
                   m->ci_b, m->val_b, m->R_b, m->sol, m->sol_part, m->fixed, m->fixinc,
-                  m->doff, m->dkind, m->madj_ptr, m->madj, m->bperm, m->binv};
+                  m->doff, m->dkind, m->madj_ptr, m->madj, m->bperm, m->binv, m->dofs_back};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (m->host_pinned) cudaFreeHost(m->host_pinned);
+  if (m->cstream) cudaStreamSynchronize(m->cstream), cudaStreamDestroy(m->cstream);
+  if (m->copy_ev) cudaEventDestroy(m->copy_ev);
+  if (m->free_ev) cudaEventDestroy(m->free_ev);
   sweep_free(m);
   delete m;
 }

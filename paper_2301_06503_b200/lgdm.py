@@ -33,7 +33,7 @@ EXPORTS = ["lgdm_create_mesh", "lgdm_set_state", "lgdm_assemble", "lgdm_update_h
            "lgdm_last_error", "lgdm_destroy", "lgdm_sdv_width", "lgdm_set_defects",
            "lgdm_update_state", "lgdm_get_blocked", "lgdm_apply_dirichlet", "lgdm_solve",
            "lgdm_add_dofs", "lgdm_delta_norms", "lgdm_reaction", "lgdm_solve_direct",
-           "lgdm_dof_offsets"]
+           "lgdm_dof_offsets", "lgdm_prefetch_dofs", "lgdm_set_state_prefetched"]
 
 
 class LGDMError(RuntimeError):
@@ -105,6 +105,8 @@ def load() -> C.CDLL:
     L.lgdm_reaction.argtypes = [vp, i64, vp, dp]
     L.lgdm_solve_direct.argtypes = [vp, vp, C.POINTER(C.c_int)]
     L.lgdm_dof_offsets.argtypes = [vp, vp, i64]
+    L.lgdm_prefetch_dofs.argtypes = [vp, vp, i64]
+    L.lgdm_set_state_prefetched.argtypes = [vp]
     for name in EXPORTS:
         if name not in ("lgdm_launch_count", "lgdm_last_error", "lgdm_destroy"):
             getattr(L, name).restype = C.c_int
@@ -202,6 +204,18 @@ class Mesh:
         _check(load().lgdm_set_state(self._h, pd, int(np.prod(getattr(dofs, "shape", (n_d,)))),
                                      pk, int(np.prod(getattr(kappa, "shape", (0,)))), on_dev))
         self._keep = [kd, kk]   # host copies are async only for pinned memory; keep alive
+
+    def prefetch_dofs(self, dofs):
+        """Start copying the next iterate's dofs (pinned host tensor / array) on the mesh's copy
+        stream, overlapped with the work already enqueued (include/lgdm.h)."""
+        p, on_dev, keep = _ptr_and_kind(dofs)
+        if on_dev:
+            raise ValueError("prefetch_dofs takes host memory")
+        self._keep_prefetch = keep
+        _check(load().lgdm_prefetch_dofs(self._h, p, self.n_dofs))
+
+    def set_state_prefetched(self):
+        _check(load().lgdm_set_state_prefetched(self._h))
 
     def assemble(self):
         """Returns (row_ptr, col_idx, val, R, first_row, n_cols) as zero-copy device views."""

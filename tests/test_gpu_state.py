@@ -203,3 +203,40 @@ def test_blocked_errors():
     with pytest.raises(lgdm.LGDMError):
         m.get_blocked()                       # not a whole single-rank mesh
     m.close()
+
+
+@pytest.mark.parametrize("etype,n", [(lgdm.QUAD4, (12, 9)), (lgdm.HEX8, (5, 4, 6))])
+def test_prefetch_dofs_matches_set_state(etype, n):
+    """lgdm_prefetch_dofs + lgdm_set_state_prefetched (overlapped input transfer): a sequence of
+    iterates gives bit-identical K and R to plain set_state, and misuse is refused"""
+    import torch
+    cfg = synth.small_config(etype, n)
+    mesh = synth.structured_mesh(cfg)
+    dofs, kappa = synth.fields(cfg, mesh)
+    seq = [dofs * s for s in (1.0, 1.3, 0.7)]
+    mat = lgdm.material(**synth.MATERIAL)
+    ref = lgdm.Mesh(etype, mesh.coords, mesh.conn, mat)
+    want = []
+    for d in seq:
+        ref.set_state(d, kappa)
+        out = ref.assemble()
+        torch.cuda.synchronize()
+        want.append((out["val"].torch().cpu().numpy().copy(), out["R"].torch().cpu().numpy().copy()))
+    m = lgdm.Mesh(etype, mesh.coords, mesh.conn, mat)
+    with pytest.raises(lgdm.LGDMError):
+        m.set_state_prefetched()                      # nothing pending
+    m.set_state(seq[0], kappa)
+    host = [torch.from_numpy(d.reshape(-1).copy()).pin_memory() for d in seq]
+    m.prefetch_dofs(host[0])
+    with pytest.raises(lgdm.LGDMError):
+        m.prefetch_dofs(host[0])                      # one pending at a time
+    for t in range(len(seq)):
+        m.set_state_prefetched()
+        if t + 1 < len(seq):
+            m.prefetch_dofs(host[t + 1])
+        out = m.assemble()
+        torch.cuda.synchronize()
+        assert np.array_equal(out["val"].torch().cpu().numpy(), want[t][0])
+        assert np.array_equal(out["R"].torch().cpu().numpy(), want[t][1])
+    m.close()
+    ref.close()
