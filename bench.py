@@ -401,7 +401,9 @@ def main():
     import torch
     torch.cuda.set_device(local)
     comm_uid = None
-    if ws > 1:
+    # under torchrun (also with one process) the multi-GPU path runs: NCCL process group,
+    # NCCL communicator of the mesh, max-over-ranks timing
+    if ws > 1 or os.environ.get("LOCAL_RANK") is not None:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
         from paper_2301_06503_b200 import lgdm
@@ -466,8 +468,8 @@ def main():
             out["mixed_order"] = mixed_secondary(args.steps, args.warmup, peak)
     if rank == 0:
         print(json.dumps(out))
-    if ws > 1:
-        import torch.distributed as dist
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
         dist.barrier()
         dist.destroy_process_group()
 

@@ -240,3 +240,24 @@ def test_prefetch_dofs_matches_set_state(etype, n):
         assert np.array_equal(out["R"].torch().cpu().numpy(), want[t][1])
     m.close()
     ref.close()
+
+
+def test_nccl_single_rank_comm():
+    """lgdm_nccl_unique_id + lgdm_set_comm (NCCL dlopen'ed) with one rank: the allreduce of
+    lgdm_residual_norms is the identity, so the norms equal the communicator-free ones"""
+    cfg = synth.small_config(lgdm.HEX8, (3, 3, 4))
+    mesh = synth.structured_mesh(cfg)
+    dofs, kappa = synth.fields(cfg, mesh)
+    mat = lgdm.material(**synth.MATERIAL)
+    a = lgdm.Mesh(lgdm.HEX8, mesh.coords, mesh.conn, mat)
+    a.set_state(dofs, kappa)
+    a.assemble()
+    want = a.residual_norms()
+    b = lgdm.Mesh(lgdm.HEX8, mesh.coords, mesh.conn, mat)
+    b.set_comm(lgdm.nccl_unique_id(), 1, 0)
+    b.set_state(dofs, kappa)
+    b.assemble()
+    got = b.residual_norms()
+    assert np.array_equal(got, want)
+    a.close()
+    b.close()
