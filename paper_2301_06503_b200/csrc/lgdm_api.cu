@@ -409,6 +409,7 @@ lgdm_status create_mixed(lgdm_elem_type type, int64_t n_nodes, const double* coo
     doff[n + 1] = doff[n] + (kind[n] == 1 ? f.dim + 1 : f.dim);
   }
   const int64_t ndof = doff[n_nodes];
+  if (ndof >= (int64_t(1) << 31)) return fail(LGDM_ERR_INVALID_ARGUMENT, "dof count exceeds int32 col_idx");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     return fail(LGDM_ERR_CUDA, "no CUDA device available (liblgdm has no CPU path)");
