@@ -588,7 +588,7 @@ template <int T> lgdm_status assemble_mixed(lgdm_mesh m) {
                                                               m->scratchK, m->scratchF);
   lgdm_status s = check_launch(m, "k_mixed_blocks");
   if (s != LGDM_OK) return s;
-  const size_t gsm = sizeof(double) * size_t(GW) * m->max_row;
+  const size_t gsm = sizeof(double) * size_t(GW) * (size_t(m->max_row) + MGStage<T>::SIZE);
   if (gsm > 48 * 1024) CU(cudaFuncSetAttribute(k_mixed_gather<T, GW>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gsm)));
   const int64_t gn = (m->n_nodes + GW - 1) / GW;
   k_mixed_gather<T, GW><<<unsigned(std::min<int64_t>(gn, int64_t(nsm) * 16)), GW * 32, gsm, m->stream>>>(

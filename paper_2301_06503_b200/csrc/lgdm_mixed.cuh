@@ -339,18 +339,37 @@ struct NodeMeta {
   int16_t nr, nk;
 };
 
+// async global -> shared copies (no registers held while the loads are in flight)
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  const unsigned d = unsigned(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_all;\n" ::: "memory");
+}
+
+// per-warp staging of the gather: MXS element row-blocks ((D+1) x NDOFE doubles, padded to
+// 32-multiples) + their residual entries
+template <int T> struct MGStage {
+  static constexpr int MXS = 4;
+  static constexpr int RB = ((MFam<T>::DIM + 1) * MFam<T>::NDOFE + 31) / 32 * 32;
+  static constexpr int SIZE = MXS * (RB + 4);
+};
+
 template <int T, int WPB>
-__global__ void __launch_bounds__(WPB * 32, 5)
+__global__ void __launch_bounds__(WPB * 32, 4)
 k_mixed_gather(int64_t nn, const NodeMeta* __restrict__ meta, const MixAdj* __restrict__ adj,
                const double* __restrict__ EB, const double* __restrict__ EF, int max_row,
                double* __restrict__ val, double* __restrict__ R) {
   using F = MFam<T>;
+  using SG = MGStage<T>;
   constexpr int ND = F::NDOFE;
-  constexpr int NQ = ((F::DIM + 1) * ND + 31) / 32;   // entries of one element's rows per lane
-  constexpr int CH = 1;                               // adjacent elements loaded per round
+  constexpr int NQ = SG::RB / 32;                     // entries of one element's rows per lane
   extern __shared__ double smem_mg[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  double* buf = smem_mg + w * max_row;
+  double* buf = smem_mg + w * (max_row + SG::SIZE);
+  double* stg = buf + max_row;                        // [MXS][RB] row-blocks, then [MXS][4] F
+  double* stf = stg + SG::MXS * SG::RB;
   const int64_t stride = int64_t(gridDim.x) * WPB;
   int64_t n = int64_t(blockIdx.x) * WPB + w;
   NodeMeta nx{};
@@ -372,38 +391,29 @@ k_mixed_gather(int64_t nn, const NodeMeta* __restrict__ meta, const MixAdj* __re
       qoff[t] = q < nr * ND ? (q / ND) * W + mdof_comp<T>(c) : -1;
     }
     double rsum = 0.0;
-    __syncwarp();
     const int64_t k0 = md.k0, k1 = md.k0 + md.nk;
-    for (int64_t k = k0; k < k1; k += CH) {
-      const int kk = int(k1 - k < CH ? k1 - k : CH);
-      double v[CH][NQ], fr[CH];
-      int pos[CH][NQ];
-      // issue every load of the round first (one memory latency per round, not per element)
+    for (int64_t k = k0; k < k1; k += SG::MXS) {
+      const int kk = int(k1 - k < SG::MXS ? k1 - k : SG::MXS);
+      // all row-blocks of the round in flight at once, straight into shared memory
+      for (int u = 0; u < kk; ++u) {
+        const MixAdj* en = adj + k + u;
+        const int64_t e = en->e;
+        const int lr = mldof<T>(en->aloc);
+        const double* src = EB + e * (ND * ND) + lr * ND;
 #pragma unroll
-      for (int u = 0; u < CH; ++u) {
-        fr[u] = 0.0;
-        if (u < kk) {
-          const MixAdj* en = adj + k + u;
-          const int64_t e = en->e;
-          const int lr = mldof<T>(en->aloc);
-          const double* src = EB + e * (ND * ND) + lr * ND;
-#pragma unroll
-          for (int t = 0; t < NQ; ++t) {       // row i, column c of the element's rows: q = i ND + c
-            v[u][t] = qoff[t] >= 0 ? src[lane + 32 * t] : 0.0;
-            pos[u][t] = qoff[t] + en->coff[qb[t]];
-          }
-          if (lane < nr) fr[u] = EF[e * ND + lr + lane];
-        }
+        for (int t = 0; t < NQ; ++t)
+          if (qoff[t] >= 0) cp_async8(stg + u * SG::RB + lane + 32 * t, src + lane + 32 * t);
+        if (lane < nr) cp_async8(stf + u * 4 + lane, EF + e * ND + lr + lane);
       }
+      cp_async_wait_all();
+      __syncwarp();
       // accumulate in ascending element order
+      for (int u = 0; u < kk; ++u) {
+        const MixAdj* en = adj + k + u;
 #pragma unroll
-      for (int u = 0; u < CH; ++u) {
-        if (u < kk) {
-#pragma unroll
-          for (int t = 0; t < NQ; ++t)
-            if (qoff[t] >= 0) buf[pos[u][t]] += v[u][t];
-          rsum += fr[u];
-        }
+        for (int t = 0; t < NQ; ++t)
+          if (qoff[t] >= 0) buf[qoff[t] + en->coff[qb[t]]] += stg[u * SG::RB + lane + 32 * t];
+        if (lane < nr) rsum += stf[u * 4 + lane];
         __syncwarp();
       }
     }
