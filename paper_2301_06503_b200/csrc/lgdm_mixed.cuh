@@ -394,11 +394,13 @@ k_mixed_gather(int64_t nn, const NodeMeta* __restrict__ meta, const MixAdj* __re
     const int64_t k0 = md.k0, k1 = md.k0 + md.nk;
     for (int64_t k = k0; k < k1; k += SG::MXS) {
       const int kk = int(k1 - k < SG::MXS ? k1 - k : SG::MXS);
-      // all row-blocks of the round in flight at once, straight into shared memory
+      // the round's adjacency entries in one parallel load (lane u), then every row-block of
+      // the round in flight at once, straight into shared memory
+      int2 ea = make_int2(0, 0);
+      if (lane < kk) ea = *reinterpret_cast<const int2*>(adj + k + lane);   // (e, aloc)
       for (int u = 0; u < kk; ++u) {
-        const MixAdj* en = adj + k + u;
-        const int64_t e = en->e;
-        const int lr = mldof<T>(en->aloc);
+        const int64_t e = __shfl_sync(0xffffffffu, ea.x, u);
+        const int lr = mldof<T>(__shfl_sync(0xffffffffu, ea.y, u));
         const double* src = EB + e * (ND * ND) + lr * ND;
 #pragma unroll
         for (int t = 0; t < NQ; ++t)
