@@ -185,6 +185,7 @@ struct lgdm_mesh_s {
   uint8_t* dkind = nullptr;       // device [ndof]
   NodeMeta* madj_ptr = nullptr;   // device [n_nodes] gather metadata
   MixAdj* madj = nullptr;         // device node -> element map of k_mixed_gather
+  int32_t* gdof = nullptr;        // device [n_elems][ndofe] global dof of each element dof
   int max_row = 0;                // largest block-row (rows x width) in doubles
   // overlapped input transfer (lgdm_prefetch_dofs)
   double* dofs_back = nullptr;
@@ -551,6 +552,18 @@ lgdm_status create_mixed(lgdm_elem_type type, int64_t n_nodes, const double* coo
   }
   if ((s = upload(m, &m->madj_ptr, meta.data(), meta.size())) != LGDM_OK) return bail(s);
   if ((s = upload(m, &m->madj, madj.data(), madj.size())) != LGDM_OK) return bail(s);
+  {
+    const int nd = f.ndofe, dim = f.dim;
+    std::vector<int32_t> gd(size_t(n_elems) * nd);
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < n_elems; ++e)
+      for (int c = 0; c < nd; ++c) {
+        const int a = c < nene * (dim + 1) ? c / (dim + 1) : nene + (c - nene * (dim + 1)) / dim;
+        const int comp = c < nene * (dim + 1) ? c % (dim + 1) : (c - nene * (dim + 1)) % dim;
+        gd[size_t(e) * nd + c] = int32_t(doff[conn[e * f.nen + a]] + comp);
+      }
+    if ((s = upload(m, &m->gdof, gd.data(), gd.size())) != LGDM_OK) return bail(s);
+  }
   if (dalloc(&m->val, size_t(m->nnz)) != cudaSuccess || dalloc(&m->R, size_t(ndof)) != cudaSuccess ||
       dalloc(&m->dofs, size_t(ndof)) != cudaSuccess || dalloc(&m->kappa, size_t(n_elems) * f.ngp) != cudaSuccess ||
       dalloc(&m->sumsq_part, size_t(2 * kSumBlocks)) != cudaSuccess || dalloc(&m->sumsq_out, 2) != cudaSuccess ||
@@ -583,7 +596,7 @@ template <int T> lgdm_status assemble_mixed(lgdm_mesh m) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mixed_blocks<T, WPB>, WPB * 32, smem);
   const int64_t nb = (m->n_elems + WPB - 1) / WPB;
   const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(nb, int64_t(nsm) * std::max(per_sm, 1))));
-  k_mixed_blocks<T, WPB><<<grid, WPB * 32, smem, m->stream>>>(m->dm, m->n_elems, m->conn, m->coords, m->doff,
+  k_mixed_blocks<T, WPB><<<grid, WPB * 32, smem, m->stream>>>(m->dm, m->n_elems, m->conn, m->coords, m->gdof,
                                                               m->dofs, m->kappa, m->k0g, m->alg,
                                                               m->scratchK, m->scratchF);
   lgdm_status s = check_launch(m, "k_mixed_blocks");
@@ -1434,7 +1447,7 @@ void lgdm_destroy(lgdm_mesh m) {
                   m->nbr_ptr, m->base, m->adj_ptr, m->adj, m->scratchK, m->scratchF,
                   m->sumsq_part, m->sumsq_out, m->k0g, m->alg, m->sdv_dev, m->rp_b,
                   m->ci_b, m->val_b, m->R_b, m->sol, m->sol_part, m->fixed, m->fixinc,
-                  m->doff, m->dkind, m->madj_ptr, m->madj, m->bperm, m->binv, m->dofs_back};
+                  m->doff, m->dkind, m->madj_ptr, m->madj, m->bperm, m->binv, m->dofs_back, m->gdof};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (m->host_pinned) cudaFreeHost(m->host_pinned);

@@ -83,7 +83,7 @@ template <int T> struct MSmem {   // doubles per warp (one element)
 template <int T, int WPB>
 __global__ void __launch_bounds__(WPB * 32)
 k_mixed_blocks(DevMat m, int64_t ne, const int32_t* __restrict__ conn, const double* __restrict__ coords,
-               const int64_t* __restrict__ doff, const double* __restrict__ dofs,
+               const int32_t* __restrict__ gdof, const double* __restrict__ dofs,
                const double* __restrict__ kappa, const double* __restrict__ k0g,
                const double* __restrict__ alg, double* __restrict__ EB, double* __restrict__ EF) {
   using F = MFam<T>;
@@ -108,8 +108,7 @@ k_mixed_blocks(DevMat m, int64_t ne, const int32_t* __restrict__ conn, const dou
       const int a = k / D, i = k % D;
       sm[SM::X + k] = coords[int64_t(conn[e * NENU + a]) * D + i];
     }
-    for (int c = lane; c < ND; c += 32)
-      sm[SM::U + c] = dofs[doff[conn[e * NENU + mdof_node<T>(c)]] + mdof_comp<T>(c)];
+    for (int c = lane; c < ND; c += 32) sm[SM::U + c] = dofs[gdof[e * ND + c]];   // gdof: host table
     __syncwarp();
     // GP cores: geometry on the u nodes (R-GEO), kinematics, Appendix A law
     if (lane < NGP) {
@@ -312,10 +311,10 @@ k_mixed_blocks(DevMat m, int64_t ne, const int32_t* __restrict__ conn, const dou
       const int a = mdof_node<T>(c), i = mdof_comp<T>(c);
       double f = 0.0;
       if (i < D) {
-#pragma unroll 1
+#pragma unroll
         for (int g = 0; g < NGP; ++g) f += sm[SM::UR + (g * NENU + a) * UR::STRIDE + UR::FU + i];
       } else {
-#pragma unroll 1
+#pragma unroll
         for (int g = 0; g < NGP; ++g) f += sm[SM::ER + (g * NENE + a) * ER::STRIDE + ER::FE];
       }
       EF[e * ND + c] = f;
