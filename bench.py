@@ -41,6 +41,30 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+# FP64 roofline: the structure-exploiting algorithmic flop count per element of
+# SURVEY Appendix C at the default reading R1 (h_sigma = h), and the FP64 peak measured on the
+# box with tools/fp64_peak.cu (64 DFMA/clk/SM at 1965 MHz: 34.1 TFLOP/s)
+FP64_FLOPS_PER_ELEMENT = {1: 350.0, 2: 4400.0, 3: 45000.0}
+FP64_PEAK_TFLOPS = 34.1
+HBM_DATASHEET_GBS = 8000.0
+
+
+def roofs(etype: int, n_elems: int, alg_bytes: float, ms: float, peak_gbs: float):
+    """HBM fraction vs the datasheet, FP64-roofline fraction and the attainable fraction
+    max(bytes / BW, flops / FP64 peak) / t of SURVEY 8d."""
+    t = ms * 1e-3
+    flops = FP64_FLOPS_PER_ELEMENT[etype] * n_elems
+    t_hbm = alg_bytes / (peak_gbs * 1e9)
+    t_fp = flops / (FP64_PEAK_TFLOPS * 1e12)
+    return {"frac_datasheet_8tbs": alg_bytes / t / 1e9 / HBM_DATASHEET_GBS,
+            "fp64": {"algorithmic_flops": flops, "achieved_tflops": flops / t / 1e12,
+                     "peak_tflops": FP64_PEAK_TFLOPS, "frac": t_fp / t,
+                     "flops_per_element": FP64_FLOPS_PER_ELEMENT[etype],
+                     "source": "SURVEY Appendix C (R1); peak tools/fp64_peak.cu"},
+            "attainable_frac": max(t_hbm, t_fp) / t,
+            "binding_roof": "fp64" if t_fp > t_hbm else "hbm"}
+
+
 def measured_traffic(workload: str):
     """DRAM bytes per launch of the assembly kernel from the latest committed ncu capture
     (profiles/rNN/traffic.json), or None."""
@@ -209,8 +233,11 @@ def run_lgdm(cfg, steps, warmup, rank, world, local, pg_barrier, allmax, comm_ui
     launches = m.launches - l0
     pg_barrier()
     ms_total = allmax(start.elapsed_time(end))
-    asm_ms = allmax(float(np.mean([a.elapsed_time(b) for a, b in evs])))
-    res = dict(ms_per_step=ms_total / steps, assemble_ms=asm_ms, launches=launches,
+    asm_all = [a.elapsed_time(b) for a, b in evs]
+    asm_ms = allmax(float(np.mean(asm_all)))
+    asm_med, asm_min = allmax(float(np.median(asm_all))), allmax(float(np.min(asm_all)))
+    res = dict(ms_per_step=ms_total / steps, assemble_ms=asm_ms, assemble_ms_median=asm_med,
+               assemble_ms_min=asm_min, launches=launches,
                launches_per_step=launches / steps, clocks=clk.summary(), info=info,
                t_gen=t_gen, t_create=t_create, owned=owned, n_elems_local=mesh.conn.shape[0])
     res["alg_bytes"] = algorithmic_bytes(ndpn, dim, nen, ngp, info["nnz"], info["n_rows"],
@@ -305,7 +332,8 @@ def secondary(cid, steps, warmup, peak):
             "assemble_elements_per_s": cfg.n_elems / (r["assemble_ms"] * 1e-3),
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                          "frac": ach / peak, "traffic": measured_traffic(cfg.name),
-                         "algorithmic_bytes": r["alg_bytes"]},
+                         "algorithmic_bytes": r["alg_bytes"],
+                         **roofs(cfg.etype, cfg.n_elems, r["alg_bytes"], r["assemble_ms"], peak)},
             "clocks": r["clocks"]}
 
 
@@ -441,11 +469,14 @@ def main():
                    "l2": "inputs >> 126 MB L2 (no flush needed)",
                    "kernel": kernel_name(cfg.etype, r["info"]["structured"], args.kernel)},
         "assemble_ms": r["assemble_ms"],
+        "assemble_ms_median": r["assemble_ms_median"], "assemble_ms_min": r["assemble_ms_min"],
         "assemble_elements_per_s": n_total / (r["assemble_ms"] * 1e-3) if ws == 1 else None,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": measured_traffic(cfg.name) if ws == 1 else None,
                      "algorithmic_bytes": r["alg_bytes"], "peak_source": peak_src,
-                     "kernel": "lgdm_assemble (all launches of one call), rank max"},
+                     "kernel": "lgdm_assemble (all launches of one call), rank max",
+                     **roofs(cfg.etype, r["n_elems_local"], r["alg_bytes"], r["assemble_ms"],
+                             peak)},   # per GPU: the rank's own elements / bytes
         "gpu_launches": r["launches"],
         "clocks": r["clocks"],
         "e2e": {"value": n_total / (r["e2e_ms_per_step"] * 1e-3), "unit": UNIT,

@@ -38,6 +38,7 @@ def test_gpu_arm_line():
     r = d["roofline"]
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-12
+    assert 0 < r["fp64"]["frac"] < 1 and r["attainable_frac"] >= max(r["frac"], r["fp64"]["frac"]) - 1e-12
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     c = d["clocks"]
