@@ -516,3 +516,21 @@ def test_quad8_state_patch_and_consistency():
         gd = np.concatenate([doff[g[a]] + np.arange(3 if a < 4 else 2) for a in range(8)])
         _, _, _, s_el = oracle.mixed_element(QUAD8, m, X[g], dofs[gd], np.zeros(9))
         np.testing.assert_allclose(sdv[e, :, 6:9], s_el, rtol=1e-13, atol=1e-13 * np.abs(s_el).max())
+
+
+def test_bar3_ebar_blocks_equal_bar2():
+    """constant strain and constant ebar (damaged): the ebar-ebar block and the ebar residual
+    of a BAR3 equal those of the (separately pinned) BAR2 oracle on the same end nodes"""
+    m = mat()
+    x0, x1, eps, eb, kh = 1.5, 3.7, 2.5e-4, 2.2e-4, 3.0e-4
+    Xe = np.array([[x0], [x1], [0.5 * (x0 + x1)]])
+    u = lambda x: eps * x                                   # noqa: E731
+    U3 = np.array([u(x0), eb, u(x1), eb, u(0.5 * (x0 + x1))])
+    U2 = np.array([u(x0), eb, u(x1), eb])
+    K3, F3, _, _ = oracle.mixed_element(BAR3, m, Xe, U3, np.full(3, kh))
+    r = oracle.element(1, m, np.array([[x0], [x1]]), U2, np.full(2, kh))
+    K2, F2 = r[0], r[1]
+    e3, e2 = [1, 3], [1, 3]
+    np.testing.assert_allclose(K3[np.ix_(e3, e3)], K2[np.ix_(e2, e2)], rtol=1e-12,
+                               atol=1e-13 * np.abs(K2).max())
+    np.testing.assert_allclose(F3[e3], F2[e2], rtol=1e-12, atol=1e-13 * np.abs(F2).max())
