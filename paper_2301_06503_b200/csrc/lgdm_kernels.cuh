@@ -300,7 +300,7 @@ __device__ __forceinline__ void state_record(const DevMat& m, const double (&Gu)
 }
 
 template <int D>
-__global__ void __launch_bounds__(128, 4)
+__global__ void __launch_bounds__(128, 5)   // 5 CTAs/SM: 96 registers (+80 B stack) measured 5 % faster than 4
 k_update_state(DevMat m, int64_t ne, const int32_t* __restrict__ conn,
                const double* __restrict__ coords, const double* __restrict__ dofs,
                double* __restrict__ kappa, const double* __restrict__ k0g,
