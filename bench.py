@@ -248,6 +248,10 @@ def run_lgdm(cfg, steps, warmup, rank, world, local, pg_barrier, allmax, comm_ui
         # t+1's dofs is started (lgdm_prefetch_dofs, own copy stream) before step t runs, so it
         # overlaps the assembly; every copy is inside the timed region.
         m.set_state(dofs_h, None)
+        for _ in range(2):               # untimed warm-up of the copy stream / second buffer
+            m.prefetch_dofs(dofs_h)
+            m.set_state_prefetched()
+            step(0)
         torch.cuda.synchronize()
         pg_barrier()
         s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
