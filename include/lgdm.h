@@ -63,8 +63,8 @@ typedef enum {
  * elements (a node that is a corner of one element and a midside node of another, or no
  * element's node, is INVALID_ARGUMENT).  Dofs stay node-interleaved with a variable count
  * per node: dof = doff[node] + comp, comp = (u_x[, u_y][, ebar]), doff = prefix sum of
- * (d + 1 for corner nodes, d for midside nodes), see lgdm_dof_offsets.  Single-rank whole
- * meshes only (global_node_offset 0, owned range = all nodes); assemble uses the element-block
+ * (d + 1 for corner nodes, d for midside nodes), see lgdm_dof_offsets.  Slabs through
+ * lgdm_create_mesh_mixed (global dof offset); assemble uses the element-block
  * + gather kernels (lgdm_set_kernel 0 or 1); lgdm_update_state writes the records of the
  * equal-order family of the same dimension (lgdm_sdv_width); lgdm_get_blocked returns the
  * u dofs (node order) then the ebar dofs (node order).  Gradients are evaluated on coordinates / dofs relative to each
@@ -123,6 +123,24 @@ lgdm_status lgdm_create_mesh(lgdm_elem_type type, int64_t n_nodes, const double*
                              int64_t global_node_offset, int64_t n_global_nodes,
                              int64_t owned_node_begin, int64_t owned_node_end, int device,
                              void* cuda_stream, lgdm_mesh* out);
+
+/* Mixed-order mesh or slab (LGDM_BAR3 / LGDM_QUAD8) with its place in the global dof
+ * numbering: as lgdm_create_mesh, plus global_dof_offset = global dof id of the slab's local
+ * dof 0 (its first local node's first dof) and n_global_dofs (the K column count).  Local
+ * dofs are numbered by lgdm_dof_offsets; a slab's local nodes must be a contiguous global node
+ * range whose node kinds (corner / midside) are those of the whole mesh, so global dof =
+ * global_dof_offset + local dof.  Rows are those of the owned nodes [owned_node_begin,
+ * owned_node_end); the elements touching them (ghosts included) are local and recomputed, so
+ * stitched slab rows equal the whole-mesh rows bitwise (ascending element order is kept when
+ * the slab's elements are a contiguous, ordered global range).  lgdm_create_mesh accepts the
+ * mixed types for whole meshes only.  Errors as lgdm_create_mesh; n_global_dofs < offset +
+ * local dofs -> LGDM_ERR_INVALID_ARGUMENT. */
+lgdm_status lgdm_create_mesh_mixed(lgdm_elem_type type, int64_t n_nodes, const double* coords,
+                                   int64_t n_elems, const int64_t* conn, const lgdm_material* mat,
+                                   int64_t global_node_offset, int64_t n_global_nodes,
+                                   int64_t owned_node_begin, int64_t owned_node_end,
+                                   int64_t global_dof_offset, int64_t n_global_dofs, int device,
+                                   void* cuda_stream, lgdm_mesh* out);
 
 /* State of the current Newton iterate (Alg. 2 line 7): dofs [n_nodes][ndpn] node-
  * interleaved, kappa [n_elems][ngp] = history kappa_hist at the start of the increment.

@@ -192,6 +192,7 @@ struct lgdm_mesh_s {
   cudaStream_t cstream = nullptr;
   cudaEvent_t copy_ev = nullptr, free_ev = nullptr;
   bool prefetch_pending = false, free_ev_set = false;
+  int64_t gdof0 = 0, n_global_dofs = 0;   // mixed slabs: global dof of local dof 0, total
   int64_t* bperm = nullptr;       // blocked order of a mixed mesh: new -> old dof
   int32_t* binv = nullptr;        // old -> new dof
 };
@@ -381,7 +382,8 @@ template <int T> lgdm_status upload_tables(lgdm_mesh m) {
 
 lgdm_status create_mixed(lgdm_elem_type type, int64_t n_nodes, const double* coords, int64_t n_elems,
                          const int64_t* conn, const lgdm_material* mat, int64_t gid0, int64_t n_global,
-                         int64_t own_b, int64_t own_e, int device, void* stream, lgdm_mesh* out) {
+                         int64_t own_b, int64_t own_e, int64_t gdof0, int64_t n_global_dofs,
+                         int device, void* stream, lgdm_mesh* out) {
   const FamInfo f = fam_info(type);
   const int T = int(type);
   const int nene = T == LGDM_BAR3 ? 2 : 4;
@@ -389,8 +391,10 @@ lgdm_status create_mixed(lgdm_elem_type type, int64_t n_nodes, const double* coo
   if (n_nodes < 2 || n_elems < 1 || n_nodes >= (int64_t(1) << 30))
     return fail(LGDM_ERR_INVALID_ARGUMENT, "bad sizes n_nodes=%lld n_elems=%lld", (long long)n_nodes,
                 (long long)n_elems);
-  if (gid0 != 0 || n_global != n_nodes || own_b != 0 || own_e != n_nodes)
-    return fail(LGDM_ERR_INVALID_ARGUMENT, "mixed-order meshes: single-rank whole mesh only");
+  if (gid0 < 0 || n_global < gid0 + n_nodes || !(0 <= own_b && own_b < own_e && own_e <= n_nodes))
+    return fail(LGDM_ERR_INVALID_ARGUMENT, "node ranges inconsistent");
+  if (gdof0 < 0 || (gid0 == 0 && n_global == n_nodes && gdof0 != 0))
+    return fail(LGDM_ERR_INVALID_ARGUMENT, "global dof offset inconsistent");
   std::string why;
   if (!validate_material(mat, &why)) return fail(LGDM_ERR_INVALID_ARGUMENT, "material: %s", why.c_str());
   std::vector<uint8_t> kind(n_nodes, 0);   // 1 corner (ebar), 2 midside
@@ -410,7 +414,11 @@ lgdm_status create_mixed(lgdm_elem_type type, int64_t n_nodes, const double* coo
     doff[n + 1] = doff[n] + (kind[n] == 1 ? f.dim + 1 : f.dim);
   }
   const int64_t ndof = doff[n_nodes];
-  if (ndof >= (int64_t(1) << 31)) return fail(LGDM_ERR_INVALID_ARGUMENT, "dof count exceeds int32 col_idx");
+  if (n_global_dofs < 0) n_global_dofs = gdof0 + ndof;   // whole mesh
+  if (n_global_dofs < gdof0 + ndof)
+    return fail(LGDM_ERR_INVALID_ARGUMENT, "n_global_dofs < global dof offset + local dofs");
+  if (n_global_dofs >= (int64_t(1) << 31)) return fail(LGDM_ERR_INVALID_ARGUMENT, "dof count exceeds int32 col_idx");
+  const int64_t no = own_e - own_b, r_b = doff[own_b], nrow = doff[own_e] - doff[own_b];
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     return fail(LGDM_ERR_CUDA, "no CUDA device available (liblgdm has no CPU path)");
@@ -422,13 +430,15 @@ lgdm_status create_mixed(lgdm_elem_type type, int64_t n_nodes, const double* coo
   m->mixed = true;
   m->n_nodes = n_nodes;
   m->n_elems = n_elems;
-  m->gid0 = 0;
-  m->n_global_nodes = n_nodes;
-  m->own_b = 0;
-  m->own_e = n_nodes;
-  m->n_owned = n_nodes;
-  m->n_rows = ndof;
+  m->gid0 = gid0;
+  m->n_global_nodes = n_global;
+  m->own_b = own_b;
+  m->own_e = own_e;
+  m->n_owned = no;
+  m->n_rows = nrow;
   m->n_dofs_local = ndof;
+  m->gdof0 = gdof0;
+  m->n_global_dofs = n_global_dofs;
   m->device = device;
   m->stream = (cudaStream_t)stream;
   m->dm = derive(*mat, f.dim);
@@ -496,27 +506,29 @@ lgdm_status create_mixed(lgdm_elem_type type, int64_t n_nodes, const double* coo
     for (int32_t b : nb) w += int32_t(doff[b + 1] - doff[b]);
     width[n] = w;
   }
-  std::vector<int64_t> row_ptr(ndof + 1, 0);
+  // rows of the owned nodes only (row r = local dof r_b + r); columns are global dof ids
+  std::vector<int64_t> row_ptr(nrow + 1, 0);
   int64_t pos = 0;
   int max_row = 0;
-  for (int64_t n = 0; n < n_nodes; ++n) {
+  for (int64_t n = own_b; n < own_e; ++n) {
     const int nr = int(doff[n + 1] - doff[n]);
     for (int i = 0; i < nr; ++i) {
-      row_ptr[doff[n] + i] = pos;
+      row_ptr[doff[n] - r_b + i] = pos;
       pos += width[n];
     }
     max_row = std::max(max_row, nr * width[n]);
   }
-  row_ptr[ndof] = pos;
+  row_ptr[nrow] = pos;
   m->nnz = pos;
   m->max_row = max_row;
   if (pos >= (int64_t(1) << 40)) return bail(fail(LGDM_ERR_INVALID_ARGUMENT, "pattern too large"));
   std::vector<int32_t> col(pos);
-  std::vector<int64_t> madj_ptr(n_nodes + 1);
-  for (int64_t n = 0; n < n_nodes; ++n) madj_ptr[n + 1] = madj_ptr[n] + (nadj[n + 1] - nadj[n]);
-  std::vector<MixAdj> madj(madj_ptr[n_nodes]);
+  std::vector<int64_t> madj_ptr(no + 1);
+  for (int64_t o = 0; o < no; ++o) madj_ptr[o + 1] = madj_ptr[o] + (nadj[own_b + o + 1] - nadj[own_b + o]);
+  std::vector<MixAdj> madj(madj_ptr[no]);
 #pragma omp parallel for schedule(static)
-  for (int64_t n = 0; n < n_nodes; ++n) {
+  for (int64_t o = 0; o < no; ++o) {
+    const int64_t n = own_b + o;
     const std::vector<int32_t>& nb = nbs[n];
     std::vector<int32_t> coff(nb.size());
     int32_t c = 0;
@@ -526,9 +538,9 @@ lgdm_status create_mixed(lgdm_elem_type type, int64_t n_nodes, const double* coo
     }
     const int nr = int(doff[n + 1] - doff[n]);
     for (int i = 0; i < nr; ++i) {
-      int64_t p = row_ptr[doff[n] + i];
+      int64_t p = row_ptr[doff[n] - r_b + i];
       for (int32_t b : nb)
-        for (int64_t d = doff[b]; d < doff[b + 1]; ++d) col[p++] = int32_t(d);
+        for (int64_t d = doff[b]; d < doff[b + 1]; ++d) col[p++] = int32_t(gdof0 + d);
     }
     for (int64_t k = nadj[n]; k < nadj[n + 1]; ++k) {
       MixAdj en{};
@@ -538,17 +550,18 @@ lgdm_status create_mixed(lgdm_elem_type type, int64_t n_nodes, const double* coo
         const int32_t nbn = int32_t(conn[int64_t(en.e) * f.nen + b]);
         en.coff[b] = coff[std::lower_bound(nb.begin(), nb.end(), nbn) - nb.begin()];
       }
-      madj[madj_ptr[n] + (k - nadj[n])] = en;
+      madj[madj_ptr[o] + (k - nadj[n])] = en;
     }
   }
   if ((s = upload(m, &m->row_ptr, row_ptr.data(), row_ptr.size())) != LGDM_OK) return bail(s);
   if ((s = upload(m, &m->col_idx, col.data(), col.size())) != LGDM_OK) return bail(s);
-  std::vector<NodeMeta> meta(n_nodes);
-  for (int64_t n = 0; n < n_nodes; ++n) {
+  std::vector<NodeMeta> meta(no);
+  for (int64_t o = 0; o < no; ++o) {
+    const int64_t n = own_b + o;
     const int nr = int(doff[n + 1] - doff[n]);
-    meta[n] = NodeMeta{row_ptr[doff[n]], doff[n], madj_ptr[n], width[n], int16_t(nr),
-                       int16_t(madj_ptr[n + 1] - madj_ptr[n])};
-    if (madj_ptr[n + 1] - madj_ptr[n] > 32767) return bail(fail(LGDM_ERR_INVALID_ARGUMENT, "node %lld has too many elements", (long long)n));
+    meta[o] = NodeMeta{row_ptr[doff[n] - r_b], doff[n] - r_b, madj_ptr[o], width[n], int16_t(nr),
+                       int16_t(madj_ptr[o + 1] - madj_ptr[o])};
+    if (madj_ptr[o + 1] - madj_ptr[o] > 32767) return bail(fail(LGDM_ERR_INVALID_ARGUMENT, "node %lld has too many elements", (long long)n));
   }
   if ((s = upload(m, &m->madj_ptr, meta.data(), meta.size())) != LGDM_OK) return bail(s);
   if ((s = upload(m, &m->madj, madj.data(), madj.size())) != LGDM_OK) return bail(s);
@@ -564,7 +577,7 @@ lgdm_status create_mixed(lgdm_elem_type type, int64_t n_nodes, const double* coo
       }
     if ((s = upload(m, &m->gdof, gd.data(), gd.size())) != LGDM_OK) return bail(s);
   }
-  if (dalloc(&m->val, size_t(m->nnz)) != cudaSuccess || dalloc(&m->R, size_t(ndof)) != cudaSuccess ||
+  if (dalloc(&m->val, size_t(m->nnz)) != cudaSuccess || dalloc(&m->R, size_t(nrow)) != cudaSuccess ||
       dalloc(&m->dofs, size_t(ndof)) != cudaSuccess || dalloc(&m->kappa, size_t(n_elems) * f.ngp) != cudaSuccess ||
       dalloc(&m->sumsq_part, size_t(2 * kSumBlocks)) != cudaSuccess || dalloc(&m->sumsq_out, 2) != cudaSuccess ||
       cudaMallocHost(&m->host_pinned, 2 * sizeof(double)) != cudaSuccess)
@@ -603,9 +616,9 @@ template <int T> lgdm_status assemble_mixed(lgdm_mesh m) {
   if (s != LGDM_OK) return s;
   const size_t gsm = sizeof(double) * size_t(GW) * (size_t(m->max_row) + MGStage<T>::SIZE);
   if (gsm > 48 * 1024) CU(cudaFuncSetAttribute(k_mixed_gather<T, GW>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gsm)));
-  const int64_t gn = (m->n_nodes + GW - 1) / GW;
+  const int64_t gn = (m->n_owned + GW - 1) / GW;
   k_mixed_gather<T, GW><<<unsigned(std::min<int64_t>(gn, int64_t(nsm) * 16)), GW * 32, gsm, m->stream>>>(
-      m->n_nodes, m->madj_ptr, m->madj, m->scratchK, m->scratchF, m->max_row, m->val, m->R);
+      m->n_owned, m->madj_ptr, m->madj, m->scratchK, m->scratchF, m->max_row, m->val, m->R);
   return check_launch(m, "k_mixed_gather");
 }
 
@@ -624,9 +637,12 @@ lgdm_status lgdm_create_mesh(lgdm_elem_type type, int64_t n_nodes, const double*
                              void* cuda_stream, lgdm_mesh* out) {
   if (!out) return fail(LGDM_ERR_INVALID_ARGUMENT, "out is NULL");
   *out = nullptr;
+  if ((type == LGDM_BAR3 || type == LGDM_QUAD8) && global_node_offset != 0)
+    return fail(LGDM_ERR_INVALID_ARGUMENT, "mixed-order slabs need their global dof offset: use lgdm_create_mesh_mixed");
   if (type == LGDM_BAR3 || type == LGDM_QUAD8)
     return create_mixed(type, n_nodes, coords, n_elems, conn, mat, global_node_offset,
-                        n_global_nodes, owned_node_begin, owned_node_end, device, cuda_stream, out);
+                        n_global_nodes, owned_node_begin, owned_node_end, 0, -1, device,
+                        cuda_stream, out);
   if (type != LGDM_BAR2 && type != LGDM_QUAD4 && type != LGDM_HEX8)
     return fail(LGDM_ERR_INVALID_ARGUMENT, "unknown element type %d", int(type));
   if (!coords || !conn || !mat) return fail(LGDM_ERR_INVALID_ARGUMENT, "NULL input pointer");
@@ -814,6 +830,21 @@ lgdm_status lgdm_create_mesh(lgdm_elem_type type, int64_t n_nodes, const double*
   return LGDM_OK;
 }
 
+lgdm_status lgdm_create_mesh_mixed(lgdm_elem_type type, int64_t n_nodes, const double* coords,
+                                   int64_t n_elems, const int64_t* conn, const lgdm_material* mat,
+                                   int64_t global_node_offset, int64_t n_global_nodes,
+                                   int64_t owned_node_begin, int64_t owned_node_end,
+                                   int64_t global_dof_offset, int64_t n_global_dofs, int device,
+                                   void* cuda_stream, lgdm_mesh* out) {
+  if (!out) return fail(LGDM_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  if (type != LGDM_BAR3 && type != LGDM_QUAD8)
+    return fail(LGDM_ERR_INVALID_ARGUMENT, "lgdm_create_mesh_mixed takes LGDM_BAR3 / LGDM_QUAD8");
+  return create_mixed(type, n_nodes, coords, n_elems, conn, mat, global_node_offset, n_global_nodes,
+                      owned_node_begin, owned_node_end, global_dof_offset, n_global_dofs, device,
+                      cuda_stream, out);
+}
+
 lgdm_status lgdm_set_state(lgdm_mesh m, const double* dofs, int64_t n_dofs, const double* kappa,
                            int64_t n_kappa, int src_on_device) {
   if (!m) return fail(LGDM_ERR_INVALID_ARGUMENT, "mesh is NULL");
@@ -930,9 +961,9 @@ lgdm_status lgdm_assemble(lgdm_mesh m, lgdm_csr* K, double** R) {
   m->assembled = true;
   if (K) {
     K->n_rows = m->n_rows;
-    K->n_cols = m->mixed ? m->n_rows : m->n_global_nodes * m->f.ndpn;
+    K->n_cols = m->mixed ? m->n_global_dofs : m->n_global_nodes * m->f.ndpn;
     K->nnz = m->nnz;
-    K->first_row = m->mixed ? 0 : (m->gid0 + m->own_b) * m->f.ndpn;
+    K->first_row = m->mixed ? m->gdof0 + m->hdoff[m->own_b] : (m->gid0 + m->own_b) * m->f.ndpn;
     K->row_ptr = m->row_ptr;
     K->col_idx = m->col_idx;
     K->val = m->val;
@@ -1330,7 +1361,7 @@ lgdm_status lgdm_residual_sumsq(lgdm_mesh m, double* out2, int on_device) {
   if (!m || !out2) return fail(LGDM_ERR_INVALID_ARGUMENT, "NULL argument");
   if (!m->assembled) return fail(LGDM_ERR_INVALID_STATE, "residual before assemble");
   CU(cudaSetDevice(m->device));
-  if (m->mixed) k_sumsq_kind<<<kSumBlocks, kSumThreads, 0, m->stream>>>(m->n_rows, m->f.dim, m->dkind, m->R, m->sumsq_part);
+  if (m->mixed) k_sumsq_kind<<<kSumBlocks, kSumThreads, 0, m->stream>>>(m->n_rows, m->f.dim, m->dkind + m->hdoff[m->own_b], m->R, m->sumsq_part);
   else k_sumsq_partial<<<kSumBlocks, kSumThreads, 0, m->stream>>>(m->n_rows, m->f.ndpn, m->f.dim, m->R, m->sumsq_part);
   lgdm_status s = check_launch(m, "k_sumsq_partial");
   if (s != LGDM_OK) return s;

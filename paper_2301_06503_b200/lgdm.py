@@ -33,7 +33,8 @@ EXPORTS = ["lgdm_create_mesh", "lgdm_set_state", "lgdm_assemble", "lgdm_update_h
            "lgdm_last_error", "lgdm_destroy", "lgdm_sdv_width", "lgdm_set_defects",
            "lgdm_update_state", "lgdm_get_blocked", "lgdm_apply_dirichlet", "lgdm_solve",
            "lgdm_add_dofs", "lgdm_delta_norms", "lgdm_reaction", "lgdm_solve_direct",
-           "lgdm_dof_offsets", "lgdm_prefetch_dofs", "lgdm_set_state_prefetched"]
+           "lgdm_dof_offsets", "lgdm_prefetch_dofs", "lgdm_set_state_prefetched",
+           "lgdm_create_mesh_mixed"]
 
 
 class LGDMError(RuntimeError):
@@ -105,6 +106,8 @@ def load() -> C.CDLL:
     L.lgdm_reaction.argtypes = [vp, i64, vp, dp]
     L.lgdm_solve_direct.argtypes = [vp, vp, C.POINTER(C.c_int)]
     L.lgdm_dof_offsets.argtypes = [vp, vp, i64]
+    L.lgdm_create_mesh_mixed.argtypes = [C.c_int, i64, vp, i64, vp, C.POINTER(Material), i64, i64,
+                                         i64, i64, i64, i64, C.c_int, vp, C.POINTER(vp)]
     L.lgdm_prefetch_dofs.argtypes = [vp, vp, i64]
     L.lgdm_set_state_prefetched.argtypes = [vp]
     for name in EXPORTS:
@@ -166,7 +169,8 @@ class Mesh:
     """One mesh (whole or one rank's slab) on one GPU.  See include/lgdm.h."""
 
     def __init__(self, etype: int, coords, conn, mat: Material, global_node_offset: int = 0,
-                 n_global_nodes: int | None = None, owned=None, device: int = 0, stream=None):
+                 n_global_nodes: int | None = None, owned=None, device: int = 0, stream=None,
+                 global_dof_offset: int | None = None, n_global_dofs: int | None = None):
         L = load()
         self.etype = etype
         self.dim, self.nen, self.ndpn, self.ngp = FAMILY[etype]
@@ -181,10 +185,17 @@ class Mesh:
             stream = torch.cuda.current_stream(device).cuda_stream
         self.device = device
         self._h = C.c_void_p()
-        _check(L.lgdm_create_mesh(etype, self.n_nodes, coords.ctypes.data, self.n_elems,
-                                  conn.ctypes.data, C.byref(mat), global_node_offset,
-                                  n_global_nodes, owned[0], owned[1], device, stream,
-                                  C.byref(self._h)))
+        if global_dof_offset is not None:          # mixed-order slab
+            _check(L.lgdm_create_mesh_mixed(etype, self.n_nodes, coords.ctypes.data, self.n_elems,
+                                            conn.ctypes.data, C.byref(mat), global_node_offset,
+                                            n_global_nodes, owned[0], owned[1], global_dof_offset,
+                                            -1 if n_global_dofs is None else n_global_dofs,
+                                            device, stream, C.byref(self._h)))
+        else:
+            _check(L.lgdm_create_mesh(etype, self.n_nodes, coords.ctypes.data, self.n_elems,
+                                      conn.ctypes.data, C.byref(mat), global_node_offset,
+                                      n_global_nodes, owned[0], owned[1], device, stream,
+                                      C.byref(self._h)))
         self._keep = []
         self.doff = np.zeros(self.n_nodes + 1, dtype=np.int64)
         _check(L.lgdm_dof_offsets(self._h, self.doff.ctypes.data, self.doff.size))

@@ -133,8 +133,13 @@ def test_mixed_errors():
     with pytest.raises(lgdm.LGDMError) as ei:
         lgdm.Mesh(lgdm.QUAD8, X, inv, lgdm.material(**MAT))
     assert ei.value.status == 2
-    with pytest.raises(lgdm.LGDMError) as ei:            # slabs: whole mesh only
-        lgdm.Mesh(lgdm.QUAD8, X, mesh.conn, lgdm.material(**MAT), owned=(0, 5))
+    with pytest.raises(lgdm.LGDMError) as ei:            # slabs need their global dof offset
+        lgdm.Mesh(lgdm.QUAD8, X, mesh.conn, lgdm.material(**MAT), global_node_offset=3,
+                  n_global_nodes=X.shape[0] + 3)
+    assert ei.value.status == 1
+    with pytest.raises(lgdm.LGDMError) as ei:            # too few global dofs
+        lgdm.Mesh(lgdm.QUAD8, X, mesh.conn, lgdm.material(**MAT), global_dof_offset=0,
+                  n_global_dofs=5)
     assert ei.value.status == 1
     dofs, kap = synth.mixed_fields(mesh)
     m, _ = _gpu(lgdm.QUAD8, X, mesh.conn, dofs, kap)
@@ -303,3 +308,64 @@ def test_quad8_strip_newton_matches_oracle():
     np.testing.assert_allclose([s["reaction"] for s in log], react_ref, rtol=1e-7)
     np.testing.assert_allclose(m.get_kappa().reshape(kh.shape), kh, rtol=1e-7, atol=1e-14)
     m.close()
+
+
+def _mixed_slabs(etype, n, P):
+    """Row-owned slabs of a mixed mesh (QUAD8: element rows along y; BAR3: elements along x):
+    the local elements are those touching owned nodes, the local nodes a contiguous global
+    range.  Returns the whole mesh, its doff and per-slab (node range, element range, owned
+    local range)."""
+    mesh = synth.mixed_mesh(etype, n, 10.0)
+    nn = mesh.coords.shape[0]
+    doff = oracle.mixed_dofs(etype, nn, mesh.conn)
+    if etype == lgdm.QUAD8:
+        nx, ny = n
+        cnt = [(2 * nx + 1) if j % 2 == 0 else (nx + 1) for j in range(2 * ny + 1)]
+        rows, per = ny, nx
+    else:
+        cnt = [1] * (2 * n[0] + 1)
+        rows, per = n[0], 1
+    start = np.concatenate([[0], np.cumsum(cnt)])       # first node of lattice row j
+    B = np.linspace(0, rows, P + 1).round().astype(int)
+    slabs = []
+    for p in range(P):
+        l0 = max(B[p] - 1, 0)
+        l1 = B[p + 1]
+        nb, ne_ = start[2 * l0], start[min(2 * l1 + 1, len(start) - 1)]
+        ob = start[2 * B[p]] - nb
+        oe = (start[2 * B[p + 1]] if p < P - 1 else nn) - nb
+        slabs.append((nb, ne_, l0 * per, l1 * per, ob, oe))
+    return mesh, doff, slabs
+
+
+@pytest.mark.parametrize("etype,n,P", [(lgdm.QUAD8, (12, 9), 3), (lgdm.BAR3, (30,), 2)])
+def test_mixed_slabs_stitch_bitwise(etype, n, P):
+    """slab rows (ghost elements recomputed, global dof columns) equal the whole mesh's rows
+    bitwise (SURVEY 8e for the mixed-order elements)"""
+    mesh, doff, slabs = _mixed_slabs(etype, n, P)
+    dofs, kap = synth.mixed_fields(mesh)
+    mw, whole = _gpu(etype, mesh.coords, mesh.conn, dofs, kap)
+    rp = whole["row_ptr"]
+    covered = 0
+    import torch
+    for nb, ne_, eb, ee, ob, oe in slabs:
+        conn = mesh.conn[eb:ee] - nb
+        assert conn.min() >= 0 and conn.max() < ne_ - nb
+        m = lgdm.Mesh(etype, mesh.coords[nb:ne_], conn, lgdm.material(**MAT),
+                      global_node_offset=int(nb), n_global_nodes=mesh.coords.shape[0],
+                      owned=(int(ob), int(oe)), global_dof_offset=int(doff[nb]),
+                      n_global_dofs=int(doff[-1]))
+        m.set_state(dofs[doff[nb]:doff[ne_]], kap[eb:ee])
+        out = m.assemble()
+        torch.cuda.synchronize()
+        r0, r1 = int(doff[nb + ob]), int(doff[nb + oe])
+        assert out["first_row"] == r0 and out["n_cols"] == doff[-1] and out["n_rows"] == r1 - r0
+        grp = out["row_ptr"].torch().cpu().numpy()
+        assert np.array_equal(grp, rp[r0:r1 + 1] - rp[r0])
+        assert np.array_equal(out["col_idx"].torch().cpu().numpy(), whole["col_idx"][rp[r0]:rp[r1]])
+        assert np.array_equal(out["val"].torch().cpu().numpy(), whole["val"][rp[r0]:rp[r1]])
+        assert np.array_equal(out["R"].torch().cpu().numpy(), whole["R"][r0:r1])
+        covered += r1 - r0
+        m.close()
+    assert covered == doff[-1]
+    mw.close()
