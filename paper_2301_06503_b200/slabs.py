@@ -65,3 +65,49 @@ def elements_per_rank(n: tuple, P: int):
     for k in n[:-1]:
         per_layer *= k
     return [slab(n, p, P).n_elem_layers * per_layer for p in range(P)]
+
+
+# ---------------------------------------------------------------------------------------
+# Mixed-order meshes (BAR3, QUAD8; lgdm_create_mesh_mixed): the half-spacing lattice of
+# synth.mixed_mesh, numbered x-fastest by lattice rows (QUAD8: corner rows of 2 nx + 1 nodes
+# and midside rows of nx + 1 nodes; BAR3: one node per lattice point).  Element row l spans
+# lattice rows 2l .. 2l + 2.  A slab owns whole element-row boundaries: rank p owns lattice
+# rows [2 B_p, 2 B_{p+1}) (the last rank also the top row), holds element rows
+# [max(B_p - 1, 0), B_{p+1}) and so the contiguous node range of lattice rows
+# [2 max(B_p - 1, 0), 2 B_{p+1}].
+# ---------------------------------------------------------------------------------------
+@dataclass(frozen=True)
+class MixedSlab:
+    node_range: tuple        # global node ids [begin, end) of the local nodes
+    elem_range: tuple        # global element ids [begin, end) of the local elements
+    owned_local: tuple       # owned local node range
+    global_dof_offset: int   # global dof id of local dof 0
+    n_global_dofs: int
+
+
+def _mixed_rows(etype: int, n: tuple):
+    """(nodes per lattice row, dofs per lattice row, element rows, elements per row)"""
+    if etype == 5:   # QUAD8
+        nx, ny = n
+        nodes = [(2 * nx + 1) if j % 2 == 0 else (nx + 1) for j in range(2 * ny + 1)]
+        dofs = [(3 * (nx + 1) + 2 * nx) if j % 2 == 0 else 2 * (nx + 1) for j in range(2 * ny + 1)]
+        return nodes, dofs, ny, nx
+    nel = n[0]       # BAR3: corners (2 dofs) at even lattice points, midsides (1 dof) at odd
+    return [1] * (2 * nel + 1), [2 if j % 2 == 0 else 1 for j in range(2 * nel + 1)], nel, 1
+
+
+def mixed_slab(etype: int, n: tuple, p: int, P: int) -> MixedSlab:
+    nodes, dofs, rows, per = _mixed_rows(etype, n)
+    if not (1 <= P <= rows) or not (0 <= p < P):
+        raise ValueError(f"cannot split {rows} element rows over {P} ranks")
+    ns, ds = [0], [0]
+    for a, b in zip(nodes, dofs):
+        ns.append(ns[-1] + a)
+        ds.append(ds[-1] + b)
+    b0, b1 = split(rows, P, p)
+    l0 = max(b0 - 1, 0)
+    top = min(2 * b1 + 1, len(nodes))
+    nb, ne = ns[2 * l0], ns[top]
+    ob = ns[2 * b0] - nb
+    oe = (ns[2 * b1] if p < P - 1 else ns[-1]) - nb
+    return MixedSlab((nb, ne), (l0 * per, b1 * per), (ob, oe), ds[2 * l0], ds[-1])

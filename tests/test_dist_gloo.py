@@ -88,3 +88,71 @@ def test_two_rank_slabs_gloo(etype, n):
         np.testing.assert_allclose(rnorm, norms, rtol=1e-13)
         covered += e - b
     assert covered == mesh.coords.shape[0]
+
+
+def _mixed_worker(rank, world, port, etype, n, q):
+    import torch
+    from paper_2301_06503_b200 import slabs as sl
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        whole = synth.mixed_mesh(etype, n, 10.0)
+        dofs_all, kap_all = synth.mixed_fields(whole)
+        S = sl.mixed_slab(etype, n, rank, world)
+        (nb, ne), (eb, ee), (ob, oe) = S.node_range, S.elem_range, S.owned_local
+        conn = whole.conn[eb:ee] - nb
+        doff_w = oracle.mixed_dofs(etype, whole.coords.shape[0], whole.conn)
+        dofs = dofs_all[doff_w[nb]:doff_w[ne]]
+        res = oracle.mixed_assemble(etype, oracle.material(**synth.MATERIAL), whole.coords[nb:ne],
+                                    conn, dofs, kap_all[eb:ee])
+        d = res["doff"]
+        r0, r1 = d[ob], d[oe]
+        lo, hi = res["row_ptr"][r0], res["row_ptr"][r1]
+        dim = synth.MFAM[etype][0]
+        kind = oracle.dof_kind(d, dim)[r0:r1]
+        R = res["R"][r0:r1]
+        part = torch.tensor([np.sum(R[kind < dim] ** 2), np.sum(R[kind == dim] ** 2)],
+                            dtype=torch.float64)
+        dist.all_reduce(part, op=dist.ReduceOp.SUM)
+        q.put((rank, S.global_dof_offset + r0, res["row_ptr"][r0:r1 + 1] - lo,
+               res["col_idx"][lo:hi].astype(np.int64) + S.global_dof_offset, res["val"][lo:hi],
+               R, np.sqrt(part.numpy())))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("etype,n", [(synth.QUAD8, (7, 6)), (synth.BAR3, (13,))])
+def test_mixed_slabs_gloo(etype, n):
+    """mixed-order slabs (slabs.mixed_slab): the owned rows of each rank's local assembly, with
+    the global dof offset, equal the whole mesh's rows; reduced norms equal the whole norms"""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_mixed_worker, args=(r, world, port, etype, n, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    got = sorted([q.get(timeout=300) for _ in range(world)], key=lambda t: t[0])
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    whole = synth.mixed_mesh(etype, n, 10.0)
+    dofs, kap = synth.mixed_fields(whole)
+    ref = oracle.mixed_assemble(etype, oracle.material(**synth.MATERIAL), whole.coords, whole.conn,
+                                dofs, kap)
+    rp = ref["row_ptr"]
+    nxt = 0
+    for rank, g0, rpl, cols, val, R, norms in got:
+        assert g0 == nxt
+        g1 = g0 + R.size
+        assert np.array_equal(rpl, rp[g0:g1 + 1] - rp[g0])
+        assert np.array_equal(cols, ref["col_idx"][rp[g0]:rp[g1]])
+        assert np.array_equal(val, ref["val"][rp[g0]:rp[g1]])
+        assert np.array_equal(R, ref["R"][g0:g1])
+        nxt = g1
+    assert nxt == ref["R"].size
+    dim = synth.MFAM[etype][0]
+    kind = oracle.dof_kind(ref["doff"], dim)
+    want = [np.linalg.norm(ref["R"][kind < dim]), np.linalg.norm(ref["R"][kind == dim])]
+    np.testing.assert_allclose(got[0][6], want, rtol=1e-14)

@@ -310,51 +310,28 @@ def test_quad8_strip_newton_matches_oracle():
     m.close()
 
 
-def _mixed_slabs(etype, n, P):
-    """Row-owned slabs of a mixed mesh (QUAD8: element rows along y; BAR3: elements along x):
-    the local elements are those touching owned nodes, the local nodes a contiguous global
-    range.  Returns the whole mesh, its doff and per-slab (node range, element range, owned
-    local range)."""
-    mesh = synth.mixed_mesh(etype, n, 10.0)
-    nn = mesh.coords.shape[0]
-    doff = oracle.mixed_dofs(etype, nn, mesh.conn)
-    if etype == lgdm.QUAD8:
-        nx, ny = n
-        cnt = [(2 * nx + 1) if j % 2 == 0 else (nx + 1) for j in range(2 * ny + 1)]
-        rows, per = ny, nx
-    else:
-        cnt = [1] * (2 * n[0] + 1)
-        rows, per = n[0], 1
-    start = np.concatenate([[0], np.cumsum(cnt)])       # first node of lattice row j
-    B = np.linspace(0, rows, P + 1).round().astype(int)
-    slabs = []
-    for p in range(P):
-        l0 = max(B[p] - 1, 0)
-        l1 = B[p + 1]
-        nb, ne_ = start[2 * l0], start[min(2 * l1 + 1, len(start) - 1)]
-        ob = start[2 * B[p]] - nb
-        oe = (start[2 * B[p + 1]] if p < P - 1 else nn) - nb
-        slabs.append((nb, ne_, l0 * per, l1 * per, ob, oe))
-    return mesh, doff, slabs
-
-
 @pytest.mark.parametrize("etype,n,P", [(lgdm.QUAD8, (12, 9), 3), (lgdm.BAR3, (30,), 2)])
 def test_mixed_slabs_stitch_bitwise(etype, n, P):
     """slab rows (ghost elements recomputed, global dof columns) equal the whole mesh's rows
     bitwise (SURVEY 8e for the mixed-order elements)"""
-    mesh, doff, slabs = _mixed_slabs(etype, n, P)
+    from paper_2301_06503_b200 import slabs as sl
+    mesh = synth.mixed_mesh(etype, n, 10.0)
+    doff = oracle.mixed_dofs(etype, mesh.coords.shape[0], mesh.conn)
     dofs, kap = synth.mixed_fields(mesh)
     mw, whole = _gpu(etype, mesh.coords, mesh.conn, dofs, kap)
     rp = whole["row_ptr"]
     covered = 0
     import torch
-    for nb, ne_, eb, ee, ob, oe in slabs:
+    for p in range(P):
+        S = sl.mixed_slab(etype, n, p, P)
+        (nb, ne_), (eb, ee), (ob, oe) = S.node_range, S.elem_range, S.owned_local
+        assert S.global_dof_offset == doff[nb] and S.n_global_dofs == doff[-1]
         conn = mesh.conn[eb:ee] - nb
         assert conn.min() >= 0 and conn.max() < ne_ - nb
         m = lgdm.Mesh(etype, mesh.coords[nb:ne_], conn, lgdm.material(**MAT),
                       global_node_offset=int(nb), n_global_nodes=mesh.coords.shape[0],
-                      owned=(int(ob), int(oe)), global_dof_offset=int(doff[nb]),
-                      n_global_dofs=int(doff[-1]))
+                      owned=(int(ob), int(oe)), global_dof_offset=S.global_dof_offset,
+                      n_global_dofs=S.n_global_dofs)
         m.set_state(dofs[doff[nb]:doff[ne_]], kap[eb:ee])
         out = m.assemble()
         torch.cuda.synchronize()
