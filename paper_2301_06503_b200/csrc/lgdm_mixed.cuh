@@ -15,9 +15,13 @@
 //                   gpLaw of lgdm_device.cuh), per-(GP, node) records in shared memory, then
 //                   node-pair Gauss sums (lanes over the NENU^2 ordered pairs) -> element
 //                   blocks Ke [NDOFE][NDOFE], Fe [NDOFE] in HBM;
-//   k_mixed_gather  one warp per node: the node's CSR block-row accumulated in shared memory
-//                   over its adjacent elements in ascending element id (atomic-free, bitwise
-//                   reproducible), then written once, coalesced.
+//   k_mixed_gather  one warp per owned node: the node's CSR block-row accumulated in shared
+//                   memory over its adjacent elements in ascending element id (atomic-free,
+//                   bitwise reproducible; the element row-blocks arrive by cp.async, all of a
+//                   node's elements in flight at once), then written once, coalesced.
+// Gradients use coordinates / dofs relative to the element's node 0 (reading R-REL).  Also
+// here: k_mixed_state (state records), k_mixed_history, k_mixed_detj, k_blocked_mixed and the
+// dof-kind reductions of the residual / increment norms.
 #pragma once
 #include <cstdint>
 
