@@ -325,3 +325,29 @@ def mixed_fields(mesh: MixedMesh, cid: int = 200):
           np.arange(ngp, dtype=np.uint64)[None, :])
     kappa = np.maximum(MATERIAL["kappa0"], 4e-4 * uniform(cfg.seed, S_KAPPA, gp))
     return dofs, kappa
+
+
+def sen_mesh(etype: int, n: tuple, extent: float = 100.0, notch: float = 0.5) -> MixedMesh:
+    """Side-edge-notched plate (SPEC default geometry: a square plate with an edge slit
+    at mid-height of length notch * extent from x = 0).  QUAD8 (n = (nx, ny), ny even): the slit
+    runs along the element-row boundary y = extent / 2; its nodes (x < notch * extent, the tip
+    excluded) are duplicated so that the elements above the slit use the copies (appended at
+    the end of the node list).  Pure geometry, no method arithmetic."""
+    assert etype == QUAD8 and n[1] % 2 == 0
+    mesh = mixed_mesh(etype, n, extent)
+    X = mesh.coords
+    ymid = extent / 2.0
+    xt = notch * extent
+    on_slit = (np.abs(X[:, 1] - ymid) < 1e-9) & (X[:, 0] < xt - 1e-9)
+    slit_ids = np.nonzero(on_slit)[0]
+    new_id = {int(g): X.shape[0] + k for k, g in enumerate(slit_ids)}
+    conn = mesh.conn.copy()
+    above = X[mesh.conn[:, :4], 1].mean(axis=1) > ymid            # elements above the slit
+    for e in np.nonzero(above)[0]:
+        for a in range(conn.shape[1]):
+            g = int(conn[e, a])
+            if g in new_id:
+                conn[e, a] = new_id[g]
+    coords = np.vstack([X, X[slit_ids]])
+    corner = np.concatenate([mesh.corner, mesh.corner[slit_ids]])
+    return MixedMesh(etype, coords, conn, corner, tuple(n))

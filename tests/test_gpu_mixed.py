@@ -346,3 +346,31 @@ def test_mixed_slabs_stitch_bitwise(etype, n, P):
         m.close()
     assert covered == doff[-1]
     mw.close()
+
+
+def test_sen2d_newton_physics():
+    """The paper's 2D side-edge-notch setting (SPEC default geometry: 100 mm plate,
+    50 mm mid-height edge slit) with its QUAD8 discretisation through the GPU Newton loop
+    (reading R2): damage starts next to the notch tip, the most damaged elements lie along the
+    ligament (y = 50 mm, x > 50 mm), and the load-displacement curve has a single peak followed
+    by softening."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "sen2d", os.path.join(os.path.dirname(__file__), "..", "tools", "sen2d.py"))
+    sen = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(sen)
+    mesh, log, r, kap = sen.run(n=16, steps=70, du=2e-4, tol=1e-5, verbose=False)
+    X = mesh.coords
+    c = X[mesh.conn[:, :4]].mean(axis=1)
+    k = kap.max(axis=1)
+    h = 100.0 / 16
+    worst = c[np.argsort(k)[-4:]]
+    assert np.all(np.abs(worst[:, 1] - 50.0) < h)            # on the ligament row
+    assert np.all(worst[:, 0] > 50.0 - 1e-9)                  # ahead of the notch tip
+    tip = c[int(k.argmax())]
+    assert abs(tip[0] - 50.0) < 2 * h                         # the tip element is the worst
+    ip = int(r.argmax())
+    assert 5 < ip < len(r) - 5
+    assert r[-1] < 0.8 * r.max()
+    assert np.all(np.diff(r[:ip]) > 0)
