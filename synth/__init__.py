@@ -351,3 +351,4 @@ def sen_mesh(etype: int, n: tuple, extent: float = 100.0, notch: float = 0.5) ->
     coords = np.vstack([X, X[slit_ids]])
     corner = np.concatenate([mesh.corner, mesh.corner[slit_ids]])
     return MixedMesh(etype, coords, conn, corner, tuple(n))
+
