@@ -193,6 +193,9 @@ struct lgdm_mesh_s {
   cudaEvent_t copy_ev = nullptr, free_ev = nullptr;
   bool prefetch_pending = false, free_ev_set = false;
   int64_t gdof0 = 0, n_global_dofs = 0;   // mixed slabs: global dof of local dof 0, total
+  cusolverSpHandle_t sp_handle = nullptr;   // lgdm_solve_direct (created once per mesh)
+  cusparseMatDescr_t sp_descr = nullptr;
+  int32_t* rp32 = nullptr;
   int64_t* bperm = nullptr;       // blocked order of a mixed mesh: new -> old dof
   int32_t* binv = nullptr;        // old -> new dof
 };
@@ -1300,24 +1303,23 @@ lgdm_status lgdm_solve_direct(lgdm_mesh m, double* delta, int* singularity) {
   if (!load_spsolver()) return fail(LGDM_ERR_UNSUPPORTED, "libcusolver / libcusparse not loadable");
   CU(cudaSetDevice(m->device));
   const int n = int(m->n_rows), nnz = int(m->nnz);
-  int32_t* rp32 = nullptr;
-  CU(dalloc(&rp32, size_t(n) + 1));
-  k_rowptr32<<<unsigned((n + 256) / 256), 256, 0, m->stream>>>(n + 1, m->row_ptr, rp32);
-  ++m->launches;
-  cusolverSpHandle_t h = nullptr;
-  cusparseMatDescr_t d = nullptr;
+  bool ok = true;
+  if (!m->sp_handle) {   // handle, descriptor and the int32 row pointers: once per mesh
+    CU(dalloc(&m->rp32, size_t(n) + 1));
+    m->device_bytes += (n + 1) * 4;
+    k_rowptr32<<<unsigned((n + 256) / 256), 256, 0, m->stream>>>(n + 1, m->row_ptr, m->rp32);
+    ++m->launches;
+    ok = g_sps.create(&m->sp_handle) == CUSOLVER_STATUS_SUCCESS &&
+         g_sps.createDescr(&m->sp_descr) == CUSPARSE_STATUS_SUCCESS &&
+         g_sps.setType(m->sp_descr, CUSPARSE_MATRIX_TYPE_GENERAL) == CUSPARSE_STATUS_SUCCESS &&
+         g_sps.setBase(m->sp_descr, CUSPARSE_INDEX_BASE_ZERO) == CUSPARSE_STATUS_SUCCESS;
+  }
   int sing = -1;
-  bool ok = g_sps.create(&h) == CUSOLVER_STATUS_SUCCESS && g_sps.setStream(h, m->stream) == CUSOLVER_STATUS_SUCCESS &&
-            g_sps.createDescr(&d) == CUSPARSE_STATUS_SUCCESS &&
-            g_sps.setType(d, CUSPARSE_MATRIX_TYPE_GENERAL) == CUSPARSE_STATUS_SUCCESS &&
-            g_sps.setBase(d, CUSPARSE_INDEX_BASE_ZERO) == CUSPARSE_STATUS_SUCCESS;
+  ok = ok && g_sps.setStream(m->sp_handle, m->stream) == CUSOLVER_STATUS_SUCCESS;
   if (ok)
-    ok = g_sps.lsvqr(h, n, nnz, d, m->val, rp32, m->col_idx, m->R, 1e-14, 1, delta, &sing) ==
-         CUSOLVER_STATUS_SUCCESS;
-  if (d) g_sps.destroyDescr(d);
-  if (h) g_sps.destroy(h);
+    ok = g_sps.lsvqr(m->sp_handle, n, nnz, m->sp_descr, m->val, m->rp32, m->col_idx, m->R, 1e-14, 1,
+                     delta, &sing) == CUSOLVER_STATUS_SUCCESS;
   cudaStreamSynchronize(m->stream);
-  cudaFree(rp32);
   if (singularity) *singularity = sing;
   if (!ok) return fail(LGDM_ERR_CUDA, "cusolverSpDcsrlsvqr failed");
   if (sing >= 0) return fail(LGDM_ERR_NOT_CONVERGED, "singular system (QR pivot %d)", sing);
@@ -1478,10 +1480,13 @@ void lgdm_destroy(lgdm_mesh m) {
                   m->nbr_ptr, m->base, m->adj_ptr, m->adj, m->scratchK, m->scratchF,
                   m->sumsq_part, m->sumsq_out, m->k0g, m->alg, m->sdv_dev, m->rp_b,
                   m->ci_b, m->val_b, m->R_b, m->sol, m->sol_part, m->fixed, m->fixinc,
-                  m->doff, m->dkind, m->madj_ptr, m->madj, m->bperm, m->binv, m->dofs_back, m->gdof};
+                  m->doff, m->dkind, m->madj_ptr, m->madj, m->bperm, m->binv, m->dofs_back, m->gdof,
+                  m->rp32};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (m->host_pinned) cudaFreeHost(m->host_pinned);
+  if (m->sp_descr && g_sps.loaded) g_sps.destroyDescr(m->sp_descr);
+  if (m->sp_handle && g_sps.loaded) g_sps.destroy(m->sp_handle);
   if (m->cstream) cudaStreamSynchronize(m->cstream), cudaStreamDestroy(m->cstream);
   if (m->copy_ev) cudaEventDestroy(m->copy_ev);
   if (m->free_ev) cudaEventDestroy(m->free_ev);
