@@ -90,6 +90,9 @@ typedef struct {
 
 typedef struct lgdm_mesh_s* lgdm_mesh;
 
+/* Equal-order meshes: the row / column counts below with ndpn = d + 1.  Mixed-order meshes
+ * (LGDM_BAR3 / LGDM_QUAD8): n_rows = dofs of the owned nodes, n_cols = n_global_dofs,
+ * first_row = global dof of the first owned node (lgdm_create_mesh_mixed). */
 typedef struct {
   int64_t n_rows;           /* owned rows = ndpn * (owned_node_end - owned_node_begin)      */
   int64_t n_cols;           /* ndpn * n_global_nodes                                        */
@@ -100,7 +103,7 @@ typedef struct {
   double* val;              /* device, [nnz]                                                */
 } lgdm_csr;
 
-typedef struct {
+typedef struct {   /* mixed-order meshes: nen = u nodes, ndpn = dofs of a corner node */
   int32_t elem_type, dim, nen, ndpn, ngp, structured;   /* structured: 1 = sweep kernel path  */
   int64_t n_nodes, n_elems, n_owned_nodes, n_rows, nnz;
   int64_t nx, ny, nz;                                    /* element counts if structured      */
