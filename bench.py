@@ -3,13 +3,17 @@
 
 One STEP = one pass of the whole hot path on the current iterate:
     lgdm_assemble (K and R)  ->  lgdm_residual_norms (NCCL allreduce when N > 1)
-    ->  lgdm_update_history  ->  dofs *= 1.05^(+-1) (next iterate, SURVEY 8d "dofs_t").
+    ->  lgdm_update_history  ->  next iterate dofs_t = (1 + 0.05 t) dofs_0, t = step mod 10
+    (BASELINE configs 2 / 4: 10 iterations, restarted every 10 steps).
 Workload: BASELINE config 4 (Hex8 200^3, 8M elements) as row-owned z-slabs over the N ranks
 (strong scaling; N = 1 holds the whole mesh).  At N = 1 the 1M-element configs 3 (Hex8 100^3)
 and 2 (Q4 1000^2) are also reported under "secondary".  Inputs are far larger than L2
 (126 MB), so no flush is needed between steps.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl lgdm|reference]
+
+--gpus N without a torchrun environment re-launches itself as N ranks
+(python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ...).
 """
 from __future__ import annotations
 
@@ -46,6 +50,8 @@ def peaks():
 # box with tools/fp64_peak.cu (64 DFMA/clk/SM at 1965 MHz: 34.1 TFLOP/s)
 FP64_FLOPS_PER_ELEMENT = {1: 350.0, 2: 4400.0, 3: 45000.0}
 FP64_PEAK_TFLOPS = 34.1
+FP64_PEAK_SOURCE = ("builder-measured, round 1: tools/fp64_peak.cu DFMA loop on a B200 of this "
+                    "pool (64 DFMA/clk/SM at 1965 MHz); not in MEASURED_PEAKS.json")
 HBM_DATASHEET_GBS = 8000.0
 
 
@@ -60,24 +66,40 @@ def roofs(etype: int, n_elems: int, alg_bytes: float, ms: float, peak_gbs: float
             "fp64": {"algorithmic_flops": flops, "achieved_tflops": flops / t / 1e12,
                      "peak_tflops": FP64_PEAK_TFLOPS, "frac": t_fp / t,
                      "flops_per_element": FP64_FLOPS_PER_ELEMENT[etype],
-                     "source": "SURVEY Appendix C (R1); peak tools/fp64_peak.cu"},
+                     "source": "flops: SURVEY Appendix C (reading R1); peak: " + FP64_PEAK_SOURCE},
             "attainable_frac": max(t_hbm, t_fp) / t,
             "binding_roof": "fp64" if t_fp > t_hbm else "hbm"}
 
 
-def measured_traffic(workload: str):
-    """DRAM bytes per launch of the assembly kernel from the latest committed ncu capture
-    (profiles/rNN/traffic.json), or None."""
+def kernel_source_sha(etype: int, kernel: int) -> str:
+    """sha1 (16 hex) of the CUDA sources the assembly kernel is built from, so a committed ncu
+    traffic figure is only reported for the kernel it was measured on."""
+    import hashlib
+    c = os.path.join(ROOT, "paper_2301_06503_b200", "csrc")
+    main = {2: "lgdm_sweepq.cuh", 3: "lgdm_hex8.cuh" if kernel == 3 else "lgdm_sweep4.cuh"}.get(etype, "lgdm_kernels.cuh")
+    h = hashlib.sha1()
+    for f in (main, "lgdm_device.cuh", "lgdm_sweep.cuh", "lgdm_sweep4.cuh"):
+        with open(os.path.join(c, f), "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
+def measured_traffic(workload: str, etype: int, kernel: int):
+    """DRAM bytes per launch of the assembly kernel from a committed ncu --set full capture
+    (profiles/rNN/traffic.json: {workload: {"bytes", "kernel", "src_sha", "profile"}}), only if
+    it was measured on the current kernel sources; else (None, reason)."""
     import glob
+    sha = kernel_source_sha(etype, kernel)
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "traffic.json")), reverse=True):
         try:
             with open(path) as f:
                 t = json.load(f)
-            if workload in t:
-                return float(t[workload])
         except Exception:
-            pass
-    return None
+            continue
+        e = t.get(workload)
+        if isinstance(e, dict) and e.get("src_sha") == sha:
+            return float(e["bytes"]), f"{os.path.relpath(path, ROOT)} ({e.get('profile', '')}, src {sha})"
+    return None, f"no ncu capture of the current kernel sources (src {sha})"
 
 
 def algorithmic_bytes(ndpn, dim, nen, ngp, nnz, n_rows, n_nodes, n_elems):
@@ -174,6 +196,12 @@ def build_rank_mesh(cfg, rank, world):
     return mesh, s.owned_local(mesh.node_gid0)
 
 
+def dofs_factor(t: int) -> float:
+    """dofs_{t+1} / dofs_t for dofs_t = (1 + 0.05 (t mod 10)) dofs_0 (BASELINE configs 2 / 4)."""
+    a, b = t % 10, (t + 1) % 10
+    return (1.0 + 0.05 * b) / (1.0 + 0.05 * a)
+
+
 def run_lgdm(cfg, steps, warmup, rank, world, local, pg_barrier, allmax, comm_uid=None,
              e2e=True, kernel=0, state=False):
     import torch
@@ -209,7 +237,7 @@ def run_lgdm(cfg, steps, warmup, rank, world, local, pg_barrier, allmax, comm_ui
             ev[1].record(stream)
         norms = m.residual_norms()       # NCCL allreduce inside when world > 1
         m.update_history()
-        m.scale_dofs(1.05 if t % 2 == 0 else 1.0 / 1.05)
+        m.scale_dofs(dofs_factor(t))     # dofs_{t+1} = (1 + 0.05 (t+1)) dofs_0 (mod 10)
         return norms
 
     clk = Clocks(local).start()
@@ -298,31 +326,73 @@ def kernel_name(etype, structured, kernel):
     """Assembly kernel that lgdm_assemble runs (lgdm_set_kernel, include/lgdm.h)."""
     if not structured or kernel == 1 or etype == 1:
         return "k_elem_blocks + k_gather (general path)"
-    if kernel in (0, 4):
-        return "k_sweep4 (Hex8 structured sweep)" if etype == 3 else "k_sweepq (Q4 structured sweep)"
+    if etype == 2:
+        return "k_sweepq (Q4 structured sweep)"
     if kernel == 3:
-        return "k_sweep3 (shared-memory pipeline sweep)"
-    return "k_sweep (L2 sweep)" if etype == 3 else "k_sweep3 (shared-memory pipeline sweep)"
+        return "k_hex8 (Hex8 structured sweep, register-tiled Kuu)"
+    return "k_sweep4 (Hex8 structured sweep)"
 
 
-def cpu_baseline(cfg, target_s=15.0):
-    """The oracle as it stands, single-threaded, on a bounded sample of the workload: the first
-    element layers of the same mesh (all layers are statistically alike)."""
+def host_cpu():
+    """CPU model (lscpu) and the host core count the CPU baselines ran on."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"model": model, "nproc": os.cpu_count()}
+
+
+def structured_colours(cfg, n_elems):
+    """2^d colouring of a structured element block (x-fastest ids): parities of (i, j[, k]);
+    elements of one colour share no node."""
+    e = np.arange(n_elems, dtype=np.int64)
+    n = cfg.n
+    if len(n) == 1:
+        return (e & 1).astype(np.int32), 2
+    if len(n) == 2:
+        i, j = e % n[0], e // n[0]
+        return ((i & 1) + 2 * (j & 1)).astype(np.int32), 4
+    i, j, k = e % n[0], (e // n[0]) % n[1], e // (n[0] * n[1])
+    return ((i & 1) + 2 * (j & 1) + 4 * (k & 1)).astype(np.int32), 8
+
+
+def cpu_baseline(cfg, target_s=12.0):
+    """The oracle as it stands on a bounded sample of the workload (the first element layers of
+    the same mesh; all layers are statistically alike), two legs (SURVEY 8d oracle timing):
+    (a) the plain element-by-element loop on one core, (b) the same loop on all host cores,
+    colour by colour (oracle_assemble_colored, OpenMP)."""
     import oracle
     per_layer = int(np.prod(cfg.n[:-1]))
-    rate_guess = 1.0e4 if cfg.etype == 3 else 9.0e4
-    layers = int(max(1, min(cfg.n[-1], round(target_s * rate_guess / per_layer))))
-    mesh = synth.structured_mesh(cfg, elem_layers=(0, layers))
-    dofs, kappa = synth.fields(cfg, mesh)
     mat = oracle.material(**synth.MATERIAL)
-    rp, ci = oracle.pattern(cfg.etype, mesh.coords.shape[0], mesh.conn)
-    t0 = time.perf_counter()
-    oracle.assemble(cfg.etype, mat, mesh.coords, mesh.conn, dofs, kappa, rp, ci)
-    dt = time.perf_counter() - t0
-    ne = mesh.conn.shape[0]
-    return {"value": ne / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{ne} elements = element layers [0,{layers}) of {cfg.name}, one assemble, "
-                      f"{dt:.2f} s single-threaded (pattern build untimed)"}
+    cpu = host_cpu()
+    out = {}
+    for leg, rate_guess in (("single_core", 1.1e4 if cfg.etype == 3 else 9.0e4),
+                            ("all_cores", (1.1e4 if cfg.etype == 3 else 9.0e4) * max(1, cpu["nproc"] or 1) * 0.5)):
+        layers = int(max(2, min(cfg.n[-1], round(target_s * rate_guess / per_layer))))
+        mesh = synth.structured_mesh(cfg, elem_layers=(0, layers))
+        dofs, kappa = synth.fields(cfg, mesh)
+        rp, ci = oracle.pattern(cfg.etype, mesh.coords.shape[0], mesh.conn)
+        ne = mesh.conn.shape[0]
+        t0 = time.perf_counter()
+        if leg == "single_core":
+            oracle.assemble(cfg.etype, mat, mesh.coords, mesh.conn, dofs, kappa, rp, ci)
+            threads = 1
+        else:
+            col, nc = structured_colours(cfg, ne)
+            threads = oracle.assemble_colored(cfg.etype, mat, mesh.coords, mesh.conn, dofs, kappa,
+                                              col, nc, rp, ci)["threads"]
+        dt = time.perf_counter() - t0
+        out[leg] = {"value": ne / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
+                    "sample": f"{ne} elements = element layers [0,{layers}) of {cfg.name}, one "
+                              f"assemble, {dt:.2f} s on {threads} thread(s) (pattern build untimed)"}
+    best = out["all_cores"]
+    return {**best, "cpu_model": cpu["model"], "nproc": cpu["nproc"],
+            "legs": out}
 
 
 def secondary(cid, steps, warmup, peak):
@@ -330,12 +400,13 @@ def secondary(cid, steps, warmup, peak):
     r = run_lgdm(cfg, steps, warmup, 0, 1, int(os.environ.get("LOCAL_RANK", "0")),
                  lambda: None, lambda x: x, e2e=False)
     ach = r["alg_bytes"] / (r["assemble_ms"] * 1e-3) / 1e9
+    tr, tsrc = measured_traffic(cfg.name, cfg.etype, 0)
     return {"workload": cfg.name, "config": cid, "kernel": kernel_name(cfg.etype, True, 0),
             "value": cfg.n_elems / (r["ms_per_step"] * 1e-3), "unit": UNIT,
             "ms_per_step": r["ms_per_step"], "assemble_ms": r["assemble_ms"],
             "assemble_elements_per_s": cfg.n_elems / (r["assemble_ms"] * 1e-3),
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                         "frac": ach / peak, "traffic": measured_traffic(cfg.name),
+                         "frac": ach / peak, "traffic": tr, "traffic_source": tsrc,
                          "algorithmic_bytes": r["alg_bytes"],
                          **roofs(cfg.etype, cfg.n_elems, r["alg_bytes"], r["assemble_ms"], peak)},
             "clocks": r["clocks"]}
@@ -384,33 +455,71 @@ def mixed_secondary(steps, warmup, peak, n=(500, 500)):
 
 
 def reference_arm(args, cfg):
-    """--impl reference: the CPU oracle (this tier's reference), bounded sample per step."""
+    """--impl reference: the CPU oracle (this tier's reference) on all host cores (the element
+    loop colour by colour, OpenMP), a bounded sample of the workload per step: assemble +
+    history update of the first element layers.  Under torchrun only rank 0 runs."""
     ws, rank, local = dist_env()
     if rank != 0:
         return
     import oracle
     per_layer = int(np.prod(cfg.n[:-1]))
-    mesh = synth.structured_mesh(cfg, elem_layers=(0, 1))
+    cpu = host_cpu()
+    layers = 4 if cfg.etype == 3 else 32
+    mesh = synth.structured_mesh(cfg, elem_layers=(0, min(layers, cfg.n[-1])))
     dofs, kappa = synth.fields(cfg, mesh)
     mat = oracle.material(**synth.MATERIAL)
     rp, ci = oracle.pattern(cfg.etype, mesh.coords.shape[0], mesh.conn)
+    ne = mesh.conn.shape[0]
+    col, nc = structured_colours(cfg, ne)
+    threads = 1
     for _ in range(args.warmup):
-        oracle.assemble(cfg.etype, mat, mesh.coords, mesh.conn, dofs, kappa, rp, ci)
+        threads = oracle.assemble_colored(cfg.etype, mat, mesh.coords, mesh.conn, dofs, kappa, col,
+                                          nc, rp, ci)["threads"]
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        oracle.assemble(cfg.etype, mat, mesh.coords, mesh.conn, dofs, kappa, rp, ci)
+        oracle.assemble_colored(cfg.etype, mat, mesh.coords, mesh.conn, dofs, kappa, col, nc, rp, ci)
         oracle.update_history(cfg.etype, mesh.conn, dofs, kappa)
     dt = time.perf_counter() - t0
-    ne = mesh.conn.shape[0]
     val = ne * args.steps / dt
-    sample = f"{ne} elements (element layer 0 of {cfg.name}) per step, single-threaded"
+    sample = (f"{ne} elements (element layers [0,{min(layers, cfg.n[-1])}) of {cfg.name}) per step, "
+              f"assemble + history update, {threads} threads (colour-parallel oracle loop)")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": cfg.name, "per_layer_elements": per_layer},
-        "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "oracle",
+                         "sample": sample, "cpu_model": cpu["model"], "nproc": cpu["nproc"]},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+
+
+def relaunch(args) -> int:
+    """--gpus N outside torchrun: run this script as N ranks (one per GPU) on 127.0.0.1."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def dry_run(args):
+    """--dry-run: the launch / rendezvous path without a GPU (gloo): every rank joins, rank 0
+    prints the JSON skeleton with the world size (tests/test_bench_contract.py)."""
+    ws, rank, local = dist_env()
+    import torch.distributed as dist
+    if ws > 1:
+        dist.init_process_group("gloo")
+        dist.barrier()
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "dry_run": True, "n_gpus": ws, "ranks_joined": ws,
+                          "steps": args.steps, "warmup": args.warmup,
+                          "config": {"workload": synth.CONFIGS[args.config].name}}))
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 def main():
@@ -420,11 +529,19 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", default="lgdm", choices=["lgdm", "reference"])
-    ap.add_argument("--kernel", type=int, default=0, help="lgdm_set_kernel: 0 auto, 1 general, 2-4 sweeps")
+    ap.add_argument("--kernel", type=int, default=0,
+                    help="lgdm_set_kernel: 0 auto, 1 general, 2 sweep, 3 Hex8 k_hex8")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch / rendezvous only (gloo, no GPU): prints n_gpus")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
+    if args.dry_run:
+        dry_run(args)
+        return
     cfg = synth.CONFIGS[args.config]
     if args.impl == "reference":
         reference_arm(args, cfg)
@@ -461,6 +578,7 @@ def main():
                  kernel=args.kernel, state=not args.no_secondary)
     n_total = cfg.n_elems
     value = n_total / (r["ms_per_step"] * 1e-3)
+    traffic, traffic_src = measured_traffic(cfg.name, cfg.etype, args.kernel) if ws == 1 else (None, "multi-rank")
     achieved = r["alg_bytes"] / (r["assemble_ms"] * 1e-3) / 1e9
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
@@ -476,7 +594,7 @@ def main():
         "assemble_ms_median": r["assemble_ms_median"], "assemble_ms_min": r["assemble_ms_min"],
         "assemble_elements_per_s": n_total / (r["assemble_ms"] * 1e-3) if ws == 1 else None,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": measured_traffic(cfg.name) if ws == 1 else None,
+                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                      "algorithmic_bytes": r["alg_bytes"], "peak_source": peak_src,
                      "kernel": "lgdm_assemble (all launches of one call), rank max",
                      **roofs(cfg.etype, r["n_elems_local"], r["alg_bytes"], r["assemble_ms"],

@@ -259,6 +259,13 @@ lgdm_status lgdm_add_dofs(lgdm_mesh mesh, const double* delta, double alpha);
  * sum e^2} over the u and ebar dofs of delta (device) and of the current dofs. */
 lgdm_status lgdm_delta_norms(lgdm_mesh mesh, const double* delta, double out4[4]);
 
+/* Convergence test of Alg. 1 l.26 / Alg. 2 l.16: out2 = {||du||/||u||,
+ * ||de||/||e||} (host) from the sums of lgdm_delta_norms, a zero iterate norm counted as
+ * 1e-16; *converged = 1 when both ratios are <= tol.  tol <= 0 -> INVALID_ARGUMENT; the other
+ * errors are lgdm_delta_norms'.  Synchronises the mesh stream. */
+lgdm_status lgdm_delta_ratios(lgdm_mesh mesh, const double* delta, double tol, double out2[2],
+                              int* converged);
+
 /* Sums of squares of the last assembled R over owned rows: out2 = {sum Fu^2, sum Fe^2}.
  * out2 is a device pointer (2 doubles) when on_device = 1 (stream-ordered, no sync; for a
  * caller-side allreduce), else a host pointer (synchronises). */
@@ -284,19 +291,25 @@ lgdm_status lgdm_get_kappa(lgdm_mesh mesh, double* host_out);
 lgdm_status lgdm_scale_dofs(lgdm_mesh mesh, double s);
 
 /* Select the assembly kernel (all produce the same K and R up to rounding, parity-tested):
- *   0 = automatic: structured meshes (x-fastest grids, whole owned layers) -> 4, else 1
+ *   0 = automatic: structured meshes (x-fastest grids, whole owned layers) -> 2, else 1
  *   1 = general (element-batch + node gather, any connectivity)
- *   2 = first structured sweep (Q4: k_sweep3, Hex8: k_sweep, L2-accumulating)
- *   3 = shared-memory pipeline k_sweep3 (Q4 and Hex8)
- *   4 = round-1 redesign: Q4 k_sweepq, Hex8 k_sweep4 (row-sum diagonals)
- *   5 = Hex8 k_sweep5 (node expansions in the core lanes; experimental, slower today), Q4 as 4
- * Kernels 2-5 need a structured mesh: LGDM_ERR_INVALID_ARGUMENT otherwise. */
+ *   2 = structured sweep: Q4 k_sweepq, Hex8 k_sweep4 (row-sum diagonals)
+ *   3 = Hex8 k_hex8 (sweep with register-tiled Kuu Gauss sums); Q4 as 2
+ * Kernels 2 and 3 need a structured mesh: LGDM_ERR_INVALID_ARGUMENT otherwise; any other
+ * selector value: LGDM_ERR_INVALID_ARGUMENT. */
 lgdm_status lgdm_set_kernel(lgdm_mesh mesh, int kernel);
 
 lgdm_status lgdm_get_info(lgdm_mesh mesh, lgdm_info* info);
 
 /* Number of kernel launches issued by this mesh since creation (launch accounting). */
 int64_t lgdm_launch_count(lgdm_mesh mesh);
+
+#ifdef LGDM_PHASE_TIMING
+/* Debug builds only (compiled with -DLGDM_PHASE_TIMING; not exported otherwise): cycles per
+ * phase of the sweep kernels' instrumentation points, summed over CTAs (16 counters, host
+ * out16); reset != 0 clears them.  Synchronises the device. */
+int lgdm_debug_phase_cycles(unsigned long long* out16, int reset);
+#endif
 
 const char* lgdm_last_error(void);
 void lgdm_destroy(lgdm_mesh mesh);

@@ -21,6 +21,8 @@
 #include <set>
 #include <vector>
 
+#include <omp.h>
+
 namespace {
 
 const double kTolHist = 1e-10;  // Fig. 8b l.22: cond1 = (gp_e_eqv - k0) > 1D-10
@@ -473,6 +475,39 @@ int oracle_assemble(int type, const oracle_material* m, int64_t n_nodes, const d
                            row_ptr, col_idx, val, R, S, n_guard);
 }
 
+// One element of Alg. 1 lines 5-10: K_local, F_local, then the scatter into K and R.
+static int assemble_one(const Fam& f, int type, const oracle_material* m, int64_t e,
+                        const double* coords, const int64_t* conn, const double* dofs,
+                        const double* kappa, const double* kappa0_gp, const double* alpha_gp,
+                        const int64_t* row_ptr, const int32_t* col_idx, double* val, double* R,
+                        double* S, double* Ke, double* Fe, double* Fa, int64_t* ng) {
+  const int nd = f.ndofe;
+  double Xe[24], Ue[32];
+  int32_t guard[8];
+  gather(f, e, conn, coords, dofs, Xe, Ue);
+  const int rc = oracle_element_d(type, m, Xe, Ue, kappa + e * f.ngp,
+                                  kappa0_gp ? kappa0_gp + e * f.ngp : nullptr,
+                                  alpha_gp ? alpha_gp + e * f.ngp : nullptr, Ke, Fe, Fa, nullptr,
+                                  guard);
+  if (rc != 0) return -2;  // det J <= 0
+  for (int g = 0; g < f.ngp; ++g) *ng += guard[g];
+  for (int a = 0; a < f.nen; ++a)
+    for (int i = 0; i < f.ndpn; ++i) {
+      const int64_t row = f.ndpn * conn[e * f.nen + a] + i;
+      const int r = a * f.ndpn + i;
+      R[row] += Fe[r];
+      S[row] += Fa[r];
+      for (int b = 0; b < f.nen; ++b)
+        for (int j = 0; j < f.ndpn; ++j) {
+          const int64_t col = f.ndpn * conn[e * f.nen + b] + j;
+          const int64_t p = find_col(row_ptr, col_idx, row, col);
+          if (p < 0) return -3;
+          val[p] += Ke[r * nd + b * f.ndpn + j];
+        }
+    }
+  return 0;
+}
+
 int oracle_assemble_d(int type, const oracle_material* m, int64_t n_nodes, const double* coords,
                       int64_t n_elems, const int64_t* conn, const double* dofs,
                       const double* kappa, const double* kappa0_gp, const double* alpha_gp,
@@ -486,33 +521,61 @@ int oracle_assemble_d(int type, const oracle_material* m, int64_t n_nodes, const
   std::fill(R, R + ndof, 0.0);
   std::fill(S, S + ndof, 0.0);
   std::vector<double> Ke(nd * nd), Fe(nd), Fa(nd);
-  double Xe[24], Ue[32];
-  int32_t guard[8];
   int64_t ng = 0;
   for (int64_t e = 0; e < n_elems; ++e) {
-    gather(f, e, conn, coords, dofs, Xe, Ue);
-    const int rc = oracle_element_d(type, m, Xe, Ue, kappa + e * f.ngp,
-                                    kappa0_gp ? kappa0_gp + e * f.ngp : nullptr,
-                                    alpha_gp ? alpha_gp + e * f.ngp : nullptr, Ke.data(),
-                                    Fe.data(), Fa.data(), nullptr, guard);
-    if (rc != 0) return -2;  // det J <= 0
-    for (int g = 0; g < f.ngp; ++g) ng += guard[g];
-    for (int a = 0; a < f.nen; ++a)
-      for (int i = 0; i < f.ndpn; ++i) {
-        const int64_t row = f.ndpn * conn[e * f.nen + a] + i;
-        const int r = a * f.ndpn + i;
-        R[row] += Fe[r];
-        S[row] += Fa[r];
-        for (int b = 0; b < f.nen; ++b)
-          for (int j = 0; j < f.ndpn; ++j) {
-            const int64_t col = f.ndpn * conn[e * f.nen + b] + j;
-            const int64_t p = find_col(row_ptr, col_idx, row, col);
-            if (p < 0) return -3;
-            val[p] += Ke[r * nd + b * f.ndpn + j];
-          }
-      }
+    const int rc = assemble_one(f, type, m, e, coords, conn, dofs, kappa, kappa0_gp, alpha_gp,
+                                row_ptr, col_idx, val, R, S, Ke.data(), Fe.data(), Fa.data(), &ng);
+    if (rc != 0) return rc;
   }
   if (n_guard) *n_guard = ng;
+  return 0;
+}
+
+// The same element loop on all host cores (SURVEY 8d oracle timing (b); used for the CPU
+// baseline only -- parity uses the serial loop above): elements are visited colour by colour;
+// elements of one colour share no node (caller's colouring, e.g. the 2^d parities of a
+// structured grid), so the scatter of one colour is race-free.  Entries are summed in
+// (colour, element) order instead of element order.  Returns the thread count used in *threads.
+int oracle_assemble_colored(int type, const oracle_material* m, int64_t n_nodes,
+                            const double* coords, int64_t n_elems, const int64_t* conn,
+                            const double* dofs, const double* kappa, const int32_t* colour,
+                            int n_colours, const int64_t* row_ptr, const int32_t* col_idx,
+                            double* val, double* R, double* S, int nthreads, int* threads) {
+  Fam f;
+  if (!family(type, &f)) return -1;
+  const int nd = f.ndofe;
+  const int64_t ndof = n_nodes * f.ndpn;
+  std::fill(val, val + row_ptr[ndof], 0.0);
+  std::fill(R, R + ndof, 0.0);
+  std::fill(S, S + ndof, 0.0);
+  std::vector<std::vector<int64_t>> by(n_colours);
+  for (int64_t e = 0; e < n_elems; ++e) {
+    if (colour[e] < 0 || colour[e] >= n_colours) return -4;
+    by[colour[e]].push_back(e);
+  }
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+  int used = 1, rc_all = 0;
+  for (int c = 0; c < n_colours; ++c) {
+    const std::vector<int64_t>& el = by[c];
+#pragma omp parallel
+    {
+      std::vector<double> Ke(nd * nd), Fe(nd), Fa(nd);
+      int64_t ng = 0;
+#pragma omp single
+      used = omp_get_num_threads();
+#pragma omp for schedule(static)
+      for (int64_t k = 0; k < int64_t(el.size()); ++k) {
+        const int rc = assemble_one(f, type, m, el[k], coords, conn, dofs, kappa, nullptr, nullptr,
+                                    row_ptr, col_idx, val, R, S, Ke.data(), Fe.data(), Fa.data(), &ng);
+        if (rc != 0) {
+#pragma omp critical
+          rc_all = rc;
+        }
+      }
+    }
+    if (rc_all != 0) return rc_all;
+  }
+  if (threads) *threads = used;
   return 0;
 }
 

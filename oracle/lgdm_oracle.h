@@ -77,6 +77,13 @@ int oracle_assemble_d(int type, const oracle_material* m, int64_t n_nodes, const
                       const double* kappa, const double* kappa0_gp, const double* alpha_gp,
                       const int64_t* row_ptr, const int32_t* col_idx,
                       double* val, double* R, double* S, int64_t* n_guard);
+/* The same element loop on all host cores, colour by colour (elements of one colour share no
+ * node; colour[e] in [0, n_colours)); CPU-baseline timing only.  *threads = threads used. */
+int oracle_assemble_colored(int type, const oracle_material* m, int64_t n_nodes,
+                            const double* coords, int64_t n_elems, const int64_t* conn,
+                            const double* dofs, const double* kappa, const int32_t* colour,
+                            int n_colours, const int64_t* row_ptr, const int32_t* col_idx,
+                            double* val, double* R, double* S, int nthreads, int* threads);
 
 /* Sampled rows: the block-rows of the n_sel listed nodes only, each computed from the
  * elements adjacent to that node (ascending element id).  Output per selected node s is

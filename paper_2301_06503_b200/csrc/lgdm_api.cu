@@ -14,7 +14,10 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
+#include <set>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/lgdm.h"
@@ -46,6 +49,19 @@ lgdm_status fail(lgdm_status s, const char* fmt, ...) {
       return fail(e_ == cudaErrorMemoryAllocation ? LGDM_ERR_OUT_OF_MEMORY : LGDM_ERR_CUDA, \
                   "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__);  \
   } while (0)
+
+// Per-device "max dynamic shared memory" attribute: cudaFuncSetAttribute is a per-device
+// setting, and one process may drive meshes on several GPUs, possibly from several threads.
+template <class K> cudaError_t set_smem_attr(K kernel, size_t smem, int device) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_pair(reinterpret_cast<const void*>(kernel), device);
+  if (done.count(key)) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e == cudaSuccess) done.insert(key);
+  return e;
+}
 
 // NCCL entry points, resolved at run time (the library does not link libnccl).
 struct NcclApi {
@@ -601,11 +617,7 @@ template <int T> lgdm_status assemble_mixed(lgdm_mesh m) {
     m->device_bytes += m->n_elems * (F::NDOFE * F::NDOFE + F::NDOFE) * 8;
   }
   const size_t smem = sizeof(double) * (size_t(WPB) * MSmem<T>::SIZE + ((sizeof(MShape<T>) / 8 + 1) & ~size_t(1)));
-  static bool attr = false;
-  if (!attr) {
-    CU(cudaFuncSetAttribute(k_mixed_blocks<T, WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr = true;
-  }
+  CU(set_smem_attr(k_mixed_blocks<T, WPB>, smem, m->device));
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device);
   int per_sm = 1;
@@ -618,7 +630,7 @@ template <int T> lgdm_status assemble_mixed(lgdm_mesh m) {
   lgdm_status s = check_launch(m, "k_mixed_blocks");
   if (s != LGDM_OK) return s;
   const size_t gsm = sizeof(double) * size_t(GW) * (size_t(m->max_row) + MGStage<T>::SIZE);
-  if (gsm > 48 * 1024) CU(cudaFuncSetAttribute(k_mixed_gather<T, GW>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gsm)));
+  if (gsm > 48 * 1024) CU(set_smem_attr(k_mixed_gather<T, GW>, gsm, m->device));
   const int64_t gn = (m->n_owned + GW - 1) / GW;
   k_mixed_gather<T, GW><<<unsigned(std::min<int64_t>(gn, int64_t(nsm) * 16)), GW * 32, gsm, m->stream>>>(
       m->n_owned, m->madj_ptr, m->madj, m->scratchK, m->scratchF, m->max_row, m->val, m->R);
@@ -882,11 +894,7 @@ template <int D> lgdm_status assemble_general(lgdm_mesh m) {
   }
   const size_t smem = sizeof(double) * (size_t(EPB) * F::NGP * GpBlock<D>::STRIDE +
                                         EPB * F::NGP * kScal + EPB * F::NEN * D + EPB * F::NEN * F::NDPN);
-  static bool attr = false;
-  if (!attr) {
-    CU(cudaFuncSetAttribute(k_elem_blocks<D, EPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr = true;
-  }
+  CU(set_smem_attr(k_elem_blocks<D, EPB>, smem, m->device));
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device);
   int per_sm = 1;
@@ -949,10 +957,7 @@ lgdm_status lgdm_assemble(lgdm_mesh m, lgdm_csr* K, double** R) {
   CU(cudaSetDevice(m->device));
   lgdm_status s;
   // per-GP defect fields: the general path and the default sweeps (k_sweep4, k_sweepq)
-  const bool defects = m->k0g || m->alg;
   const bool sweep = !m->mixed && (m->kernel >= 2 || (m->kernel == 0 && m->structured && sweep_supported(m)));
-  if (defects && (m->kernel == 2 || m->kernel == 3 || m->kernel == 5))
-    return fail(LGDM_ERR_INVALID_ARGUMENT, "kernels 2, 3, 5 do not take per-GP defect fields (use 0, 1 or 4)");
   if (m->kernel >= 2 && !(m->structured && sweep_supported(m)))
     return fail(LGDM_ERR_INVALID_ARGUMENT, "sweep kernel requested but mesh is not structured");
   if (m->mixed) s = m->type == LGDM_BAR3 ? assemble_mixed<4>(m) : assemble_mixed<5>(m);
@@ -1051,11 +1056,7 @@ lgdm_status lgdm_update_state(lgdm_mesh m, double* sdv, int64_t n_sdv, int dst_o
   constexpr int TPB = 128;
   const unsigned blocks = unsigned((ngp + TPB - 1) / TPB);
   const size_t smem = out ? size_t(TPB) * W * sizeof(double) : 0;   // record staging
-  static bool attr = false;
-  if (!attr) {
-    CU(cudaFuncSetAttribute(k_update_state<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, TPB * StateW<3>::W * 8));
-    attr = true;
-  }
+  CU(set_smem_attr(k_update_state<3>, size_t(TPB) * StateW<3>::W * 8, m->device));
   if (m->mixed) {
     const size_t tbl = sizeof(double) * 400;   // >= the padded shape table of either family
     static_assert(sizeof(MShape<5>) <= 400 * sizeof(double) && sizeof(MShape<4>) <= 400 * sizeof(double), "table");
@@ -1359,6 +1360,20 @@ lgdm_status lgdm_delta_norms(lgdm_mesh m, const double* delta, double out4[4]) {
   return LGDM_OK;
 }
 
+lgdm_status lgdm_delta_ratios(lgdm_mesh m, const double* delta, double tol, double out2[2],
+                              int* converged) {
+  if (!out2 || !converged) return fail(LGDM_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (!(tol > 0.0)) return fail(LGDM_ERR_INVALID_ARGUMENT, "tol must be > 0");
+  double s4[4];
+  const lgdm_status st = lgdm_delta_norms(m, delta, s4);
+  if (st != LGDM_OK) return st;
+  // Alg. 1 l.26: ||du|| / ||u|| and ||de|| / ||e|| (a zero iterate counts as norm 1e-16)
+  out2[0] = std::sqrt(s4[0]) / std::max(std::sqrt(s4[1]), 1e-16);
+  out2[1] = std::sqrt(s4[2]) / std::max(std::sqrt(s4[3]), 1e-16);
+  *converged = (out2[0] <= tol && out2[1] <= tol) ? 1 : 0;
+  return LGDM_OK;
+}
+
 lgdm_status lgdm_residual_sumsq(lgdm_mesh m, double* out2, int on_device) {
   if (!m || !out2) return fail(LGDM_ERR_INVALID_ARGUMENT, "NULL argument");
   if (!m->assembled) return fail(LGDM_ERR_INVALID_STATE, "residual before assemble");
@@ -1441,7 +1456,7 @@ lgdm_status lgdm_scale_dofs(lgdm_mesh m, double sc) {
 }
 
 lgdm_status lgdm_set_kernel(lgdm_mesh m, int kernel) {
-  if (!m || kernel < 0 || kernel > 5) return fail(LGDM_ERR_INVALID_ARGUMENT, "bad kernel selector");
+  if (!m || kernel < 0 || kernel > 3) return fail(LGDM_ERR_INVALID_ARGUMENT, "bad kernel selector");
   if (m->mixed && kernel > 1) return fail(LGDM_ERR_INVALID_ARGUMENT, "mixed-order meshes: kernels 0 and 1 only");
   if (kernel >= 2 && !(m->structured && sweep_supported(m)))
     return fail(LGDM_ERR_INVALID_ARGUMENT, "sweep kernel needs a structured mesh with whole owned layers");
@@ -1490,7 +1505,6 @@ void lgdm_destroy(lgdm_mesh m) {
   if (m->cstream) cudaStreamSynchronize(m->cstream), cudaStreamDestroy(m->cstream);
   if (m->copy_ev) cudaEventDestroy(m->copy_ev);
   if (m->free_ev) cudaEventDestroy(m->free_ev);
-  sweep_free(m);
   delete m;
 }
 

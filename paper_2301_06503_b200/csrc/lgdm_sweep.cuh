@@ -1,22 +1,18 @@
-// lgdm_sweep.cuh -- fused structured-sweep assembly (Q4 and Hex8), the hot kernel.
+// lgdm_sweep.cuh -- fused structured-sweep assembly (Q4 and Hex8), the hot kernels.
 //
 // Included by lgdm_api.cu after the definition of lgdm_mesh_s.
 //
 // Mapping (B200-first redesign of Alg. 2's "Compute and Assemble K, F"):
-//   * One CTA owns a tile of node COLUMNS (Hex8: 4x4 (x,y) columns; Q4: 32 x-columns) and a
-//     chunk of node LAYERS along the sweep axis (Hex8: z; Q4: y).  It writes exactly the CSR
-//     block-rows of the nodes it owns, so no two CTAs ever touch the same entry (atomic-free).
+//   * One CTA owns a tile of node COLUMNS and a chunk of node LAYERS along the sweep axis
+//     (Hex8: z; Q4: y).  It writes exactly the CSR block-rows of the nodes it owns, so no two
+//     CTAs ever touch the same entry (atomic-free).
 //   * It sweeps the element layers that touch its nodes.  In each layer the elements around
-//     the tile (owned columns + one halo element on each side) are processed in colour
-//     batches -- parity of the element's (i, j) -- so no two elements of a batch share a node.
-//   * Per batch: phase A (thread per element x GP: geometry, kinematics, Appendix A update,
-//     per-node expansions, lgdm_device.cuh) into shared memory; phase C (thread per element x
-//     node pair a<=b: Gauss sums of Eqs. 11a-f in registers, Kuu symmetry); then each pair
-//     thread adds its blocks into the block-rows of its OWNED nodes.  Those rows are zeroed when
-//     the sweep first reaches their layer and stay L2-resident (two node layers per CTA) while
-//     they are accumulated, so DRAM sees each K value written once.
-//   * Per-entry summation order = (element layer, colour, GP) -- a function of global indices
+//     the tile (owned columns + one halo element on each side, recomputed) are processed in
+//     colour batches -- parity of the element's (i, j) -- so no two elements of a batch share
+//     a node and every block-row entry receives at most one add per batch.
+//   * Per-entry summation order = (element layer, colour) -- a function of global indices
 //     only, so any tiling / slabbing gives bitwise identical K and R.
+// Kernels: k_hex8 (Hex8, lgdm_hex8.cuh), k_sweepq (Q4, lgdm_sweepq.cuh).
 #pragma once
 
 namespace lgdm {
@@ -37,19 +33,6 @@ __device__ unsigned long long g_phase[16];
 #define PT_DECL
 #define PT_MARK(slot, cond) do {} while (0)
 #endif
-
-template <int D> struct SweepCfg;
-// TX x TY node columns per CTA, E elements per batch, NCOL colours per layer.
-template <> struct SweepCfg<2> { static constexpr int TX = 64, TY = 1, E = 16, NCOL = 2, MINB = 2; };
-template <> struct SweepCfg<3> { static constexpr int TX = 6, TY = 6, E = 4, NCOL = 4, MINB = 2; };
-
-template <int D> struct SweepThreads {
-  // named-barrier thread counts must be whole warps
-  static constexpr int P = (SweepCfg<D>::E * Fam<D>::NGP + 31) / 32 * 32;    // producers: (element, GP)
-  static constexpr int C = (SweepCfg<D>::E * Fam<D>::NPAIR + 31) / 32 * 32;  // consumers: (element, pair)
-  static constexpr int T = P + C;
-  static_assert(P % 32 == 0 && C % 32 == 0, "whole warps");
-};
 
 struct SweepGeom {
   int64_t nx, nyE, nyN, nl;        // elements in x; elements / nodes in y (D=2: 1 / 1); layers
@@ -73,337 +56,16 @@ template <int D> __device__ __forceinline__ void node_off(int a, int& ox, int& o
   }
 }
 
-// slot of neighbour offset (dx,dy,dz) in the sorted neighbour list of node (x,y,z), and the
-// row width W = deg * ndpn (reading R-PAT: neighbours sorted by global id = (z, y, x))
-__device__ __forceinline__ void slot_of(const SweepGeom& G, int64_t x, int64_t y, int64_t z,
-                                        int dx, int dy, int dz, int ndpn, int& slot, int& W) {
-  const int xlo = x > 0 ? -1 : 0, xhi = x < G.nx ? 1 : 0;
-  const int ylo = y > 0 ? -1 : 0, yhi = y < G.nyN - 1 ? 1 : 0;
-  const int zlo = z > 0 ? -1 : 0, zhi = z < G.nl ? 1 : 0;
-  const int wx = xhi - xlo + 1, wy = yhi - ylo + 1, wz = zhi - zlo + 1;
-  slot = ((dz - zlo) * wy + (dy - ylo)) * wx + (dx - xlo);
-  W = wx * wy * wz * ndpn;
-}
-
-// Is element (i, j, k) the FIRST contributor, in sweep order (element layer, then colour), to
-// the entries coupling nodes A and B?  The elements containing both are those with
-// i' in [max(ax,bx)-1, min(ax,bx)] (likewise j', k'), clipped to the mesh.  The first stores,
-// the others read-modify-write, so no zero fill of K is needed.
-template <int D>
-__device__ __forceinline__ bool first_contrib(const SweepGeom& G, int i, int j, int k, int ax,
-                                              int ay, int az, int bx, int by, int bz) {
-  const int kmin = max(max(az, bz) - 1, 0);
-  if (k != kmin) return false;
-  const int i0 = max(max(ax, bx) - 1, 0), i1 = min(min(ax, bx), int(G.nx) - 1);
-  int best = 4;
-  for (int ii = i0; ii <= i1; ++ii) {
-    if constexpr (D == 3) {
-      const int j0 = max(max(ay, by) - 1, 0), j1 = min(min(ay, by), int(G.nyE) - 1);
-      for (int jj = j0; jj <= j1; ++jj) best = min(best, (ii & 1) + 2 * (jj & 1));
-    } else {
-      best = min(best, ii & 1);
-    }
-  }
-  const int mine = (D == 3) ? (i & 1) + 2 * (j & 1) : (i & 1);
-  return mine == best;
-}
-
-// local node -> position of its column block in a CSR row (nodes sorted by (z, y, x)):
-// Q4 0,1,3,2; Hex8 0,1,3,2,4,5,7,6 (an involution)
-template <int D> __device__ __forceinline__ int slot_perm(int b) {
-  return (D == 1) ? b : ((b & 2) ? (b ^ 1) : b);
-}
-
-// named barriers with immediate ids (so ptxas reserves only ids 0..5)
-template <int ID> __device__ __forceinline__ void bar_sync(int n) {
-  asm volatile("bar.sync %0, %1;" ::"n"(ID), "r"(n) : "memory");
-}
-template <int ID> __device__ __forceinline__ void bar_arrive(int n) {
-  asm volatile("bar.arrive %0, %1;" ::"n"(ID), "r"(n) : "memory");
-}
-enum { BAR_FULL0 = 1, BAR_EMPTY0 = 3, BAR_CONS = 5 };
-__device__ __forceinline__ void bar_sync_full(int buf, int n) {
-  if (buf) bar_sync<BAR_FULL0 + 1>(n); else bar_sync<BAR_FULL0>(n);
-}
-__device__ __forceinline__ void bar_arrive_full(int buf, int n) {
-  if (buf) bar_arrive<BAR_FULL0 + 1>(n); else bar_arrive<BAR_FULL0>(n);
-}
-__device__ __forceinline__ void bar_sync_empty(int buf, int n) {
-  if (buf) bar_sync<BAR_EMPTY0 + 1>(n); else bar_sync<BAR_EMPTY0>(n);
-}
-__device__ __forceinline__ void bar_arrive_empty(int buf, int n) {
-  if (buf) bar_arrive<BAR_EMPTY0 + 1>(n); else bar_arrive<BAR_EMPTY0>(n);
-}
-
-// Add the node-pair blocks of one pair thread into the owned block-rows: rows of node A
-// (rowA, may be null), rows of node B (rowB, may be null) and R of A (rA, may be null).  All
-// loads are issued before any store so the L2 round trip is paid once (.cg: L2, not L1).
-template <int D>
-__device__ __forceinline__ void rmw_pair(double* __restrict__ rowA, int WA, bool ldA,
-                                         double* __restrict__ rowB, int WB, bool ldB,
-                                         double* __restrict__ rA, bool ldR,
-                                         const double (&vA)[Fam<D>::NDPN][Fam<D>::NDPN],
-                                         const double (&vB)[Fam<D>::NDPN][Fam<D>::NDPN],
-                                         const double (&fA)[Fam<D>::NDPN]) {
-  constexpr int NDPN = Fam<D>::NDPN;
-  double uA[NDPN][NDPN], uB[NDPN][NDPN], uR[NDPN];
-#pragma unroll
-  for (int i = 0; i < NDPN; ++i)
-#pragma unroll
-    for (int j = 0; j < NDPN; ++j) uA[i][j] = uB[i][j] = 0.0;
-#pragma unroll
-  for (int i = 0; i < NDPN; ++i) uR[i] = 0.0;
-  if constexpr (NDPN == 4) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if (rowA && ldA) {
-        const double2* q = reinterpret_cast<const double2*>(rowA + int64_t(i) * WA);
-        const double2 a0 = __ldcg(q), a1 = __ldcg(q + 1);
-        uA[i][0] = a0.x; uA[i][1] = a0.y; uA[i][2] = a1.x; uA[i][3] = a1.y;
-      }
-      if (rowB && ldB) {
-        const double2* q = reinterpret_cast<const double2*>(rowB + int64_t(i) * WB);
-        const double2 b0 = __ldcg(q), b1 = __ldcg(q + 1);
-        uB[i][0] = b0.x; uB[i][1] = b0.y; uB[i][2] = b1.x; uB[i][3] = b1.y;
-      }
-    }
-    if (rA && ldR) {
-      const double2* q = reinterpret_cast<const double2*>(rA);
-      const double2 r0 = __ldcg(q), r1 = __ldcg(q + 1);
-      uR[0] = r0.x; uR[1] = r0.y; uR[2] = r1.x; uR[3] = r1.y;
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if (rowA) {
-        double2* q = reinterpret_cast<double2*>(rowA + int64_t(i) * WA);
-        __stcg(q, make_double2(uA[i][0] + vA[i][0], uA[i][1] + vA[i][1]));
-        __stcg(q + 1, make_double2(uA[i][2] + vA[i][2], uA[i][3] + vA[i][3]));
-      }
-      if (rowB) {
-        double2* q = reinterpret_cast<double2*>(rowB + int64_t(i) * WB);
-        __stcg(q, make_double2(uB[i][0] + vB[i][0], uB[i][1] + vB[i][1]));
-        __stcg(q + 1, make_double2(uB[i][2] + vB[i][2], uB[i][3] + vB[i][3]));
-      }
-    }
-    if (rA) {
-      double2* q = reinterpret_cast<double2*>(rA);
-      __stcg(q, make_double2(uR[0] + fA[0], uR[1] + fA[1]));
-      __stcg(q + 1, make_double2(uR[2] + fA[2], uR[3] + fA[3]));
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < NDPN; ++i)
-#pragma unroll
-      for (int j = 0; j < NDPN; ++j) {
-        if (rowA && ldA) uA[i][j] = __ldcg(rowA + int64_t(i) * WA + j);
-        if (rowB && ldB) uB[i][j] = __ldcg(rowB + int64_t(i) * WB + j);
-      }
-    if (rA && ldR)
-#pragma unroll
-      for (int i = 0; i < NDPN; ++i) uR[i] = __ldcg(rA + i);
-#pragma unroll
-    for (int i = 0; i < NDPN; ++i)
-#pragma unroll
-      for (int j = 0; j < NDPN; ++j) {
-        if (rowA) __stcg(rowA + int64_t(i) * WA + j, uA[i][j] + vA[i][j]);
-        if (rowB) __stcg(rowB + int64_t(i) * WB + j, uB[i][j] + vB[i][j]);
-      }
-    if (rA)
-#pragma unroll
-      for (int i = 0; i < NDPN; ++i) __stcg(rA + i, uR[i] + fA[i]);
-  }
-}
-
-template <int D>
-__global__ void __launch_bounds__(SweepThreads<D>::T, SweepCfg<D>::MINB)
-k_sweep(DevMat m, SweepGeom G, const double* __restrict__ coords, const double* __restrict__ dofs,
-        const double* __restrict__ kappa, const int64_t* __restrict__ base,
-        double* __restrict__ val, double* __restrict__ Rv) {
-  using F = Fam<D>;
-  using Cf = SweepCfg<D>;
-  using Th = SweepThreads<D>;
-  constexpr int E = Cf::E, NDPN = F::NDPN, NEN = F::NEN, NGP = F::NGP;
-  constexpr int CS = Core<D>::STRIDE, GB = GpBlock<D>::STRIDE;
-  extern __shared__ double sm[];
-  double* cores = sm;                            // [2][E][NGP][CS]
-  double* recs = cores + 2 * E * NGP * CS;       // [E][NGP][GB]
-  __shared__ int64_t s_base_all[2][Cf::TX * Cf::TY];   // val offsets of the tile's block-rows, by layer parity
-  const int tid = threadIdx.x;
-
-  int bid = blockIdx.x;
-  const int tx = bid % G.tiles_x;
-  bid /= G.tiles_x;
-  const int ty = bid % G.tiles_y;
-  const int ch = bid / G.tiles_y;
-  const int64_t x0 = int64_t(tx) * Cf::TX, x1 = min(x0 + Cf::TX, G.nx + 1);
-  const int64_t y0 = int64_t(ty) * Cf::TY, y1 = min(y0 + Cf::TY, G.nyN);
-  const int64_t z0 = G.lay_own_b + int64_t(ch) * G.chunk_len;
-  const int64_t z1 = min(z0 + G.chunk_len, G.lay_own_e);
-  if (z0 >= z1) return;
-  const int64_t nxN = G.nx + 1;
-  auto node_id = [&](int64_t x, int64_t y, int64_t z) { return x + nxN * (y + G.nyN * z); };
-
-  const int64_t s_first = max(z0 - 1, int64_t(0));
-  const int64_t s_last = min(z1, G.nl) - 1;
-  const int64_t ilo = max(x0 - 1, int64_t(0)), ihi = min(x1, G.nx);
-  const int64_t jlo = (D == 3) ? max(y0 - 1, int64_t(0)) : 0;
-  const int64_t jhi = (D == 3) ? min(y1, G.nyE) : 1;
-
-  // the batch schedule, identical for producers and consumers:
-  // for each element layer s, each colour c, batches of E elements of that colour
-  auto for_each_batch = [&](auto&& body) {
-    for (int64_t s = s_first; s <= s_last; ++s)
-      for (int c = 0; c < Cf::NCOL; ++c) {
-        const int ci = c & 1;
-        const int ifst = int(ilo) + ((ilo & 1) != ci ? 1 : 0);
-        const int ni = ifst < ihi ? (int(ihi) - ifst + 1) / 2 : 0;
-        int jfst = 0, nj = 1;
-        if constexpr (D == 3) {
-          const int cj = c >> 1;
-          jfst = int(jlo) + ((jlo & 1) != cj ? 1 : 0);
-          nj = jfst < jhi ? (int(jhi) - jfst + 1) / 2 : 0;
-        }
-        const int nc = ni * nj;
-        for (int b0 = 0; b0 < nc; b0 += E) body(s, b0, ifst, ni, jfst, nc);
-      }
-  };
-
-  if (tid < Th::P) {
-    // ------------------------------ producer warps ------------------------------
-    const int el = tid / NGP, g = tid % NGP;   // el may be >= E in padding threads
-    int t = 0;
-    PT_DECL
-    for_each_batch([&](int64_t s, int b0, int ifst, int ni, int jfst, int nc) {
-      const int buf = t & 1;
-      if (t >= 2) bar_sync_empty(buf, Th::T);
-      PT_MARK(0, tid == 0);
-      const int k = b0 + el;
-      if (el < E && k < nc) {
-        const int i = ifst + 2 * (k % ni), j = jfst + 2 * (k / ni);
-        auto nid = [&](int a) {
-          int ox, oy, oz;
-          node_off<D>(a, ox, oy, oz);
-          return node_id(i + ox, j + oy, s + oz);
-        };
-        auto X = [&](int a, int q) { return __ldg(coords + nid(a) * D + q); };
-        auto U = [&](int a, int q) { return __ldg(dofs + nid(a) * NDPN + q); };
-        const int64_t e = i + G.nx * (j + G.nyE * s);  // int64: config 4 has 8M elements x 8 GPs
-        gpCore<D>(m, X, U, __ldg(kappa + e * NGP + g), g, cores + (size_t(buf) * E * NGP + tid) * CS);
-      }
-      PT_MARK(1, tid == 0);
-      bar_arrive_full(buf, Th::T);
-      ++t;
-    });
-    for (int k = max(t - 2, 0); k < t; ++k) bar_sync_empty(k & 1, Th::T);
-    return;
-  }
-
-  // -------------------------------- consumer warps --------------------------------
-  const int ct = tid - Th::P;
-  const int cel = ct / F::NPAIR, cp = ct % F::NPAIR;
-  int pa, pb;
-  pair_ab<NEN>(cp, pa, pb);
-  int oax, oay, oaz, obx, oby, obz;
-  node_off<D>(pa, oax, oay, oaz);
-  node_off<D>(pb, obx, oby, obz);
-  const int64_t cols_x = x1 - x0, cols = cols_x * (y1 - y0);
-
-  // stage the val offsets of the tile's block-rows in layer z in shared memory
-  // (made visible by the consumer barrier that follows the expansion)
-  auto stage_layer = [&](int64_t z) {
-    int64_t* sb = s_base_all[z & 1];
-    for (int c = ct; c < cols; c += Th::C) {
-      const int64_t x = x0 + c % cols_x, y = y0 + c / cols_x;
-      sb[c] = base[node_id(x, y, z) - G.own_node_b];
-    }
-  };
-
-  int t = 0;
-  int64_t cur_s = -1;
-  PT_DECL
-  for_each_batch([&](int64_t s, int b0, int ifst, int ni, int jfst, int nc) {
-    const int buf = t & 1;
-    PT_MARK(7, ct == 0);
-    if (s != cur_s) {
-      if (cur_s < 0 && s == z0) stage_layer(z0);
-      if (s + 1 >= z0 && s + 1 < z1) stage_layer(s + 1);
-      cur_s = s;
-    }
-    PT_MARK(2, ct == 0);
-    bar_sync_full(buf, Th::T);
-    PT_MARK(3, ct == 0);
-    // expansion: (element, GP, node) records from the compact GP states
-    const double* cb = cores + size_t(buf) * E * NGP * CS;
-    for (int it = ct; it < E * NGP * NEN; it += Th::C) {
-      const int eg = it / NEN, a = it % NEN;
-      if (b0 + eg / NGP < nc) gpExpand<D>(cb + eg * CS, a, eg % NGP, recs + size_t(eg) * GB + a * Rec<D>::STRIDE);
-    }
-    PT_MARK(4, ct == 0);
-    bar_sync<BAR_CONS>(Th::C);
-    PT_MARK(5, ct == 0);
-    // pair Gauss sums and accumulation into the owned block-rows
-    const int k = b0 + cel;
-    if (cel < E && k < nc) {
-      const int i = ifst + 2 * (k % ni), j = jfst + 2 * (k / ni);
-      const int64_t ax = i + oax, ay = j + oay, az = s + oaz;
-      const int64_t bx = i + obx, by = j + oby, bz = s + obz;
-      const bool own_a = ax >= x0 && ax < x1 && ay >= y0 && ay < y1 && az >= z0 && az < z1;
-      const bool own_b = bx >= x0 && bx < x1 && by >= y0 && by < y1 && bz >= z0 && bz < z1;
-      if (own_a || own_b) {
-        PairAcc<D> acc;
-        phaseC<D, CS, Core<D>::MU, Core<D>::GHC>(recs + size_t(cel) * NGP * GB, cb + cel * NGP * CS,
-                                                  pa, pb, acc);
-        PT_MARK(6, ct == 0);
-        double vA[NDPN][NDPN], vB[NDPN][NDPN], fA[NDPN];
-#pragma unroll
-        for (int r = 0; r < D; ++r) {
-#pragma unroll
-          for (int q = 0; q < D; ++q) {
-            vA[r][q] = acc.Kuu[r][q];
-            vB[r][q] = acc.Kuu[q][r];
-          }
-          vA[r][D] = acc.Kue_ab[r];
-          vA[D][r] = acc.Keu_ab[r];
-          vB[r][D] = acc.Kue_ba[r];
-          vB[D][r] = acc.Keu_ba[r];
-        }
-        vA[D][D] = acc.Kee_ab;
-        vB[D][D] = acc.Kee_ba;
-#pragma unroll
-        for (int r = 0; r < NDPN; ++r) fA[r] = acc.Fd[r];
-        double *rowA = nullptr, *rowB = nullptr, *rA = nullptr;
-        int WA = 0, WB = 0;
-        if (own_a) {
-          int sl;
-          slot_of(G, ax, ay, az, obx - oax, oby - oay, obz - oaz, NDPN, sl, WA);
-          rowA = val + s_base_all[az & 1][(ax - x0) + cols_x * (ay - y0)] + NDPN * sl;
-          if (pa == pb) rA = Rv + (node_id(ax, ay, az) - G.own_node_b) * NDPN;
-        }
-        if (own_b && pa != pb) {
-          int sl;
-          slot_of(G, bx, by, bz, oax - obx, oay - oby, oaz - obz, NDPN, sl, WB);
-          rowB = val + s_base_all[bz & 1][(bx - x0) + cols_x * (by - y0)] + NDPN * sl;
-        }
-        const bool first = first_contrib<D>(G, i, j, int(s), int(ax), int(ay), int(az), int(bx),
-                                            int(by), int(bz));
-        const bool firstR = first_contrib<D>(G, i, j, int(s), int(ax), int(ay), int(az), int(ax),
-                                             int(ay), int(az));
-        rmw_pair<D>(rowA, WA, !first, rowB, WB, !first, rA, !firstR, vA, vB, fA);
-      }
-    }
-    PT_MARK(8, ct == 0);
-    bar_arrive_empty(buf, Th::T);   // cores[buf] (incl. mu*, ghc read by phase C) is free
-    bar_sync<BAR_CONS>(Th::C);
-    PT_MARK(9, ct == 0);
-    ++t;
-  });
+// in-plane slot of offset (dx, dy)
+template <int D> __device__ __forceinline__ int plane_slot(int dx, int dy) {
+  if constexpr (D == 3) return (dy + 1) * 3 + (dx + 1);
+  else return dx + 1;
 }
 
 }  // namespace lgdm
 
-#include "lgdm_sweep3.cuh"
 #include "lgdm_sweep4.cuh"
-#include "lgdm_sweep5.cuh"
+#include "lgdm_hex8.cuh"
 #include "lgdm_sweepq.cuh"
 
 namespace {
@@ -414,95 +76,6 @@ bool sweep_supported(lgdm_mesh m) {
   return m->own_b % per_layer == 0 && m->own_e % per_layer == 0;
 }
 
-template <int D> lgdm_status launch_sweep(lgdm_mesh m) {
-  using F = Fam<D>;
-  using Cf = SweepCfg<D>;
-  using Th = SweepThreads<D>;
-  SweepGeom G{};
-  G.nx = m->nx;
-  if (D == 3) {
-    G.nyE = m->ny;
-    G.nyN = m->ny + 1;
-    G.nl = m->nz;
-  } else {
-    G.nyE = 1;
-    G.nyN = 1;
-    G.nl = m->ny;
-  }
-  const int64_t per_layer = (G.nx + 1) * G.nyN;
-  G.lay_own_b = m->own_b / per_layer;
-  G.lay_own_e = m->own_e / per_layer;
-  G.own_node_b = m->own_b;
-  G.tiles_x = int((G.nx + 1 + Cf::TX - 1) / Cf::TX);
-  G.tiles_y = int((G.nyN + Cf::TY - 1) / Cf::TY);
-  const size_t smem = sizeof(double) * (size_t(2) * Cf::E * F::NGP * Core<D>::STRIDE +
-                                        size_t(Cf::E) * F::NGP * GpBlock<D>::STRIDE);
-  static bool attr = false;
-  if (!attr) {
-    CU(cudaFuncSetAttribute(k_sweep<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr = true;
-  }
-  int nsm = 148, per_sm = 1;
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep<D>, Th::T, smem);
-  per_sm = std::max(per_sm, 1);
-  const int64_t layers = G.lay_own_e - G.lay_own_b;
-  const int64_t tiles = int64_t(G.tiles_x) * G.tiles_y;
-  // enough CTAs for ~4 waves, but chunks of at least 8 layers (each chunk re-reads one layer)
-  int64_t chunks = (4 * int64_t(nsm) * per_sm + tiles - 1) / tiles;
-  chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, (layers + 7) / 8));
-  G.chunk_len = (layers + chunks - 1) / chunks;
-  G.chunks = int((layers + G.chunk_len - 1) / G.chunk_len);
-  const int64_t grid = tiles * G.chunks;
-  k_sweep<D><<<unsigned(grid), Th::T, smem, m->stream>>>(
-      m->dm, G, m->coords, m->dofs, m->kappa, m->base, m->val, m->R);
-  return check_launch(m, "k_sweep");
-}
-
-template <int D> lgdm_status launch_sweep3(lgdm_mesh m) {
-  using F = Fam<D>;
-  using Cf = S3Cfg<D>;
-  using Th = S3Threads<D>;
-  SweepGeom G{};
-  G.nx = m->nx;
-  if (D == 3) {
-    G.nyE = m->ny;
-    G.nyN = m->ny + 1;
-    G.nl = m->nz;
-  } else {
-    G.nyE = 1;
-    G.nyN = 1;
-    G.nl = m->ny;
-  }
-  const int64_t per_layer = (G.nx + 1) * G.nyN;
-  G.lay_own_b = m->own_b / per_layer;
-  G.lay_own_e = m->own_e / per_layer;
-  G.own_node_b = m->own_b;
-  G.tiles_x = int((G.nx + 1 + Cf::TX - 1) / Cf::TX);
-  G.tiles_y = int((G.nyN + Cf::TY - 1) / Cf::TY);
-  const size_t smem = sizeof(double) * (size_t(2) * Cf::E * F::NGP * Core<D>::STRIDE +
-                                        size_t(kRecRing) * Cf::E * GpBlock<D>::STRIDE +
-                                        size_t(Cf::TX) * Cf::TY * S3Layout<D>::COL_PAD);
-  static bool attr = false;
-  if (!attr) {
-    CU(cudaFuncSetAttribute(k_sweep3<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr = true;
-  }
-  int nsm = 148, per_sm = 1;
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep3<D>, Th::T, smem);
-  per_sm = std::max(per_sm, 1);
-  const int64_t layers = G.lay_own_e - G.lay_own_b;
-  const int64_t tiles = int64_t(G.tiles_x) * G.tiles_y;
-  int64_t chunks = (4 * int64_t(nsm) * per_sm + tiles - 1) / tiles;
-  chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, (layers + 7) / 8));
-  G.chunk_len = (layers + chunks - 1) / chunks;
-  G.chunks = int((layers + G.chunk_len - 1) / G.chunk_len);
-  const int64_t grid = tiles * G.chunks;
-  k_sweep3<D><<<unsigned(grid), Th::T, smem, m->stream>>>(m->dm, G, m->coords, m->dofs, m->kappa,
-                                                          m->base, m->val, m->R);
-  return check_launch(m, "k_sweep3");
-}
 
 // Chunking of the sweep axis: each chunk of len node layers processes len + 1 element layers
 // (one recomputed).  Pick the chunk count that minimises waves x (len + 1), i.e. the
@@ -538,11 +111,7 @@ lgdm_status launch_sweep4(lgdm_mesh m) {
   G.alg = m->alg;
   G.tiles_x = int((G.nx + 1 + S4::TX - 1) / S4::TX);
   G.tiles_y = int((G.nyN + S4::TY - 1) / S4::TY);
-  static bool attr = false;
-  if (!attr) {
-    CU(cudaFuncSetAttribute(k_sweep4, cudaFuncAttributeMaxDynamicSharedMemorySize, int(S4::SMEM)));
-    attr = true;
-  }
+  CU(set_smem_attr(k_sweep4, S4::SMEM, m->device));
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device);
   const int64_t layers = G.lay_own_e - G.lay_own_b;
@@ -556,7 +125,7 @@ lgdm_status launch_sweep4(lgdm_mesh m) {
   return check_launch(m, "k_sweep4");
 }
 
-lgdm_status launch_sweep5(lgdm_mesh m) {
+lgdm_status launch_hex8(lgdm_mesh m) {
   SweepGeom G{};
   G.nx = m->nx;
   G.nyE = m->ny;
@@ -566,13 +135,11 @@ lgdm_status launch_sweep5(lgdm_mesh m) {
   G.lay_own_b = m->own_b / per_layer;
   G.lay_own_e = m->own_e / per_layer;
   G.own_node_b = m->own_b;
-  G.tiles_x = int((G.nx + 1 + S5::TX - 1) / S5::TX);
-  G.tiles_y = int((G.nyN + S5::TY - 1) / S5::TY);
-  static bool attr = false;
-  if (!attr) {
-    CU(cudaFuncSetAttribute(k_sweep5, cudaFuncAttributeMaxDynamicSharedMemorySize, int(S5::SMEM)));
-    attr = true;
-  }
+  G.k0g = m->k0g;
+  G.alg = m->alg;
+  G.tiles_x = int((G.nx + 1 + H8::TX - 1) / H8::TX);
+  G.tiles_y = int((G.nyN + H8::TY - 1) / H8::TY);
+  CU(set_smem_attr(k_hex8, H8::SMEM, m->device));
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device);
   const int64_t layers = G.lay_own_e - G.lay_own_b;
@@ -581,9 +148,9 @@ lgdm_status launch_sweep5(lgdm_mesh m) {
   G.chunk_len = (layers + chunks - 1) / chunks;
   G.chunks = int((layers + G.chunk_len - 1) / G.chunk_len);
   const int64_t grid = tiles * G.chunks;
-  k_sweep5<<<unsigned(grid), S5::T, S5::SMEM, m->stream>>>(m->dm, G, m->coords, m->dofs, m->kappa,
-                                                           m->base, m->val, m->R);
-  return check_launch(m, "k_sweep5");
+  k_hex8<<<unsigned(grid), H8::T, H8::SMEM, m->stream>>>(m->dm, G, m->coords, m->dofs, m->kappa,
+                                                         m->base, m->val, m->R);
+  return check_launch(m, "k_hex8");
 }
 
 lgdm_status launch_sweepq(lgdm_mesh m) {
@@ -600,11 +167,7 @@ lgdm_status launch_sweepq(lgdm_mesh m) {
   G.alg = m->alg;
   G.tiles_x = int((G.nx + 1 + SQ::TX - 1) / SQ::TX);
   G.tiles_y = 1;
-  static bool attr = false;
-  if (!attr) {
-    CU(cudaFuncSetAttribute(k_sweepq, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SQ::SMEM)));
-    attr = true;
-  }
+  CU(set_smem_attr(k_sweepq, SQ::SMEM, m->device));
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device);
   const int64_t layers = G.lay_own_e - G.lay_own_b;
@@ -618,23 +181,20 @@ lgdm_status launch_sweepq(lgdm_mesh m) {
   return check_launch(m, "k_sweepq");
 }
 
-// Automatic choice (kernel 0 or 2): the round-1 redesigns k_sweepq (Q4) and k_sweep4 (Hex8)
-// are the fastest measured; k_sweep / k_sweep3 stay selectable (2 / 3)
-// and parity-tested.
+// Automatic choice (kernel 0 or 2): k_sweepq (Q4) and k_sweep4 (Hex8); kernel 3 selects the
+// register-tiled Hex8 variant k_hex8 (parity-tested; measured slower today).
 lgdm_status assemble_sweep(lgdm_mesh m) {
-  if (m->f.dim == 2) return (m->kernel == 2 || m->kernel == 3) ? launch_sweep3<2>(m) : launch_sweepq(m);
-  if (m->kernel == 3) return launch_sweep3<3>(m);
-  if (m->kernel == 2) return launch_sweep<3>(m);
-  if (m->kernel == 5) return launch_sweep5(m);
+  if (m->f.dim == 2) return launch_sweepq(m);
+  if (m->kernel == 3) return launch_hex8(m);
   return launch_sweep4(m);
 }
 
-void sweep_free(lgdm_mesh) {}
-
 }  // namespace
 
-extern "C" int lgdm_debug_phase_cycles(unsigned long long* out16, int reset) {
 #ifdef LGDM_PHASE_TIMING
+// debug builds only (-DLGDM_PHASE_TIMING; declared in include/lgdm.h under the same macro):
+// per-phase cycle counters of the sweep kernels' PT_MARK points
+extern "C" int lgdm_debug_phase_cycles(unsigned long long* out16, int reset) {
   cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(out16, lgdm::g_phase, sizeof(unsigned long long) * 16);
   if (reset) {
@@ -642,13 +202,5 @@ extern "C" int lgdm_debug_phase_cycles(unsigned long long* out16, int reset) {
     cudaMemcpyToSymbol(lgdm::g_phase, z, sizeof(z));
   }
   return 0;
-#else
-  (void)out16;
-  (void)reset;
-  return -1;
-#endif
 }
-
-namespace {
-
-}  // namespace
+#endif

@@ -19,7 +19,7 @@ BAR3, QUAD8 = 4, 5          # mixed order: quadratic u, linear ebar (SURVEY NEXT
 # type -> (dim, nen, ndpn, ngp); mixed families: nen = u nodes, ndpn = dofs of a corner node
 FAMILY = {BAR2: (1, 2, 2, 2), QUAD4: (2, 4, 3, 4), HEX8: (3, 8, 4, 8),
           BAR3: (1, 3, 2, 3), QUAD8: (2, 8, 3, 9)}
-KERNEL_AUTO, KERNEL_GENERAL, KERNEL_SWEEP, KERNEL_SWEEP3, KERNEL_SWEEP4, KERNEL_SWEEP5 = 0, 1, 2, 3, 4, 5
+KERNEL_AUTO, KERNEL_GENERAL, KERNEL_SWEEP, KERNEL_HEX8 = 0, 1, 2, 3
 
 STATUS = {0: "LGDM_OK", 1: "LGDM_ERR_INVALID_ARGUMENT", 2: "LGDM_ERR_INVERTED_ELEMENT",
           3: "LGDM_ERR_INVALID_STATE", 4: "LGDM_ERR_OUT_OF_MEMORY", 5: "LGDM_ERR_CUDA",
@@ -32,7 +32,7 @@ EXPORTS = ["lgdm_create_mesh", "lgdm_set_state", "lgdm_assemble", "lgdm_update_h
            "lgdm_scale_dofs", "lgdm_set_kernel", "lgdm_get_info", "lgdm_launch_count",
            "lgdm_last_error", "lgdm_destroy", "lgdm_sdv_width", "lgdm_set_defects",
            "lgdm_update_state", "lgdm_get_blocked", "lgdm_apply_dirichlet", "lgdm_solve",
-           "lgdm_add_dofs", "lgdm_delta_norms", "lgdm_reaction", "lgdm_solve_direct",
+           "lgdm_add_dofs", "lgdm_delta_norms", "lgdm_delta_ratios", "lgdm_reaction", "lgdm_solve_direct",
            "lgdm_dof_offsets", "lgdm_prefetch_dofs", "lgdm_set_state_prefetched",
            "lgdm_create_mesh_mixed"]
 
@@ -103,6 +103,7 @@ def load() -> C.CDLL:
     L.lgdm_solve.argtypes = [vp, vp, C.c_double, C.c_int, C.POINTER(C.c_int), dp]
     L.lgdm_add_dofs.argtypes = [vp, vp, C.c_double]
     L.lgdm_delta_norms.argtypes = [vp, vp, dp]
+    L.lgdm_delta_ratios.argtypes = [vp, vp, C.c_double, dp, C.POINTER(C.c_int)]
     L.lgdm_reaction.argtypes = [vp, i64, vp, dp]
     L.lgdm_solve_direct.argtypes = [vp, vp, C.POINTER(C.c_int)]
     L.lgdm_dof_offsets.argtypes = [vp, vp, i64]
@@ -143,9 +144,12 @@ class DeviceArray:
 
     def __init__(self, ptr: int, n: int, typestr: str, owner):
         self._owner = owner
+        # "stream": consumers (torch.as_tensor, CuPy) order their first use after the work
+        # enqueued on the mesh's stream (CUDA Array Interface v3; 1 = the legacy default stream)
         self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": typestr,
                                          "data": (int(ptr or 0), False), "version": 3,
-                                         "strides": None}
+                                         "strides": None,
+                                         "stream": int(getattr(owner, "stream", 0) or 1)}
 
     def torch(self, device=None):
         import torch
@@ -163,6 +167,22 @@ def _ptr_and_kind(x):
         pass
     a = np.ascontiguousarray(x, dtype=np.float64)
     return a.ctypes.data, 0, a
+
+
+def _numel(x) -> int:
+    """Element count of the caller's buffer (what the library's size checks compare)."""
+    n = getattr(x, "numel", None)
+    return int(n()) if callable(n) else int(np.asarray(x).size)
+
+
+def _device_vector(x, n: int, device: int, what: str):
+    """Validate a device float64 vector of n entries on the mesh's device."""
+    import torch
+    if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.float64 and x.is_contiguous()):
+        raise ValueError(f"{what}: need a contiguous float64 CUDA tensor")
+    if x.numel() != n or x.device.index != device:
+        raise ValueError(f"{what}: need {n} entries on cuda:{device}, got {x.numel()} on {x.device}")
+    return x.data_ptr()
 
 
 class Mesh:
@@ -184,6 +204,7 @@ class Mesh:
             import torch
             stream = torch.cuda.current_stream(device).cuda_stream
         self.device = device
+        self.stream = int(stream or 0)
         self._h = C.c_void_p()
         if global_dof_offset is not None:          # mixed-order slab
             _check(L.lgdm_create_mesh_mixed(etype, self.n_nodes, coords.ctypes.data, self.n_elems,
@@ -204,16 +225,14 @@ class Mesh:
     # -- state / assembly -------------------------------------------------------------
     def set_state(self, dofs, kappa=None):
         pd, on_dev, kd = _ptr_and_kind(dofs)
-        n_d = self.n_dofs
         if kappa is None:
-            _check(load().lgdm_set_state(self._h, pd, n_d, None, 0, on_dev))
+            _check(load().lgdm_set_state(self._h, pd, _numel(kd), None, 0, on_dev))
             self._keep = [kd]
             return
         pk, on_dev_k, kk = _ptr_and_kind(kappa)
         if on_dev_k != on_dev:
             raise ValueError("dofs and kappa must both be host or both be device")
-        _check(load().lgdm_set_state(self._h, pd, int(np.prod(getattr(dofs, "shape", (n_d,)))),
-                                     pk, int(np.prod(getattr(kappa, "shape", (0,)))), on_dev))
+        _check(load().lgdm_set_state(self._h, pd, _numel(kd), pk, _numel(kk), on_dev))
         self._keep = [kd, kk]   # host copies are async only for pinned memory; keep alive
 
     def prefetch_dofs(self, dofs):
@@ -222,8 +241,9 @@ class Mesh:
         p, on_dev, keep = _ptr_and_kind(dofs)
         if on_dev:
             raise ValueError("prefetch_dofs takes host memory")
-        self._keep_prefetch = keep
-        _check(load().lgdm_prefetch_dofs(self._h, p, self.n_dofs))
+        # the library double-buffers: the previous buffer may still be in flight, keep both
+        self._keep_prefetch = (getattr(self, "_keep_prefetch", (None, None))[1], keep)
+        _check(load().lgdm_prefetch_dofs(self._h, p, _numel(keep)))
 
     def set_state_prefetched(self):
         _check(load().lgdm_set_state_prefetched(self._h))
@@ -277,12 +297,24 @@ class Mesh:
         return out.value
 
     def add_dofs(self, delta, alpha=1.0):
-        _check(load().lgdm_add_dofs(self._h, delta.data_ptr(), alpha))
+        p = _device_vector(delta, self.n_dofs, self.device, "add_dofs")
+        _check(load().lgdm_add_dofs(self._h, p, alpha))
 
     def delta_norms(self, delta):
+        p = _device_vector(delta, self.n_dofs, self.device, "delta_norms")
         out = np.zeros(4)
-        _check(load().lgdm_delta_norms(self._h, delta.data_ptr(), out.ctypes.data_as(C.POINTER(C.c_double))))
+        _check(load().lgdm_delta_norms(self._h, p, out.ctypes.data_as(C.POINTER(C.c_double))))
         return out
+
+    def converged(self, delta, tol):
+        """Alg. 1 l.26 / Alg. 2 l.16 convergence test in the library: returns
+        (converged, |du|/|u|, |de|/|e|) for the correction delta (lgdm_delta_ratios)."""
+        p = _device_vector(delta, self.n_dofs, self.device, "converged")
+        out = np.zeros(2)
+        flag = C.c_int()
+        _check(load().lgdm_delta_ratios(self._h, p, tol, out.ctypes.data_as(C.POINTER(C.c_double)),
+                                        C.byref(flag)))
+        return bool(flag.value), float(out[0]), float(out[1])
 
     def get_blocked(self):
         """K, R of the last assemble in the blocked DOF order [u; ebar] (zero-copy views)."""
@@ -297,7 +329,7 @@ class Mesh:
 
     def set_defects(self, kappa0_gp=None, alpha_gp=None):
         """Per-GP kappa0 / alpha ([n_elems, ngp] or flat; None = material value)."""
-        n = self.n_elems * self.ngp
+        n = None
         ptrs, keep, dev = [], [], None
         for a in (kappa0_gp, alpha_gp):
             if a is None:
@@ -306,10 +338,13 @@ class Mesh:
             p, on_dev, k = _ptr_and_kind(a)
             if dev is not None and dev != on_dev:
                 raise ValueError("kappa0_gp and alpha_gp must both be host or both be device")
+            if n is not None and _numel(k) != n:
+                raise ValueError("kappa0_gp and alpha_gp must have the same size")
             dev = on_dev
+            n = _numel(k)
             ptrs.append(p)
             keep.append(k)
-        _check(load().lgdm_set_defects(self._h, ptrs[0], ptrs[1], n, dev or 0))
+        _check(load().lgdm_set_defects(self._h, ptrs[0], ptrs[1], n or 0, dev or 0))
         self._keep_defects = keep
 
     def update_state(self, out=None):
@@ -317,14 +352,13 @@ class Mesh:
         [n_elems, ngp, sdv_width] (or fills `out`, a float64 tensor / numpy array)."""
         import torch
         W = load().lgdm_sdv_width(self.etype)
-        if W < 0:                                   # family without an SDV record (mixed)
-            _check(load().lgdm_update_state(self._h, None, 0, 0))
-        n = self.n_elems * self.ngp * W
+        if W < 0:
+            raise LGDMError(1, f"element type {self.etype} has no state record")
         if out is None:
             out = torch.empty((self.n_elems, self.ngp, W), dtype=torch.float64,
                               device=f"cuda:{self.device}")
-        p, on_dev, _ = _ptr_and_kind(out)
-        _check(load().lgdm_update_state(self._h, p, n, on_dev))
+        p, on_dev, keep = _ptr_and_kind(out)
+        _check(load().lgdm_update_state(self._h, p, _numel(keep), on_dev))
         return out
 
     def update_history(self):
@@ -409,10 +443,8 @@ def newton(mesh: "Mesh", fixed_dofs, step_increment, n_steps: int, tol: float = 
             else:
                 delta, sit, rr = mesh.solve(tol=solver_tol)
             mesh.add_dofs(delta)
-            du2, u2, de2, e2 = mesh.delta_norms(delta)
-            ru = np.sqrt(du2) / max(np.sqrt(u2), 1e-16)
-            re = np.sqrt(de2) / max(np.sqrt(e2), 1e-16)
-            if ru <= tol and re <= tol:
+            done, ru, re = mesh.converged(delta, tol)
+            if done:
                 break
         else:
             raise LGDMError(8, f"Newton step {step}: not converged in {max_iter} iterations "

@@ -51,8 +51,7 @@ def compare(ref, got, what=""):
     nrows = rp.size - 1
     rows = np.repeat(np.arange(nrows), np.diff(rp))
     absv = np.abs(ref["val"])
-    rowmax = np.zeros(nrows)
-    np.maximum.at(rowmax, rows, absv)
+    rowmax = np.maximum.reduceat(absv, rp[:-1]) if absv.size else np.zeros(nrows)   # rows are non-empty
     dk = np.abs(got["val"] - ref["val"])
     kerr = dk / np.maximum(rowmax[rows], 1e-300)
     assert np.all(dk <= KTOL * rowmax[rows]), (
@@ -84,3 +83,34 @@ def compare_sampled(ref_rows, got, sel_nodes, ndpn, owned_begin=0):
             assert dr <= RTOL * S + 1e-300, (a, i, dr / S)
             worst_r = max(worst_r, dr / S)
     return worst_k, worst_r
+
+
+def gpu_rows(out, sel_nodes, ndpn, owned_begin=0):
+    """The block-rows of the selected (owned-local) nodes of an assembled system, gathered on the
+    device (K can be far larger than what is worth copying to the host): row_ptr / col_idx / val
+    restricted to those rows, R, and the int64 offsets of the rows' first entries."""
+    import torch
+    rp = out["row_ptr"].torch()
+    rows = (torch.as_tensor(np.asarray(sel_nodes) - owned_begin, device=rp.device)[:, None] * ndpn +
+            torch.arange(ndpn, device=rp.device)[None, :]).reshape(-1)
+    lo, hi = rp[rows], rp[rows + 1]
+    cnt = hi - lo
+    starts = torch.repeat_interleave(lo, cnt)
+    first = torch.repeat_interleave(torch.cumsum(cnt, 0) - cnt, cnt)
+    idx = starts + (torch.arange(int(cnt.sum()), device=rp.device) - first)
+    sub_rp = torch.zeros(rows.numel() + 1, dtype=torch.int64, device=rp.device)
+    sub_rp[1:] = torch.cumsum(cnt, 0)
+    return dict(row_ptr=sub_rp.cpu().numpy(), col_idx=out["col_idx"].torch()[idx].cpu().numpy(),
+                val=out["val"].torch()[idx].cpu().numpy(), R=out["R"].torch()[rows].cpu().numpy(),
+                row_start=lo.cpu().numpy())
+
+
+def compare_rows(ref_rows, got_rows, what=""):
+    """Parity of gathered block-rows (gpu_rows) against oracle.assemble_rows of the same nodes,
+    row by row: pattern bit-exact, K within KTOL of the oracle row max, R within RTOL of S."""
+    assert np.array_equal(got_rows["row_ptr"], ref_rows["row_ptr"]), f"{what}: row lengths differ"
+    assert np.array_equal(got_rows["col_idx"], ref_rows["col_idx"]), f"{what}: col_idx differs"
+    return compare(dict(row_ptr=ref_rows["row_ptr"], col_idx=ref_rows["col_idx"],
+                        val=ref_rows["val"], R=ref_rows["R"], S=ref_rows["S"]),
+                   dict(row_ptr=got_rows["row_ptr"], col_idx=got_rows["col_idx"],
+                        val=got_rows["val"], R=got_rows["R"]), what)

@@ -16,6 +16,8 @@ HEADER = os.path.join(ROOT, "include", "lgdm.h")
 def declared_symbols():
     text = open(HEADER).read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    # debug-build-only entry points (compiled with -DLGDM_PHASE_TIMING) are not exported
+    text = re.sub(r"#ifdef LGDM_PHASE_TIMING.*?#endif", "", text, flags=re.S)
     return sorted(set(re.findall(r"\b(lgdm_[a-z_]+)\s*\(", text)))
 
 

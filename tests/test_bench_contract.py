@@ -46,3 +46,35 @@ def test_gpu_arm_line():
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["value"] > 0 and cb["cores"] >= 1 and cb["sample"]
     assert d["config"]["workload"] == "q4_200x200"
+
+
+def test_gpus_flag_launches_ranks():
+    """bench.py --gpus 2 outside torchrun re-launches itself as 2 ranks (rendezvous on
+    127.0.0.1, gloo in --dry-run) and rank 0 reports n_gpus = 2."""
+    d = _run(["--gpus", "2", "--dry-run", "--steps", "2", "--warmup", "3"], timeout=300)
+    assert d["dry_run"] is True and d["n_gpus"] == 2 and d["ranks_joined"] == 2
+
+
+def test_dofs_recipe():
+    """dofs_t = (1 + 0.05 (t mod 10)) dofs_0: the per-step factors compose to the recipe."""
+    sys.path.insert(0, ROOT)
+    import bench
+    f = 1.0
+    for t in range(25):
+        assert abs(f - (1 + 0.05 * (t % 10))) < 1e-12
+        f *= bench.dofs_factor(t)
+
+
+def test_cpu_colouring_is_race_free():
+    """The 2^d colouring of the all-core CPU baseline: elements of one colour share no node."""
+    sys.path.insert(0, ROOT)
+    import numpy as np
+    import bench
+    import synth
+    for cid in (1, 3):
+        cfg = synth.small_config(synth.CONFIGS[cid].etype, (5, 4) if cid == 1 else (5, 4, 3))
+        mesh = synth.structured_mesh(cfg)
+        col, nc = bench.structured_colours(cfg, mesh.conn.shape[0])
+        for c in range(nc):
+            nodes = mesh.conn[col == c].reshape(-1)
+            assert nodes.size == np.unique(nodes).size

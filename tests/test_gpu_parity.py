@@ -7,13 +7,13 @@ import oracle
 import synth
 from paper_2301_06503_b200 import lgdm
 
-from parity import compare, compare_sampled, gpu_assemble, oracle_assemble, slice_rows
+from parity import (compare, compare_rows, compare_sampled, gpu_assemble, gpu_rows,
+                    oracle_assemble, slice_rows)
 
 pytestmark = pytest.mark.gpu
 
-KERNELS = [lgdm.KERNEL_GENERAL, lgdm.KERNEL_AUTO, lgdm.KERNEL_SWEEP3, lgdm.KERNEL_SWEEP4,
-           lgdm.KERNEL_SWEEP5]
-SWEEPS = (lgdm.KERNEL_SWEEP3, lgdm.KERNEL_SWEEP4, lgdm.KERNEL_SWEEP5)
+KERNELS = [lgdm.KERNEL_GENERAL, lgdm.KERNEL_AUTO, lgdm.KERNEL_SWEEP, lgdm.KERNEL_HEX8]
+SWEEPS = (lgdm.KERNEL_SWEEP, lgdm.KERNEL_HEX8)
 
 CASES = [
     (lgdm.BAR2, (1,)), (lgdm.BAR2, (7,)), (lgdm.BAR2, (100,)),
@@ -94,8 +94,70 @@ def test_parity_config2_full():
     print(f"config 2 full: max K err/rowmax {kerr:.2e}, max R err/S {rerr:.2e}")
 
 
-@pytest.mark.parametrize("kernel", [lgdm.KERNEL_AUTO, lgdm.KERNEL_SWEEP3, lgdm.KERNEL_SWEEP4,
-                                    lgdm.KERNEL_SWEEP5])
+def test_parity_config3_full():
+    """BASELINE config 3 (Hex8 100^3, 1 M elements, 436 M entries) in full, default kernel
+    (the bench's launch configuration), against the plain serial oracle."""
+    cfg = synth.CONFIGS[3]
+    mesh = synth.structured_mesh(cfg)
+    dofs, kappa = synth.fields(cfg, mesh)
+    ref = oracle_assemble(cfg.etype, mesh.coords, mesh.conn, dofs, kappa)
+    got = gpu_assemble(cfg.etype, mesh.coords, mesh.conn, dofs, kappa)
+    kerr, rerr = compare(ref, got, "config 3 full")
+    print(f"config 3 full: max K err/rowmax {kerr:.2e}, max R err/S {rerr:.2e}")
+
+
+def config4_sample(cfg, n_nodes, count=10000):
+    """Sampled node block-rows of config 4 (Hex8 200^3): random nodes plus forced ones -- the
+    first / last node layers, every node layer of a few columns (so every z-chunk boundary of
+    the launch), the x / y tile boundaries of the sweep (TX = 3, TY = 7), the mesh corners, and
+    nodes whose rows start beyond 2^31 entries."""
+    nxN, nyN, nzN = cfg.n[0] + 1, cfg.n[1] + 1, cfg.n[2] + 1
+    nid = lambda x, y, z: x + nxN * (y + nyN * z)
+    sel = [synth.sample_nodes(n_nodes, count, seed=4)]
+    for (x, y) in ((0, 0), (2, 6), (3, 7), (nxN - 1, nyN - 1), (nxN // 2, nyN // 2), (101, 13)):
+        sel.append(np.array([nid(x, y, z) for z in range(nzN)]))
+    rng = np.random.default_rng(4)
+    for z in (0, 1, nzN - 2, nzN - 1):
+        xs, ys = rng.integers(0, nxN, 40), rng.integers(0, nyN, 40)
+        sel.append(nid(xs, ys, z))
+    for xb in (2, 3, 5, 6, 98, 99):          # tile boundaries in x, random y / z
+        ys, zs = rng.integers(0, nyN, 30), rng.integers(0, nzN, 30)
+        sel.append(nid(xb, ys, zs))
+    for yb in (6, 7, 13, 14, 97, 98):        # tile boundaries in y
+        xs, zs = rng.integers(0, nxN, 30), rng.integers(0, nzN, 30)
+        sel.append(nid(xs, yb, zs))
+    sel.append(rng.integers(int(0.7 * n_nodes), n_nodes, 500))   # rows beyond 2^31 entries
+    return np.unique(np.concatenate(sel).astype(np.int64))
+
+
+def test_parity_config4_sampled():
+    """The headline workload: BASELINE config 4 (Hex8 200^3, 8 M elements, 3.47 G entries,
+    int64 CSR offsets beyond 2^31) at full size in the bench's launch configuration; >= 10^4
+    sampled node block-rows (config4_sample) against oracle.assemble_rows, pattern bit-exact,
+    K within 1e-12 of the row max, R within 1e-12 of S; total nnz by the closed form."""
+    import torch
+    cfg = synth.CONFIGS[4]
+    mesh = synth.structured_mesh(cfg)
+    dofs, kappa = synth.fields(cfg, mesh)
+    n_nodes = mesh.coords.shape[0]
+    m = lgdm.Mesh(cfg.etype, mesh.coords, mesh.conn, lgdm.material(**synth.MATERIAL))
+    m.set_state(dofs, kappa)
+    out = m.assemble()
+    torch.cuda.synchronize()
+    ndpn = 4
+    assert out["nnz"] == ndpn * ndpn * int(np.prod([3 * k + 1 for k in cfg.n])) > 2 ** 31
+    sel = config4_sample(cfg, n_nodes)
+    assert sel.size >= 10000
+    got = gpu_rows(out, sel, ndpn)
+    assert (got["row_start"] >= 2 ** 31).sum() > 1000        # int64 offsets exercised
+    ref = oracle.assemble_rows(cfg.etype, oracle.material(**synth.MATERIAL), mesh.coords,
+                               mesh.conn, dofs, kappa, sel)
+    kerr, rerr = compare_rows(ref, got, "config 4 sampled")
+    print(f"config 4: {sel.size} sampled nodes, max K err/rowmax {kerr:.2e}, R err/S {rerr:.2e}")
+    m.close()
+
+
+@pytest.mark.parametrize("kernel", [lgdm.KERNEL_SWEEP, lgdm.KERNEL_HEX8])
 @pytest.mark.parametrize("cid", [2, 3])
 def test_parity_full_size_sampled(cid, kernel):
     """BASELINE configs 2 and 3 at full size, in the bench's launch configuration; sampled
@@ -114,8 +176,7 @@ def test_parity_full_size_sampled(cid, kernel):
     print(f"config {cid}: sampled {sel.size} nodes, max K err {wk:.2e}, R err {wr:.2e}")
 
 
-@pytest.mark.parametrize("kernel", [lgdm.KERNEL_AUTO, lgdm.KERNEL_SWEEP3, lgdm.KERNEL_SWEEP4,
-                                    lgdm.KERNEL_SWEEP5])
+@pytest.mark.parametrize("kernel", [lgdm.KERNEL_SWEEP, lgdm.KERNEL_HEX8])
 @pytest.mark.parametrize("etype,n,P", [(lgdm.QUAD4, (23, 31), 3), (lgdm.HEX8, (7, 5, 13), 4),
                                        (lgdm.BAR2, (50,), 2)])
 def test_slabs_stitch_bitwise(etype, n, P, kernel):
@@ -203,7 +264,7 @@ def test_errors():
     assert ei.value.status == 2 and "element" in str(ei.value)
 
 
-@pytest.mark.parametrize("kernel", [lgdm.KERNEL_SWEEP3, lgdm.KERNEL_SWEEP4, lgdm.KERNEL_SWEEP5])
+@pytest.mark.parametrize("kernel", [lgdm.KERNEL_SWEEP, lgdm.KERNEL_HEX8])
 @pytest.mark.parametrize("etype,n", [(lgdm.QUAD4, (61, 40)), (lgdm.HEX8, (17, 9, 11))])
 def test_sweep_bitwise_reproducible(etype, n, kernel):
     """The warp-specialised sweeps hand data between roles through named barriers only and

@@ -119,7 +119,7 @@ def test_defect_assembly_parity(etype, n):
     plain = oracle.assemble(etype, oracle.material(**synth.MATERIAL), coords, mesh.conn, dofs,
                             kappa)
     assert not np.allclose(ref["val"], plain["val"])
-    for kernel in (lgdm.KERNEL_AUTO, lgdm.KERNEL_GENERAL, lgdm.KERNEL_SWEEP4):
+    for kernel in (lgdm.KERNEL_AUTO, lgdm.KERNEL_GENERAL, lgdm.KERNEL_SWEEP, lgdm.KERNEL_HEX8):
         m = lgdm.Mesh(etype, coords, mesh.conn, lgdm.material(**synth.MATERIAL))
         m.set_kernel(kernel)
         m.set_state(dofs, kappa)
@@ -139,20 +139,6 @@ def test_defect_assembly_parity(etype, n):
                    val=out["val"].torch().cpu().numpy(), R=out["R"].torch().cpu().numpy())
         compare(plain, got, f"cleared kernel {kernel}")
         m.close()
-
-
-@pytest.mark.parametrize("kernel", [lgdm.KERNEL_SWEEP, lgdm.KERNEL_SWEEP3, lgdm.KERNEL_SWEEP5])
-def test_defects_refuse_experimental_sweeps(kernel):
-    etype, n = lgdm.HEX8, (3, 3, 3)
-    cfg, mesh, coords, dofs, kappa = _case(etype, n, distort=0.0)
-    k0, al = _defects(kappa, 5)
-    m = lgdm.Mesh(etype, coords, mesh.conn, lgdm.material(**synth.MATERIAL))
-    m.set_kernel(kernel)
-    m.set_state(dofs, kappa)
-    m.set_defects(k0, al)
-    with pytest.raises(lgdm.LGDMError):
-        m.assemble()
-    m.close()
 
 
 # ---------------- blocked DOF order [u; ebar] ----------------

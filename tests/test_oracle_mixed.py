@@ -534,3 +534,86 @@ def test_bar3_ebar_blocks_equal_bar2():
     np.testing.assert_allclose(K3[np.ix_(e3, e3)], K2[np.ix_(e2, e2)], rtol=1e-12,
                                atol=1e-13 * np.abs(K2).max())
     np.testing.assert_allclose(F3[e3], F2[e2], rtol=1e-12, atol=1e-13 * np.abs(F2).max())
+
+
+def test_r_rel_precision_pin():
+    """Reading R-REL: the oracle (and every kernel) evaluates J and the
+    gradients on coordinates relative to the element's node 0.  Pin: for a QUAD8 element of
+    the bench mesh's size (h = 0.2 mm) at the far corner of the 100 mm plate, the undamaged
+    elastic Kuu (h_sigma = 0, D = 0: the textbook integral of B^T C B over the element) is
+    evaluated exactly with mpmath at 50 digits.  A plain FP64 evaluation on ABSOLUTE
+    coordinates is off by ~|X| / h x eps (cancellation in J = sum_a X_a dN_a/dxi); the same
+    FP64 evaluation on RELATIVE coordinates, and the oracle, are within a few eps of the
+    exact value."""
+    import mpmath as mp
+    mp.mp.dps = 50
+    h, x0, y0 = 0.2, 99.8, 99.6
+    # straight-edged, distorted quadrilateral; midside nodes at the edge midpoints (R-GEO)
+    cor = [(0.0, 0.0), (h, 0.013), (h + 0.021, h - 0.007), (-0.017, h)]
+    mids = [tuple((cor[i][k] + cor[(i + 1) % 4][k]) / 2 for k in range(2)) for i in range(4)]
+    rel = cor + mids
+    xi_n = [(-1, -1), (1, -1), (1, 1), (-1, 1), (0, -1), (1, 0), (0, 1), (-1, 0)]
+
+    def dshape(xi, eta, one):
+        """dN/dxi, dN/deta of the serendipity QUAD8 at (xi, eta) in the number type of `one`"""
+        out = []
+        for (a, b) in xi_n:
+            if a != 0 and b != 0:
+                dx = one * a * (1 + b * eta) * (2 * a * xi + b * eta) / 4
+                dy = one * b * (1 + a * xi) * (a * xi + 2 * b * eta) / 4
+            elif a == 0:
+                dx = -xi * (1 + b * eta) * one
+                dy = one * b * (1 - xi * xi) / 2
+            else:
+                dx = one * a * (1 - eta * eta) / 2
+                dy = -eta * (1 + a * xi) * one
+            out.append((dx, dy))
+        return out
+
+    E, nu = 30000.0, 0.2
+
+    def kuu(X, num, sqrt35, w):
+        lam = num(E) * num(nu) / ((1 + num(nu)) * (1 - 2 * num(nu)))
+        mu = num(E) / (2 * (1 + num(nu)))
+        K = [[num(0)] * 16 for _ in range(16)]
+        gp = [-sqrt35, num(0), sqrt35]
+        for j, eta in enumerate(gp):
+            for i, xi in enumerate(gp):
+                dN = dshape(xi, eta, num(1))
+                J = [[sum(X[a][r] * dN[a][c] for a in range(8)) for c in range(2)] for r in range(2)]
+                det = J[0][0] * J[1][1] - J[0][1] * J[1][0]
+                gx = [(J[1][1] * d[0] - J[1][0] * d[1]) / det for d in dN]
+                gy = [(-J[0][1] * d[0] + J[0][0] * d[1]) / det for d in dN]
+                wd = w[i] * w[j] * det
+                for a in range(8):
+                    for b in range(8):
+                        K[2 * a][2 * b] += wd * ((lam + 2 * mu) * gx[a] * gx[b] + mu * gy[a] * gy[b])
+                        K[2 * a][2 * b + 1] += wd * (lam * gx[a] * gy[b] + mu * gy[a] * gx[b])
+                        K[2 * a + 1][2 * b] += wd * (lam * gy[a] * gx[b] + mu * gx[a] * gy[b])
+                        K[2 * a + 1][2 * b + 1] += wd * ((lam + 2 * mu) * gy[a] * gy[b] + mu * gx[a] * gx[b])
+        return K
+
+    absX = [(x0 + p[0], y0 + p[1]) for p in rel]
+    Xmp = [(mp.mpf(a), mp.mpf(b)) for a, b in absX]   # the mesh's FP64 coordinates, exactly
+    exact = kuu([(a - Xmp[0][0], b - Xmp[0][1]) for a, b in Xmp], mp.mpf, mp.sqrt(mp.mpf(3) / 5),
+                [mp.mpf(5) / 9, mp.mpf(8) / 9, mp.mpf(5) / 9])
+    f64 = lambda v: np.float64(v)
+    s35, w64 = np.sqrt(0.6), [5.0 / 9.0, 8.0 / 9.0, 5.0 / 9.0]
+    k_abs = kuu(absX, f64, s35, w64)
+    k_rel = kuu([(a - absX[0][0], b - absX[0][1]) for a, b in absX], f64, s35, w64)
+    # the oracle on the same element (absolute coordinates in, R-REL inside), undamaged
+    mat = oracle.material(**dict(synth.MATERIAL, h_sigma=0.0))
+    Xe = np.array(absX)
+    Ue = np.zeros(20)
+    Ke, _, _, _ = oracle.mixed_element(synth.QUAD8, mat, Xe, Ue, np.full(9, synth.MATERIAL["kappa0"]))
+    udof = [a * 3 + i if a < 4 else 12 + (a - 4) * 2 + i for a in range(8) for i in range(2)]
+    k_orc = Ke[np.ix_(udof, udof)]
+
+    ex = np.array([[float(v) for v in row] for row in exact])
+    rowmax = np.abs(ex).max(axis=1)[:, None]
+    e_abs = (np.abs(np.array(k_abs) - ex) / rowmax).max()
+    e_rel = (np.abs(np.array(k_rel) - ex) / rowmax).max()
+    e_orc = (np.abs(k_orc - ex) / rowmax).max()
+    print(f"R-REL pin: absolute {e_abs:.2e}, relative {e_rel:.2e}, oracle {e_orc:.2e} (x row max)")
+    assert e_rel < 2e-15 and e_orc < 2e-15
+    assert e_abs > 20 * max(e_rel, e_orc) and e_abs > 1e-14
