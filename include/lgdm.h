@@ -276,6 +276,18 @@ lgdm_status lgdm_residual_sumsq(lgdm_mesh mesh, double* out2, int on_device);
  * out2 is host memory; synchronises. */
 lgdm_status lgdm_residual_norms(lgdm_mesh mesh, double out2[2]);
 
+/* One pass of the hot path per Newton iteration (Alg. 2 l.4-5 and the
+ * residual check of l.16): lgdm_assemble -> sums of squares of R (u rows, ebar rows)
+ * -> ncclAllReduce of the 2 sums when a communicator is set -> out2 = {||Fu||, ||Fe||} (host)
+ * -> with LGDM_STEP_HISTORY also lgdm_update_history.  With LGDM_STEP_GRAPH the pass is captured
+ * once into a CUDA graph on the mesh stream (per dofs buffer, kernel selector, defect fields,
+ * communicator and flags; at most two kept) and replayed on later calls -- the first call runs
+ * eagerly.  K and R stay on the device (as after lgdm_assemble).  Synchronises the mesh stream.
+ * Errors: those of lgdm_assemble / lgdm_residual_norms / lgdm_update_history; unknown flags ->
+ * INVALID_ARGUMENT; a failed capture -> LGDM_ERR_CUDA. */
+enum { LGDM_STEP_GRAPH = 1, LGDM_STEP_HISTORY = 2 };
+lgdm_status lgdm_step(lgdm_mesh mesh, int flags, double out2[2]);
+
 /* Attach an NCCL communicator (ncclUniqueId bytes from rank 0, e.g. broadcast through
  * torch.distributed).  NCCL is loaded at run time (dlopen libnccl.so.2). */
 lgdm_status lgdm_set_comm(lgdm_mesh mesh, const void* nccl_unique_id, int nranks, int rank);

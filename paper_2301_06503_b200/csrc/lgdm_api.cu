@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdint>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -24,6 +25,7 @@
 #include "lgdm_kernels.cuh"
 #include "lgdm_solver.cuh"
 #include "lgdm_mixed.cuh"
+#include "lgdm_pattern.cuh"
 #include <cusolverSp.h>
 
 using namespace lgdm;
@@ -187,6 +189,19 @@ struct lgdm_mesh_s {
   int kernel = 0;  // 0 auto, 1 general, 2 sweep
   // structured topology (x-fastest lexicographic grid) -> sweep kernels
   bool structured = false;
+  // lgdm_step: instantiated graphs of one hot-path pass, keyed by what the captured kernels read
+  struct StepGraph {
+    cudaGraphExec_t exec = nullptr;
+    const double* dofs = nullptr;
+    const double* k0g = nullptr;
+    const double* alg = nullptr;
+    int kernel = -1, flags = -1;
+    void* comm = nullptr;
+    int64_t launches = 0;
+  } sgraph[2];
+  int sgraph_next = 0;
+  bool step_warm = false;
+  int max_deg = 0;                // largest node degree (neighbours incl. itself), equal order
   int64_t nx = 0, ny = 0, nz = 0;  // local element counts per axis (nz = layers for 3D, ny for 2D)
   int64_t launches = 0;
   ncclComm_t comm = nullptr;
@@ -473,7 +488,8 @@ lgdm_status create_mixed(lgdm_elem_type type, int64_t n_nodes, const double* coo
   };
   lgdm_status s;
   std::vector<int32_t> conn32(size_t(n_elems) * f.nen);
-  for (size_t i = 0; i < conn32.size(); ++i) conn32[i] = int32_t(conn[i]);
+#pragma omp parallel for if (conn32.size() > (size_t(1) << 20))
+  for (int64_t i = 0; i < int64_t(conn32.size()); ++i) conn32[i] = int32_t(conn[i]);
   if ((s = upload(m, &m->coords, coords, size_t(n_nodes) * f.dim)) != LGDM_OK) return bail(s);
   if ((s = upload(m, &m->conn, conn32.data(), conn32.size())) != LGDM_OK) return bail(s);
   if ((s = upload(m, &m->doff, doff.data(), doff.size())) != LGDM_OK) return bail(s);
@@ -641,6 +657,133 @@ template <int T> lgdm_status assemble_mixed(lgdm_mesh m) {
 
 #include "lgdm_sweep.cuh"
 
+namespace {
+
+// SURVEY 8a row A0 on the GPU: node adjacency, CSR row_ptr / base / col_idx and the element ->
+// block-row slot map of the owned nodes (lgdm_pattern.cuh), from the device connectivity.
+lgdm_status build_pattern(lgdm_mesh m, int64_t global_node_offset) {
+  const FamInfo& f = m->f;
+  const int nen = f.nen;
+  const int64_t nn = m->n_nodes, ne = m->n_elems, no = m->n_owned, nsl = ne * nen;
+  if (nsl >= (int64_t(1) << 31)) return fail(LGDM_ERR_UNSUPPORTED, "n_elems * nen >= 2^31");
+  cudaStream_t st = m->stream;
+  // scratch (freed at the end)
+  int32_t *keys = nullptr, *vals = nullptr, *keys2 = nullptr, *adj_slot = nullptr, *counts = nullptr,
+          *nbr = nullptr;
+  int64_t *nadj_ptr = nullptr, *deg = nullptr;
+  int* status = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  lgdm_status rc = LGDM_OK;
+  auto cleanup = [&]() {
+    cudaFree(keys); cudaFree(vals); cudaFree(keys2); cudaFree(adj_slot); cudaFree(counts);
+    cudaFree(nbr); cudaFree(nadj_ptr); cudaFree(deg); cudaFree(status); cudaFree(tmp);
+  };
+#define PCU(call)                                                                         \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess) {                                                              \
+      rc = fail(e_ == cudaErrorMemoryAllocation ? LGDM_ERR_OUT_OF_MEMORY : LGDM_ERR_CUDA,  \
+                "pattern: %s: %s", #call, cudaGetErrorString(e_));                        \
+      cleanup();                                                                          \
+      return rc;                                                                          \
+    }                                                                                     \
+  } while (0)
+  PCU(cudaMalloc(&keys, nsl * 4));
+  PCU(cudaMalloc(&vals, nsl * 4));
+  PCU(cudaMalloc(&keys2, nsl * 4));
+  PCU(cudaMalloc(&adj_slot, nsl * 4));
+  PCU(cudaMalloc(&counts, (nn + 1) * 4));
+  PCU(cudaMalloc(&nadj_ptr, (nn + 1) * 8));
+  PCU(cudaMalloc(&deg, (no + 1) * 8));
+  PCU(cudaMalloc(&status, sizeof(int)));
+  PCU(cudaMemsetAsync(counts, 0, (nn + 1) * 4, st));
+  PCU(cudaMemsetAsync(deg, 0, (no + 1) * 8, st));
+  PCU(cudaMemsetAsync(status, 0, sizeof(int), st));
+  k_adj_keys<<<unsigned((nsl + 255) / 256), 256, 0, st>>>(nsl, m->conn, keys, vals, counts);
+  ++m->launches;
+  // node -> element slots, stable by slot index (= ascending element id)
+  int end_bit = 1;
+  while ((int64_t(1) << end_bit) < nn) ++end_bit;
+  size_t need = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, need, keys, keys2, vals, adj_slot, int(nsl), 0, end_bit, st);
+  tmp_bytes = std::max(tmp_bytes, need);
+  cub::DeviceScan::ExclusiveSum(nullptr, need, counts, nadj_ptr, int(nn + 1), st);
+  tmp_bytes = std::max(tmp_bytes, need);
+  cub::DeviceScan::ExclusiveSum(nullptr, need, deg, deg, int(no + 1), st);
+  tmp_bytes = std::max(tmp_bytes, need);
+  PCU(cudaMalloc(&tmp, tmp_bytes));
+  PCU(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, vals, adj_slot, int(nsl), 0, end_bit, st));
+  PCU(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, counts, nadj_ptr, int(nn + 1), st));
+  m->launches += 4;
+  // pass 1: degrees -> nbr_ptr (exclusive scan in place), base, row_ptr
+  const unsigned pb = unsigned((no + kPatWarps - 1) / kPatWarps);
+  k_pat_degree<<<pb, kPatWarps * 32, 0, st>>>(no, m->own_b, nen, nadj_ptr, adj_slot, m->conn, deg, status);
+  PCU(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, deg, deg, int(no + 1), st));
+  int hstat = 0;
+  int64_t nbr_total = 0, adj_lo = 0, adj_hi = 0;
+  PCU(cudaMemcpyAsync(&hstat, status, sizeof(int), cudaMemcpyDeviceToHost, st));
+  PCU(cudaMemcpyAsync(&nbr_total, deg + no, 8, cudaMemcpyDeviceToHost, st));
+  PCU(cudaMemcpyAsync(&adj_lo, nadj_ptr + m->own_b, 8, cudaMemcpyDeviceToHost, st));
+  PCU(cudaMemcpyAsync(&adj_hi, nadj_ptr + m->own_e, 8, cudaMemcpyDeviceToHost, st));
+  PCU(cudaStreamSynchronize(st));
+  m->launches += 3;
+  if (hstat != 0) {
+    cleanup();
+    return fail(LGDM_ERR_UNSUPPORTED, "%s", (hstat & 1) ? "a node has more than 1024 candidate neighbours"
+                                                        : "a node has more than 255 neighbours");
+  }
+  m->nnz = int64_t(f.ndpn) * f.ndpn * nbr_total;
+  if (dalloc(&m->nbr_ptr, size_t(no + 1)) != cudaSuccess || dalloc(&m->base, size_t(no)) != cudaSuccess ||
+      dalloc(&m->row_ptr, size_t(m->n_rows + 1)) != cudaSuccess ||
+      dalloc(&m->adj_ptr, size_t(no + 1)) != cudaSuccess ||
+      cudaMalloc(&m->adj, size_t(adj_hi - adj_lo) * sizeof(AdjEntry)) != cudaSuccess ||
+      cudaMalloc(&nbr, size_t(nbr_total) * 4) != cudaSuccess) {
+    cleanup();
+    return fail(LGDM_ERR_OUT_OF_MEMORY, "cudaMalloc pattern");
+  }
+  m->device_bytes += (no + 1) * 24 + no * 8 + (m->n_rows + 1) * 8 + (adj_hi - adj_lo) * int64_t(sizeof(AdjEntry));
+  PCU(cudaMemcpyAsync(m->nbr_ptr, deg, (no + 1) * 8, cudaMemcpyDeviceToDevice, st));
+  const unsigned rb = unsigned((no + 1 + 255) / 256);
+  if (f.ndpn == 2) k_pat_rows<2><<<rb, 256, 0, st>>>(no, m->nbr_ptr, m->base, m->row_ptr);
+  else if (f.ndpn == 3) k_pat_rows<3><<<rb, 256, 0, st>>>(no, m->nbr_ptr, m->base, m->row_ptr);
+  else k_pat_rows<4><<<rb, 256, 0, st>>>(no, m->nbr_ptr, m->base, m->row_ptr);
+  k_adj_ptr<<<rb, 256, 0, st>>>(no, nadj_ptr + m->own_b, m->adj_ptr);
+  // pass 2: sorted neighbour lists and adjacency entries
+  k_pat_fill<<<pb, kPatWarps * 32, 0, st>>>(no, m->own_b, nen, nadj_ptr, adj_slot, m->conn,
+                                           m->nbr_ptr, nbr, m->adj);
+  m->launches += 3;
+  if (dalloc(&m->col_idx, size_t(m->nnz)) != cudaSuccess || dalloc(&m->val, size_t(m->nnz)) != cudaSuccess ||
+      dalloc(&m->R, size_t(m->n_rows)) != cudaSuccess) {
+    cleanup();
+    return fail(LGDM_ERR_OUT_OF_MEMORY, "cudaMalloc CSR (nnz=%lld)", (long long)m->nnz);
+  }
+  m->device_bytes += m->nnz * (4 + 8) + m->n_rows * 8;
+  {
+    const unsigned blocks = unsigned((no * 32 + 255) / 256);
+    if (f.ndpn == 2) k_cols<2><<<blocks, 256, 0, st>>>(no, m->nbr_ptr, nbr, m->base, global_node_offset, m->col_idx);
+    else if (f.ndpn == 3) k_cols<3><<<blocks, 256, 0, st>>>(no, m->nbr_ptr, nbr, m->base, global_node_offset, m->col_idx);
+    else k_cols<4><<<blocks, 256, 0, st>>>(no, m->nbr_ptr, nbr, m->base, global_node_offset, m->col_idx);
+    ++m->launches;
+  }
+  // the largest degree sizes the general path's per-warp block-row buffer
+  {
+    std::vector<int64_t> hp(no + 1);
+    // (a host copy of nbr_ptr: one int64 per owned node, read once)
+    PCU(cudaMemcpyAsync(hp.data(), m->nbr_ptr, (no + 1) * 8, cudaMemcpyDeviceToHost, st));
+    PCU(cudaStreamSynchronize(st));
+    int64_t mx = 0;
+    for (int64_t o = 0; o < no; ++o) mx = std::max(mx, hp[o + 1] - hp[o]);
+    m->max_deg = int(mx);
+  }
+  lgdm_status cs = check_launch(m, "pattern");
+  cleanup();
+#undef PCU
+  return cs;
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* lgdm_last_error(void) { return g_err.c_str(); }
@@ -674,10 +817,15 @@ lgdm_status lgdm_create_mesh(lgdm_elem_type type, int64_t n_nodes, const double*
     return fail(LGDM_ERR_INVALID_ARGUMENT, "global dof count exceeds int32 col_idx");
   std::string why;
   if (!validate_material(mat, &why)) return fail(LGDM_ERR_INVALID_ARGUMENT, "material: %s", why.c_str());
-  for (int64_t i = 0; i < n_elems * f.nen; ++i)
-    if (conn[i] < 0 || conn[i] >= n_nodes)
-      return fail(LGDM_ERR_INVALID_ARGUMENT, "conn[%lld] = %lld out of range", (long long)i,
-                  (long long)conn[i]);
+  {
+    int64_t bad_i = INT64_MAX;   // smallest offending index (deterministic message)
+#pragma omp parallel for reduction(min : bad_i) if (n_elems * f.nen > (1 << 20))
+    for (int64_t i = 0; i < n_elems * f.nen; ++i)
+      if (conn[i] < 0 || conn[i] >= n_nodes) bad_i = std::min(bad_i, i);
+    if (bad_i != INT64_MAX)
+      return fail(LGDM_ERR_INVALID_ARGUMENT, "conn[%lld] = %lld out of range", (long long)bad_i,
+                  (long long)conn[bad_i]);
+  }
 
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -711,7 +859,8 @@ lgdm_status lgdm_create_mesh(lgdm_elem_type type, int64_t n_nodes, const double*
 
   // ---- coordinates and connectivity (int32 local ids on device) ----
   std::vector<int32_t> conn32(size_t(n_elems) * f.nen);
-  for (size_t i = 0; i < conn32.size(); ++i) conn32[i] = int32_t(conn[i]);
+#pragma omp parallel for if (conn32.size() > (size_t(1) << 20))
+  for (int64_t i = 0; i < int64_t(conn32.size()); ++i) conn32[i] = int32_t(conn[i]);
   if ((s = upload(m, &m->coords, coords, size_t(n_nodes) * f.dim)) != LGDM_OK) return bail(s);
   if ((s = upload(m, &m->conn, conn32.data(), conn32.size())) != LGDM_OK) return bail(s);
 
@@ -733,113 +882,19 @@ lgdm_status lgdm_create_mesh(lgdm_elem_type type, int64_t n_nodes, const double*
     return bail(fail(LGDM_ERR_INVERTED_ELEMENT, "det J <= 0 in element %lld at Gauss point %d",
                      (long long)(hbad / f.ngp), int(hbad % f.ngp)));
 
-  // ---- pattern (reading R-PAT): neighbours of owned nodes, row_ptr, base, element maps ----
-  // node -> adjacent elements (ascending e) by counting sort
-  std::vector<int64_t> nadj(n_nodes + 1, 0);
-  for (int64_t i = 0; i < n_elems * f.nen; ++i) ++nadj[conn[i] + 1];
-  for (int64_t n = 0; n < n_nodes; ++n) nadj[n + 1] += nadj[n];
-  std::vector<int32_t> adj_e(nadj[n_nodes]);
-  std::vector<uint8_t> adj_a(nadj[n_nodes]);
-  {
-    std::vector<int64_t> fillp(nadj.begin(), nadj.end() - 1);
-    for (int64_t e = 0; e < n_elems; ++e)
-      for (int a = 0; a < f.nen; ++a) {
-        const int64_t n = conn[e * f.nen + a];
-        adj_e[fillp[n]] = int32_t(e);
-        adj_a[fillp[n]] = uint8_t(a);
-        ++fillp[n];
-      }
-  }
-  const int64_t no = m->n_owned;
-  std::vector<int64_t> nbr_ptr(no + 1, 0);
-  std::vector<int32_t> nbr(size_t(no) * f.maxdeg);
-  std::vector<int32_t> deg(no);
-#pragma omp parallel for schedule(static)
-  for (int64_t o = 0; o < no; ++o) {
-    const int64_t n = o + owned_node_begin;
-    int32_t tmp[64 * 8];
-    int cnt = 0;
-    for (int64_t k = nadj[n]; k < nadj[n + 1]; ++k)
-      for (int b = 0; b < f.nen; ++b) tmp[cnt++] = int32_t(conn[int64_t(adj_e[k]) * f.nen + b]);
-    std::sort(tmp, tmp + cnt);
-    cnt = int(std::unique(tmp, tmp + cnt) - tmp);
-    deg[o] = cnt;
-    std::copy(tmp, tmp + cnt, nbr.begin() + o * f.maxdeg);
-  }
-  for (int64_t o = 0; o < no; ++o) nbr_ptr[o + 1] = nbr_ptr[o] + deg[o];
-  std::vector<int32_t> nbr_c(nbr_ptr[no]);
-#pragma omp parallel for schedule(static)
-  for (int64_t o = 0; o < no; ++o)
-    std::copy(nbr.begin() + o * f.maxdeg, nbr.begin() + o * f.maxdeg + deg[o], nbr_c.begin() + nbr_ptr[o]);
-  std::vector<int64_t> base(no), row_ptr(m->n_rows + 1);
-  int64_t pos = 0;
-  for (int64_t o = 0; o < no; ++o) {
-    base[o] = pos;
-    for (int i = 0; i < f.ndpn; ++i) {
-      row_ptr[o * f.ndpn + i] = pos;
-      pos += int64_t(deg[o]) * f.ndpn;
-    }
-  }
-  row_ptr[m->n_rows] = pos;
-  m->nnz = pos;
-  // element -> CSR map for owned nodes (general path)
-  std::vector<int64_t> adj_ptr(no + 1, 0);
-  for (int64_t o = 0; o < no; ++o) {
-    const int64_t n = o + owned_node_begin;
-    adj_ptr[o + 1] = adj_ptr[o] + (nadj[n + 1] - nadj[n]);
-  }
-  std::vector<AdjEntry> adj(adj_ptr[no]);
-#pragma omp parallel for schedule(static)
-  for (int64_t o = 0; o < no; ++o) {
-    const int64_t n = o + owned_node_begin;
-    const int32_t* nb = nbr_c.data() + nbr_ptr[o];
-    const int dg = deg[o];
-    for (int64_t k = nadj[n]; k < nadj[n + 1]; ++k) {
-      AdjEntry en{};
-      en.e = adj_e[k];
-      en.aloc = adj_a[k];
-      for (int b = 0; b < f.nen; ++b) {
-        const int32_t nbn = int32_t(conn[int64_t(en.e) * f.nen + b]);
-        en.slot[b] = uint8_t(std::lower_bound(nb, nb + dg, nbn) - nb);
-      }
-      adj[adj_ptr[o] + (k - nadj[n])] = en;
-    }
-  }
-  if ((s = upload(m, &m->row_ptr, row_ptr.data(), row_ptr.size())) != LGDM_OK) return bail(s);
-  if ((s = upload(m, &m->base, base.data(), base.size())) != LGDM_OK) return bail(s);
-  if ((s = upload(m, &m->nbr_ptr, nbr_ptr.data(), nbr_ptr.size())) != LGDM_OK) return bail(s);
-  if ((s = upload(m, &m->adj_ptr, adj_ptr.data(), adj_ptr.size())) != LGDM_OK) return bail(s);
-  if ((s = upload(m, &m->adj, adj.data(), adj.size())) != LGDM_OK) return bail(s);
-  int32_t* nbr_d = nullptr;
-  if (cudaMalloc(&nbr_d, nbr_c.size() * sizeof(int32_t)) != cudaSuccess)
-    return bail(fail(LGDM_ERR_OUT_OF_MEMORY, "cudaMalloc nbr"));
-  cudaMemcpyAsync(nbr_d, nbr_c.data(), nbr_c.size() * sizeof(int32_t), cudaMemcpyHostToDevice, m->stream);
-  if (dalloc(&m->col_idx, size_t(m->nnz)) != cudaSuccess || dalloc(&m->val, size_t(m->nnz)) != cudaSuccess ||
-      dalloc(&m->R, size_t(m->n_rows)) != cudaSuccess) {
-    cudaFree(nbr_d);
-    return bail(fail(LGDM_ERR_OUT_OF_MEMORY, "cudaMalloc CSR (nnz=%lld)", (long long)m->nnz));
-  }
-  m->device_bytes += m->nnz * (4 + 8) + m->n_rows * 8;
-  {
-    const unsigned blocks = unsigned((no * 32 + 255) / 256);
-    if (f.ndpn == 2) k_cols<2><<<blocks, 256, 0, m->stream>>>(no, m->nbr_ptr, nbr_d, m->base, global_node_offset, m->col_idx);
-    else if (f.ndpn == 3) k_cols<3><<<blocks, 256, 0, m->stream>>>(no, m->nbr_ptr, nbr_d, m->base, global_node_offset, m->col_idx);
-    else k_cols<4><<<blocks, 256, 0, m->stream>>>(no, m->nbr_ptr, nbr_d, m->base, global_node_offset, m->col_idx);
-    if ((s = check_launch(m, "k_cols")) != LGDM_OK) { cudaFree(nbr_d); return bail(s); }
-  }
+  // ---- pattern (reading R-PAT) and element maps, built on the GPU (lgdm_pattern.cuh) ----
+  if ((s = build_pattern(m, global_node_offset)) != LGDM_OK) return bail(s);
   // ---- state, reductions ----
   if (dalloc(&m->dofs, size_t(n_nodes) * f.ndpn) != cudaSuccess ||
       dalloc(&m->kappa, size_t(n_elems) * f.ngp) != cudaSuccess ||
       dalloc(&m->sumsq_part, size_t(2 * kSumBlocks)) != cudaSuccess ||
       dalloc(&m->sumsq_out, 2) != cudaSuccess ||
       cudaMallocHost(&m->host_pinned, 2 * sizeof(double)) != cudaSuccess) {
-    cudaFree(nbr_d);
     return bail(fail(LGDM_ERR_OUT_OF_MEMORY, "cudaMalloc state"));
   }
   m->device_bytes += (n_nodes * f.ndpn + n_elems * f.ngp) * 8;
   m->structured = detect_structured(type, n_nodes, n_elems, conn, &m->nx, &m->ny, &m->nz);
   ce = cudaStreamSynchronize(m->stream);
-  cudaFree(nbr_d);
   if (ce != cudaSuccess) return bail(fail(LGDM_ERR_CUDA, "create: %s", cudaGetErrorString(ce)));
   *out = m;
   return LGDM_OK;
@@ -907,8 +962,12 @@ template <int D> lgdm_status assemble_general(lgdm_mesh m) {
   lgdm_status s = check_launch(m, "k_elem_blocks");
   if (s != LGDM_OK) return s;
   constexpr int WPB = 8;
-  k_gather<D, WPB><<<unsigned((m->n_owned + WPB - 1) / WPB), WPB * 32, 0, m->stream>>>(
-      m->n_owned, m->adj_ptr, m->adj, m->nbr_ptr, m->base, m->scratchK, m->scratchF, m->val, m->R);
+  // per-warp block-row buffer sized by the mesh's largest degree (any connectivity)
+  const size_t gsm = sizeof(double) * WPB * F::NDPN * size_t(m->max_deg) * F::NDPN;
+  if (gsm > 48 * 1024) CU(set_smem_attr(k_gather<D, WPB>, gsm, m->device));
+  k_gather<D, WPB><<<unsigned((m->n_owned + WPB - 1) / WPB), WPB * 32, gsm, m->stream>>>(
+      m->n_owned, m->adj_ptr, m->adj, m->nbr_ptr, m->base, m->scratchK, m->scratchF, m->max_deg,
+      m->val, m->R);
   return check_launch(m, "k_gather");
 }
 
@@ -1410,6 +1469,74 @@ lgdm_status lgdm_residual_norms(lgdm_mesh m, double out2[2]) {
   return LGDM_OK;
 }
 
+// one hot-path pass on the mesh stream (no host synchronisation inside)
+static lgdm_status step_enqueue(lgdm_mesh m, bool hist) {
+  lgdm_status s = lgdm_assemble(m, nullptr, nullptr);
+  if (s != LGDM_OK) return s;
+  if ((s = lgdm_residual_sumsq(m, m->sumsq_out, 1)) != LGDM_OK) return s;
+  if (m->comm) {
+    ncclResult_t r = g_nccl.allReduce(m->sumsq_out, m->sumsq_out, 2, ncclFloat64, ncclSum, m->comm, m->stream);
+    if (r != ncclSuccess)
+      return fail(LGDM_ERR_NCCL, "ncclAllReduce: %s", g_nccl.getErrorString ? g_nccl.getErrorString(r) : "?");
+  }
+  CU(cudaMemcpyAsync(m->host_pinned, m->sumsq_out, 2 * sizeof(double), cudaMemcpyDeviceToHost, m->stream));
+  if (hist) return lgdm_update_history(m);
+  return LGDM_OK;
+}
+
+lgdm_status lgdm_step(lgdm_mesh m, int flags, double out2[2]) {
+  if (!m || !out2) return fail(LGDM_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (flags & ~3) return fail(LGDM_ERR_INVALID_ARGUMENT, "unknown step flags %d", flags);
+  if (!m->have_state || !m->have_kappa) return fail(LGDM_ERR_INVALID_STATE, "step before set_state");
+  CU(cudaSetDevice(m->device));
+  const bool use_graph = flags & LGDM_STEP_GRAPH, hist = flags & LGDM_STEP_HISTORY;
+  lgdm_status s;
+  if (!use_graph || !m->step_warm) {
+    // eager pass; the first one also allocates any lazily created scratch, so a later capture
+    // records kernels and copies only
+    if ((s = step_enqueue(m, hist)) != LGDM_OK) return s;
+    m->step_warm = true;
+  } else {
+    lgdm_mesh_s::StepGraph* g = nullptr;
+    for (auto& c : m->sgraph)
+      if (c.exec && c.dofs == m->dofs && c.k0g == m->k0g && c.alg == m->alg && c.kernel == m->kernel &&
+          c.flags == flags && c.comm == (void*)m->comm)
+        g = &c;
+    if (!g) {
+      g = &m->sgraph[m->sgraph_next];
+      m->sgraph_next ^= 1;
+      if (g->exec) cudaGraphExecDestroy(g->exec), g->exec = nullptr;
+      cudaGraph_t graph = nullptr;
+      CU(cudaStreamBeginCapture(m->stream, cudaStreamCaptureModeThreadLocal));
+      const int64_t l0 = m->launches;
+      s = step_enqueue(m, hist);
+      const cudaError_t ec = cudaStreamEndCapture(m->stream, &graph);
+      if (s != LGDM_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return s;
+      }
+      if (ec != cudaSuccess) return fail(LGDM_ERR_CUDA, "step capture: %s", cudaGetErrorString(ec));
+      const cudaError_t ei = cudaGraphInstantiate(&g->exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ei != cudaSuccess) return fail(LGDM_ERR_CUDA, "step graph instantiate: %s", cudaGetErrorString(ei));
+      g->launches = m->launches - l0;
+      m->launches = l0;
+      g->dofs = m->dofs;
+      g->k0g = m->k0g;
+      g->alg = m->alg;
+      g->kernel = m->kernel;
+      g->flags = flags;
+      g->comm = (void*)m->comm;
+    }
+    CU(cudaGraphLaunch(g->exec, m->stream));
+    m->launches += g->launches;
+  }
+  CU(cudaStreamSynchronize(m->stream));
+  out2[0] = std::sqrt(m->host_pinned[0]);
+  out2[1] = std::sqrt(m->host_pinned[1]);
+  return LGDM_OK;
+}
+
 lgdm_status lgdm_set_comm(lgdm_mesh m, const void* uid, int nranks, int rank) {
   if (!m || !uid || nranks < 1 || rank < 0 || rank >= nranks)
     return fail(LGDM_ERR_INVALID_ARGUMENT, "bad communicator arguments");
@@ -1490,6 +1617,8 @@ void lgdm_destroy(lgdm_mesh m) {
   if (!m) return;
   cudaSetDevice(m->device);
   if (m->stream) cudaStreamSynchronize(m->stream);
+  for (auto& g : m->sgraph)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
   if (m->comm && g_nccl.loaded) g_nccl.commDestroy(m->comm);
   void* ptrs[] = {m->coords, m->conn, m->dofs, m->kappa, m->row_ptr, m->col_idx, m->val, m->R,
                   m->nbr_ptr, m->base, m->adj_ptr, m->adj, m->scratchK, m->scratchF,

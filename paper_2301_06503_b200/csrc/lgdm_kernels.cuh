@@ -145,17 +145,16 @@ template <int D, int WPB>
 __global__ void __launch_bounds__(WPB * 32)
 k_gather(int64_t n_owned, const int64_t* __restrict__ adj_ptr, const AdjEntry* __restrict__ adj,
          const int64_t* __restrict__ nbr_ptr, const int64_t* __restrict__ base,
-         const double* __restrict__ Ke_in, const double* __restrict__ Fe_in,
+         const double* __restrict__ Ke_in, const double* __restrict__ Fe_in, int max_deg,
          double* __restrict__ val, double* __restrict__ Rv) {
   using F = Fam<D>;
-  constexpr int MAXW = F::NDPN * (D == 1 ? 3 : (D == 2 ? 9 : 27));
-  __shared__ double buf[WPB][F::NDPN * MAXW];
+  extern __shared__ double gbuf[];   // [WPB][NDPN x max_deg NDPN]: sized by the largest degree
   const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t n = int64_t(blockIdx.x) * WPB + wl;
   if (n >= n_owned) return;
   const int deg = int(nbr_ptr[n + 1] - nbr_ptr[n]);
   const int W = deg * F::NDPN;
-  double* B = buf[wl];
+  double* B = gbuf + size_t(wl) * F::NDPN * max_deg * F::NDPN;
   for (int idx = lane; idx < F::NDPN * W; idx += 32) B[idx] = 0.0;
   double r = 0.0;
   __syncwarp();

@@ -32,7 +32,7 @@ EXPORTS = ["lgdm_create_mesh", "lgdm_set_state", "lgdm_assemble", "lgdm_update_h
            "lgdm_scale_dofs", "lgdm_set_kernel", "lgdm_get_info", "lgdm_launch_count",
            "lgdm_last_error", "lgdm_destroy", "lgdm_sdv_width", "lgdm_set_defects",
            "lgdm_update_state", "lgdm_get_blocked", "lgdm_apply_dirichlet", "lgdm_solve",
-           "lgdm_add_dofs", "lgdm_delta_norms", "lgdm_delta_ratios", "lgdm_reaction", "lgdm_solve_direct",
+           "lgdm_add_dofs", "lgdm_delta_norms", "lgdm_delta_ratios", "lgdm_step", "lgdm_reaction", "lgdm_solve_direct",
            "lgdm_dof_offsets", "lgdm_prefetch_dofs", "lgdm_set_state_prefetched",
            "lgdm_create_mesh_mixed"]
 
@@ -104,6 +104,7 @@ def load() -> C.CDLL:
     L.lgdm_add_dofs.argtypes = [vp, vp, C.c_double]
     L.lgdm_delta_norms.argtypes = [vp, vp, dp]
     L.lgdm_delta_ratios.argtypes = [vp, vp, C.c_double, dp, C.POINTER(C.c_int)]
+    L.lgdm_step.argtypes = [vp, C.c_int, dp]
     L.lgdm_reaction.argtypes = [vp, i64, vp, dp]
     L.lgdm_solve_direct.argtypes = [vp, vp, C.POINTER(C.c_int)]
     L.lgdm_dof_offsets.argtypes = [vp, vp, i64]
@@ -371,6 +372,15 @@ class Mesh:
             return None
         out = np.zeros(2)
         _check(load().lgdm_residual_sumsq(self._h, out.ctypes.data, 0))
+        return out
+
+    def step(self, graph: bool = True, history: bool = False):
+        """One hot-path pass (lgdm_step): assemble, residual norms (allreduce across ranks),
+        optionally the history commit; CUDA-graph replay after the first call.  Returns the
+        norms {||Fu||, ||Fe||}."""
+        out = np.zeros(2)
+        _check(load().lgdm_step(self._h, (1 if graph else 0) | (2 if history else 0),
+                                out.ctypes.data_as(C.POINTER(C.c_double))))
         return out
 
     def residual_norms(self):
