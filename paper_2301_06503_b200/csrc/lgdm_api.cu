@@ -201,6 +201,10 @@ struct lgdm_mesh_s {
   } sgraph[2];
   int sgraph_next = 0;
   bool step_warm = false;
+  // graphs are captured and replayed on a private stream (the mesh stream may be the legacy
+  // default stream, which cannot be captured), ordered with the mesh stream by events
+  cudaStream_t gstream = nullptr;
+  cudaEvent_t gev_in = nullptr, gev_out = nullptr;
   int max_deg = 0;                // largest node degree (neighbours incl. itself), equal order
   int64_t nx = 0, ny = 0, nz = 0;  // local element counts per axis (nz = layers for 3D, ny for 2D)
   int64_t launches = 0;
@@ -1497,6 +1501,13 @@ lgdm_status lgdm_step(lgdm_mesh m, int flags, double out2[2]) {
     if ((s = step_enqueue(m, hist)) != LGDM_OK) return s;
     m->step_warm = true;
   } else {
+    if (!m->gstream) {
+      CU(cudaStreamCreateWithFlags(&m->gstream, cudaStreamNonBlocking));
+      CU(cudaEventCreateWithFlags(&m->gev_in, cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&m->gev_out, cudaEventDisableTiming));
+    }
+    CU(cudaEventRecord(m->gev_in, m->stream));
+    CU(cudaStreamWaitEvent(m->gstream, m->gev_in, 0));
     lgdm_mesh_s::StepGraph* g = nullptr;
     for (auto& c : m->sgraph)
       if (c.exec && c.dofs == m->dofs && c.k0g == m->k0g && c.alg == m->alg && c.kernel == m->kernel &&
@@ -1507,10 +1518,13 @@ lgdm_status lgdm_step(lgdm_mesh m, int flags, double out2[2]) {
       m->sgraph_next ^= 1;
       if (g->exec) cudaGraphExecDestroy(g->exec), g->exec = nullptr;
       cudaGraph_t graph = nullptr;
-      CU(cudaStreamBeginCapture(m->stream, cudaStreamCaptureModeThreadLocal));
+      CU(cudaStreamBeginCapture(m->gstream, cudaStreamCaptureModeThreadLocal));
       const int64_t l0 = m->launches;
+      cudaStream_t keep = m->stream;
+      m->stream = m->gstream;   // every launch of the pass goes to the capturing stream
       s = step_enqueue(m, hist);
-      const cudaError_t ec = cudaStreamEndCapture(m->stream, &graph);
+      m->stream = keep;
+      const cudaError_t ec = cudaStreamEndCapture(m->gstream, &graph);
       if (s != LGDM_OK) {
         if (graph) cudaGraphDestroy(graph);
         return s;
@@ -1528,8 +1542,10 @@ lgdm_status lgdm_step(lgdm_mesh m, int flags, double out2[2]) {
       g->flags = flags;
       g->comm = (void*)m->comm;
     }
-    CU(cudaGraphLaunch(g->exec, m->stream));
+    CU(cudaGraphLaunch(g->exec, m->gstream));
     m->launches += g->launches;
+    CU(cudaEventRecord(m->gev_out, m->gstream));
+    CU(cudaStreamWaitEvent(m->stream, m->gev_out, 0));
   }
   CU(cudaStreamSynchronize(m->stream));
   out2[0] = std::sqrt(m->host_pinned[0]);
@@ -1619,6 +1635,9 @@ void lgdm_destroy(lgdm_mesh m) {
   if (m->stream) cudaStreamSynchronize(m->stream);
   for (auto& g : m->sgraph)
     if (g.exec) cudaGraphExecDestroy(g.exec);
+  if (m->gstream) cudaStreamSynchronize(m->gstream), cudaStreamDestroy(m->gstream);
+  if (m->gev_in) cudaEventDestroy(m->gev_in);
+  if (m->gev_out) cudaEventDestroy(m->gev_out);
   if (m->comm && g_nccl.loaded) g_nccl.commDestroy(m->comm);
   void* ptrs[] = {m->coords, m->conn, m->dofs, m->kappa, m->row_ptr, m->col_idx, m->val, m->R,
                   m->nbr_ptr, m->base, m->adj_ptr, m->adj, m->scratchK, m->scratchF,
