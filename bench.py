@@ -76,7 +76,7 @@ def kernel_source_sha(etype: int, kernel: int) -> str:
     traffic figure is only reported for the kernel it was measured on."""
     import hashlib
     c = os.path.join(ROOT, "paper_2301_06503_b200", "csrc")
-    main = {2: "lgdm_sweepq.cuh", 3: "lgdm_hex8.cuh" if kernel == 3 else "lgdm_sweep4.cuh"}.get(etype, "lgdm_kernels.cuh")
+    main = {2: "lgdm_sweepq.cuh", 3: "lgdm_sweep4.cuh"}.get(etype, "lgdm_kernels.cuh")
     h = hashlib.sha1()
     for f in (main, "lgdm_device.cuh", "lgdm_sweep.cuh", "lgdm_sweep4.cuh"):
         with open(os.path.join(c, f), "rb") as fh:
@@ -330,8 +330,6 @@ def kernel_name(etype, structured, kernel):
         return "k_elem_blocks + k_gather (general path)"
     if etype == 2:
         return "k_sweepq (Q4 structured sweep)"
-    if kernel == 3:
-        return "k_hex8 (Hex8 structured sweep, register-tiled Kuu)"
     return "k_sweep4 (Hex8 structured sweep)"
 
 
@@ -532,7 +530,7 @@ def main():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", default="lgdm", choices=["lgdm", "reference"])
     ap.add_argument("--kernel", type=int, default=0,
-                    help="lgdm_set_kernel: 0 auto, 1 general, 2 sweep, 3 Hex8 k_hex8")
+                    help="lgdm_set_kernel: 0 auto, 1 general, 2 sweep")
     ap.add_argument("--dry-run", action="store_true",
                     help="launch / rendezvous only (gloo, no GPU): prints n_gpus")
     ap.add_argument("--no-secondary", action="store_true")

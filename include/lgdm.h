@@ -306,8 +306,7 @@ lgdm_status lgdm_scale_dofs(lgdm_mesh mesh, double s);
  *   0 = automatic: structured meshes (x-fastest grids, whole owned layers) -> 2, else 1
  *   1 = general (element-batch + node gather, any connectivity)
  *   2 = structured sweep: Q4 k_sweepq, Hex8 k_sweep4 (row-sum diagonals)
- *   3 = Hex8 k_hex8 (sweep with register-tiled Kuu Gauss sums); Q4 as 2
- * Kernels 2 and 3 need a structured mesh: LGDM_ERR_INVALID_ARGUMENT otherwise; any other
+ * Kernel 2 needs a structured mesh: LGDM_ERR_INVALID_ARGUMENT otherwise; any other
  * selector value: LGDM_ERR_INVALID_ARGUMENT. */
 lgdm_status lgdm_set_kernel(lgdm_mesh mesh, int kernel);
 

@@ -1599,7 +1599,7 @@ lgdm_status lgdm_scale_dofs(lgdm_mesh m, double sc) {
 }
 
 lgdm_status lgdm_set_kernel(lgdm_mesh m, int kernel) {
-  if (!m || kernel < 0 || kernel > 3) return fail(LGDM_ERR_INVALID_ARGUMENT, "bad kernel selector");
+  if (!m || kernel < 0 || kernel > 2) return fail(LGDM_ERR_INVALID_ARGUMENT, "bad kernel selector");
   if (m->mixed && kernel > 1) return fail(LGDM_ERR_INVALID_ARGUMENT, "mixed-order meshes: kernels 0 and 1 only");
   if (kernel >= 2 && !(m->structured && sweep_supported(m)))
     return fail(LGDM_ERR_INVALID_ARGUMENT, "sweep kernel needs a structured mesh with whole owned layers");

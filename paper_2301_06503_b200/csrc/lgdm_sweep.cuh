@@ -12,7 +12,7 @@
 //     a node and every block-row entry receives at most one add per batch.
 //   * Per-entry summation order = (element layer, colour) -- a function of global indices
 //     only, so any tiling / slabbing gives bitwise identical K and R.
-// Kernels: k_hex8 (Hex8, lgdm_hex8.cuh), k_sweepq (Q4, lgdm_sweepq.cuh).
+// Kernels: k_sweep4 (Hex8, lgdm_sweep4.cuh), k_sweepq (Q4, lgdm_sweepq.cuh).
 #pragma once
 
 namespace lgdm {
@@ -65,7 +65,6 @@ template <int D> __device__ __forceinline__ int plane_slot(int dx, int dy) {
 }  // namespace lgdm
 
 #include "lgdm_sweep4.cuh"
-#include "lgdm_hex8.cuh"
 #include "lgdm_sweepq.cuh"
 
 namespace {
@@ -125,34 +124,6 @@ lgdm_status launch_sweep4(lgdm_mesh m) {
   return check_launch(m, "k_sweep4");
 }
 
-lgdm_status launch_hex8(lgdm_mesh m) {
-  SweepGeom G{};
-  G.nx = m->nx;
-  G.nyE = m->ny;
-  G.nyN = m->ny + 1;
-  G.nl = m->nz;
-  const int64_t per_layer = (G.nx + 1) * G.nyN;
-  G.lay_own_b = m->own_b / per_layer;
-  G.lay_own_e = m->own_e / per_layer;
-  G.own_node_b = m->own_b;
-  G.k0g = m->k0g;
-  G.alg = m->alg;
-  G.tiles_x = int((G.nx + 1 + H8::TX - 1) / H8::TX);
-  G.tiles_y = int((G.nyN + H8::TY - 1) / H8::TY);
-  CU(set_smem_attr(k_hex8, H8::SMEM, m->device));
-  int nsm = 148;
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device);
-  const int64_t layers = G.lay_own_e - G.lay_own_b;
-  const int64_t tiles = int64_t(G.tiles_x) * G.tiles_y;
-  const int64_t chunks = pick_chunks(tiles, layers, nsm, 8);
-  G.chunk_len = (layers + chunks - 1) / chunks;
-  G.chunks = int((layers + G.chunk_len - 1) / G.chunk_len);
-  const int64_t grid = tiles * G.chunks;
-  k_hex8<<<unsigned(grid), H8::T, H8::SMEM, m->stream>>>(m->dm, G, m->coords, m->dofs, m->kappa,
-                                                         m->base, m->val, m->R);
-  return check_launch(m, "k_hex8");
-}
-
 lgdm_status launch_sweepq(lgdm_mesh m) {
   SweepGeom G{};
   G.nx = m->nx;
@@ -181,11 +152,9 @@ lgdm_status launch_sweepq(lgdm_mesh m) {
   return check_launch(m, "k_sweepq");
 }
 
-// Automatic choice (kernel 0 or 2): k_sweepq (Q4) and k_sweep4 (Hex8); kernel 3 selects the
-// register-tiled Hex8 variant k_hex8 (parity-tested; measured slower today).
+// Automatic choice (kernel 0 or 2): k_sweepq (Q4) and k_sweep4 (Hex8).
 lgdm_status assemble_sweep(lgdm_mesh m) {
   if (m->f.dim == 2) return launch_sweepq(m);
-  if (m->kernel == 3) return launch_hex8(m);
   return launch_sweep4(m);
 }
 

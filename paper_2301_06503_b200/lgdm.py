@@ -19,7 +19,7 @@ BAR3, QUAD8 = 4, 5          # mixed order: quadratic u, linear ebar (SURVEY NEXT
 # type -> (dim, nen, ndpn, ngp); mixed families: nen = u nodes, ndpn = dofs of a corner node
 FAMILY = {BAR2: (1, 2, 2, 2), QUAD4: (2, 4, 3, 4), HEX8: (3, 8, 4, 8),
           BAR3: (1, 3, 2, 3), QUAD8: (2, 8, 3, 9)}
-KERNEL_AUTO, KERNEL_GENERAL, KERNEL_SWEEP, KERNEL_HEX8 = 0, 1, 2, 3
+KERNEL_AUTO, KERNEL_GENERAL, KERNEL_SWEEP = 0, 1, 2
 
 STATUS = {0: "LGDM_OK", 1: "LGDM_ERR_INVALID_ARGUMENT", 2: "LGDM_ERR_INVERTED_ELEMENT",
           3: "LGDM_ERR_INVALID_STATE", 4: "LGDM_ERR_OUT_OF_MEMORY", 5: "LGDM_ERR_CUDA",

@@ -12,8 +12,8 @@ from parity import (compare, compare_rows, compare_sampled, gpu_assemble, gpu_ro
 
 pytestmark = pytest.mark.gpu
 
-KERNELS = [lgdm.KERNEL_GENERAL, lgdm.KERNEL_AUTO, lgdm.KERNEL_SWEEP, lgdm.KERNEL_HEX8]
-SWEEPS = (lgdm.KERNEL_SWEEP, lgdm.KERNEL_HEX8)
+KERNELS = [lgdm.KERNEL_GENERAL, lgdm.KERNEL_AUTO, lgdm.KERNEL_SWEEP]
+SWEEPS = (lgdm.KERNEL_SWEEP,)
 
 CASES = [
     (lgdm.BAR2, (1,)), (lgdm.BAR2, (7,)), (lgdm.BAR2, (100,)),
@@ -157,7 +157,7 @@ def test_parity_config4_sampled():
     m.close()
 
 
-@pytest.mark.parametrize("kernel", [lgdm.KERNEL_SWEEP, lgdm.KERNEL_HEX8])
+@pytest.mark.parametrize("kernel", [lgdm.KERNEL_SWEEP])
 @pytest.mark.parametrize("cid", [2, 3])
 def test_parity_full_size_sampled(cid, kernel):
     """BASELINE configs 2 and 3 at full size, in the bench's launch configuration; sampled
@@ -176,7 +176,7 @@ def test_parity_full_size_sampled(cid, kernel):
     print(f"config {cid}: sampled {sel.size} nodes, max K err {wk:.2e}, R err {wr:.2e}")
 
 
-@pytest.mark.parametrize("kernel", [lgdm.KERNEL_SWEEP, lgdm.KERNEL_HEX8])
+@pytest.mark.parametrize("kernel", [lgdm.KERNEL_SWEEP])
 @pytest.mark.parametrize("etype,n,P", [(lgdm.QUAD4, (23, 31), 3), (lgdm.HEX8, (7, 5, 13), 4),
                                        (lgdm.BAR2, (50,), 2)])
 def test_slabs_stitch_bitwise(etype, n, P, kernel):
@@ -264,7 +264,7 @@ def test_errors():
     assert ei.value.status == 2 and "element" in str(ei.value)
 
 
-@pytest.mark.parametrize("kernel", [lgdm.KERNEL_SWEEP, lgdm.KERNEL_HEX8])
+@pytest.mark.parametrize("kernel", [lgdm.KERNEL_SWEEP])
 @pytest.mark.parametrize("etype,n", [(lgdm.QUAD4, (61, 40)), (lgdm.HEX8, (17, 9, 11))])
 def test_sweep_bitwise_reproducible(etype, n, kernel):
     """The warp-specialised sweeps hand data between roles through named barriers only and

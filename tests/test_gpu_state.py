@@ -119,7 +119,7 @@ def test_defect_assembly_parity(etype, n):
     plain = oracle.assemble(etype, oracle.material(**synth.MATERIAL), coords, mesh.conn, dofs,
                             kappa)
     assert not np.allclose(ref["val"], plain["val"])
-    for kernel in (lgdm.KERNEL_AUTO, lgdm.KERNEL_GENERAL, lgdm.KERNEL_SWEEP, lgdm.KERNEL_HEX8):
+    for kernel in (lgdm.KERNEL_AUTO, lgdm.KERNEL_GENERAL, lgdm.KERNEL_SWEEP):
         m = lgdm.Mesh(etype, coords, mesh.conn, lgdm.material(**synth.MATERIAL))
         m.set_kernel(kernel)
         m.set_state(dofs, kappa)
