@@ -190,19 +190,28 @@ k_sweepq(DevMat m, SweepGeom G, const double* __restrict__ coords,
               }
               reinterpret_cast<double2*>(eb + SQ::HDR)[g] = make_double2(c[Co::MU], c[Co::GHC]);
             }
-            // node sums over the element's 4 GP lanes (lanes 4 el .. 4 el + 3), fixed order
+            // node sums over the element's 4 GP lanes (lanes 4 el .. 4 el + 3): a transpose-
+            // reduce that leaves lane g with the sums of node g, ((g0 + g1) + (g2 + g3)) in every
+            // lane (commutative pairs: the same bits as a butterfly all-reduce).
+            // step 1 (lane ^ 1): lanes keep the nodes a with (a & 1) == (g & 1)
+            double h[2][6];
 #pragma unroll
-            for (int a = 0; a < NEN; ++a)
+            for (int u = 0; u < 2; ++u)
 #pragma unroll
               for (int q = 0; q < 6; ++q) {
-                ns[a][q] += __shfl_xor_sync(0xffffffffu, ns[a][q], 1);
-                ns[a][q] += __shfl_xor_sync(0xffffffffu, ns[a][q], 2);
+                const double snd = (g & 1) ? ns[2 * u][q] : ns[2 * u + 1][q];
+                const double rcv = __shfl_xor_sync(0xffffffffu, snd, 1);
+                h[u][q] = ((g & 1) ? ns[2 * u + 1][q] : ns[2 * u][q]) + rcv;
               }
-            if (k < nc) {   // every GP lane holds the reduced sums; lane g writes node g
-              double v[6];
+            // step 2 (lane ^ 2): lane g keeps node g = 2 (g >> 1) + (g & 1), i.e. h[g >> 1]
+            double v[6];
 #pragma unroll
-              for (int q = 0; q < 6; ++q)
-                v[q] = g == 0 ? ns[0][q] : g == 1 ? ns[1][q] : g == 2 ? ns[2][q] : ns[3][q];
+            for (int q = 0; q < 6; ++q) {
+              const double snd = (g >> 1) ? h[0][q] : h[1][q];
+              const double rcv = __shfl_xor_sync(0xffffffffu, snd, 2);
+              v[q] = ((g >> 1) ? h[1][q] : h[0][q]) + rcv;
+            }
+            if (k < nc) {
 #pragma unroll
               for (int q = 0; q < 6; q += 2)
                 *reinterpret_cast<double2*>(eb + SQ::NSUM + g * 6 + q) = make_double2(v[q], v[q + 1]);
