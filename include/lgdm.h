@@ -215,12 +215,18 @@ lgdm_status lgdm_update_state(lgdm_mesh mesh, double* sdv, int64_t n_sdv, int ds
 lgdm_status lgdm_get_blocked(lgdm_mesh mesh, lgdm_csr* K, double** R);
 
 /* ---- Newton loop pieces (Alg. 2 lines 4-7 and 16) ----
- * Single-rank whole meshes only (else LGDM_ERR_UNSUPPORTED).  All work runs on the mesh
- * stream; the calls below synchronise it where they return host values.
+ * A whole mesh on one rank, or row-owned slabs with a communicator (lgdm_set_comm): rank p
+ * owns a contiguous node range that follows rank p-1's, and keeps one ghost layer per
+ * interior face (the layout of the slab partition; lgdm_set_comm checks it, and a slab mesh
+ * without a validated layout -> LGDM_ERR_UNSUPPORTED).  Across ranks: dof ids are GLOBAL (every
+ * rank passes the same lists), delta vectors are LOCAL dof vectors (the mesh's owned + ghost
+ * dofs in node order, lgdm_dof_offsets), their ghost dofs filled from the neighbouring slabs by
+ * an NCCL send / recv halo exchange, and every sum is an NCCL allreduce.  All work runs on the
+ * mesh stream; the calls below synchronise it where they return host values.
  *
  * Symmetric Dirichlet elimination on the last assembled K, R (in place; the paper does not
  * state its scheme -- SPEC.md apply_dirichlet): constrained u dofs dof_ids[n_fixed] (host,
- * node-interleaved ids) get unit rows and R = increments[k] (the step's prescribed increment
+ * node-interleaved global ids; a rank uses those among its local dofs) get unit rows and R = increments[k] (the step's prescribed increment
  * on the first iteration, 0 afterwards, since Eq. 11 solves for increments); every free row
  * moves K_ij increments_j to its RHS and zeroes K_ij.  An ebar dof or an id out of range ->
  * LGDM_ERR_INVALID_ARGUMENT; before lgdm_assemble -> LGDM_ERR_INVALID_STATE. */
@@ -228,14 +234,17 @@ lgdm_status lgdm_apply_dirichlet(lgdm_mesh mesh, int64_t n_fixed, const int64_t*
                                  const double* increments);
 
 /* Solve K delta = R (Alg. 2 l.6; the paper uses a direct `mldivide`) with
- * Jacobi-preconditioned BiCGSTAB on the GPU: delta (device, n_rows doubles) from 0 until
+ * Jacobi-preconditioned BiCGSTAB on the GPU, across the ranks of a communicator (owned-row
+ * SpMV after a ghost-dof halo exchange, allreduced dot products): delta (device, local dofs =
+ * lgdm_dof_offsets' last entry doubles, ghost dofs filled on return) from 0 until
  * ||R - K delta|| <= tol ||R||; iters / relres (host, nullable) report the iterations and the
  * true relative residual.  Not within 10 tol after max_iter -> LGDM_ERR_NOT_CONVERGED (delta
  * holds the last iterate).  Reductions are fixed-order: bitwise reproducible. */
 lgdm_status lgdm_solve(lgdm_mesh mesh, double* delta, double tol, int max_iter, int* iters,
                        double* relres);
 
-/* Direct solve of K delta = R on the GPU (the paper's `mldivide`): sparse QR of
+/* Direct solve of K delta = R on the GPU (the paper's `mldivide`; single-rank whole
+ * meshes only, else LGDM_ERR_UNSUPPORTED -- across ranks use lgdm_solve): sparse QR of
  * cuSOLVER (cusolverSpDcsrlsvqr with symrcm reordering; libcusolver / libcusparse dlopen'ed,
  * missing -> LGDM_ERR_UNSUPPORTED; nnz >= 2^31 -> LGDM_ERR_UNSUPPORTED).  delta device;
  * singularity (host, nullable) = -1 or the first rank-deficient pivot, in which case
@@ -249,14 +258,16 @@ lgdm_status lgdm_dof_offsets(lgdm_mesh mesh, int64_t* host_out, int64_t n);
 
 /* Reaction of a displacement-controlled problem (the load of the paper's load-displacement
  * curves, Fig. 11 / P:418; SPEC reaction_force): -sum of the last assembled R over the listed
- * dofs (host ids), to be called after lgdm_assemble and BEFORE lgdm_apply_dirichlet.  Host out. */
+ * dofs (host, global ids; summed over the ranks that own them), to be called after
+ * lgdm_assemble and BEFORE lgdm_apply_dirichlet.  Host out. */
 lgdm_status lgdm_reaction(lgdm_mesh mesh, int64_t n, const int64_t* dof_ids, double* out);
 
-/* dofs += alpha * delta (delta device, n_nodes * ndpn doubles; Alg. 2 l.7). */
+/* dofs += alpha * delta (delta device, the local dofs incl. ghosts; Alg. 2 l.7). */
 lgdm_status lgdm_add_dofs(lgdm_mesh mesh, const double* delta, double alpha);
 
 /* Convergence sums of Alg. 1 l.26 / Alg. 2 l.16 (host out4): {sum du^2, sum u^2, sum de^2,
- * sum e^2} over the u and ebar dofs of delta (device) and of the current dofs. */
+ * sum e^2} over the owned u and ebar dofs of delta (device) and of the current dofs, summed
+ * over the ranks. */
 lgdm_status lgdm_delta_norms(lgdm_mesh mesh, const double* delta, double out4[4]);
 
 /* Convergence test of Alg. 1 l.26 / Alg. 2 l.16: out2 = {||du||/||u||,

@@ -75,6 +75,12 @@ struct NcclApi {
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
   const char* (*getErrorString)(ncclResult_t) = nullptr;
+  // point-to-point (ghost-dof halo exchange of the multi-rank Newton pieces) and all-gather
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
 };
 NcclApi g_nccl;
 
@@ -123,7 +129,13 @@ bool load_nccl() {
   g_nccl.commDestroy = (decltype(g_nccl.commDestroy))dlsym(h, "ncclCommDestroy");
   g_nccl.getErrorString = (decltype(g_nccl.getErrorString))dlsym(h, "ncclGetErrorString");
   g_nccl.getUniqueId = (decltype(g_nccl.getUniqueId))dlsym(h, "ncclGetUniqueId");
-  g_nccl.loaded = g_nccl.commInitRank && g_nccl.allReduce && g_nccl.commDestroy && g_nccl.getUniqueId;
+  g_nccl.send = (decltype(g_nccl.send))dlsym(h, "ncclSend");
+  g_nccl.recv = (decltype(g_nccl.recv))dlsym(h, "ncclRecv");
+  g_nccl.groupStart = (decltype(g_nccl.groupStart))dlsym(h, "ncclGroupStart");
+  g_nccl.groupEnd = (decltype(g_nccl.groupEnd))dlsym(h, "ncclGroupEnd");
+  g_nccl.allGather = (decltype(g_nccl.allGather))dlsym(h, "ncclAllGather");
+  g_nccl.loaded = g_nccl.commInitRank && g_nccl.allReduce && g_nccl.commDestroy && g_nccl.getUniqueId &&
+                  g_nccl.send && g_nccl.recv && g_nccl.groupStart && g_nccl.groupEnd && g_nccl.allGather;
   return g_nccl.loaded;
 }
 
@@ -211,6 +223,7 @@ struct lgdm_mesh_s {
   int64_t launches = 0;
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
+  bool halo_ok = false;           // slab neighbour layout validated (lgdm_set_comm)
   void* sweep = nullptr;  // sweep-path state (lgdm_sweep.cuh)
   // mixed-order meshes (lgdm_mixed.cuh)
   bool mixed = false;
@@ -1205,34 +1218,90 @@ static bool whole_single_rank(lgdm_mesh m) {
   return m->own_b == 0 && m->own_e == m->n_nodes && m->gid0 == 0 && m->n_global_nodes == m->n_nodes;
 }
 
+// Local dof ranges of the Newton pieces.  Local dofs = the mesh's nodes (owned + ghosts) in
+// node order; the owned ones [own_b, own_e) are the rows of K / R; a CSR column c (global dof)
+// is local dof c - col_off.
+struct DofRange {
+  int64_t own_b, own_e, nloc, col_off;
+};
+static DofRange dof_range(lgdm_mesh m) {
+  if (m->mixed) return {m->hdoff[m->own_b], m->hdoff[m->own_e], m->n_dofs_local, m->gdof0};
+  const int64_t k = m->f.ndpn;
+  return {m->own_b * k, m->own_e * k, m->n_nodes * k, m->gid0 * k};
+}
+static bool multi_rank(lgdm_mesh m) { return m->comm && m->nranks > 1; }
+
+// the Newton pieces need the whole system on one rank, or a communicator over the row-owned
+// slabs (lgdm_set_comm validated the neighbour layout)
+static lgdm_status newton_ready(lgdm_mesh m) {
+  if (multi_rank(m)) return m->halo_ok ? LGDM_OK : fail(LGDM_ERR_UNSUPPORTED, "slab layout not validated by lgdm_set_comm");
+  if (whole_single_rank(m) || (m->mixed && m->own_b == 0 && m->own_e == m->n_nodes && m->gdof0 == 0 &&
+                               m->n_global_dofs == m->n_dofs_local))
+    return LGDM_OK;
+  return fail(LGDM_ERR_UNSUPPORTED, "a slab mesh needs a communicator (lgdm_set_comm) for the Newton pieces");
+}
+
+// Ghost-dof halo exchange (SURVEY 8e future exchange step): the ghost dofs of x (local dof
+// vector) receive the owned values of the neighbouring slabs -- rank - 1 holds the nodes below
+// the owned range, rank + 1 those above; each rank sends its first / last owned dofs, as many
+// as the neighbour keeps as ghosts (mirror sizes, checked by lgdm_set_comm).
+static lgdm_status halo_exchange(lgdm_mesh m, double* x) {
+  if (!multi_rank(m)) return LGDM_OK;
+  const DofRange d = dof_range(m);
+  const int64_t glo = d.own_b, ghi = d.nloc - d.own_e;
+  ncclResult_t r = g_nccl.groupStart();
+  if (glo > 0 && r == ncclSuccess) r = g_nccl.send(x + d.own_b, size_t(glo), ncclFloat64, m->rank - 1, m->comm, m->stream);
+  if (glo > 0 && r == ncclSuccess) r = g_nccl.recv(x, size_t(glo), ncclFloat64, m->rank - 1, m->comm, m->stream);
+  if (ghi > 0 && r == ncclSuccess) r = g_nccl.send(x + d.own_e - ghi, size_t(ghi), ncclFloat64, m->rank + 1, m->comm, m->stream);
+  if (ghi > 0 && r == ncclSuccess) r = g_nccl.recv(x + d.own_e, size_t(ghi), ncclFloat64, m->rank + 1, m->comm, m->stream);
+  const ncclResult_t re = g_nccl.groupEnd();
+  if (r != ncclSuccess || re != ncclSuccess)
+    return fail(LGDM_ERR_NCCL, "halo exchange: %s", g_nccl.getErrorString ? g_nccl.getErrorString(r != ncclSuccess ? r : re) : "?");
+  return LGDM_OK;
+}
+
+// sum of n device doubles over the ranks, in place (no-op on one rank)
+static lgdm_status allreduce_sum(lgdm_mesh m, double* dev, int n) {
+  if (!multi_rank(m)) return LGDM_OK;
+  const ncclResult_t r = g_nccl.allReduce(dev, dev, size_t(n), ncclFloat64, ncclSum, m->comm, m->stream);
+  if (r != ncclSuccess) return fail(LGDM_ERR_NCCL, "ncclAllReduce: %s", g_nccl.getErrorString ? g_nccl.getErrorString(r) : "?");
+  return LGDM_OK;
+}
+
 lgdm_status lgdm_apply_dirichlet(lgdm_mesh m, int64_t n_fixed, const int64_t* dof_ids,
                                  const double* increments) {
   if (!m) return fail(LGDM_ERR_INVALID_ARGUMENT, "mesh is NULL");
   if (!m->assembled) return fail(LGDM_ERR_INVALID_STATE, "apply_dirichlet before assemble");
-  if (!whole_single_rank(m)) return fail(LGDM_ERR_UNSUPPORTED, "Newton pieces need a single-rank whole mesh");
+  lgdm_status s = newton_ready(m);
+  if (s != LGDM_OK) return s;
   if (n_fixed < 0 || (n_fixed && (!dof_ids || !increments)))
     return fail(LGDM_ERR_INVALID_ARGUMENT, "dof_ids / increments");
-  const int64_t n = m->n_rows;
-  std::vector<uint8_t> mask(n, 0);
-  std::vector<double> inc(n, 0.0);
+  const DofRange d = dof_range(m);
+  const int64_t nglob = m->mixed ? m->n_global_dofs : m->n_global_nodes * m->f.ndpn;
+  std::vector<uint8_t> mask(d.nloc, 0);   // over the local dofs (owned + ghosts)
+  std::vector<double> inc(d.nloc, 0.0);
   for (int64_t k = 0; k < n_fixed; ++k) {
-    const int64_t d = dof_ids[k];
-    if (d < 0 || d >= n) return fail(LGDM_ERR_INVALID_ARGUMENT, "dof id %lld out of range", (long long)d);
-    if (m->mixed ? m->hkind[d] == m->f.dim : d % m->f.ndpn == m->f.dim)
-      return fail(LGDM_ERR_INVALID_ARGUMENT, "dof %lld is an ebar dof (only u dofs can be constrained)", (long long)d);
-    mask[d] = 1;
-    inc[d] = increments[k];
+    const int64_t g = dof_ids[k];   // global dof id (every rank passes the same list)
+    if (g < 0 || g >= nglob) return fail(LGDM_ERR_INVALID_ARGUMENT, "dof id %lld out of range", (long long)g);
+    const int64_t l = g - d.col_off;
+    if (m->mixed ? (l >= 0 && l < d.nloc && m->hkind[l] == m->f.dim) : g % m->f.ndpn == m->f.dim)
+      return fail(LGDM_ERR_INVALID_ARGUMENT, "dof %lld is an ebar dof (only u dofs can be constrained)", (long long)g);
+    if (l < 0 || l >= d.nloc) continue;   // another rank's dof, not coupled to this rank's rows
+    mask[l] = 1;
+    inc[l] = increments[k];
   }
   CU(cudaSetDevice(m->device));
   if (!m->fixed) {
-    CU(dalloc(&m->fixed, size_t(n)));
-    CU(dalloc(&m->fixinc, size_t(n)));
-    m->device_bytes += n * 9;
+    CU(dalloc(&m->fixed, size_t(d.nloc)));
+    CU(dalloc(&m->fixinc, size_t(d.nloc)));
+    m->device_bytes += d.nloc * 9;
   }
-  CU(cudaMemcpyAsync(m->fixed, mask.data(), size_t(n), cudaMemcpyHostToDevice, m->stream));
-  CU(cudaMemcpyAsync(m->fixinc, inc.data(), size_t(n) * 8, cudaMemcpyHostToDevice, m->stream));
-  k_dirichlet<<<unsigned((n * 32 + 255) / 256), 256, 0, m->stream>>>(n, m->row_ptr, m->col_idx, m->val, m->R, m->fixed, m->fixinc);
-  lgdm_status s = check_launch(m, "k_dirichlet");
+  CU(cudaMemcpyAsync(m->fixed, mask.data(), size_t(d.nloc), cudaMemcpyHostToDevice, m->stream));
+  CU(cudaMemcpyAsync(m->fixinc, inc.data(), size_t(d.nloc) * 8, cudaMemcpyHostToDevice, m->stream));
+  const int64_t n = m->n_rows;
+  k_dirichlet<<<unsigned((n * 32 + 255) / 256), 256, 0, m->stream>>>(
+      n, d.col_off + d.own_b, d.own_b, d.col_off, m->row_ptr, m->col_idx, m->val, m->R, m->fixed, m->fixinc);
+  s = check_launch(m, "k_dirichlet");
   if (s != LGDM_OK) return s;
   CU(cudaStreamSynchronize(m->stream));   // host staging vectors go out of scope
   return LGDM_OK;
@@ -1242,40 +1311,56 @@ lgdm_status lgdm_solve(lgdm_mesh m, double* delta, double tol, int max_iter, int
                        double* relres_out) {
   if (!m) return fail(LGDM_ERR_INVALID_ARGUMENT, "mesh is NULL");
   if (!m->assembled) return fail(LGDM_ERR_INVALID_STATE, "solve before assemble");
-  if (!whole_single_rank(m)) return fail(LGDM_ERR_UNSUPPORTED, "Newton pieces need a single-rank whole mesh");
+  lgdm_status s = newton_ready(m);
+  if (s != LGDM_OK) return s;
   if (!delta || !(tol > 0) || max_iter < 1) return fail(LGDM_ERR_INVALID_ARGUMENT, "delta / tol / max_iter");
+  // rows: the owned rows (n); delta, ph, sh: local dof vectors (owned + ghost dofs, nloc) whose
+  // ghosts come from the neighbouring slabs before every SpMV; dots over the owned rows,
+  // summed over the ranks (multi-rank Jacobi-BiCGSTAB)
   const int64_t n = m->n_rows;
+  const DofRange d = dof_range(m);
+  const int64_t nl = d.nloc, ob = d.own_b, row_g0 = d.col_off + d.own_b;
   CU(cudaSetDevice(m->device));
   if (!m->sol) {
-    CU(dalloc(&m->sol, size_t(n) * 9));
+    CU(dalloc(&m->sol, size_t(n) * 7 + size_t(nl) * 2));
     CU(dalloc(&m->sol_part, size_t(kRedBlocks) * 4 + 4));
-    m->device_bytes += n * 72 + kRedBlocks * 32 + 32;
+    m->device_bytes += (n * 7 + nl * 2) * 8 + kRedBlocks * 32 + 32;
   }
-  double *r = m->sol, *r0 = r + n, *p = r0 + n, *v = p + n, *sv = v + n, *t = sv + n,
-         *ph = t + n, *sh = ph + n, *dinv = sh + n;
+  double *r = m->sol, *r0 = r + n, *p = r0 + n, *v = p + n, *sv = v + n, *t = sv + n, *dinv = t + n,
+         *ph = dinv + n, *sh = ph + nl;
   double* part = m->sol_part;
   double* fin = part + size_t(kRedBlocks) * 4;
   cudaStream_t st = m->stream;
   const unsigned gw = unsigned((n * 32 + 255) / 256), ge = unsigned((n + 255) / 256);
-  auto dots = [&](const double* a, const double* b, const double* c, const double* d, double* h) -> lgdm_status {
-    k_dot2<<<kRedBlocks, 256, 0, st>>>(n, a, b, c, d, part);
+  auto dots = [&](const double* a, const double* b, const double* c, const double* dd, double* h) -> lgdm_status {
+    k_dot2<<<kRedBlocks, 256, 0, st>>>(n, a, b, c, dd, part);
     k_final<2><<<1, 256, 0, st>>>(kRedBlocks, part, fin);
+    m->launches += 2;
+    lgdm_status sr = allreduce_sum(m, fin, 2);
+    if (sr != LGDM_OK) return sr;
     CU(cudaMemcpyAsync(h, fin, 16, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
-    m->launches += 2;
+    return LGDM_OK;
+  };
+  auto spmv = [&](double* x_local, double* y) -> lgdm_status {   // ghosts first
+    lgdm_status sh_ = halo_exchange(m, x_local);
+    if (sh_ != LGDM_OK) return sh_;
+    k_spmv<<<gw, 256, 0, st>>>(n, m->row_ptr, m->col_idx, m->val, x_local, d.col_off, y);
+    ++m->launches;
     return LGDM_OK;
   };
   // x = 0, r = r0 = b, p = v = 0, Jacobi M = diag(K)
-  CU(cudaMemsetAsync(delta, 0, size_t(n) * 8, st));
+  CU(cudaMemsetAsync(delta, 0, size_t(nl) * 8, st));
+  CU(cudaMemsetAsync(ph, 0, size_t(nl) * 8, st));
+  CU(cudaMemsetAsync(sh, 0, size_t(nl) * 8, st));
   CU(cudaMemcpyAsync(r, m->R, size_t(n) * 8, cudaMemcpyDeviceToDevice, st));
   CU(cudaMemcpyAsync(r0, m->R, size_t(n) * 8, cudaMemcpyDeviceToDevice, st));
   CU(cudaMemsetAsync(p, 0, size_t(n) * 8, st));
   CU(cudaMemsetAsync(v, 0, size_t(n) * 8, st));
-  k_invdiag<<<ge, 256, 0, st>>>(n, m->row_ptr, m->col_idx, m->val, dinv);
+  k_invdiag<<<ge, 256, 0, st>>>(n, row_g0, m->row_ptr, m->col_idx, m->val, dinv);
   ++m->launches;
   double h[2];
-  lgdm_status s = dots(r, r, nullptr, nullptr, h);
-  if (s != LGDM_OK) return s;
+  if ((s = dots(r, r, nullptr, nullptr, h)) != LGDM_OK) return s;
   const double bnorm = std::sqrt(h[0]);
   int it = 0;
   double rel = 0.0;
@@ -1292,9 +1377,9 @@ lgdm_status lgdm_solve(lgdm_mesh m, double* delta, double tol, int max_iter, int
     if (rho_new == 0.0 || omega == 0.0) break;   // breakdown
     const double beta = (rho_new / rho) * (alpha / omega);
     k_p_update<<<ge, 256, 0, st>>>(n, beta, omega, r, v, p);
-    k_scale_mul<<<ge, 256, 0, st>>>(n, dinv, p, ph);
-    k_spmv<<<gw, 256, 0, st>>>(n, m->row_ptr, m->col_idx, m->val, ph, v);
-    m->launches += 3;
+    k_scale_mul<<<ge, 256, 0, st>>>(n, dinv, p, ph + ob);
+    m->launches += 2;
+    if ((s = spmv(ph, v)) != LGDM_OK) return s;
     if ((s = dots(r0, v, nullptr, nullptr, h)) != LGDM_OK) return s;
     if (h[0] == 0.0) break;
     alpha = rho_new / h[0];
@@ -1302,17 +1387,17 @@ lgdm_status lgdm_solve(lgdm_mesh m, double* delta, double tol, int max_iter, int
     ++m->launches;
     if ((s = dots(sv, sv, nullptr, nullptr, h)) != LGDM_OK) return s;
     if (std::sqrt(h[0]) / bnorm <= tol) {
-      k_axpy<<<ge, 256, 0, st>>>(n, alpha, ph, delta);
+      k_axpy<<<ge, 256, 0, st>>>(n, alpha, ph + ob, delta + ob);
       ++m->launches;
       rel = std::sqrt(h[0]) / bnorm;
       break;
     }
-    k_scale_mul<<<ge, 256, 0, st>>>(n, dinv, sv, sh);
-    k_spmv<<<gw, 256, 0, st>>>(n, m->row_ptr, m->col_idx, m->val, sh, t);
-    m->launches += 2;
+    k_scale_mul<<<ge, 256, 0, st>>>(n, dinv, sv, sh + ob);
+    ++m->launches;
+    if ((s = spmv(sh, t)) != LGDM_OK) return s;
     if ((s = dots(t, sv, t, t, h)) != LGDM_OK) return s;
     omega = h[1] != 0.0 ? h[0] / h[1] : 0.0;
-    k_x_update<<<ge, 256, 0, st>>>(n, alpha, omega, ph, sh, delta);
+    k_x_update<<<ge, 256, 0, st>>>(n, alpha, omega, ph + ob, sh + ob, delta + ob);
     k_r_update<<<ge, 256, 0, st>>>(n, omega, sv, t, r);
     m->launches += 2;
     if ((s = dots(r, r, nullptr, nullptr, h)) != LGDM_OK) return s;
@@ -1320,10 +1405,11 @@ lgdm_status lgdm_solve(lgdm_mesh m, double* delta, double tol, int max_iter, int
     if (rel <= tol) break;
     rho = rho_new;
   }
-  // true residual of the returned delta (||b - K delta|| / ||b||)
-  k_spmv<<<gw, 256, 0, st>>>(n, m->row_ptr, m->col_idx, m->val, delta, t);
+  // true residual of the returned delta (||b - K delta|| / ||b||); the SpMV also fills the
+  // ghost dofs of delta, so lgdm_add_dofs updates every local dof consistently
+  if ((s = spmv(delta, t)) != LGDM_OK) return s;
   k_s_update<<<ge, 256, 0, st>>>(n, 1.0, m->R, t, sv);
-  m->launches += 2;
+  ++m->launches;
   if ((s = dots(sv, sv, nullptr, nullptr, h)) != LGDM_OK) return s;
   rel = std::sqrt(h[0]) / bnorm;
   if (iters_out) *iters_out = std::min(it, max_iter);
@@ -1343,20 +1429,31 @@ lgdm_status lgdm_dof_offsets(lgdm_mesh m, int64_t* host_out, int64_t n) {
 lgdm_status lgdm_reaction(lgdm_mesh m, int64_t n, const int64_t* dof_ids, double* out) {
   if (!m || !out || (n > 0 && !dof_ids)) return fail(LGDM_ERR_INVALID_ARGUMENT, "NULL argument");
   if (!m->assembled) return fail(LGDM_ERR_INVALID_STATE, "reaction before assemble");
-  if (!whole_single_rank(m)) return fail(LGDM_ERR_UNSUPPORTED, "Newton pieces need a single-rank whole mesh");
-  for (int64_t k = 0; k < n; ++k)
-    if (dof_ids[k] < 0 || dof_ids[k] >= m->n_rows) return fail(LGDM_ERR_INVALID_ARGUMENT, "dof id out of range");
+  lgdm_status s = newton_ready(m);
+  if (s != LGDM_OK) return s;
+  const DofRange d = dof_range(m);
+  const int64_t nglob = m->mixed ? m->n_global_dofs : m->n_global_nodes * m->f.ndpn;
+  std::vector<int64_t> rows;   // this rank's owned rows among the (global) dof ids
+  for (int64_t k = 0; k < n; ++k) {
+    if (dof_ids[k] < 0 || dof_ids[k] >= nglob) return fail(LGDM_ERR_INVALID_ARGUMENT, "dof id out of range");
+    const int64_t r = dof_ids[k] - d.col_off - d.own_b;
+    if (r >= 0 && r < m->n_rows) rows.push_back(r);
+  }
   CU(cudaSetDevice(m->device));
+  const int64_t nr = int64_t(rows.size());
   int64_t* ids = nullptr;
-  CU(dalloc(&ids, size_t(std::max<int64_t>(n, 1)) + 1));   // + 1 double-sized slot for the sum
-  double* sum = reinterpret_cast<double*>(ids + std::max<int64_t>(n, 1));
-  if (n) CU(cudaMemcpyAsync(ids, dof_ids, size_t(n) * 8, cudaMemcpyHostToDevice, m->stream));
-  k_reaction<<<1, 256, 0, m->stream>>>(n, ids, m->R, sum);
+  CU(dalloc(&ids, size_t(std::max<int64_t>(nr, 1)) + 1));   // + 1 double-sized slot for the sum
+  double* sum = reinterpret_cast<double*>(ids + std::max<int64_t>(nr, 1));
+  if (nr) CU(cudaMemcpyAsync(ids, rows.data(), size_t(nr) * 8, cudaMemcpyHostToDevice, m->stream));
+  k_reaction<<<1, 256, 0, m->stream>>>(nr, ids, m->R, sum);
   ++m->launches;
-  CU(cudaMemcpyAsync(out, sum, 8, cudaMemcpyDeviceToHost, m->stream));
-  CU(cudaStreamSynchronize(m->stream));
+  s = allreduce_sum(m, sum, 1);
+  if (s == LGDM_OK) {
+    cudaMemcpyAsync(out, sum, 8, cudaMemcpyDeviceToHost, m->stream);
+    cudaStreamSynchronize(m->stream);
+  }
   cudaFree(ids);
-  return LGDM_OK;
+  return s;
 }
 
 lgdm_status lgdm_solve_direct(lgdm_mesh m, double* delta, int* singularity) {
@@ -1394,7 +1491,8 @@ lgdm_status lgdm_solve_direct(lgdm_mesh m, double* delta, int* singularity) {
 lgdm_status lgdm_add_dofs(lgdm_mesh m, const double* delta, double alpha) {
   if (!m || !delta) return fail(LGDM_ERR_INVALID_ARGUMENT, "mesh / delta is NULL");
   if (!m->have_state) return fail(LGDM_ERR_INVALID_STATE, "add_dofs before set_state");
-  if (!whole_single_rank(m)) return fail(LGDM_ERR_UNSUPPORTED, "Newton pieces need a single-rank whole mesh");
+  lgdm_status s0 = newton_ready(m);
+  if (s0 != LGDM_OK) return s0;
   CU(cudaSetDevice(m->device));
   const int64_t n = m->n_dofs_local;
   k_axpy<<<unsigned((n + 255) / 256), 256, 0, m->stream>>>(n, alpha, delta, m->dofs);
@@ -1404,21 +1502,25 @@ lgdm_status lgdm_add_dofs(lgdm_mesh m, const double* delta, double alpha) {
 lgdm_status lgdm_delta_norms(lgdm_mesh m, const double* delta, double out4[4]) {
   if (!m || !delta || !out4) return fail(LGDM_ERR_INVALID_ARGUMENT, "NULL argument");
   if (!m->have_state) return fail(LGDM_ERR_INVALID_STATE, "delta_norms before set_state");
-  if (!whole_single_rank(m)) return fail(LGDM_ERR_UNSUPPORTED, "Newton pieces need a single-rank whole mesh");
+  lgdm_status s0 = newton_ready(m);
+  if (s0 != LGDM_OK) return s0;
   CU(cudaSetDevice(m->device));
   if (!m->sol_part) {
     CU(dalloc(&m->sol_part, size_t(kRedBlocks) * 4 + 4));
     m->device_bytes += kRedBlocks * 32 + 32;
   }
-  const int64_t n = m->n_dofs_local;
+  // sums over the owned dofs (ghost dofs belong to another rank), then over the ranks
+  const DofRange d = dof_range(m);
+  const int64_t n = d.own_e - d.own_b, ob = d.own_b;
   double* part = m->sol_part;
   double* fin = part + size_t(kRedBlocks) * 4;
-  if (m->mixed) k_delta_sumsq_kind<<<kRedBlocks, 256, 0, m->stream>>>(n, m->f.dim, m->dkind, delta, m->dofs, part);
-  else if (m->f.ndpn == 2) k_delta_sumsq<2><<<kRedBlocks, 256, 0, m->stream>>>(n, delta, m->dofs, part);
-  else if (m->f.ndpn == 3) k_delta_sumsq<3><<<kRedBlocks, 256, 0, m->stream>>>(n, delta, m->dofs, part);
-  else k_delta_sumsq<4><<<kRedBlocks, 256, 0, m->stream>>>(n, delta, m->dofs, part);
+  if (m->mixed) k_delta_sumsq_kind<<<kRedBlocks, 256, 0, m->stream>>>(n, m->f.dim, m->dkind + ob, delta + ob, m->dofs + ob, part);
+  else if (m->f.ndpn == 2) k_delta_sumsq<2><<<kRedBlocks, 256, 0, m->stream>>>(n, delta + ob, m->dofs + ob, part);
+  else if (m->f.ndpn == 3) k_delta_sumsq<3><<<kRedBlocks, 256, 0, m->stream>>>(n, delta + ob, m->dofs + ob, part);
+  else k_delta_sumsq<4><<<kRedBlocks, 256, 0, m->stream>>>(n, delta + ob, m->dofs + ob, part);
   k_final<4><<<1, 256, 0, m->stream>>>(kRedBlocks, part, fin);
   m->launches += 2;
+  if ((s0 = allreduce_sum(m, fin, 4)) != LGDM_OK) return s0;
   CU(cudaMemcpyAsync(out4, fin, 32, cudaMemcpyDeviceToHost, m->stream));
   CU(cudaStreamSynchronize(m->stream));
   return LGDM_OK;
@@ -1567,6 +1669,36 @@ lgdm_status lgdm_set_comm(lgdm_mesh m, const void* uid, int nranks, int rank) {
     return fail(LGDM_ERR_NCCL, "ncclCommInitRank: %s", g_nccl.getErrorString ? g_nccl.getErrorString(r) : "?");
   m->nranks = nranks;
   m->rank = rank;
+  m->halo_ok = false;
+  if (nranks > 1) {
+    // the Newton pieces' halo exchange assumes row-owned slabs in rank order: rank p's first
+    // owned node follows rank p-1's last owned node, and the ghosts mirror (rank p-1 keeps as
+    // many ghosts above as rank p keeps below, nodes and dofs).  All-gather every rank's
+    // ranges and check; a layout that does not fit leaves the Newton pieces unsupported (the
+    // assembly and the residual norms do not depend on it).
+    const DofRange d = dof_range(m);
+    const int64_t mine[8] = {m->gid0, m->own_b, m->own_e, m->n_nodes, d.col_off, d.own_b, d.own_e, d.nloc};
+    int64_t* buf = nullptr;
+    CU(dalloc(&buf, size_t(8) * (nranks + 1)));
+    std::vector<int64_t> all(size_t(8) * nranks);
+    CU(cudaMemcpyAsync(buf, mine, 64, cudaMemcpyHostToDevice, m->stream));
+    r = g_nccl.allGather(buf, buf + 8, 8, ncclInt64, m->comm, m->stream);
+    if (r == ncclSuccess) {
+      cudaMemcpyAsync(all.data(), buf + 8, all.size() * 8, cudaMemcpyDeviceToHost, m->stream);
+      cudaStreamSynchronize(m->stream);
+    }
+    cudaFree(buf);
+    if (r != ncclSuccess)
+      return fail(LGDM_ERR_NCCL, "ncclAllGather: %s", g_nccl.getErrorString ? g_nccl.getErrorString(r) : "?");
+    bool ok = all[1] == 0 && all[size_t(8) * (nranks - 1) + 2] == all[size_t(8) * (nranks - 1) + 3];
+    for (int p = 1; p < nranks && ok; ++p) {
+      const int64_t* a = &all[size_t(8) * (p - 1)];
+      const int64_t* b = &all[size_t(8) * p];
+      ok = a[0] + a[2] == b[0] + b[1] && a[3] - a[2] == b[1] &&      // nodes
+           a[4] + a[6] == b[4] + b[5] && a[7] - a[6] == b[5];         // dofs
+    }
+    m->halo_ok = ok;
+  }
   return LGDM_OK;
 }
 

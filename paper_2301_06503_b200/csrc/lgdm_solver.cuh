@@ -11,8 +11,11 @@ namespace lgdm {
 constexpr int kRedBlocks = 592;   // 4 x 148 SMs; partial sums, then one final block
 
 // constrained rows become unit rows with R = increment; free rows move K_ij inc_j of the
-// constrained columns to the RHS and zero them (one warp per row, fixed-order reduction)
-__global__ void k_dirichlet(int64_t nrows, const int64_t* __restrict__ row_ptr,
+// constrained columns to the RHS and zero them (one warp per row, fixed-order reduction).
+// Rows are the owned rows (global id row_g0 + row, local dof own_b + row); fixed / inc are
+// over the local dofs (owned + ghosts), a column c is local dof c - col_off.
+__global__ void k_dirichlet(int64_t nrows, int64_t row_g0, int64_t own_b, int64_t col_off,
+                            const int64_t* __restrict__ row_ptr,
                             const int32_t* __restrict__ col_idx, double* __restrict__ val,
                             double* __restrict__ R, const uint8_t* __restrict__ fixed,
                             const double* __restrict__ inc) {
@@ -20,14 +23,14 @@ __global__ void k_dirichlet(int64_t nrows, const int64_t* __restrict__ row_ptr,
   const int lane = threadIdx.x & 31;
   if (row >= nrows) return;
   const int64_t lo = row_ptr[row], hi = row_ptr[row + 1];
-  if (fixed[row]) {
-    for (int64_t q = lo + lane; q < hi; q += 32) val[q] = col_idx[q] == row ? 1.0 : 0.0;
-    if (lane == 0) R[row] = inc[row];
+  if (fixed[own_b + row]) {
+    for (int64_t q = lo + lane; q < hi; q += 32) val[q] = col_idx[q] == row_g0 + row ? 1.0 : 0.0;
+    if (lane == 0) R[row] = inc[own_b + row];
     return;
   }
   double s = 0.0;
   for (int64_t q = lo + lane; q < hi; q += 32) {
-    const int32_t c = col_idx[q];
+    const int64_t c = col_idx[q] - col_off;
     if (fixed[c]) {
       s = fma(val[q], inc[c], s);
       val[q] = 0.0;
@@ -38,29 +41,30 @@ __global__ void k_dirichlet(int64_t nrows, const int64_t* __restrict__ row_ptr,
   if (lane == 0 && s != 0.0) R[row] -= s;
 }
 
-// y = A x (one warp per row, fixed-order lane partials + tree)
+// y = A x over the owned rows (one warp per row, fixed-order lane partials + tree); x is a
+// local dof vector (owned + ghost dofs), column c is local dof c - col_off
 __global__ void k_spmv(int64_t nrows, const int64_t* __restrict__ row_ptr,
                        const int32_t* __restrict__ col_idx, const double* __restrict__ val,
-                       const double* __restrict__ x, double* __restrict__ y) {
+                       const double* __restrict__ x, int64_t col_off, double* __restrict__ y) {
   const int64_t row = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (row >= nrows) return;
   double s = 0.0;
-  for (int64_t q = row_ptr[row] + lane; q < row_ptr[row + 1]; q += 32) s = fma(val[q], x[col_idx[q]], s);
+  for (int64_t q = row_ptr[row] + lane; q < row_ptr[row + 1]; q += 32) s = fma(val[q], x[col_idx[q] - col_off], s);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (lane == 0) y[row] = s;
 }
 
-// inverse diagonal for the Jacobi preconditioner (0 -> 1)
-__global__ void k_invdiag(int64_t nrows, const int64_t* __restrict__ row_ptr,
+// inverse diagonal for the Jacobi preconditioner (0 -> 1); row_g0 = global id of row 0
+__global__ void k_invdiag(int64_t nrows, int64_t row_g0, const int64_t* __restrict__ row_ptr,
                           const int32_t* __restrict__ col_idx, const double* __restrict__ val,
                           double* __restrict__ dinv) {
   const int64_t row = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (row >= nrows) return;
   double d = 0.0;
   for (int64_t q = row_ptr[row]; q < row_ptr[row + 1]; ++q)
-    if (col_idx[q] == row) d = val[q];
+    if (col_idx[q] == row_g0 + row) d = val[q];
   dinv[row] = d != 0.0 ? 1.0 / d : 1.0;
 }
 

@@ -206,6 +206,7 @@ class Mesh:
             stream = torch.cuda.current_stream(device).cuda_stream
         self.device = device
         self.stream = int(stream or 0)
+        self.nranks, self.rank = 1, 0
         self._h = C.c_void_p()
         if global_dof_offset is not None:          # mixed-order slab
             _check(L.lgdm_create_mesh_mixed(etype, self.n_nodes, coords.ctypes.data, self.n_elems,
@@ -390,6 +391,7 @@ class Mesh:
 
     def set_comm(self, unique_id: bytes, nranks: int, rank: int):
         _check(load().lgdm_set_comm(self._h, unique_id, nranks, rank))
+        self.nranks, self.rank = nranks, rank
 
     def get_kappa(self):
         out = np.zeros((self.n_elems, self.ngp))
@@ -439,6 +441,8 @@ def newton(mesh: "Mesh", fixed_dofs, step_increment, n_steps: int, tol: float = 
     dofs (nonzero increments) and commit the history.  Returns one dict per step (iterations,
     final ratios, solver iterations, reaction).  Raises LGDMError if a step does
     not converge in max_iter iterations."""
+    if solver == "direct" and getattr(mesh, "nranks", 1) > 1:
+        solver = "bicgstab"                   # the sparse QR is single-rank; Krylov across slabs
     fixed = np.ascontiguousarray(fixed_dofs, dtype=np.int64)
     inc = np.broadcast_to(np.asarray(step_increment, dtype=np.float64), fixed.shape).copy()
     zero = np.zeros_like(inc)

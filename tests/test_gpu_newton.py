@@ -196,3 +196,26 @@ def test_softening_bar_matches_oracle():
     kel = kap.reshape(n, 2).max(axis=1)
     assert kel[defect].min() > kel[~defect].max()  # damage localises in the defect region
     m.close()
+
+
+def test_slab_without_comm_refuses_newton_pieces():
+    """A row-owned slab has no consistent Newton system without its neighbours: the Newton
+    pieces need lgdm_set_comm (validated slab layout) -> LGDM_ERR_UNSUPPORTED otherwise."""
+    import torch
+    from paper_2301_06503_b200 import slabs
+    cfg = synth.small_config(lgdm.HEX8, (3, 3, 6))
+    part = slabs.slab(cfg.n, 1, 3)
+    sm = synth.structured_mesh(cfg, elem_layers=part.elem_layers)
+    d, k = synth.fields(cfg, sm)
+    m = lgdm.Mesh(lgdm.HEX8, sm.coords, sm.conn, lgdm.material(**synth.MATERIAL),
+                  global_node_offset=sm.node_gid0, n_global_nodes=cfg.n_nodes,
+                  owned=part.owned_local(sm.node_gid0))
+    m.set_state(d, k)
+    m.assemble()
+    delta = torch.zeros(m.n_dofs, dtype=torch.float64, device="cuda")
+    for call in (lambda: m.solve(out=delta), lambda: m.apply_dirichlet([0], [0.0]),
+                 lambda: m.add_dofs(delta), lambda: m.delta_norms(delta)):
+        with pytest.raises(lgdm.LGDMError) as ei:
+            call()
+        assert ei.value.status == 7
+    m.close()

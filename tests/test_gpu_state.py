@@ -247,3 +247,28 @@ def test_nccl_single_rank_comm():
     assert np.array_equal(got, want)
     a.close()
     b.close()
+
+
+def test_mesh_on_every_visible_device():
+    """One process drives a mesh on every visible GPU (the sweeps' dynamic shared-memory
+    attribute is a per-device setting, set once per device) and assembles with the default
+    sweep on each; every device gives the same bits."""
+    import torch
+    etype, n = lgdm.HEX8, (7, 5, 4)
+    cfg = synth.small_config(etype, n)
+    mesh = synth.structured_mesh(cfg)
+    dofs, kappa = synth.fields(cfg, mesh)
+    outs = []
+    for dev in range(torch.cuda.device_count()):
+        with torch.cuda.device(dev):
+            m = lgdm.Mesh(etype, mesh.coords, mesh.conn, lgdm.material(**synth.MATERIAL), device=dev,
+                          stream=torch.cuda.current_stream(dev).cuda_stream)
+            m.set_kernel(lgdm.KERNEL_SWEEP)
+            m.set_state(dofs, kappa)
+            o = m.assemble()
+            torch.cuda.synchronize(dev)
+            outs.append(o["val"].torch(device=f"cuda:{dev}").cpu().numpy())
+            m.close()
+    assert len(outs) >= 1
+    for v in outs[1:]:
+        np.testing.assert_array_equal(v, outs[0])
