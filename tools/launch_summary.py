@@ -4,7 +4,7 @@ import collections
 import csv
 import sys
 
-SETUP = ("k_detj", "k_cols", "k_mixed_detj")
+SETUP = ("k_detj", "k_cols", "k_mixed_detj", "k_adj_keys", "k_pat_", "DeviceRadixSort", "DeviceScan", "k_adj_ptr")
 
 
 def main(path, title):
