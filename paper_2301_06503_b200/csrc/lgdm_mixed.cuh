@@ -11,10 +11,11 @@
 // component c = doff[n] + c.
 //
 // Two kernels, as the general equal-order path (k_elem_blocks + k_gather):
-//   k_mixed_blocks  one warp per element: GP cores (lanes g < NGP; the constitutive part is
-//                   gpLaw of lgdm_device.cuh), per-(GP, node) records in shared memory, then
-//                   node-pair Gauss sums (lanes over the NENU^2 ordered pairs) -> element
-//                   blocks Ke [NDOFE][NDOFE], Fe [NDOFE] in HBM;
+//   k_mixed_blocks  one warp per two elements (mixed_elements): GP cores of both at once (the
+//                   constitutive part is gpLaw of lgdm_device.cuh), per-(GP, node) records in
+//                   shared memory, node-pair Gauss sums (one lane per pair a < b, both
+//                   directions), diagonal blocks by the row-sum identity -> element blocks
+//                   Ke [NDOFE][NDOFE], Fe [NDOFE] in HBM;
 //   k_mixed_gather  one warp per owned node: the node's CSR block-row accumulated in shared
 //                   memory over its adjacent elements in ascending element id (atomic-free,
 //                   bitwise reproducible; the element row-blocks arrive by cp.async, all of a
@@ -75,62 +76,83 @@ template <int D> struct MERec {
   static constexpr int N = 0, GN = 1, E = 1 + D, FE = 2 + D, STRIDE = 3 + D + ((3 + D) % 2 == 0);
 };
 
-template <int T> struct MSmem {   // doubles per warp (one element)
+// per-warp shared memory of mixed_elements (doubles): coordinates + element dofs and the GP
+// cores of two elements, the records of one element (reused as the block staging
+// [NENU][NENU][D+1][D+1] once the pair sums are done), the coupling sums U, V of the corners
+template <int T> struct MSmem {
   using F = MFam<T>;
   static constexpr int D = F::DIM;
-  static constexpr int X = 0, U = X + F::NENU * D, CORE = U + F::NDOFE,
-                       UR = CORE + F::NGP * Core<D>::STRIDE,
+  static constexpr int NPE = F::NENU * D + F::NDOFE;             // X [NENU][D], U [NDOFE]
+  static constexpr int XU = 0, CORE = XU + 2 * NPE, CS = F::NGP * Core<D>::STRIDE,
+                       UR = CORE + 2 * CS,
                        ER = UR + F::NGP * F::NENU * MURec<D>::STRIDE,
-                       SIZE = ER + F::NGP * F::NENE * MERec<D>::STRIDE;
+                       UV = ER + F::NGP * F::NENE * MERec<D>::STRIDE,
+                       SIZE = (UV + F::NENE * (D + 1) + 1) & ~1;
+  static constexpr int ST = F::NDOFE * F::NDOFE;   // staging of Ke (row-major), at UR
+  static_assert(ST <= ER - UR, "block staging fits in the record area");
+  static_assert(UR % 2 == 0 && SIZE % 2 == 0, "16-byte aligned staging");
+  static constexpr int NP = F::NENU * (F::NENU - 1) / 2;             // node pairs a < b
+  static_assert(NP + F::NENE <= 32, "one lane per pair plus the coupling lanes");
 };
 
-template <int T, int WPB>
-__global__ void __launch_bounds__(WPB * 32)
-k_mixed_blocks(DevMat m, int64_t ne, const int32_t* __restrict__ conn, const double* __restrict__ coords,
-               const int32_t* __restrict__ gdof, const double* __restrict__ dofs,
-               const double* __restrict__ kappa, const double* __restrict__ k0g,
-               const double* __restrict__ alg, double* __restrict__ EB, double* __restrict__ EF) {
+// Element tangent Ke [NDOFE][NDOFE] (local dof order, row-major) and residual Fe [NDOFE] of up
+// to two elements (e1 < 0: one), by one warp.  out(k, Ke, Fe) supplies element k's output
+// pointers (HBM scratch or shared memory).
+//   * GP cores of both elements in one pass: lanes 16 k + g (two elements' 2 x NGP lanes);
+//   * per element: per-(GP, node) records; one lane per node pair a < b Gauss-sums K_ab and
+//     K_ba together (Kuu_ba = Kuu_ab^T: the integrand lam gA gB^T + Ams (gA SgB^T + SgA gB^T) +
+//     Ass SgA SgB^T + mu (gB gA^T + gA.gB I) is symmetric under a <-> b with transposition);
+//   * diagonal blocks by the partition-of-unity row-sum identity, as in the sweeps (sum_b N_b
+//     = 1 for the u and the ebar families alike): Kuu_aa = -sum_{b!=a} Kuu_ab,
+//     Keu_aa = -sum_{b!=a} Keu_ab, Kue_aa = U_a - sum_{b!=a corner} Kue_ab with
+//     U_a = sum_g W' grad N_a, Kee_aa = V_a - sum_{b!=a corner} Kee_ab with V_a = sum_g E_a.
+template <int T, class OUT>
+__device__ __forceinline__ void mixed_elements(const DevMat& m, const MShape<T>& S, double* sm, int lane,
+                                               int64_t e0, int64_t e1, const int32_t* __restrict__ conn,
+                                               const double* __restrict__ coords,
+                                               const int32_t* __restrict__ gdof,
+                                               const double* __restrict__ dofs,
+                                               const double* __restrict__ kappa,
+                                               const double* __restrict__ k0g,
+                                               const double* __restrict__ alg, OUT&& out) {
   using F = MFam<T>;
   constexpr int D = F::DIM, NGP = F::NGP, NENU = F::NENU, NENE = F::NENE, ND = F::NDOFE;
+  constexpr int DB = D + 1;
   using SM = MSmem<T>;
   using UR = MURec<D>;
   using ER = MERec<D>;
   using Co = Core<D>;
-  extern __shared__ double smem_mx[];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  // the shape table in shared memory: lanes read different Gauss points (divergent constant
-  // cache reads would serialise)
-  MShape<T>& S = *reinterpret_cast<MShape<T>*>(smem_mx);
-  constexpr int TBL = (int(sizeof(MShape<T>)) / 8 + 1) & ~1;
-  for (int k = threadIdx.x; k < int(sizeof(MShape<T>)) / 8; k += blockDim.x)
-    smem_mx[k] = reinterpret_cast<const double*>(&mshape<T>())[k];
-  __syncthreads();
-  double* sm = smem_mx + TBL + w * SM::SIZE;
-  for (int64_t e = int64_t(blockIdx.x) * WPB + w; e < ne; e += int64_t(gridDim.x) * WPB) {
-    // gather coordinates and element dofs
-    for (int k = lane; k < NENU * D; k += 32) {
-      const int a = k / D, i = k % D;
-      sm[SM::X + k] = coords[int64_t(conn[e * NENU + a]) * D + i];
-    }
-    for (int c = lane; c < ND; c += 32) sm[SM::U + c] = dofs[gdof[e * ND + c]];   // gdof: host table
-    __syncwarp();
-    // GP cores: geometry on the u nodes (R-GEO), kinematics, Appendix A law
-    if (lane < NGP) {
-      const int g = lane;
+  // gather coordinates and element dofs of both elements
+  for (int t = lane; t < 2 * SM::NPE; t += 32) {
+    const int k = t >= SM::NPE ? 1 : 0, q = t - k * SM::NPE;
+    const int64_t e = k ? e1 : e0;
+    if (e < 0) continue;
+    double v;
+    if (q < NENU * D) v = coords[int64_t(conn[e * NENU + q / D]) * D + q % D];
+    else v = dofs[gdof[e * ND + q - NENU * D]];   // gdof: host table
+    sm[SM::XU + t] = v;
+  }
+  __syncwarp();
+  // GP cores: geometry on the u nodes (R-GEO), kinematics, Appendix A law
+  {
+    const int k = lane >> 4, g = lane & 15;
+    const int64_t e = k ? e1 : e0;
+    if (g < NGP && e >= 0) {
+      const double* X = sm + SM::XU + k * SM::NPE;
+      const double* U = X + NENU * D;
       double J[D][D];
 #pragma unroll
       for (int i = 0; i < D; ++i)
 #pragma unroll
         for (int j = 0; j < D; ++j) J[i][j] = 0.0;
-      // J = sum_a X_a dN_a/dxi = sum_a (X_a - X_0) dN_a/dxi (sum_a dN_a = 0): node coordinates
-      // relative to node 0 (exact differences) remove the cancellation of |X| >> element size
+      // J = sum_a (X_a - X_0) dN_a/dxi (sum_a dN_a = 0): coordinates relative to node 0
+      // (exact differences) remove the cancellation of |X| >> element size (R-REL)
 #pragma unroll
       for (int a = 1; a < NENU; ++a)
 #pragma unroll
         for (int j = 0; j < D; ++j)
 #pragma unroll
-          for (int i = 0; i < D; ++i)
-            J[i][j] = fma(sm[SM::X + a * D + i] - sm[SM::X + i], S.dNu[g][a][j], J[i][j]);
+          for (int i = 0; i < D; ++i) J[i][j] = fma(X[a * D + i] - X[i], S.dNu[g][a][j], J[i][j]);
       double detJ, Ji[D][D];
       if constexpr (D == 1) {
         detJ = J[0][0];
@@ -163,17 +185,17 @@ k_mixed_blocks(DevMat m, int64_t ne, const int32_t* __restrict__ conn, const dou
         }
 #pragma unroll
         for (int i = 0; i < D; ++i) {
-          const double ua = sm[SM::U + mldof<T>(a) + i] - sm[SM::U + i];
+          const double ua = U[mldof<T>(a) + i] - U[i];
 #pragma unroll
           for (int j = 0; j < D; ++j) eps[i][j] = fma(ua, gn[j], eps[i][j]);
         }
       }
 #pragma unroll
       for (int a = 0; a < NENE; ++a) {
-        const double ea = sm[SM::U + mldof<T>(a) + D];
+        const double ea = U[mldof<T>(a) + D];
         ebar = fma(S.Ne[g][a], ea, ebar);
         if (a == 0) continue;
-        const double da = ea - sm[SM::U + D];
+        const double da = ea - U[D];
 #pragma unroll
         for (int i = 0; i < D; ++i) {
           double s = 0.0;
@@ -192,14 +214,31 @@ k_mixed_blocks(DevMat m, int64_t ne, const int32_t* __restrict__ conn, const dou
       }
       const int64_t q = e * NGP + g;
       gpLaw<D>(m, Ji, dV, es, ebar, gb, kappa[q], k0g ? k0g[q] : m.kappa0, alg ? alg[q] : m.alpha,
-               sm + SM::CORE + g * Co::STRIDE);
+               sm + SM::CORE + k * SM::CS + g * Co::STRIDE);
     }
-    __syncwarp();
+  }
+  __syncwarp();
+  // this lane's node pair a < b (lanes < NP)
+  int pa = 0, pb = 0;
+  {
+    int r = lane;
+    for (int a = 0; a < NENU - 1; ++a) {
+      if (r < NENU - 1 - a) {
+        pa = a;
+        pb = a + 1 + r;
+        break;
+      }
+      r -= NENU - 1 - a;
+    }
+  }
+  for (int k = 0; k < 2; ++k) {
+    if ((k ? e1 : e0) < 0) continue;
+    const double* cores = sm + SM::CORE + k * SM::CS;
     // per-(GP, node) records
-    for (int k = lane; k < NGP * NENU; k += 32) {
-      const int g = k / NENU, a = k % NENU;
-      const double* core = sm + SM::CORE + g * Co::STRIDE;
-      double* r = sm + SM::UR + k * UR::STRIDE;
+    for (int t = lane; t < NGP * NENU; t += 32) {
+      const int g = t / NENU, a = t % NENU;
+      const double* core = cores + g * Co::STRIDE;
+      double* r = sm + SM::UR + t * UR::STRIDE;
       double gn[D], SgN[D], WgN[D], DgN[D], fu[D];
 #pragma unroll
       for (int i = 0; i < D; ++i) {
@@ -221,10 +260,10 @@ k_mixed_blocks(DevMat m, int64_t ne, const int32_t* __restrict__ conn, const dou
         r[UR::FU + i] = fu[i];
       }
     }
-    for (int k = lane; k < NGP * NENE; k += 32) {
-      const int g = k / NENE, a = k % NENE;
-      const double* core = sm + SM::CORE + g * Co::STRIDE;
-      double* r = sm + SM::ER + k * ER::STRIDE;
+    for (int t = lane; t < NGP * NENE; t += 32) {
+      const int g = t / NENE, a = t % NENE;
+      const double* core = cores + g * Co::STRIDE;
+      double* r = sm + SM::ER + t * ER::STRIDE;
       double gvd = 0.0, fvd = 0.0;
 #pragma unroll
       for (int i = 0; i < D; ++i) {
@@ -241,23 +280,21 @@ k_mixed_blocks(DevMat m, int64_t ne, const int32_t* __restrict__ conn, const dou
       r[ER::FE] = fma(core[Co::FE0], Na, fvd);
     }
     __syncwarp();
-    // node-pair Gauss sums (Eqs. 11a-d), written in the local dof order
-    double* Ke = EB + e * (ND * ND);
-    for (int p = lane; p < NENU * NENU; p += 32) {
-      const int a = p / NENU, b = p % NENU;
-      const bool ea = a < NENE, eb = b < NENE;
-      double Kuu[D][D], Kue[D], Keu[D], Kee = 0.0;
+    // node-pair Gauss sums (Eqs. 11a-d), both directions
+    double Kuu[D][D], Kue_ab[D], Kue_ba[D], Keu_ab[D], Keu_ba[D], Kee_ab = 0.0, Kee_ba = 0.0;
 #pragma unroll
-      for (int i = 0; i < D; ++i) {
-        Kue[i] = Keu[i] = 0.0;
+    for (int i = 0; i < D; ++i) {
+      Kue_ab[i] = Kue_ba[i] = Keu_ab[i] = Keu_ba[i] = 0.0;
 #pragma unroll
-        for (int j = 0; j < D; ++j) Kuu[i][j] = 0.0;
-      }
+      for (int j = 0; j < D; ++j) Kuu[i][j] = 0.0;
+    }
+    const bool ca = pa < NENE, cb = pb < NENE;   // corners carry ebar (cb implies ca)
+    if (lane < SM::NP) {
 #pragma unroll 1
       for (int g = 0; g < NGP; ++g) {
-        const double* A = sm + SM::UR + (g * NENU + a) * UR::STRIDE;
-        const double* B = sm + SM::UR + (g * NENU + b) * UR::STRIDE;
-        const double* core = sm + SM::CORE + g * Co::STRIDE;
+        const double* A = sm + SM::UR + (g * NENU + pa) * UR::STRIDE;
+        const double* B = sm + SM::UR + (g * NENU + pb) * UR::STRIDE;
+        const double* core = cores + g * Co::STRIDE;
         const double mu = core[Co::MU];
         const double lamS = core[Co::LAM], Ams = core[Co::AMS], Ass = core[Co::ASS];
         double t1[D], t2[D];
@@ -282,37 +319,51 @@ k_mixed_blocks(DevMat m, int64_t ne, const int32_t* __restrict__ conn, const dou
           }
           Kuu[i][i] = fma(mu, dot, Kuu[i][i]);
         }
-        if (eb) {
-          const double NB = sm[SM::ER + (g * NENE + b) * ER::STRIDE + ER::N];
+        if (ca) {
+          const double* EA = sm + SM::ER + (g * NENE + pa) * ER::STRIDE;
+          const double NA = EA[ER::N];
 #pragma unroll
-          for (int i = 0; i < D; ++i) Kue[i] = fma(NB, A[UR::WGN + i], Kue[i]);
-        }
-        if (ea) {
-          const double* EA = sm + SM::ER + (g * NENE + a) * ER::STRIDE;
+          for (int i = 0; i < D; ++i) {
+            Kue_ba[i] = fma(NA, B[UR::WGN + i], Kue_ba[i]);
+            Keu_ab[i] = fma(NA, B[UR::DGN + i], Keu_ab[i]);
+          }
+          if (cb) {
+            const double* EBr = sm + SM::ER + (g * NENE + pb) * ER::STRIDE;
+            const double NB = EBr[ER::N];
 #pragma unroll
-          for (int i = 0; i < D; ++i) Keu[i] = fma(EA[ER::N], B[UR::DGN + i], Keu[i]);
-          if (eb) {
-            const double* EBr = sm + SM::ER + (g * NENE + b) * ER::STRIDE;
+            for (int i = 0; i < D; ++i) {
+              Kue_ab[i] = fma(NB, A[UR::WGN + i], Kue_ab[i]);
+              Keu_ba[i] = fma(NB, A[UR::DGN + i], Keu_ba[i]);
+            }
             double dote = 0.0;
 #pragma unroll
             for (int i = 0; i < D; ++i) dote = fma(EA[ER::GN + i], EBr[ER::GN + i], dote);
-            Kee = fma(EBr[ER::N], EA[ER::E], fma(core[Co::GHC], dote, Kee));
+            const double gd = core[Co::GHC] * dote;
+            Kee_ab = fma(NB, EA[ER::E], gd + Kee_ab);
+            Kee_ba = fma(NA, EBr[ER::E], gd + Kee_ba);
           }
         }
       }
-      const int ra = mldof<T>(a), cb = mldof<T>(b);
+    } else if (lane < SM::NP + NENE) {   // coupling sums of corner a: U_a = sum W' grad N_a, V_a = sum E_a
+      const int a = lane - SM::NP;
+      double u[D], v = 0.0;
 #pragma unroll
-      for (int i = 0; i < D; ++i) {
+      for (int i = 0; i < D; ++i) u[i] = 0.0;
+      for (int g = 0; g < NGP; ++g) {
 #pragma unroll
-        for (int j = 0; j < D; ++j) Ke[(ra + i) * ND + cb + j] = Kuu[i][j];
-        if (eb) Ke[(ra + i) * ND + cb + D] = Kue[i];
-        if (ea) Ke[(ra + D) * ND + cb + i] = Keu[i];
+        for (int i = 0; i < D; ++i) u[i] += sm[SM::UR + (g * NENU + a) * UR::STRIDE + UR::WGN + i];
+        v += sm[SM::ER + (g * NENE + a) * ER::STRIDE + ER::E];
       }
-      if (ea && eb) Ke[(ra + D) * ND + cb + D] = Kee;
+#pragma unroll
+      for (int i = 0; i < D; ++i) sm[SM::UV + a * DB + i] = u[i];
+      sm[SM::UV + a * DB + D] = v;
     }
-    // residual (Eqs. 11e, 11f)
-    for (int c = lane; c < ND; c += 32) {
-      const int a = mdof_node<T>(c), i = mdof_comp<T>(c);
+    // residual (Eqs. 11e, 11f), from the records before the staging overwrites them
+    double* Ke;
+    double* Fe;
+    out(k, Ke, Fe);
+    if (lane < ND) {
+      const int a = mdof_node<T>(lane), i = mdof_comp<T>(lane);
       double f = 0.0;
       if (i < D) {
 #pragma unroll
@@ -321,9 +372,85 @@ k_mixed_blocks(DevMat m, int64_t ne, const int32_t* __restrict__ conn, const dou
 #pragma unroll
         for (int g = 0; g < NGP; ++g) f += sm[SM::ER + (g * NENE + a) * ER::STRIDE + ER::FE];
       }
-      EF[e * ND + c] = f;
+      Fe[lane] = f;
     }
     __syncwarp();
+    // off-diagonal blocks into the staging: Ke itself (local dof order, row-major)
+    double* st = sm + SM::UR;
+    auto stg = [&](int a, int b, int i, int j) -> double& { return st[(mldof<T>(a) + i) * ND + mldof<T>(b) + j]; };
+    if (lane < SM::NP) {
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          stg(pa, pb, i, j) = Kuu[i][j];
+          stg(pb, pa, j, i) = Kuu[i][j];
+        }
+        if (cb) stg(pa, pb, i, D) = Kue_ab[i];
+        if (ca) stg(pb, pa, i, D) = Kue_ba[i];
+        if (ca) stg(pa, pb, D, i) = Keu_ab[i];
+        if (cb) stg(pb, pa, D, i) = Keu_ba[i];
+      }
+      if (cb) {
+        stg(pa, pb, D, D) = Kee_ab;
+        stg(pb, pa, D, D) = Kee_ba;
+      }
+    }
+    __syncwarp();
+    // diagonal blocks: coupling - the row's other blocks, ascending b
+    for (int t = lane; t < NENU * DB * DB; t += 32) {
+      const int a = t / (DB * DB), i = (t / DB) % DB, j = t % DB;
+      if (a >= NENE && (i == D || j == D)) continue;   // midsides carry no ebar
+      const double* row = st + (mldof<T>(a) + i) * ND + j;
+      const int bmax = j < D ? NENU : NENE;            // ebar columns: corners only
+      double sum = 0.0;
+      for (int b = 0; b < bmax; ++b)
+        if (b != a) sum += row[mldof<T>(b)];
+      const double c = j == D ? sm[SM::UV + a * DB + i] : 0.0;
+      st[(mldof<T>(a) + i) * ND + mldof<T>(a) + j] = c - sum;
+    }
+    __syncwarp();
+    // Ke out: a straight copy of the staging (16-byte vectors, coalesced)
+    if constexpr ((ND * ND) % 2 == 0) {   // QUAD8: every element's Ke is 16-byte aligned
+      const double2* s2 = reinterpret_cast<const double2*>(st);
+      double2* k2 = reinterpret_cast<double2*>(Ke);
+      for (int t = lane; t < ND * ND / 2; t += 32) k2[t] = s2[t];
+    } else {
+      for (int t = lane; t < ND * ND; t += 32) Ke[t] = st[t];
+    }
+    __syncwarp();
+  }
+}
+
+template <int T, int WPB>
+__global__ void __launch_bounds__(WPB * 32)
+k_mixed_blocks(DevMat m, int64_t ne, const int32_t* __restrict__ conn, const double* __restrict__ coords,
+               const int32_t* __restrict__ gdof, const double* __restrict__ dofs,
+               const double* __restrict__ kappa, const double* __restrict__ k0g,
+               const double* __restrict__ alg, double* __restrict__ EB, double* __restrict__ EF) {
+  using F = MFam<T>;
+  constexpr int ND = F::NDOFE;
+  using SM = MSmem<T>;
+  extern __shared__ double smem_mx[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  // the shape table in shared memory: lanes read different Gauss points (divergent constant
+  // cache reads would serialise)
+  MShape<T>& S = *reinterpret_cast<MShape<T>*>(smem_mx);
+  constexpr int TBL = (int(sizeof(MShape<T>)) / 8 + 1) & ~1;
+  for (int k = threadIdx.x; k < int(sizeof(MShape<T>)) / 8; k += blockDim.x)
+    smem_mx[k] = reinterpret_cast<const double*>(&mshape<T>())[k];
+  __syncthreads();
+  double* sm = smem_mx + TBL + w * SM::SIZE;
+  // two elements per warp pass (e, e + stride)
+  const int64_t stride = int64_t(gridDim.x) * WPB;
+  for (int64_t e = int64_t(blockIdx.x) * WPB + w; e < ne; e += 2 * stride) {
+    const int64_t e1 = e + stride < ne ? e + stride : -1;
+    mixed_elements<T>(m, S, sm, lane, e, e1, conn, coords, gdof, dofs, kappa, k0g, alg,
+                      [&](int k, double*& Ke, double*& Fe) {
+                        const int64_t ek = k ? e1 : e;
+                        Ke = EB + ek * (ND * ND);
+                        Fe = EF + ek * ND;
+                      });
   }
 }
 

@@ -114,3 +114,27 @@ def compare_rows(ref_rows, got_rows, what=""):
                         val=ref_rows["val"], R=ref_rows["R"], S=ref_rows["S"]),
                    dict(row_ptr=got_rows["row_ptr"], col_idx=got_rows["col_idx"],
                         val=got_rows["val"], R=got_rows["R"]), what)
+
+
+def record_groups(W):
+    """component groups of a state record [eps_v, d eeq/d eps_v, sigma, eeq, ebar, kappa, D, g]"""
+    nv = (W - 5) // 3
+    strain = list(range(nv)) + [3 * nv, 3 * nv + 1, 3 * nv + 2]
+    return [strain, list(range(nv, 2 * nv)), list(range(2 * nv, 3 * nv)), [3 * nv + 3, 3 * nv + 4]]
+
+
+def check_records(W, got, ref):
+    """state records (lgdm_update_state) against the oracle's: per GP record and component
+    group, within 1e-12 of the group's largest magnitude in that record"""
+    got = got.reshape(-1, W)
+    ref = ref.reshape(-1, W)
+    worst, where = 0.0, None
+    for grp in record_groups(W):
+        scale = np.maximum(np.abs(ref[:, grp]).max(axis=1, keepdims=True), 1e-300)   # per record
+        err = np.abs(got[:, grp] - ref[:, grp]) / scale
+        if err.max() > worst:
+            worst = float(err.max())
+            r, c = np.unravel_index(err.argmax(), err.shape)
+            where = (int(r), grp[c])
+    assert worst <= 1e-12, f"worst {worst:.3e} at (GP record, component) {where}"
+    return worst

@@ -2,8 +2,10 @@
 l.8-14, Fig. 9a) and of the per-GP defect fields (lgdm_set_defects) against the CPU
 oracle, through the C ABI.
 
-Tolerances: every record component within 1e-12 of that component's largest magnitude over
-the mesh (the FP64 evaluation orders differ); the committed history within 1e-13 relative
+Tolerances (the per-row rule of the K parity carried to the records): within every GP record,
+each component within 1e-12 of the largest magnitude of its group in THAT record -- strains
+(eps_v, eeq, ebar, kappa), d eeq / d eps_v, stresses, damage (D, g) -- (the FP64 evaluation
+orders differ); the committed history within 1e-13 relative
 (a copy of ebar -- interpolated in a different FMA order -- or of kappa_hist; both sides take
 the same threshold decision on inputs kept away from it); K / R of the defect-field assembly
 as in parity.py.
@@ -15,7 +17,7 @@ import oracle
 import synth
 from paper_2301_06503_b200 import lgdm
 
-from parity import compare
+from parity import check_records, compare
 
 pytestmark = pytest.mark.gpu
 
@@ -40,15 +42,6 @@ def _defects(kappa, seed):
     return k0, al
 
 
-def _check_records(etype, got, ref):
-    W = oracle.sdv_width(etype)
-    got = got.reshape(-1, W)
-    ref = ref.reshape(-1, W)
-    scale = np.maximum(np.abs(ref).max(axis=0), 1e-300)
-    err = np.abs(got - ref) / scale
-    assert err.max() <= 1e-12, f"worst {err.max():.3e} in component {np.unravel_index(err.argmax(), err.shape)[1]}"
-
-
 @pytest.mark.parametrize("etype,n", CASES)
 @pytest.mark.parametrize("defects", [False, True])
 def test_update_state_parity(etype, n, defects):
@@ -63,7 +56,7 @@ def test_update_state_parity(etype, n, defects):
         m.set_defects(k0, al)
     got = m.update_state()
     torch.cuda.synchronize()
-    _check_records(etype, got.cpu().numpy(), ref)
+    check_records(oracle.sdv_width(etype), got.cpu().numpy(), ref)
     np.testing.assert_allclose(m.get_kappa().reshape(-1), kref.reshape(-1), rtol=1e-13, atol=0)
     # the record's kappa is the committed history
     W = oracle.sdv_width(etype)
@@ -272,3 +265,40 @@ def test_mesh_on_every_visible_device():
     assert len(outs) >= 1
     for v in outs[1:]:
         np.testing.assert_array_equal(v, outs[0])
+
+
+def _state_sample(cfg, n_elems, rng):
+    """elements of the bench-size state check: random ones plus the first / last element
+    layers and the x / y boundary columns"""
+    nx = cfg.n[0]
+    per = int(np.prod(cfg.n[:-1]))
+    sel = [rng.integers(0, n_elems, 20000), np.arange(min(per, 2000)),
+           np.arange(max(n_elems - per, 0), n_elems)[:2000],
+           np.arange(0, n_elems, nx)[:3000], np.arange(nx - 1, n_elems, nx)[:3000]]
+    return np.unique(np.concatenate(sel).astype(np.int64))
+
+
+@pytest.mark.parametrize("cid", [2, 4])
+def test_update_state_bench_size_sampled(cid):
+    """lgdm_update_state at the bench's sizes (BASELINE config 2: Q4 1000^2; config 4: Hex8
+    200^3, 64 M GP records) through the same call the bench times; ~3e4 sampled elements'
+    records (random + boundary layers / columns) against the oracle, per-record groups as
+    above, and the committed history of the sampled GPs."""
+    import torch
+    cfg = synth.CONFIGS[cid]
+    mesh = synth.structured_mesh(cfg)
+    dofs, kappa = synth.fields(cfg, mesh)
+    ngp = kappa.reshape(mesh.conn.shape[0], -1).shape[1]
+    m = lgdm.Mesh(cfg.etype, mesh.coords, mesh.conn, lgdm.material(**synth.MATERIAL))
+    m.set_state(dofs, kappa)
+    got = m.update_state()
+    torch.cuda.synchronize()
+    sel = _state_sample(cfg, mesh.conn.shape[0], np.random.default_rng(11 + cid))
+    got_s = got[torch.as_tensor(sel, device=got.device)].cpu().numpy()
+    kap_s = m.get_kappa().reshape(-1, ngp)[sel]
+    m.close()
+    ref, kref = oracle.update_state(cfg.etype, oracle.material(**synth.MATERIAL), mesh.coords,
+                                    mesh.conn[sel], dofs, kappa.reshape(-1, ngp)[sel])
+    worst = check_records(oracle.sdv_width(cfg.etype), got_s, ref)
+    np.testing.assert_allclose(kap_s.reshape(-1), kref.reshape(-1), rtol=1e-13, atol=0)
+    print(f"config {cid}: {sel.size} sampled elements, worst record error / group max {worst:.2e}")
