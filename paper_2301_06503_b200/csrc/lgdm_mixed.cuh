@@ -96,8 +96,9 @@ template <int T> struct MSmem {
 };
 
 // Element tangent Ke [NDOFE][NDOFE] (local dof order, row-major) and residual Fe [NDOFE] of up
-// to two elements (e1 < 0: one), by one warp.  out(k, Ke, Fe) supplies element k's output
-// pointers (HBM scratch or shared memory).
+// to two elements (e1 < 0: one), by one warp, from their coordinates / dofs staged in sm[XU]
+// (MInputs::store + __syncwarp).  out(k, Ke, Fe) supplies element k's output pointers (HBM
+// scratch or shared memory).
 //   * GP cores of both elements in one pass: lanes 16 k + g (two elements' 2 x NGP lanes);
 //   * per element: per-(GP, node) records; one lane per node pair a < b Gauss-sums K_ab and
 //     K_ba together (Kuu_ba = Kuu_ab^T: the integrand lam gA gB^T + Ams (gA SgB^T + SgA gB^T) +
@@ -106,12 +107,46 @@ template <int T> struct MSmem {
 //     = 1 for the u and the ebar families alike): Kuu_aa = -sum_{b!=a} Kuu_ab,
 //     Keu_aa = -sum_{b!=a} Keu_ab, Kue_aa = U_a - sum_{b!=a corner} Kue_ab with
 //     U_a = sum_g W' grad N_a, Kee_aa = V_a - sum_{b!=a corner} Kee_ab with V_a = sum_g E_a.
+// Inputs of an element pair, software-pipelined by the caller: each lane holds <= 3 of the
+// 2 x NPE values (coordinates, element dofs); the gather indices are loaded one pass before
+// the values, the values one pass before they are used.
+template <int T> struct MInputs {
+  static constexpr int NPE = MSmem<T>::NPE, NQ = (2 * NPE + 31) / 32;
+  int64_t idx[NQ];
+  double v[NQ];
+  // global index of value t of the pair (e0, e1): coords or dofs offset, -1 = none
+  __device__ __forceinline__ void load_idx(int lane, int64_t e0, int64_t e1, const int32_t* __restrict__ conn,
+                                           const int32_t* __restrict__ gdof) {
+    constexpr int D = MFam<T>::DIM, NENU = MFam<T>::NENU, ND = MFam<T>::NDOFE;
+#pragma unroll
+    for (int u = 0; u < NQ; ++u) {
+      const int t = lane + 32 * u;
+      const int k = t >= NPE ? 1 : 0, q = t - k * NPE;
+      const int64_t e = k ? e1 : e0;
+      idx[u] = -1;
+      if (t < 2 * NPE && e >= 0)
+        idx[u] = q < NENU * D ? int64_t(conn[e * NENU + q / D]) * D + q % D : int64_t(gdof[e * ND + q - NENU * D]);
+    }
+  }
+  __device__ __forceinline__ void load_vals(int lane, const double* __restrict__ coords,
+                                            const double* __restrict__ dofs) {
+    constexpr int D = MFam<T>::DIM, NENU = MFam<T>::NENU;
+#pragma unroll
+    for (int u = 0; u < NQ; ++u) {
+      const int q = (lane + 32 * u) % NPE;
+      v[u] = idx[u] < 0 ? 0.0 : (q < NENU * D ? coords[idx[u]] : dofs[idx[u]]);
+    }
+  }
+  __device__ __forceinline__ void store(int lane, double* sm) const {
+#pragma unroll
+    for (int u = 0; u < NQ; ++u)
+      if (lane + 32 * u < 2 * NPE) sm[MSmem<T>::XU + lane + 32 * u] = v[u];
+  }
+};
+
 template <int T, class OUT>
 __device__ __forceinline__ void mixed_elements(const DevMat& m, const MShape<T>& S, double* sm, int lane,
-                                               int64_t e0, int64_t e1, const int32_t* __restrict__ conn,
-                                               const double* __restrict__ coords,
-                                               const int32_t* __restrict__ gdof,
-                                               const double* __restrict__ dofs,
+                                               int64_t e0, int64_t e1,
                                                const double* __restrict__ kappa,
                                                const double* __restrict__ k0g,
                                                const double* __restrict__ alg, OUT&& out) {
@@ -122,17 +157,7 @@ __device__ __forceinline__ void mixed_elements(const DevMat& m, const MShape<T>&
   using UR = MURec<D>;
   using ER = MERec<D>;
   using Co = Core<D>;
-  // gather coordinates and element dofs of both elements
-  for (int t = lane; t < 2 * SM::NPE; t += 32) {
-    const int k = t >= SM::NPE ? 1 : 0, q = t - k * SM::NPE;
-    const int64_t e = k ? e1 : e0;
-    if (e < 0) continue;
-    double v;
-    if (q < NENU * D) v = coords[int64_t(conn[e * NENU + q / D]) * D + q % D];
-    else v = dofs[gdof[e * ND + q - NENU * D]];   // gdof: host table
-    sm[SM::XU + t] = v;
-  }
-  __syncwarp();
+  // (coordinates and element dofs of both elements are in sm[XU], see MInputs)
   // GP cores: geometry on the u nodes (R-GEO), kinematics, Appendix A law
   {
     const int k = lane >> 4, g = lane & 15;
@@ -397,15 +422,26 @@ __device__ __forceinline__ void mixed_elements(const DevMat& m, const MShape<T>&
       }
     }
     __syncwarp();
-    // diagonal blocks: coupling - the row's other blocks, ascending b
-    for (int t = lane; t < NENU * DB * DB; t += 32) {
-      const int a = t / (DB * DB), i = (t / DB) % DB, j = t % DB;
-      if (a >= NENE && (i == D || j == D)) continue;   // midsides carry no ebar
+    // diagonal blocks: coupling - the row's other blocks, ascending b.  Entries (a, i, j):
+    // corners DB x DB, midsides D x D, enumerated corners first
+    constexpr int NDG = NENE * DB * DB + (NENU - NENE) * D * D;
+    for (int t = lane; t < NDG; t += 32) {
+      int a, i, j;
+      if (t < NENE * DB * DB) {
+        a = t / (DB * DB);
+        i = (t / DB) % DB;
+        j = t % DB;
+      } else {
+        const int u = t - NENE * DB * DB;
+        a = NENE + u / (D * D);
+        i = (u / D) % D;
+        j = u % D;
+      }
       const double* row = st + (mldof<T>(a) + i) * ND + j;
-      const int bmax = j < D ? NENU : NENE;            // ebar columns: corners only
       double sum = 0.0;
-      for (int b = 0; b < bmax; ++b)
-        if (b != a) sum += row[mldof<T>(b)];
+#pragma unroll
+      for (int b = 0; b < NENU; ++b)   // ebar columns (j == D): corners only
+        if (b != a && (j < D || b < NENE)) sum += row[mldof<T>(b)];
       const double c = j == D ? sm[SM::UV + a * DB + i] : 0.0;
       st[(mldof<T>(a) + i) * ND + mldof<T>(a) + j] = c - sum;
     }
@@ -441,11 +477,22 @@ k_mixed_blocks(DevMat m, int64_t ne, const int32_t* __restrict__ conn, const dou
     smem_mx[k] = reinterpret_cast<const double*>(&mshape<T>())[k];
   __syncthreads();
   double* sm = smem_mx + TBL + w * SM::SIZE;
-  // two elements per warp pass (e, e + stride)
+  // two elements per warp pass (e, e + stride); inputs pipelined (MInputs)
   const int64_t stride = int64_t(gridDim.x) * WPB;
-  for (int64_t e = int64_t(blockIdx.x) * WPB + w; e < ne; e += 2 * stride) {
-    const int64_t e1 = e + stride < ne ? e + stride : -1;
-    mixed_elements<T>(m, S, sm, lane, e, e1, conn, coords, gdof, dofs, kappa, k0g, alg,
+  auto second = [&](int64_t e) { return e < ne && e + stride < ne ? e + stride : int64_t(-1); };
+  auto first = [&](int64_t e) { return e < ne ? e : int64_t(-1); };
+  int64_t e = int64_t(blockIdx.x) * WPB + w;
+  MInputs<T> in;
+  in.load_idx(lane, first(e), second(e), conn, gdof);
+  in.load_vals(lane, coords, dofs);
+  in.load_idx(lane, first(e + 2 * stride), second(e + 2 * stride), conn, gdof);
+  for (; e < ne; e += 2 * stride) {
+    const int64_t e1 = second(e);
+    in.store(lane, sm);
+    __syncwarp();
+    in.load_vals(lane, coords, dofs);                                          // pass + 1
+    in.load_idx(lane, first(e + 4 * stride), second(e + 4 * stride), conn, gdof);   // pass + 2
+    mixed_elements<T>(m, S, sm, lane, e, e1, kappa, k0g, alg,
                       [&](int k, double*& Ke, double*& Fe) {
                         const int64_t ek = k ? e1 : e;
                         Ke = EB + ek * (ND * ND);

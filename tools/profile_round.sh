@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round evidence (B200_PROFILING.md recipe): plain runs first, then
 #   1. the launch list of a short bench (gpu__time_duration per launch, --clock-control none);
-#   2. ncu --set full of k_sweep4 (config 3) and k_sweepq (config 2);
+#   2. ncu --set full of k_sweep4 (configs 3 and 4, the bench workload) and k_sweepq (config 2);
 # and traffic.json (DRAM bytes per launch keyed by workload, with the kernel-source sha that
 # bench.py checks).  Output under gpurun_out/prof_round/.
 set -u
@@ -10,7 +10,7 @@ mkdir -p $OUT
 python bench.py --steps 2 --warmup 3 --no-secondary --no-cpu-baseline > $OUT/bench_plain.json 2> $OUT/bench_plain.err && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches_c4.csv \
     python bench.py --steps 2 --warmup 3 --no-secondary --no-cpu-baseline > $OUT/ncu_launch.log 2>&1
-for spec in "3 k_sweep4 sweep4_c3" "2 k_sweepq sweepq_c2"; do
+for spec in "4 k_sweep4 sweep4_c4" "3 k_sweep4 sweep4_c3" "2 k_sweepq sweepq_c2"; do
   set -- $spec
   python tools/assemble_once.py $1 0 > $OUT/plain_$3.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:$2 -c 1 -o $OUT/prof_$3 \
@@ -21,7 +21,8 @@ import csv, json, subprocess, sys
 sys.path.insert(0, ".")
 import bench
 out = {}
-for cid, k, tag, wl in ((3, "k_sweep4", "sweep4_c3", "hex8_100^3"), (2, "k_sweepq", "sweepq_c2", "q4_1000x1000")):
+for cid, k, tag, wl in ((4, "k_sweep4", "sweep4_c4", "hex8_200^3"), (3, "k_sweep4", "sweep4_c3", "hex8_100^3"),
+                       (2, "k_sweepq", "sweepq_c2", "q4_1000x1000")):
     r = subprocess.run(["ncu", "-i", f"gpurun_out/prof_round/prof_{tag}.ncu-rep", "--page", "raw", "--csv"],
                        capture_output=True, text=True).stdout
     rows = list(csv.reader(r.splitlines()))
