@@ -120,7 +120,10 @@ typedef struct {   /* mixed-order meshes: nen = u nodes, ndpn = dofs of a corner
  *   device: CUDA ordinal; cuda_stream: cudaStream_t (NULL = legacy default stream).
  * Builds the CSR pattern (reading R-PAT) and the element->CSR maps once.  det J <= 0 at any
  * GP -> LGDM_ERR_INVERTED_ELEMENT.  Connectivity of an x-fastest structured grid (any
- * coordinates) is detected and enables the fused sweep kernels. */
+ * coordinates) is detected and enables the fused sweep kernels.  Rejected with
+ * LGDM_ERR_INVALID_ARGUMENT before any device work: an empty mesh (n_elems < 1 or n_nodes < 2),
+ * an empty or out-of-range owned range, conn entries outside [0, n_nodes), NULL inputs, an
+ * unknown type, an invalid material; no CUDA device -> LGDM_ERR_CUDA (there is no CPU path). */
 lgdm_status lgdm_create_mesh(lgdm_elem_type type, int64_t n_nodes, const double* coords,
                              int64_t n_elems, const int64_t* conn, const lgdm_material* mat,
                              int64_t global_node_offset, int64_t n_global_nodes,
