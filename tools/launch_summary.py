@@ -27,4 +27,4 @@ def main(path, title):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else path)
+    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else sys.argv[1])

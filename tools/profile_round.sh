@@ -37,7 +37,7 @@ for cid, k, tag, wl in ((4, "k_sweep4", "sweep4_c4", "hex8_200^3"), (3, "k_sweep
     etype = 3 if tag.startswith("sweep4") else 2
     out[wl] = {"bytes": num("dram__bytes_read.sum") + num("dram__bytes_write.sum"), "kernel": k,
                "src_sha": bench.kernel_source_sha(etype, 0), "profile": f"prof_{tag}.ncu-rep",
-               "duration_ms": float(d["gpu__time_duration.sum"].replace(",", "")) * {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}[rows[1][rows[0].index("gpu__time_duration.sum")]]}
+               "duration_ms": float(d["gpu__time_duration.sum"].replace(",", "")) * {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0, "second": 1e3, "s": 1e3}[rows[1][rows[0].index("gpu__time_duration.sum")]]}
 json.dump(out, open("gpurun_out/prof_round/traffic.json", "w"), indent=1)
 print(json.dumps(out, indent=1))
 PY
