@@ -319,7 +319,16 @@ def run_lgdm(cfg, steps, warmup, rank, world, local, pg_barrier, allmax, comm_ui
         res["state_bytes"] = (ne_l * nen * 4 + nn_l * (dim + ndpn) * 8 +
                               ne_l * ngp * (16 + W * 8))
         res["state_width"] = W
-        del buf
+        # branch mix of the workload's GPs, from the records just written:
+        # loading = the history moved (kappa = ebar > kappa_hist), damaged = D > 0
+        nv = (W - 5) // 3
+        rec = buf.view(-1, W)
+        kh = kappa_d.view(-1)
+        res["branch_mix"] = {
+            "loading_pct": float((rec[:, 3 * nv + 2] != kh).double().mean()) * 100.0,
+            "damaged_pct": float((rec[:, 3 * nv + 3] > 0).double().mean()) * 100.0,
+            "gps": int(kh.numel()), "from": "lgdm_update_state records of the bench state (dofs_0)"}
+        del buf, rec
     m.close()
     return res
 
@@ -614,6 +623,8 @@ def main():
             "ms": r["state_ms"], "elements_per_s": n_total / (r["state_ms"] * 1e-3),
             "roofline": {"bound": "hbm", "achieved": sa, "peak": peak, "unit": "GB/s",
                          "frac": sa / peak, "algorithmic_bytes": r["state_bytes"]}}
+        if "branch_mix" in r:
+            out["state_update"]["branch_mix"] = r["branch_mix"]
     if ws == 1 and rank == 0:
         if not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(cfg)
