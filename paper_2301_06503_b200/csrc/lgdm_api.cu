@@ -183,6 +183,8 @@ struct lgdm_mesh_s {
   int64_t* base = nullptr;      // [n_owned] val offset of the node's first row
   int64_t* adj_ptr = nullptr;   // [n_owned+1]
   AdjEntry* adj = nullptr;      // general-path element->CSR map
+  int64_t* react_buf = nullptr;  // lgdm_reaction: owned row ids + the sum (grown on demand)
+  int64_t react_cap = 0;
   double* scratchK = nullptr;   // general path element blocks
   double* scratchF = nullptr;
   double* sumsq_part = nullptr; // [kSumBlocks*2]
@@ -1441,18 +1443,23 @@ lgdm_status lgdm_reaction(lgdm_mesh m, int64_t n, const int64_t* dof_ids, double
   }
   CU(cudaSetDevice(m->device));
   const int64_t nr = int64_t(rows.size());
-  int64_t* ids = nullptr;
-  CU(dalloc(&ids, size_t(std::max<int64_t>(nr, 1)) + 1));   // + 1 double-sized slot for the sum
-  double* sum = reinterpret_cast<double*>(ids + std::max<int64_t>(nr, 1));
+  if (m->react_cap < nr + 1) {   // the mesh's buffer, grown (never per call)
+    CU(cudaStreamSynchronize(m->stream));
+    if (m->react_buf) cudaFree(m->react_buf);
+    m->react_buf = nullptr;
+    m->react_cap = 0;
+    const int64_t cap = std::max<int64_t>(2 * (nr + 1), 64);
+    CU(dalloc(&m->react_buf, size_t(cap)));
+    m->react_cap = cap;
+  }
+  int64_t* ids = m->react_buf;
+  double* sum = reinterpret_cast<double*>(ids + nr);   // one double-sized slot after the ids
   if (nr) CU(cudaMemcpyAsync(ids, rows.data(), size_t(nr) * 8, cudaMemcpyHostToDevice, m->stream));
   k_reaction<<<1, 256, 0, m->stream>>>(nr, ids, m->R, sum);
   ++m->launches;
   s = allreduce_sum(m, sum, 1);
-  if (s == LGDM_OK) {
-    cudaMemcpyAsync(out, sum, 8, cudaMemcpyDeviceToHost, m->stream);
-    cudaStreamSynchronize(m->stream);
-  }
-  cudaFree(ids);
+  if (s == LGDM_OK) cudaMemcpyAsync(out, sum, 8, cudaMemcpyDeviceToHost, m->stream);
+  cudaStreamSynchronize(m->stream);   // `rows` and `out` are the caller's / this frame's
   return s;
 }
 
@@ -1777,7 +1784,7 @@ void lgdm_destroy(lgdm_mesh m) {
                   m->sumsq_part, m->sumsq_out, m->k0g, m->alg, m->sdv_dev, m->rp_b,
                   m->ci_b, m->val_b, m->R_b, m->sol, m->sol_part, m->fixed, m->fixinc,
                   m->doff, m->dkind, m->madj_ptr, m->madj, m->bperm, m->binv, m->dofs_back, m->gdof,
-                  m->rp32};
+                  m->rp32, m->react_buf};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (m->host_pinned) cudaFreeHost(m->host_pinned);
