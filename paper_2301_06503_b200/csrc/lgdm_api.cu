@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <nvtx3/nvToolsExt.h>
 #include <mutex>
 #include <set>
 #include <string>
@@ -151,6 +152,15 @@ FamInfo fam_info(int type) {
     default: return {3, 8, 4, 8, 32, 27};
   }
 }
+
+// NVTX ranges around the ABI calls (header-only NVTX3: inert unless a tool such as Nsight
+// Systems is attached), so a trace shows create / assemble / step / solve phases by name
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 template <class T> cudaError_t dalloc(T** p, size_t count) {
   *p = nullptr;
@@ -813,6 +823,7 @@ lgdm_status lgdm_create_mesh(lgdm_elem_type type, int64_t n_nodes, const double*
                              int64_t global_node_offset, int64_t n_global_nodes,
                              int64_t owned_node_begin, int64_t owned_node_end, int device,
                              void* cuda_stream, lgdm_mesh* out) {
+  const NvtxRange nvtx_range("lgdm_create_mesh");
   if (!out) return fail(LGDM_ERR_INVALID_ARGUMENT, "out is NULL");
   *out = nullptr;
   if ((type == LGDM_BAR3 || type == LGDM_QUAD8) && global_node_offset != 0)
@@ -926,6 +937,7 @@ lgdm_status lgdm_create_mesh_mixed(lgdm_elem_type type, int64_t n_nodes, const d
                                    int64_t owned_node_begin, int64_t owned_node_end,
                                    int64_t global_dof_offset, int64_t n_global_dofs, int device,
                                    void* cuda_stream, lgdm_mesh* out) {
+  const NvtxRange nvtx_range("lgdm_create_mesh_mixed");
   if (!out) return fail(LGDM_ERR_INVALID_ARGUMENT, "out is NULL");
   *out = nullptr;
   if (type != LGDM_BAR3 && type != LGDM_QUAD8)
@@ -1031,6 +1043,7 @@ lgdm_status lgdm_set_state_prefetched(lgdm_mesh m) {
 }
 
 lgdm_status lgdm_assemble(lgdm_mesh m, lgdm_csr* K, double** R) {
+  const NvtxRange nvtx_range("lgdm_assemble");
   if (!m) return fail(LGDM_ERR_INVALID_ARGUMENT, "mesh is NULL");
   if (!m->have_state || !m->have_kappa) return fail(LGDM_ERR_INVALID_STATE, "assemble before set_state");
   CU(cudaSetDevice(m->device));
@@ -1060,6 +1073,7 @@ lgdm_status lgdm_assemble(lgdm_mesh m, lgdm_csr* K, double** R) {
 }
 
 lgdm_status lgdm_update_history(lgdm_mesh m) {
+  const NvtxRange nvtx_range("lgdm_update_history");
   if (!m) return fail(LGDM_ERR_INVALID_ARGUMENT, "mesh is NULL");
   if (!m->have_state || !m->have_kappa) return fail(LGDM_ERR_INVALID_STATE, "update_history before set_state");
   CU(cudaSetDevice(m->device));
@@ -1115,6 +1129,7 @@ lgdm_status lgdm_set_defects(lgdm_mesh m, const double* kappa0_gp, const double*
 }
 
 lgdm_status lgdm_update_state(lgdm_mesh m, double* sdv, int64_t n_sdv, int dst_on_device) {
+  const NvtxRange nvtx_range("lgdm_update_state");
   if (!m) return fail(LGDM_ERR_INVALID_ARGUMENT, "mesh is NULL");
   if (!m->have_state || !m->have_kappa) return fail(LGDM_ERR_INVALID_STATE, "update_state before set_state");
   const int W = lgdm_sdv_width(lgdm_elem_type(m->type));
@@ -1311,6 +1326,7 @@ lgdm_status lgdm_apply_dirichlet(lgdm_mesh m, int64_t n_fixed, const int64_t* do
 
 lgdm_status lgdm_solve(lgdm_mesh m, double* delta, double tol, int max_iter, int* iters_out,
                        double* relres_out) {
+  const NvtxRange nvtx_range("lgdm_solve");
   if (!m) return fail(LGDM_ERR_INVALID_ARGUMENT, "mesh is NULL");
   if (!m->assembled) return fail(LGDM_ERR_INVALID_STATE, "solve before assemble");
   lgdm_status s = newton_ready(m);
@@ -1464,6 +1480,7 @@ lgdm_status lgdm_reaction(lgdm_mesh m, int64_t n, const int64_t* dof_ids, double
 }
 
 lgdm_status lgdm_solve_direct(lgdm_mesh m, double* delta, int* singularity) {
+  const NvtxRange nvtx_range("lgdm_solve_direct");
   if (!m || !delta) return fail(LGDM_ERR_INVALID_ARGUMENT, "mesh / delta is NULL");
   if (!m->assembled) return fail(LGDM_ERR_INVALID_STATE, "solve before assemble");
   if (!whole_single_rank(m)) return fail(LGDM_ERR_UNSUPPORTED, "Newton pieces need a single-rank whole mesh");
@@ -1548,6 +1565,7 @@ lgdm_status lgdm_delta_ratios(lgdm_mesh m, const double* delta, double tol, doub
 }
 
 lgdm_status lgdm_residual_sumsq(lgdm_mesh m, double* out2, int on_device) {
+  const NvtxRange nvtx_range("lgdm_residual_sumsq");
   if (!m || !out2) return fail(LGDM_ERR_INVALID_ARGUMENT, "NULL argument");
   if (!m->assembled) return fail(LGDM_ERR_INVALID_STATE, "residual before assemble");
   CU(cudaSetDevice(m->device));
@@ -1568,6 +1586,7 @@ lgdm_status lgdm_residual_sumsq(lgdm_mesh m, double* out2, int on_device) {
 }
 
 lgdm_status lgdm_residual_norms(lgdm_mesh m, double out2[2]) {
+  const NvtxRange nvtx_range("lgdm_residual_norms");
   if (!m || !out2) return fail(LGDM_ERR_INVALID_ARGUMENT, "NULL argument");
   lgdm_status s = lgdm_residual_sumsq(m, m->sumsq_out, 1);
   if (s != LGDM_OK) return s;
@@ -1599,6 +1618,7 @@ static lgdm_status step_enqueue(lgdm_mesh m, bool hist) {
 }
 
 lgdm_status lgdm_step(lgdm_mesh m, int flags, double out2[2]) {
+  const NvtxRange nvtx_range("lgdm_step");
   if (!m || !out2) return fail(LGDM_ERR_INVALID_ARGUMENT, "NULL argument");
   if (flags & ~3) return fail(LGDM_ERR_INVALID_ARGUMENT, "unknown step flags %d", flags);
   if (!m->have_state || !m->have_kappa) return fail(LGDM_ERR_INVALID_STATE, "step before set_state");
