@@ -1149,8 +1149,9 @@ lgdm_status lgdm_update_state(lgdm_mesh m, double* sdv, int64_t n_sdv, int dst_o
   }
   constexpr int TPB = 128;
   const unsigned blocks = unsigned((ngp + TPB - 1) / TPB);
-  const size_t smem = out ? size_t(TPB) * W * sizeof(double) : 0;   // record staging
-  CU(set_smem_attr(k_update_state<3>, size_t(TPB) * StateW<3>::W * 8, m->device));
+  // record staging [TPB][W] + per-warp node values [TPB][dim + ndpn] (k_update_state)
+  const size_t smem = size_t(TPB) * (W + m->f.dim + m->f.ndpn) * sizeof(double);
+  CU(set_smem_attr(k_update_state<3>, size_t(TPB) * (StateW<3>::W + 7) * 8, m->device));
   if (m->mixed) {
     const size_t tbl = sizeof(double) * 400;   // >= the padded shape table of either family
     static_assert(sizeof(MShape<5>) <= 400 * sizeof(double) && sizeof(MShape<4>) <= 400 * sizeof(double), "table");

@@ -266,10 +266,10 @@ __device__ __forceinline__ void state_record(const DevMat& m, const double (&Gu)
     const double Qv = m.c2 * I1 * I1 + m.c3 * J2;
     const double sQ = sqrt(Qv);
     eeq = m.c1 * I1 + sQ / (2.0 * m.k);
+    const double r4k = Qv < 1e-30 ? 0.0 : 1.0 / (4.0 * m.k * sQ);   // reading R-SQ: no sqrt term
 #pragma unroll
     for (int V = 0; V < NV; ++V)
-      dv[V] = Qv < 1e-30 ? m.c1 * mv[V]                                   // reading R-SQ
-                         : m.c1 * mv[V] + (2.0 * m.c2 * I1 * mv[V] + m.c3 * sv[V]) / (4.0 * m.k * sQ);
+      dv[V] = m.c1 * mv[V] + (2.0 * m.c2 * I1 * mv[V] + m.c3 * sv[V]) * r4k;
   }
   // history (Fig. 9a l.22-24), damage (Eq. A.1, l.27-31), interaction (Eq. A.4)
   const double kap = (ebar - kh) > 1e-10 ? ebar : kh;
@@ -306,28 +306,43 @@ k_update_state(DevMat m, int64_t ne, const int32_t* __restrict__ conn,
                const double* __restrict__ alg, double* __restrict__ sdv) {
   using F = Fam<D>;
   constexpr int W = StateW<D>::W;
-  extern __shared__ double stage[];   // [blockDim][W]: records, written out coalesced
+  // a warp = 32 consecutive GPs = EPW whole elements = exactly 32 (element, node) slots
+  constexpr int EPW = 32 / F::NGP, NV = D + F::NDPN;   // node values: coords, dofs
+  static_assert(EPW * F::NEN == 32, "one node per lane");
+  extern __shared__ double stage[];   // [blockDim][W]: records, written out coalesced; then
+                                      // per warp [32][NV] node values
+  double* nodes = stage + blockDim.x * W + (threadIdx.x >> 5) * (32 * NV);   // [EPW][NEN][NV]
+  const int lane = threadIdx.x & 31;
   const int64_t t0 = int64_t(blockIdx.x) * blockDim.x;
   const int64_t t = t0 + threadIdx.x;
   const int64_t ngp = ne * F::NGP;
+  {
+    // each lane gathers one node of the warp's elements (one conn load, NV value loads),
+    // instead of every GP thread loading all nodes of its element
+    const int64_t ew = (t0 + (threadIdx.x & ~31)) / F::NGP + lane / F::NEN;
+    if (ew < ne) {
+      const int64_t n = conn[ew * F::NEN + lane % F::NEN];
+#pragma unroll
+      for (int i = 0; i < D; ++i) nodes[lane * NV + i] = __ldg(coords + n * D + i);
+#pragma unroll
+      for (int i = 0; i < F::NDPN; ++i) nodes[lane * NV + D + i] = __ldg(dofs + n * F::NDPN + i);
+    }
+    __syncwarp();
+  }
   if (t < ngp) {
-    const int64_t e = t / F::NGP;
     const int g = int(t % F::NGP);
-    const int32_t* ce = conn + e * F::NEN;
-    // geometry: J_ij = sum_a X_ai dN_a/dxi_j (node data streamed; the element's GP threads
-    // share the loads through L1)
+    const double* en = nodes + (lane / F::NGP) * (F::NEN * NV);   // this element's nodes
+    // geometry: J_ij = sum_a X_ai dN_a/dxi_j
     double J[D][D];
 #pragma unroll
     for (int i = 0; i < D; ++i)
 #pragma unroll
       for (int j = 0; j < D; ++j) J[i][j] = 0.0;
-    const int64_t n0 = ce[0];
 #pragma unroll
     for (int a = 1; a < F::NEN; ++a) {        // relative to node 0 (reading R-REL)
-      const int64_t n = ce[a];
 #pragma unroll
       for (int i = 0; i < D; ++i) {
-        const double x = __ldg(coords + n * D + i) - __ldg(coords + n0 * D + i);
+        const double x = en[a * NV + i] - en[i];
 #pragma unroll
         for (int j = 0; j < D; ++j) J[i][j] = fma(x, shape_dxi<D>(a, g, j), J[i][j]);
       }
@@ -364,7 +379,6 @@ k_update_state(DevMat m, int64_t ne, const int32_t* __restrict__ conn,
       for (int j = 0; j < D; ++j) Gu[i][j] = 0.0;
 #pragma unroll
     for (int a = 0; a < F::NEN; ++a) {
-      const int64_t n = ce[a];
       double gn[D];
 #pragma unroll
       for (int j = 0; j < D; ++j) {
@@ -375,11 +389,11 @@ k_update_state(DevMat m, int64_t ne, const int32_t* __restrict__ conn,
       }
 #pragma unroll
       for (int i = 0; i < D; ++i) {
-        const double u = __ldg(dofs + n * F::NDPN + i) - __ldg(dofs + n0 * F::NDPN + i);
+        const double u = en[a * NV + D + i] - en[D + i];
 #pragma unroll
         for (int j = 0; j < D; ++j) Gu[i][j] = fma(u, gn[j], Gu[i][j]);
       }
-      ebar = fma(shapeN<D>(a, g), __ldg(dofs + n * F::NDPN + D), ebar);
+      ebar = fma(shapeN<D>(a, g), en[a * NV + D + D], ebar);
     }
     double kap;
     state_record<D>(m, Gu, ebar, kappa[t], k0g ? k0g[t] : m.kappa0, alg ? alg[t] : m.alpha,
