@@ -327,6 +327,8 @@ DevMat derive(const lgdm_material& m, int dim) {
   d.c1 = (k - 1.0) / (2.0 * k * (1.0 - 2.0 * nu));
   d.c2 = ((k - 1.0) / (1.0 - 2.0 * nu)) * ((k - 1.0) / (1.0 - 2.0 * nu));
   d.c3 = m.eq_variant == 1 ? 2.0 * k / ((1.0 - nu) * (1.0 - nu)) : 12.0 * k / ((1.0 + nu) * (1.0 + nu));
+  d.i2k = 1.0 / (2.0 * k);
+  d.i4k = 1.0 / (4.0 * k);
   (void)dim;
   return d;
 }

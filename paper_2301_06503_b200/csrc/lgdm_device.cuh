@@ -28,6 +28,7 @@ struct DevMat {
   double n, ga, gb;        // g(D) = ga * exp(-n D) + gb   (Eq. A.4 rearranged)
   double t;                // area (1D) / thickness
   double c1, c2, c3;       // Eq. A.3 constants (reading R-A3)
+  double i2k, i4k;         // 1 / (2k), 1 / (4k) (host-side; the state record's law)
 };
 
 template <int D> struct Fam;

@@ -265,8 +265,8 @@ __device__ __forceinline__ void state_record(const DevMat& m, const double (&Gu)
     }
     const double Qv = m.c2 * I1 * I1 + m.c3 * J2;
     const double sQ = sqrt(Qv);
-    eeq = m.c1 * I1 + sQ / (2.0 * m.k);
-    const double r4k = Qv < 1e-30 ? 0.0 : 1.0 / (4.0 * m.k * sQ);   // reading R-SQ: no sqrt term
+    eeq = m.c1 * I1 + sQ * m.i2k;
+    const double r4k = Qv < 1e-30 ? 0.0 : m.i4k / sQ;   // reading R-SQ: no sqrt term
 #pragma unroll
     for (int V = 0; V < NV; ++V)
       dv[V] = m.c1 * mv[V] + (2.0 * m.c2 * I1 * mv[V] + m.c3 * sv[V]) * r4k;
