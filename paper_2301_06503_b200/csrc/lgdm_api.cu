@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <nvtx3/nvToolsExt.h>
+#include <chrono>
 #include <mutex>
 #include <set>
 #include <string>
@@ -160,6 +161,19 @@ struct NvtxRange {
   ~NvtxRange() { nvtxRangePop(); }
   NvtxRange(const NvtxRange&) = delete;
   NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
+// LGDM_CREATE_TIMING=1: per-phase wall times of lgdm_create_mesh on stderr (diagnostic)
+struct PhaseTimer {
+  bool on = getenv("LGDM_CREATE_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what, cudaStream_t st) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    const auto n = std::chrono::steady_clock::now();
+    fprintf(stderr, "[lgdm create] %-22s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
 };
 
 template <class T> cudaError_t dalloc(T** p, size_t count) {
@@ -826,6 +840,7 @@ lgdm_status lgdm_create_mesh(lgdm_elem_type type, int64_t n_nodes, const double*
                              int64_t owned_node_begin, int64_t owned_node_end, int device,
                              void* cuda_stream, lgdm_mesh* out) {
   const NvtxRange nvtx_range("lgdm_create_mesh");
+  PhaseTimer pt;
   if (!out) return fail(LGDM_ERR_INVALID_ARGUMENT, "out is NULL");
   *out = nullptr;
   if ((type == LGDM_BAR3 || type == LGDM_QUAD8) && global_node_offset != 0)
@@ -859,6 +874,7 @@ lgdm_status lgdm_create_mesh(lgdm_elem_type type, int64_t n_nodes, const double*
       return fail(LGDM_ERR_INVALID_ARGUMENT, "conn[%lld] = %lld out of range", (long long)bad_i,
                   (long long)conn[bad_i]);
   }
+  pt.mark("validate", nullptr);
 
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -896,6 +912,7 @@ lgdm_status lgdm_create_mesh(lgdm_elem_type type, int64_t n_nodes, const double*
   for (int64_t i = 0; i < int64_t(conn32.size()); ++i) conn32[i] = int32_t(conn[i]);
   if ((s = upload(m, &m->coords, coords, size_t(n_nodes) * f.dim)) != LGDM_OK) return bail(s);
   if ((s = upload(m, &m->conn, conn32.data(), conn32.size())) != LGDM_OK) return bail(s);
+  pt.mark("conn32 + upload", m->stream);
 
   // ---- det J > 0 at every GP ----
   unsigned long long* bad = nullptr;
@@ -914,9 +931,11 @@ lgdm_status lgdm_create_mesh(lgdm_elem_type type, int64_t n_nodes, const double*
   if (hbad != ~0ull)
     return bail(fail(LGDM_ERR_INVERTED_ELEMENT, "det J <= 0 in element %lld at Gauss point %d",
                      (long long)(hbad / f.ngp), int(hbad % f.ngp)));
+  pt.mark("det J", m->stream);
 
   // ---- pattern (reading R-PAT) and element maps, built on the GPU (lgdm_pattern.cuh) ----
   if ((s = build_pattern(m, global_node_offset)) != LGDM_OK) return bail(s);
+  pt.mark("pattern", m->stream);
   // ---- state, reductions ----
   if (dalloc(&m->dofs, size_t(n_nodes) * f.ndpn) != cudaSuccess ||
       dalloc(&m->kappa, size_t(n_elems) * f.ngp) != cudaSuccess ||
@@ -927,6 +946,7 @@ lgdm_status lgdm_create_mesh(lgdm_elem_type type, int64_t n_nodes, const double*
   }
   m->device_bytes += (n_nodes * f.ndpn + n_elems * f.ngp) * 8;
   m->structured = detect_structured(type, n_nodes, n_elems, conn, &m->nx, &m->ny, &m->nz);
+  pt.mark("state + structure", m->stream);
   ce = cudaStreamSynchronize(m->stream);
   if (ce != cudaSuccess) return bail(fail(LGDM_ERR_CUDA, "create: %s", cudaGetErrorString(ce)));
   *out = m;
