@@ -1,8 +1,8 @@
-// lgdm_sweep4.cuh -- Hex8 hot kernel (k_sweep4): the structured-sweep K/R assembly redesigned
-// from the ncu profile of k_sweep3 (profiles/r01).  Included by lgdm_sweep.cuh (needs
+// lgdm_sweep4.cuh -- Hex8 hot kernel (k_sweep4): the structured-sweep K/R assembly, designed
+// from the ncu profile of the round-1 sweep (profiles/r01).  Included by lgdm_sweep.cuh (needs
 // SweepGeom, node_off, plane_slot, Core/gpCore).
 //
-// Same contract as k_sweep3: one CTA owns TX x TY node columns and a chunk of node layers,
+// Contract (lgdm_sweep.cuh): one CTA owns TX x TY node columns and a chunk of node layers,
 // sweeps the element layers touching them (ghost elements recomputed), writes exactly the
 // CSR block-rows of its nodes; per-entry summation order = (element layer, colour), so K and
 // R are bitwise independent of tiling and slabbing.  What changed:

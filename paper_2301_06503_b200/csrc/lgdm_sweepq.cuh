@@ -2,7 +2,7 @@
 // plane-strain 4-node quads.  Included by lgdm_sweep.cuh (needs SweepGeom, node_off, Core<2>,
 // gpCore<2>, symv<2>, bsync/barrive from lgdm_sweep4.cuh).
 //
-// Contract as k_sweep3/k_sweep4: one CTA owns TX node columns (x) and a chunk of node rows
+// Contract as k_sweep4: one CTA owns TX node columns (x) and a chunk of node rows
 // (y, the sweep axis), sweeps the element rows touching them (ghost elements recomputed),
 // writes exactly the CSR block-rows of its nodes; per-entry summation order = (element row,
 // colour) only, so K and R are bitwise independent of tiling and slabbing.

@@ -1,4 +1,4 @@
-"""Debug helper: which nodes of a Q4 mesh disagree with the oracle (kernel 4)."""
+"""Debug helper: which nodes of a Q4 mesh disagree with the oracle (the sweep kernel)."""
 import sys
 import numpy as np
 sys.path.insert(0, 'tests'); sys.path.insert(0, '.')
@@ -10,7 +10,7 @@ cfg = synth.CONFIGS[cid]
 mesh = synth.structured_mesh(cfg)
 d, k = synth.fields(cfg, mesh)
 ref = oracle.assemble(cfg.etype, oracle.material(**synth.MATERIAL), mesh.coords, mesh.conn, d, k)
-got = gpu_assemble(cfg.etype, mesh.coords, mesh.conn, d, k, kernel=4)
+got = gpu_assemble(cfg.etype, mesh.coords, mesh.conn, d, k, kernel=lgdm.KERNEL_SWEEP)
 rp = ref['row_ptr']; nrows = rp.size - 1
 rows = np.repeat(np.arange(nrows), np.diff(rp))
 rowmax = np.zeros(nrows); np.maximum.at(rowmax, rows, np.abs(ref['val']))

@@ -1,4 +1,4 @@
-"""Per-phase cycle breakdown of k_sweep4 (debug build exp/lib_timing.so, -DLGDM_PHASE_TIMING):
+"""Per-phase cycle breakdown of k_sweep4 (debug build lib_timing.so from tools/build_timing.sh):
 thread 0 of the PC role and of the C role accumulate clock64 deltas per phase."""
 import ctypes as C
 import os
@@ -6,7 +6,7 @@ import sys
 import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-os.environ["LGDM_LIB"] = os.path.join(ROOT, "exp", "lib_timing.so")
+os.environ["LGDM_LIB"] = os.path.join(ROOT, "lib_timing.so")
 import torch
 import synth
 from paper_2301_06503_b200 import lgdm

@@ -1,4 +1,4 @@
-"""Per-phase cycle breakdown of k_sweepq (debug build lib_timing.so, -DLGDM_PHASE_TIMING):
+"""Per-phase cycle breakdown of k_sweepq (debug build lib_timing.so from tools/build_timing.sh):
 thread 0 of the PC, C and flush roles accumulate clock64 deltas per phase."""
 import ctypes as C
 import os
