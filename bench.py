@@ -72,15 +72,19 @@ def roofs(etype: int, n_elems: int, alg_bytes: float, ms: float, peak_gbs: float
 
 
 def kernel_source_sha(etype: int, kernel: int) -> str:
-    """sha1 (16 hex) of the CUDA sources the assembly kernel is built from, so a committed ncu
-    traffic figure is only reported for the kernel it was measured on."""
+    """sha1 (16 hex) of the CUDA sources the assembly kernel is built from -- comments and
+    blank lines stripped, so a comment edit keeps the measurement but any code change drops
+    it: a committed ncu traffic figure is only reported for the kernel it was measured on."""
     import hashlib
+    import re
     c = os.path.join(ROOT, "paper_2301_06503_b200", "csrc")
     main = {2: "lgdm_sweepq.cuh", 3: "lgdm_sweep4.cuh"}.get(etype, "lgdm_kernels.cuh")
     h = hashlib.sha1()
     for f in (main, "lgdm_device.cuh", "lgdm_sweep.cuh", "lgdm_sweep4.cuh"):
-        with open(os.path.join(c, f), "rb") as fh:
-            h.update(fh.read())
+        with open(os.path.join(c, f)) as fh:
+            src = re.sub(r"/\*.*?\*/", "", fh.read(), flags=re.S)
+        code = [ln.split("//")[0].rstrip() for ln in src.splitlines()]
+        h.update("\n".join(ln for ln in code if ln.strip()).encode())
     return h.hexdigest()[:16]
 
 
