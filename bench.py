@@ -106,6 +106,23 @@ def measured_traffic(workload: str, etype: int, kernel: int):
     return None, f"no ncu capture of the current kernel sources (src {sha})"
 
 
+def measured_pipes(workload: str, etype: int, kernel: int):
+    """ncu FP64-pipe and issue utilisation of the assembly kernel from the same committed
+    capture as measured_traffic (None unless the kernel-source hash matches)."""
+    import glob
+    sha = kernel_source_sha(etype, kernel)
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "traffic.json")), reverse=True):
+        try:
+            with open(path) as f:
+                e = json.load(f).get(workload)
+        except Exception:
+            continue
+        if isinstance(e, dict) and e.get("src_sha") == sha and e.get("fp64_pipe_pct") is not None:
+            return {"fp64_pipe_pct": e["fp64_pipe_pct"], "issue_active_pct": e.get("issue_active_pct"),
+                    "source": f"ncu --set full, {os.path.relpath(path, ROOT)} ({e.get('profile', '')})"}
+    return None
+
+
 def algorithmic_bytes(ndpn, dim, nen, ngp, nnz, n_rows, n_nodes, n_elems):
     """8 nnz (K) + 8 ndof (R) + 8 ndof (dofs) + 8 nel ngp (kappa) + 8 d nnodes
     (coords) + 4 nen nel (conn); rows/dofs/elements are the rank's own."""
@@ -592,6 +609,7 @@ def main():
     n_total = cfg.n_elems
     value = n_total / (r["ms_per_step"] * 1e-3)
     traffic, traffic_src = measured_traffic(cfg.name, cfg.etype, args.kernel) if ws == 1 else (None, "multi-rank")
+    pipes = measured_pipes(cfg.name, cfg.etype, args.kernel) if ws == 1 else None
     achieved = r["alg_bytes"] / (r["assemble_ms"] * 1e-3) / 1e9
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
@@ -609,6 +627,7 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                      "algorithmic_bytes": r["alg_bytes"], "peak_source": peak_src,
+                     "ncu_pipes": pipes,
                      "kernel": "lgdm_assemble (all launches of one call), rank max",
                      **roofs(cfg.etype, r["n_elems_local"], r["alg_bytes"], r["assemble_ms"],
                              peak)},   # per GPU: the rank's own elements / bytes

@@ -35,7 +35,11 @@ for cid, k, tag, wl in ((4, "k_sweep4", "sweep4_c4", "hex8_200^3"), (3, "k_sweep
         mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
         return float(v.replace(",", "")) * mult
     etype = 3 if tag.startswith("sweep4") else 2
+    pct = lambda key: float(d[key].replace(",", "")) if key in d else None
     out[wl] = {"bytes": num("dram__bytes_read.sum") + num("dram__bytes_write.sum"), "kernel": k,
+               "fp64_pipe_pct": pct("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+               "issue_active_pct": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+               "smem_wavefronts": pct("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"),
                "src_sha": bench.kernel_source_sha(etype, 0), "profile": f"prof_{tag}.ncu-rep",
                "duration_ms": float(d["gpu__time_duration.sum"].replace(",", "")) * {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0, "second": 1e3, "s": 1e3}[rows[1][rows[0].index("gpu__time_duration.sum")]]}
 json.dump(out, open("gpurun_out/prof_round/traffic.json", "w"), indent=1)
