@@ -219,9 +219,11 @@ lgdm_status lgdm_get_blocked(lgdm_mesh mesh, lgdm_csr* K, double** R);
 
 /* ---- Newton loop pieces (Alg. 2 lines 4-7 and 16) ----
  * A whole mesh on one rank, or row-owned slabs with a communicator (lgdm_set_comm): rank p
- * owns a contiguous node range that follows rank p-1's, and keeps one ghost layer per
- * interior face (the layout of the slab partition; lgdm_set_comm checks it, and a slab mesh
- * without a validated layout -> LGDM_ERR_UNSUPPORTED).  Across ranks: dof ids are GLOBAL (every
+ * owns a contiguous node range that follows rank p-1's; its ghost dofs below are rank p-1's
+ * last owned dofs and rank p-1's ghosts above are rank p's first owned dofs (the slab
+ * partitions of slabs.py: one node layer each way for equal order; two lattice rows below and
+ * one above for mixed order -- the exchange counts need not match).  lgdm_set_comm checks it;
+ * a slab mesh without a validated layout -> LGDM_ERR_UNSUPPORTED.  Across ranks: dof ids are GLOBAL (every
  * rank passes the same lists), delta vectors are LOCAL dof vectors (the mesh's owned + ghost
  * dofs in node order, lgdm_dof_offsets), their ghost dofs filled from the neighbouring slabs by
  * an NCCL send / recv halo exchange, and every sum is an NCCL allreduce.  All work runs on the

@@ -250,6 +250,8 @@ struct lgdm_mesh_s {
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
   bool halo_ok = false;           // slab neighbour layout validated (lgdm_set_comm)
+  // halo exchange counts (dofs): sent to / received from the rank below and above
+  int64_t halo_send_lo = 0, halo_recv_lo = 0, halo_send_hi = 0, halo_recv_hi = 0;
   void* sweep = nullptr;  // sweep-path state (lgdm_sweep.cuh)
   // mixed-order meshes (lgdm_mixed.cuh)
   bool mixed = false;
@@ -711,7 +713,8 @@ lgdm_status build_pattern(lgdm_mesh m, int64_t global_node_offset) {
   const FamInfo& f = m->f;
   const int nen = f.nen;
   const int64_t nn = m->n_nodes, ne = m->n_elems, no = m->n_owned, nsl = ne * nen;
-  if (nsl >= (int64_t(1) << 31)) return fail(LGDM_ERR_UNSUPPORTED, "n_elems * nen >= 2^31");
+  if (nsl >= (int64_t(1) << 31) || nn + 1 >= (int64_t(1) << 31))   // CUB item counts are int
+    return fail(LGDM_ERR_UNSUPPORTED, "n_elems * nen or n_nodes + 1 >= 2^31");
   cudaStream_t st = m->stream;
   // scratch (freed at the end)
   int32_t *keys = nullptr, *vals = nullptr, *keys2 = nullptr, *adj_slot = nullptr, *counts = nullptr,
@@ -1288,12 +1291,14 @@ static lgdm_status newton_ready(lgdm_mesh m) {
 static lgdm_status halo_exchange(lgdm_mesh m, double* x) {
   if (!multi_rank(m)) return LGDM_OK;
   const DofRange d = dof_range(m);
-  const int64_t glo = d.own_b, ghi = d.nloc - d.own_e;
+  // below: my first owned dofs are the lower rank's upper ghosts; my lower ghosts are its last
+  // owned dofs (counts from lgdm_set_comm: the two sides may differ, e.g. mixed-order slabs)
+  const int64_t sl = m->halo_send_lo, rl = m->halo_recv_lo, sh = m->halo_send_hi, rh = m->halo_recv_hi;
   ncclResult_t r = g_nccl.groupStart();
-  if (glo > 0 && r == ncclSuccess) r = g_nccl.send(x + d.own_b, size_t(glo), ncclFloat64, m->rank - 1, m->comm, m->stream);
-  if (glo > 0 && r == ncclSuccess) r = g_nccl.recv(x, size_t(glo), ncclFloat64, m->rank - 1, m->comm, m->stream);
-  if (ghi > 0 && r == ncclSuccess) r = g_nccl.send(x + d.own_e - ghi, size_t(ghi), ncclFloat64, m->rank + 1, m->comm, m->stream);
-  if (ghi > 0 && r == ncclSuccess) r = g_nccl.recv(x + d.own_e, size_t(ghi), ncclFloat64, m->rank + 1, m->comm, m->stream);
+  if (sl > 0 && r == ncclSuccess) r = g_nccl.send(x + d.own_b, size_t(sl), ncclFloat64, m->rank - 1, m->comm, m->stream);
+  if (rl > 0 && r == ncclSuccess) r = g_nccl.recv(x + d.own_b - rl, size_t(rl), ncclFloat64, m->rank - 1, m->comm, m->stream);
+  if (sh > 0 && r == ncclSuccess) r = g_nccl.send(x + d.own_e - sh, size_t(sh), ncclFloat64, m->rank + 1, m->comm, m->stream);
+  if (rh > 0 && r == ncclSuccess) r = g_nccl.recv(x + d.own_e, size_t(rh), ncclFloat64, m->rank + 1, m->comm, m->stream);
   const ncclResult_t re = g_nccl.groupEnd();
   if (r != ncclSuccess || re != ncclSuccess)
     return fail(LGDM_ERR_NCCL, "halo exchange: %s", g_nccl.getErrorString ? g_nccl.getErrorString(r != ncclSuccess ? r : re) : "?");
@@ -1722,10 +1727,11 @@ lgdm_status lgdm_set_comm(lgdm_mesh m, const void* uid, int nranks, int rank) {
   m->halo_ok = false;
   if (nranks > 1) {
     // the Newton pieces' halo exchange assumes row-owned slabs in rank order: rank p's first
-    // owned node follows rank p-1's last owned node, and the ghosts mirror (rank p-1 keeps as
-    // many ghosts above as rank p keeps below, nodes and dofs).  All-gather every rank's
-    // ranges and check; a layout that does not fit leaves the Newton pieces unsupported (the
-    // assembly and the residual norms do not depend on it).
+    // owned node follows rank p-1's last owned node, rank p's lower ghosts are rank p-1's
+    // last owned nodes / dofs and rank p-1's upper ghosts rank p's first ones (the two counts
+    // may differ: a mixed-order slab keeps two lattice rows below, one above).  All-gather
+    // every rank's ranges and check; a layout that does not fit leaves the Newton pieces
+    // unsupported (the assembly and the residual norms do not depend on it).
     const DofRange d = dof_range(m);
     const int64_t mine[8] = {m->gid0, m->own_b, m->own_e, m->n_nodes, d.col_off, d.own_b, d.own_e, d.nloc};
     int64_t* buf = nullptr;
@@ -1740,14 +1746,24 @@ lgdm_status lgdm_set_comm(lgdm_mesh m, const void* uid, int nranks, int rank) {
     cudaFree(buf);
     if (r != ncclSuccess)
       return fail(LGDM_ERR_NCCL, "ncclAllGather: %s", g_nccl.getErrorString ? g_nccl.getErrorString(r) : "?");
-    bool ok = all[1] == 0 && all[size_t(8) * (nranks - 1) + 2] == all[size_t(8) * (nranks - 1) + 3];
+    // (per rank: gid0, own_b, own_e, n_nodes, dof col_off, dof own_b, dof own_e, dof nloc)
+    bool ok = all[1] == 0 && all[5] == 0 && all[size_t(8) * (nranks - 1) + 2] == all[size_t(8) * (nranks - 1) + 3] &&
+              all[size_t(8) * (nranks - 1) + 6] == all[size_t(8) * (nranks - 1) + 7];
     for (int p = 1; p < nranks && ok; ++p) {
       const int64_t* a = &all[size_t(8) * (p - 1)];
       const int64_t* b = &all[size_t(8) * p];
-      ok = a[0] + a[2] == b[0] + b[1] && a[3] - a[2] == b[1] &&      // nodes
-           a[4] + a[6] == b[4] + b[5] && a[7] - a[6] == b[5];         // dofs
+      ok = a[0] + a[2] == b[0] + b[1] && a[4] + a[6] == b[4] + b[5] &&   // owned ranges adjoin
+           b[1] <= a[2] - a[1] && b[5] <= a[6] - a[5] &&                  // lower ghosts in p-1's
+           a[3] - a[2] <= b[2] - b[1] && a[7] - a[6] <= b[6] - b[5];      // upper ghosts in p's
     }
     m->halo_ok = ok;
+    if (ok) {
+      const int64_t* me = &all[size_t(8) * rank];
+      m->halo_recv_lo = me[5];
+      m->halo_recv_hi = me[7] - me[6];
+      m->halo_send_lo = rank > 0 ? all[size_t(8) * (rank - 1) + 7] - all[size_t(8) * (rank - 1) + 6] : 0;
+      m->halo_send_hi = rank + 1 < nranks ? all[size_t(8) * (rank + 1) + 5] : 0;
+    }
   }
   return LGDM_OK;
 }
