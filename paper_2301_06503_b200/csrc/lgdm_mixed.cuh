@@ -530,7 +530,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
 template <int T> struct MGStage {
   static constexpr int MXS = 4;
   static constexpr int RB = ((MFam<T>::DIM + 1) * MFam<T>::NDOFE + 31) / 32 * 32;
-  static constexpr int SIZE = MXS * (RB + 4);
+  static constexpr int SIZE = MXS * (RB + 4 + 4);   // row-blocks, F, column offsets (8 x int32)
 };
 
 template <int T, int WPB>
@@ -547,6 +547,7 @@ k_mixed_gather(int64_t nn, const NodeMeta* __restrict__ meta, const MixAdj* __re
   double* buf = smem_mg + w * (max_row + SG::SIZE);
   double* stg = buf + max_row;                        // [MXS][RB] row-blocks, then [MXS][4] F
   double* stf = stg + SG::MXS * SG::RB;
+  int32_t* sco = reinterpret_cast<int32_t*>(stf + SG::MXS * 4);   // [MXS][8] column offsets
   const int64_t stride = int64_t(gridDim.x) * WPB;
   int64_t n = int64_t(blockIdx.x) * WPB + w;
   NodeMeta nx{};
@@ -584,14 +585,18 @@ k_mixed_gather(int64_t nn, const NodeMeta* __restrict__ meta, const MixAdj* __re
           if (qoff[t] >= 0) cp_async8(stg + u * SG::RB + lane + 32 * t, src + lane + 32 * t);
         if (lane < nr) cp_async8(stf + u * 4 + lane, EF + e * ND + lr + lane);
       }
+      // the round's column offsets (8 int32 per adjacency entry) join the same async group
+      if (lane < 8 * kk) {
+        const unsigned d = unsigned(__cvta_generic_to_shared(sco + lane));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(&adj[k + (lane >> 3)].coff[lane & 7]) : "memory");
+      }
       cp_async_wait_all();
       __syncwarp();
       // accumulate in ascending element order
       for (int u = 0; u < kk; ++u) {
-        const MixAdj* en = adj + k + u;
 #pragma unroll
         for (int t = 0; t < NQ; ++t)
-          if (qoff[t] >= 0) buf[qoff[t] + en->coff[qb[t]]] += stg[u * SG::RB + lane + 32 * t];
+          if (qoff[t] >= 0) buf[qoff[t] + sco[u * 8 + qb[t]]] += stg[u * SG::RB + lane + 32 * t];
         if (lane < nr) rsum += stf[u * 4 + lane];
         __syncwarp();
       }
