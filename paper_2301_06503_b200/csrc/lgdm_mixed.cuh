@@ -550,6 +550,14 @@ k_mixed_gather(int64_t nn, const NodeMeta* __restrict__ meta, const MixAdj* __re
   int32_t* sco = reinterpret_cast<int32_t*>(stf + SG::MXS * 4);   // [MXS][8] column offsets
   const int64_t stride = int64_t(gridDim.x) * WPB;
   int64_t n = int64_t(blockIdx.x) * WPB + w;
+  int qb[NQ], qrow[NQ], qcomp[NQ];   // local node, row and component of this lane's entries
+#pragma unroll
+  for (int t = 0; t < NQ; ++t) {
+    const int q = lane + 32 * t, c = q % ND;
+    qb[t] = mdof_node<T>(c);
+    qrow[t] = q / ND;
+    qcomp[t] = mdof_comp<T>(c);
+  }
   NodeMeta nx{};
   if (n < nn) nx = meta[n];
   for (; n < nn; n += stride) {
@@ -559,15 +567,11 @@ k_mixed_gather(int64_t nn, const NodeMeta* __restrict__ meta, const MixAdj* __re
     const int nr = md.nr, W = md.W;
     const int tot = nr * W;
     for (int k = lane; k < tot; k += 32) buf[k] = 0.0;
-    // this lane's entries (row i, element dof c) of an element block: fixed for the node
-    int qb[NQ], qoff[NQ];   // local node of the column; row * W + component (-1: no entry)
+    // this lane's entries (row i, element dof c) of an element block: row * W + component of
+    // the node's block-row (-1: no entry); qb / qrow / qcomp depend on the lane only
+    int qoff[NQ];
 #pragma unroll
-    for (int t = 0; t < NQ; ++t) {
-      const int q = lane + 32 * t;
-      const int c = q % ND;
-      qb[t] = mdof_node<T>(c);
-      qoff[t] = q < nr * ND ? (q / ND) * W + mdof_comp<T>(c) : -1;
-    }
+    for (int t = 0; t < NQ; ++t) qoff[t] = lane + 32 * t < nr * ND ? qrow[t] * W + qcomp[t] : -1;
     double rsum = 0.0;
     const int64_t k0 = md.k0, k1 = md.k0 + md.nk;
     for (int64_t k = k0; k < k1; k += SG::MXS) {
