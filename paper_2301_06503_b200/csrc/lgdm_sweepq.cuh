@@ -307,30 +307,18 @@ k_sweepq(DevMat m, SweepGeom G, const double* __restrict__ coords,
             // 16-byte vectors when the CSR range and the row buffer are co-aligned
             const int head = ((reinterpret_cast<uintptr_t>(out) & 15) != 0) ? 1 : 0;
             const bool co = ((reinterpret_cast<uintptr_t>(out) ^ reinterpret_cast<uintptr_t>(src)) & 15) == 0;
+            // (no reset: the next node row's first contributors store, see add_blocks)
             if (co) {
-              if (head && ft == 0) {
-                __stcs(out, src[0]);
-                src[0] = 0.0;
-              }
+              if (head && ft == 0) __stcs(out, src[0]);
               const int nv = (cnt - head) >> 1;
               double2* o2 = reinterpret_cast<double2*>(out + head);
-              double2* s2 = reinterpret_cast<double2*>(src + head);
-              const double2 zero = make_double2(0.0, 0.0);
+              const double2* s2 = reinterpret_cast<const double2*>(src + head);
 #pragma unroll 4
-              for (int k = ft; k < nv; k += F_T) {
-                __stcs(o2 + k, s2[k]);
-                s2[k] = zero;
-              }
-              if (((cnt - head) & 1) && ft == 0) {
-                __stcs(out + cnt - 1, src[cnt - 1]);
-                src[cnt - 1] = 0.0;
-              }
+              for (int k = ft; k < nv; k += F_T) __stcs(o2 + k, s2[k]);
+              if (((cnt - head) & 1) && ft == 0) __stcs(out + cnt - 1, src[cnt - 1]);
             } else {
 #pragma unroll 4
-              for (int k = ft; k < cnt; k += F_T) {
-                __stcs(out + k, src[k]);
-                src[k] = 0.0;
-              }
+              for (int k = ft; k < cnt; k += F_T) __stcs(out + k, src[k]);
             }
           }
           for (int x = ix0; x < xa; ++x) flush_edge(x, zn);   // edge columns (x = 0) or rows
@@ -346,6 +334,13 @@ k_sweepq(DevMat m, SweepGeom G, const double* __restrict__ coords,
             ns_of(ix0, zn)[k] = 0.0;
             ns_of(ix0, zn)[k + SQ::NSC] = 0.0;
           }
+          // this buffer serves node row zn + 3 next; the mesh's top node row has no neighbours
+          // above, so its (never written) dy = +1 slots must read as zero in the diagonal sums
+          if (zn + 3 == G.nl)
+            for (int k = ft; k < cols * 27; k += F_T) {
+              const int cc = k / 27, q = k - 27 * cc, r = q / 9;
+              row_of(ix0 + cc, zn)[r * 27 + 18 + (q - 9 * r)] = 0.0;
+            }
           PT_MARK(7, ptf);
           bsync(SQ::B_FW, F_T);
           PT_MARK(8, ptf);
@@ -417,28 +412,32 @@ k_sweepq(DevMat m, SweepGeom G, const double* __restrict__ coords,
   };
   // block (row node, neighbour offset) inside the row buffer: [r][dy][dx][j]
   auto blk_of = [&](int x, int64_t zn, int dx, int dy) { return row_of(x, zn) + (dy + 1) * 9 + (dx + 1) * 3; };
-  auto add_blocks = [&](double* Pb, double* Qb, const PairQ& P) {
+  // first: this element is the first contributor to these entries in the add order (element
+  // row, colour), so it stores instead of adding -- the row buffers need no reset after a
+  // flush (only the never-written slots of edge nodes are kept at zero)
+  auto add_blocks = [&](double* Pb, double* Qb, const PairQ& P, bool first) {
+    auto put = [&](double* q, double v) { *q = first ? v : *q + v; };
     if (Pb) {   // K_AB into A's row at B's slot
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
-        Pb[r * 27 + 0] += P.Kuu[r][0];
-        Pb[r * 27 + 1] += P.Kuu[r][1];
-        Pb[r * 27 + 2] += P.Kue_ab[r];
+        put(Pb + r * 27 + 0, P.Kuu[r][0]);
+        put(Pb + r * 27 + 1, P.Kuu[r][1]);
+        put(Pb + r * 27 + 2, P.Kue_ab[r]);
       }
-      Pb[54 + 0] += P.Keu_ab[0];
-      Pb[54 + 1] += P.Keu_ab[1];
-      Pb[54 + 2] += P.Kee_ab;
+      put(Pb + 54 + 0, P.Keu_ab[0]);
+      put(Pb + 54 + 1, P.Keu_ab[1]);
+      put(Pb + 54 + 2, P.Kee_ab);
     }
     if (Qb) {   // K_BA into B's row at A's slot
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
-        Qb[r * 27 + 0] += P.Kuu[0][r];
-        Qb[r * 27 + 1] += P.Kuu[1][r];
-        Qb[r * 27 + 2] += P.Kue_ba[r];
+        put(Qb + r * 27 + 0, P.Kuu[0][r]);
+        put(Qb + r * 27 + 1, P.Kuu[1][r]);
+        put(Qb + r * 27 + 2, P.Kue_ba[r]);
       }
-      Qb[54 + 0] += P.Keu_ba[0];
-      Qb[54 + 1] += P.Keu_ba[1];
-      Qb[54 + 2] += P.Kee_ba;
+      put(Qb + 54 + 0, P.Keu_ba[0]);
+      put(Qb + 54 + 1, P.Keu_ba[1]);
+      put(Qb + 54 + 2, P.Kee_ba);
     }
   };
   auto owned = [&](int x, int64_t z) { return x >= ix0 && x < ix1 && z >= z0 && z < z1; };
@@ -494,10 +493,17 @@ k_sweepq(DevMat m, SweepGeom G, const double* __restrict__ coords,
           const int ax = i + oax, b1x = i + ob1x, b2x = i + ob2x;
           const int64_t az = s + oaz, b1z = s + ob1z, b2z = s + ob2z;
           const bool oa = owned(ax, az), ob1 = owned(b1x, b1z), ob2 = owned(b2x, b2z);
+          // first contributor of the pair's entries (shared with the neighbour across an edge):
+          // star 0: (0,1) bottom edge -- element row s-1 adds first unless s = 0; (0,3) left
+          // edge -- the even column of {i-1, i} (colour 0) first; star 1: (1,2) right edge
+          // likewise, (1,3) diagonal; star 2: (2,0) diagonal, (2,3) top edge (row s+1 later)
+          const bool ev = (i & 1) == 0;
+          const bool first1 = ck == 0 ? s == 0 : (ck == 1 ? (ev || i + 1 == G.nx) : true);
+          const bool first2 = ck == 0 ? (ev || i == 0) : true;
           add_blocks(oa ? blk_of(ax, az, b1x - ax, int(b1z - az)) : nullptr,
-                     ob1 ? blk_of(b1x, b1z, ax - b1x, int(az - b1z)) : nullptr, P1);
+                     ob1 ? blk_of(b1x, b1z, ax - b1x, int(az - b1z)) : nullptr, P1, first1);
           add_blocks(oa ? blk_of(ax, az, b2x - ax, int(b2z - az)) : nullptr,
-                     ob2 ? blk_of(b2x, b2z, ax - b2x, int(az - b2z)) : nullptr, P2);
+                     ob2 ? blk_of(b2x, b2z, ax - b2x, int(az - b2z)) : nullptr, P2, first2);
           auto add_ns = [&](int x, int64_t z, const double (&v)[6]) {
             double* np = ns_of(x, z) + cg * SQ::NSC;   // this colour's node sums
             double w[6];
