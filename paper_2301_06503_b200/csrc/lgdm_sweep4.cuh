@@ -354,14 +354,9 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
     if (own_s) finish_node(x, y, s, colp, s < G.nl, inner);
     if (top) finish_node(x, y, s + 1, colp, false, inner);
     __syncwarp();
-    double2* z2 = reinterpret_cast<double2*>(colp + ((s & 1) ? S4::Z1 : S4::Z0));
-    double2* ud = reinterpret_cast<double2*>(colp + S4::UP);
-    double2* dn2 = reinterpret_cast<double2*>(colp + S4::DN);
-    const double2 zero = make_double2(0.0, 0.0);
-    for (int k2 = lane; k2 < S4::PLD / 2; k2 += 32) z2[k2] = zero;
-    for (int k2 = lane; k2 < S4::PLD / 2; k2 += 32) ud[k2] = zero;
-    for (int k2 = lane; k2 < S4::PLD / 2; k2 += 32) dn2[k2] = zero;
-    if (lane < 4) reinterpret_cast<double2*>(colp + S4::NS + (s & 1) * 8)[lane] = zero;
+    // the planes need no reset: every entry's first contributor stores (see the C adds), and
+    // the slots of a column's missing neighbours (mesh sides) are never written (zero)
+    if (lane < 4) reinterpret_cast<double2*>(colp + S4::NS + (s & 1) * 8)[lane] = make_double2(0.0, 0.0);
   };
   // the layer flush is split: the C warps take columns 0 .. NC-1 right after the layer's adds,
   // the PC warps (idle ~70 %) the rest while the C warps compute the next layer's first batch
@@ -640,6 +635,22 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
           const int bx = i + obx, by = j + oby, bzr = sz + obz;
           const bool own_a = ax >= ix0 && ax < ix1 && ay >= iy0 && ay < iy1 && azr >= 0 && s + oaz < z1;
           const bool own_b = bx >= ix0 && bx < ix1 && by >= iy0 && by < iy1 && bzr >= 0 && s + obz < z1;
+          // Is this element the first contributor (add order: layer, then colour (i&1) + 2 (j&1))
+          // to the pair's entries?  The elements sharing nodes A and B differ from this one only
+          // along the axes where A and B coincide: not first if the layer below shares them (A,
+          // B on this element's bottom face), or a sharing neighbour in this layer has the
+          // smaller colour (this element's parity bit is 1 on such an axis).  The first
+          // contributor stores, the others add: the planes need no reset after a flush.
+          bool first = !(obz == oaz && oaz == 0 && s >= 1);
+          if (obx == oax) {
+            const int ia = oax ? i + 1 : i - 1;
+            if ((i & 1) && ia >= 0 && ia < G.nx) first = false;
+          }
+          if (oby == oay) {
+            const int ja = oay ? j + 1 : j - 1;
+            if ((j & 1) && ja >= 0 && ja < G.nyE) first = false;
+          }
+          const double2 zero2 = make_double2(0.0, 0.0);
           if (own_a) {
             double* Pp = plane_of(col_of(ax, ay), (zpar_s ^ oaz) & 1, oaz == 0, dzAB);
             // all 8 loads of the block first: the compiler cannot prove the rows distinct and
@@ -648,8 +659,8 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
               const double2* q = reinterpret_cast<const double2*>(Pp + r * 36);
-              lo[r] = q[qAB0];
-              hi[r] = q[qAB1];
+              lo[r] = first ? zero2 : q[qAB0];
+              hi[r] = first ? zero2 : q[qAB1];
             }
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
@@ -669,8 +680,8 @@ k_sweep4(DevMat m, SweepGeom G, const double* __restrict__ coords,
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
               const double2* q = reinterpret_cast<const double2*>(Pp + r * 36);
-              lo[r] = q[qBA0];
-              hi[r] = q[qBA1];
+              lo[r] = first ? zero2 : q[qBA0];
+              hi[r] = first ? zero2 : q[qBA1];
             }
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
